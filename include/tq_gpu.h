@@ -1,0 +1,114 @@
+/*
+ * tq_gpu.h — the drop-in C-ABI of libtq_gpu.so (B200 / sm_100a).
+ *
+ * Plain C: pointers, sizes, status codes.  No exceptions cross it; status
+ * 0 = OK, else 1 + tierq::Errc ordinal (tq_types.h).  Every entry point
+ * replaces an operator or tier move the reference specifies; each line cites
+ * the reference interface it stands in for.  `stream` is a cudaStream_t
+ * (NULL = the context's own stream).  Calls that produce data-dependent
+ * output sizes (filter, partition, probe, aggregate) read the size back and
+ * block until the output batch is allocated; the data itself is written
+ * asynchronously on `stream`.
+ */
+#ifndef TQ_GPU_H
+#define TQ_GPU_H
+
+#include "tq_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tq_ctx tq_ctx;
+typedef struct tq_join_table tq_join_table;
+
+typedef struct tq_opts {
+  int device;                    /* CUDA device ordinal */
+  uint32_t ctas_per_sm;          /* persistent grid = ctas_per_sm x SMs (0 = auto) */
+  uint64_t device_budget_bytes;  /* Device-tier capacity for the ledger (0 = unlimited);
+                                    SPEC.md:259-276 reserve/alloc_within */
+} tq_opts;
+
+/* ---- context / errors (reference common.hpp:57-74 Error, Errc) --------- */
+tq_status tq_ctx_create(const tq_opts* opts, tq_ctx** out);
+void tq_ctx_destroy(tq_ctx* ctx);
+const char* tq_last_error(void);                 /* thread-local message of the last failure */
+const char* tq_errc_name(tq_status status);      /* common.cpp:19-41 errc_name */
+tq_status tq_sync(tq_ctx* ctx, void* stream);
+uint64_t tq_device_bytes_in_use(tq_ctx* ctx);    /* ledger: allocated Device-tier bytes */
+uint32_t tq_kernel_launches(tq_ctx* ctx);        /* kernels this context has launched */
+
+/* ---- batches (reference types.hpp:125-143 ColumnBatch; types.cpp:146-170) --- */
+/* Allocate an uninitialised device batch with the schema of `like`
+ * (kind/precision/scale; a column gets a bitmap iff like->cols[i].validity != NULL). */
+tq_status tq_batch_alloc(tq_ctx* ctx, const tq_batch* like, uint64_t rows, tq_batch* out, void* stream);
+/* Host -> device copy into a new device batch (pinned or pageable host memory). */
+tq_status tq_batch_upload(tq_ctx* ctx, const tq_batch* host, tq_batch* out, void* stream);
+/* Device -> host copy into malloc'ed buffers (free with tq_host_batch_free). Synchronous. */
+tq_status tq_batch_download(tq_ctx* ctx, const tq_batch* dev, tq_batch* out, void* stream);
+void tq_batch_free(tq_ctx* ctx, tq_batch* b);
+void tq_host_batch_free(tq_batch* b);
+
+/* ---- columnar substrate (reference transform.cpp) ---------------------- */
+/* take: transform.cpp:90-120.  ids: DEVICE array of n row ids. */
+tq_status tq_take(tq_ctx* ctx, const tq_batch* in, const uint64_t* ids, uint64_t n, tq_batch* out,
+                  void* stream);
+/* concat: transform.cpp:49-88 (bitmap iff any input has one). */
+tq_status tq_concat(tq_ctx* ctx, const tq_batch* ins, uint32_t n, tq_batch* out, void* stream);
+/* slice: transform.cpp:21-47. */
+tq_status tq_slice(tq_ctx* ctx, const tq_batch* in, uint64_t start, uint64_t len, tq_batch* out,
+                   void* stream);
+
+/* ---- operators ---------------------------------------- */
+/* filter_execute: rows where pred is true; schema unchanged. */
+tq_status tq_filter(tq_ctx* ctx, const tq_batch* in, tq_expr pred, tq_batch* out, void* stream);
+/* project_execute: one output column per expr. */
+tq_status tq_project(tq_ctx* ctx, const tq_batch* in, const tq_expr* exprs, uint32_t nexprs, tq_batch* out,
+                     void* stream);
+/* hash_partition: part(r) = fnv1a64(keys(r)) mod nparts
+ * (common.hpp:128-136).  `out` holds the parts contiguously in part order
+ * (stable within a part); part p is rows [part_offsets[p], part_offsets[p+1])
+ * (host array of nparts+1). */
+tq_status tq_hash_partition(tq_ctx* ctx, const tq_batch* in, const uint32_t* keys, uint32_t nkeys,
+                            uint32_t nparts, tq_batch* out, uint64_t* part_offsets, void* stream);
+/* join_execute build side: open-addressing table over the
+ * build batch (which must stay alive until the table is destroyed). */
+tq_status tq_join_build(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
+                        tq_join_table** out, void* stream);
+/* join_execute probe side: inner equi-join, null keys never match; output =
+ * build columns then probe columns. */
+tq_status tq_join_probe(tq_ctx* ctx, const tq_join_table* table, const tq_batch* probe, const uint32_t* keys,
+                        uint32_t nkeys, tq_batch* out, void* stream);
+void tq_join_table_destroy(tq_ctx* ctx, tq_join_table* t);
+/* aggregate_execute: keys then one column per aggregate. */
+tq_status tq_aggregate(tq_ctx* ctx, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs,
+                       uint32_t naggs, tq_batch* out, void* stream);
+
+/* ---- fused pipelines: Filter -> Project -> sink in one pass over the batch
+ * (the per-batch operator chain of one compute task).
+ * pred may be NULL; keys/aggs index the PROJECTED columns. ------------- */
+tq_status tq_pipeline_materialize(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                  uint32_t nexprs, tq_batch* out, void* stream);
+tq_status tq_pipeline_aggregate(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                uint32_t nexprs, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs,
+                                uint32_t naggs, tq_batch* out, void* stream);
+tq_status tq_pipeline_partition(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                uint32_t nexprs, const uint32_t* keys, uint32_t nkeys, uint32_t nparts,
+                                tq_batch* out, uint64_t* part_offsets, void* stream);
+/* probe output = build columns listed in build_cols, then projected probe columns */
+tq_status tq_pipeline_probe(tq_ctx* ctx, const tq_join_table* table, const tq_batch* in, const tq_expr* pred,
+                            const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,
+                            const uint32_t* build_cols, uint32_t nbuild_cols, tq_batch* out, void* stream);
+tq_status tq_pipeline_build(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
+                            uint32_t nkeys, tq_join_table** out, void* stream);
+
+/* ---- synthetic TPC-H-style tables generated on the device,
+ * bit-identical to the CPU generator (counter-based SplitMix64,
+ * common.hpp:139-158).  table: 0 orders, 1 lineitem, 2 customer,
+ * 3 supplier, 4 part, 5 partsupp, 6 nation, 7 region. */
+tq_status tq_datagen(tq_ctx* ctx, int table, double sf, tq_batch* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQ_GPU_H */

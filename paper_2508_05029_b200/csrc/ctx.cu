@@ -1,0 +1,253 @@
+// ctx.cu — context, Device-tier ledger/allocator and batch movement.
+//
+// Device memory comes from a per-device stream-ordered pool
+// (cudaMallocFromPoolAsync) with the release threshold at "never", so a
+// steady-state query reuses its buffers without driver calls.  Every
+// allocation is charged to the context ledger (SPEC.md:240-276,
+// MemoryLedger / alloc_within); exceeding the configured Device capacity
+// returns ReservationExceeded, the signal the Compute Executor's on_oom
+// retry path consumes.
+#include <cstdlib>
+#include <cstring>
+
+#include "ctx.h"
+
+namespace tq {
+
+thread_local std::string g_err;
+
+void fail(int status, const std::string& msg) { throw Fail{status, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(TQ_INTERNAL, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+void counted_launch(tq_ctx* c) { c->launches.fetch_add(1, std::memory_order_relaxed); }
+
+size_t width_of(uint8_t kind) {
+  switch (kind) {
+    case TQ_INT64: return 8;
+    case TQ_FLOAT64: return 8;
+    case TQ_BOOL: return 1;
+    case TQ_DECIMAL: return 16;
+    default: return 0;
+  }
+}
+
+void* dalloc(tq_ctx* c, uint64_t bytes, cudaStream_t st) {
+  uint64_t b = round_up(bytes ? bytes : 1, 256) + 256;  // tail pad: 16-B bulk copies never run off the end
+  uint64_t now = c->in_use.fetch_add(b) + b;
+  if (c->budget && now > c->budget) {
+    c->in_use.fetch_sub(b);
+    fail(TQ_RESERVATION_EXCEEDED, "device budget exceeded: need " + std::to_string(now) + " of " +
+                                      std::to_string(c->budget) + " bytes");
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&p, b, c->pool, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c->in_use.fetch_sub(b);
+    fail(TQ_RESERVATION_EXCEEDED, std::string("device allocation failed: ") + cudaGetErrorString(e));
+  }
+  return p;
+}
+
+void dfree(tq_ctx* c, void* p, uint64_t bytes, cudaStream_t st) {
+  if (!p) return;
+  uint64_t b = round_up(bytes ? bytes : 1, 256) + 256;
+  cudaFreeAsync(p, st);
+  c->in_use.fetch_sub(b);
+}
+
+void alloc_batch(tq_ctx* c, uint64_t rows, const std::vector<tq_column>& schema, const std::vector<bool>& want_valid,
+                 tq_batch* out, cudaStream_t st, const std::vector<uint64_t>* utf8_bytes) {
+  Owner* own = new Owner{c, st, {}};
+  out->rows = rows;
+  out->ncols = (uint32_t)schema.size();
+  out->mem = TQ_MEM_DEVICE;
+  out->owner = own;
+  out->cols = (tq_column*)std::calloc(schema.size() ? schema.size() : 1, sizeof(tq_column));
+  try {
+    for (size_t i = 0; i < schema.size(); ++i) {
+      tq_column& d = out->cols[i];
+      d.kind = schema[i].kind;
+      d.precision = schema[i].precision;
+      d.scale = schema[i].scale;
+      uint64_t vb = d.kind == TQ_UTF8 ? (utf8_bytes ? (*utf8_bytes)[i] : 0) : rows * width_of(d.kind);
+      d.values_bytes = vb;
+      d.values = dalloc(c, vb, st);
+      own->bufs.push_back({d.values, vb});
+      if (d.kind == TQ_UTF8) {
+        uint64_t ob = (rows + 1) * 4;
+        d.offsets = (int32_t*)dalloc(c, ob, st);
+        own->bufs.push_back({d.offsets, ob});
+      }
+      if (want_valid[i] && rows > 0) {
+        uint64_t bb = (rows + 7) / 8;
+        d.validity = (uint8_t*)dalloc(c, bb, st);
+        own->bufs.push_back({d.validity, bb});
+        TQ_CUDA(cudaMemsetAsync(d.validity, 0, round_up(bb, 4), st));
+      }
+    }
+  } catch (...) {
+    tq_batch_free(c, out);
+    throw;
+  }
+}
+
+}  // namespace tq
+
+using namespace tq;
+
+extern "C" {
+
+const char* tq_last_error(void) { return tq::g_err.c_str(); }
+
+const char* tq_errc_name(tq_status s) {
+  static const char* names[] = {"OK", "PoolExhausted", "CorruptLayout", "MalformedBatch", "SchemaMismatch", "NotTcf",
+                                "CorruptFooter", "UnknownColumn", "CorruptRowGroup", "IoError",
+                                "ReservationImpossible", "ReservationExceeded", "NoEligibleVictims",
+                                "OutOfMemoryUnsplittable", "CorruptFrame", "PeerDisconnected", "InvalidPlan",
+                                "WorkerFailure", "Internal"};
+  if (s < 0 || s > TQ_INTERNAL) return "Unknown";
+  return names[s];
+}
+
+tq_status tq_ctx_create(const tq_opts* opts, tq_ctx** out) {
+  return guard([&] {
+    int dev = opts ? opts->device : 0;
+    int n = 0;
+    TQ_CUDA(cudaGetDeviceCount(&n));
+    if (dev < 0 || dev >= n) fail(TQ_INTERNAL, "no such CUDA device");
+    TQ_CUDA(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    TQ_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10) fail(TQ_INTERNAL, "libtq_gpu.so is built for sm_100a (B200) only");
+    tq_ctx* c = new tq_ctx();
+    c->device = dev;
+    c->sms = prop.multiProcessorCount;
+    c->ctas_per_sm = opts ? opts->ctas_per_sm : 0;
+    c->budget = opts ? opts->device_budget_bytes : 0;
+    TQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    TQ_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, dev));
+    uint64_t thresh = ~0ull;
+    TQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    TQ_CUDA(cudaHostAlloc(&c->pinned, 4096, cudaHostAllocPortable));
+    *out = c;
+  });
+}
+
+void tq_ctx_destroy(tq_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->prog_cache) cudaFree(kv.second);
+  cudaFreeHost(c->pinned);
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+tq_status tq_sync(tq_ctx* c, void* stream) {
+  return guard([&] { TQ_CUDA(cudaStreamSynchronize(pick(c, stream))); });
+}
+
+uint64_t tq_device_bytes_in_use(tq_ctx* c) { return c->in_use.load(); }
+uint32_t tq_kernel_launches(tq_ctx* c) { return c->launches.load(); }
+
+tq_status tq_batch_alloc(tq_ctx* c, const tq_batch* like, uint64_t rows, tq_batch* out, void* stream) {
+  return guard([&] {
+    std::vector<tq_column> sch(like->cols, like->cols + like->ncols);
+    std::vector<bool> wv;
+    for (uint32_t i = 0; i < like->ncols; ++i) {
+      if (like->cols[i].kind == TQ_UTF8) fail(TQ_INVALID_PLAN, "tq_batch_alloc: utf8 needs byte sizes");
+      wv.push_back(like->cols[i].validity != nullptr);
+    }
+    alloc_batch(c, rows, sch, wv, out, pick(c, stream));
+  });
+}
+
+tq_status tq_batch_upload(tq_ctx* c, const tq_batch* h, tq_batch* out, void* stream) {
+  return guard([&] {
+    cudaStream_t st = pick(c, stream);
+    std::vector<tq_column> sch(h->cols, h->cols + h->ncols);
+    std::vector<bool> wv;
+    std::vector<uint64_t> ub;
+    for (uint32_t i = 0; i < h->ncols; ++i) {
+      wv.push_back(h->cols[i].validity != nullptr);
+      ub.push_back(h->cols[i].values_bytes);
+      if (h->cols[i].kind != TQ_UTF8 && h->cols[i].values_bytes != h->rows * width_of(h->cols[i].kind))
+        fail(TQ_MALFORMED_BATCH, "values length mismatch");
+    }
+    alloc_batch(c, h->rows, sch, wv, out, st, &ub);
+    for (uint32_t i = 0; i < h->ncols; ++i) {
+      const tq_column& s = h->cols[i];
+      tq_column& d = out->cols[i];
+      if (s.values_bytes) TQ_CUDA(cudaMemcpyAsync(d.values, s.values, s.values_bytes, cudaMemcpyHostToDevice, st));
+      if (d.validity && h->rows)
+        TQ_CUDA(cudaMemcpyAsync(d.validity, s.validity, (h->rows + 7) / 8, cudaMemcpyHostToDevice, st));
+      if (s.kind == TQ_UTF8)
+        TQ_CUDA(cudaMemcpyAsync(d.offsets, s.offsets, (h->rows + 1) * 4, cudaMemcpyHostToDevice, st));
+    }
+  });
+}
+
+tq_status tq_batch_download(tq_ctx* c, const tq_batch* d, tq_batch* out, void* stream) {
+  return guard([&] {
+    cudaStream_t st = pick(c, stream);
+    out->rows = d->rows;
+    out->ncols = d->ncols;
+    out->mem = TQ_MEM_HOST;
+    out->owner = nullptr;
+    out->cols = (tq_column*)std::calloc(d->ncols ? d->ncols : 1, sizeof(tq_column));
+    for (uint32_t i = 0; i < d->ncols; ++i) {
+      const tq_column& s = d->cols[i];
+      tq_column& h = out->cols[i];
+      h.kind = s.kind;
+      h.precision = s.precision;
+      h.scale = s.scale;
+      h.values_bytes = s.values_bytes;
+      h.values = std::malloc(s.values_bytes ? s.values_bytes : 1);
+      if (s.values_bytes) TQ_CUDA(cudaMemcpyAsync(h.values, s.values, s.values_bytes, cudaMemcpyDeviceToHost, st));
+      if (s.validity && d->rows) {
+        h.validity = (uint8_t*)std::malloc((d->rows + 7) / 8);
+        TQ_CUDA(cudaMemcpyAsync(h.validity, s.validity, (d->rows + 7) / 8, cudaMemcpyDeviceToHost, st));
+      }
+      if (s.kind == TQ_UTF8) {
+        h.offsets = (int32_t*)std::malloc((d->rows + 1) * 4);
+        TQ_CUDA(cudaMemcpyAsync(h.offsets, s.offsets, (d->rows + 1) * 4, cudaMemcpyDeviceToHost, st));
+      }
+    }
+    TQ_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+void tq_batch_free(tq_ctx* c, tq_batch* b) {
+  if (!b) return;
+  if (b->owner) {
+    Owner* o = (Owner*)b->owner;
+    for (auto& pb : o->bufs) dfree(o->ctx, pb.first, pb.second, o->stream);
+    delete o;
+  }
+  (void)c;
+  std::free(b->cols);
+  b->cols = nullptr;
+  b->ncols = 0;
+  b->rows = 0;
+  b->owner = nullptr;
+}
+
+void tq_host_batch_free(tq_batch* b) {
+  if (!b || !b->cols) return;
+  for (uint32_t i = 0; i < b->ncols; ++i) {
+    std::free(b->cols[i].values);
+    std::free(b->cols[i].validity);
+    std::free(b->cols[i].offsets);
+  }
+  std::free(b->cols);
+  b->cols = nullptr;
+}
+
+}  // extern "C"

@@ -1,0 +1,1163 @@
+// ops.cu — host orchestration of the operators on top of
+// the pipeline kernels, plus the small helper kernels: tile-count scan,
+// aggregation-table init/finalize, take / concat / slice.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ctx.h"
+#include "device.cuh"
+#include "pipeline.h"
+
+struct tq_join_table {
+  tq_ctx* ctx;
+  tq::JoinTable jt;
+  uint64_t bytes;
+  cudaStream_t stream;
+  tq_batch build;                      // borrowed descriptors (cols copied)
+  std::vector<uint8_t> key_cls, key_scale;
+};
+
+namespace tq {
+
+cudaError_t launch_pipeline(int sink, const PipeParams& p, u32 smem_bytes, u32 grid, cudaStream_t st);
+
+// ================================================================== scan
+constexpr int kScanItems = 8;
+constexpr int kScanBlock = 256 * kScanItems;
+
+__device__ __forceinline__ u64 block_excl_scan(u64 v, u64* s_warp, u64& total) {
+  u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u64 incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u64 y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= (u32)o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    u64 x = lane < 8 ? s_warp[lane] : 0;
+    u64 xi = x;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      u64 y = __shfl_up_sync(kFull, xi, o);
+      if (lane >= (u32)o) xi += y;
+    }
+    if (lane < 8) s_warp[8 + lane] = xi - x;
+    if (lane == 7) s_warp[16] = xi;
+  }
+  __syncthreads();
+  total = s_warp[16];
+  u64 r = s_warp[8 + warp] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void k_scan_partials(const u32* in, u64 n, u64* partial) {
+  __shared__ u64 s[24];
+  u64 base = (u64)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
+  u64 sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) sum += in[base + i];
+  u64 tot;
+  block_excl_scan(sum, s, tot);
+  if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+__global__ void k_scan_prefix(u64* partial, u64 nb, u64* total) {
+  __shared__ u64 s[24];
+  u64 carry = 0;
+  for (u64 b0 = 0; b0 < nb; b0 += 256) {
+    u64 i = b0 + threadIdx.x;
+    u64 v = i < nb ? partial[i] : 0;
+    u64 tot;
+    u64 ex = block_excl_scan(v, s, tot);
+    if (i < nb) partial[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void k_scan_apply(const u32* in, u64 n, const u64* partial, u64* out) {
+  __shared__ u64 s[24];
+  u64 base = (u64)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
+  u32 v[kScanItems];
+  u64 sum = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? in[base + i] : 0;
+    sum += v[i];
+  }
+  u64 tot;
+  u64 run = partial[blockIdx.x] + block_excl_scan(sum, s, tot);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) {
+      out[base + i] = run;
+      run += v[i];
+    }
+}
+
+// exclusive scan of n u32 -> u64; *total_dev = sum
+static void scan_u32(tq_ctx* c, const u32* in, u64 n, u64* out, u64* total_dev, cudaStream_t st) {
+  u64 nb = (n + kScanBlock - 1) / kScanBlock;
+  if (nb == 0) nb = 1;
+  u64* partial = (u64*)dalloc(c, nb * 8, st);
+  k_scan_partials<<<(u32)nb, 256, 0, st>>>(in, n, partial);
+  k_scan_prefix<<<1, 256, 0, st>>>(partial, nb, total_dev);
+  k_scan_apply<<<(u32)nb, 256, 0, st>>>(in, n, partial, out);
+  for (int i = 0; i < 3; ++i) counted_launch(c);
+  TQ_CUDA(cudaGetLastError());
+  dfree(c, partial, nb * 8, st);
+}
+
+// offsets[d*ntiles] for each dest + total -> pinned[0..ndest]
+__global__ void k_dest_starts(const u64* offsets, u32 ntiles, u32 ndest, const u64* total, u64* pinned) {
+  u32 d = threadIdx.x;
+  if (d < ndest) pinned[d] = offsets[(u64)d * ntiles];
+  if (d == 0) pinned[ndest] = *total;
+}
+
+// ================================================================== program setup
+struct Prog {
+  ProgramBuilder pb;
+  bool has_pred = false;
+  int pred_h = -1;
+  std::vector<int> outs;  // root handles of projected columns
+  explicit Prog(std::vector<ColumnDesc> s) : pb(std::move(s)) {}
+};
+
+static std::vector<ColumnDesc> schema_of(const tq_batch* in) {
+  std::vector<ColumnDesc> s;
+  for (uint32_t i = 0; i < in->ncols; ++i)
+    s.push_back({in->cols[i].kind, in->cols[i].precision, in->cols[i].scale,
+                 in->rows > 0 && in->cols[i].validity != nullptr});
+  return s;
+}
+
+static void check_device_batch(const tq_batch* b) {
+  if (!b || b->mem != TQ_MEM_DEVICE) fail(TQ_INTERNAL, "expected a device batch");
+  for (uint32_t i = 0; i < b->ncols; ++i) {
+    const tq_column& c = b->cols[i];
+    if (c.kind > TQ_DECIMAL) fail(TQ_MALFORMED_BATCH, "bad column kind");
+    if (c.kind != TQ_UTF8 && c.values_bytes != b->rows * width_of(c.kind))
+      fail(TQ_MALFORMED_BATCH, "values length mismatch");
+  }
+}
+
+// pred may be null; exprs==null && all_cols -> every input column passes through
+static void compile_prog(Prog& P, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs, uint32_t nexprs,
+                         bool all_cols) {
+  try {
+    if (pred) {
+      P.pred_h = P.pb.add_root(*pred);
+      P.has_pred = true;
+      P.pb.end_predicate();
+    }
+    if (exprs)
+      for (uint32_t i = 0; i < nexprs; ++i) P.outs.push_back(P.pb.add_root(exprs[i]));
+    else if (all_cols)
+      for (uint32_t i = 0; i < in->ncols; ++i) P.outs.push_back(P.pb.add_column(i));
+    P.pb.finish();
+    if (P.has_pred && P.pb.root(P.pred_h).cls != C_B) fail(TQ_INVALID_PLAN, "predicate must be boolean");
+  } catch (const CompileError& e) {
+    fail(e.status, e.msg);
+  }
+}
+
+static const void* upload_program(tq_ctx* c, const ProgramBuilder& pb, const DInstr** code, const DLit** lits) {
+  std::string key;
+  key.append((const char*)pb.code().data(), pb.code().size() * sizeof(DInstr));
+  key.push_back('|');
+  key.append((const char*)pb.lits().data(), pb.lits().size() * sizeof(DLit));
+  std::lock_guard<std::mutex> g(c->mu);
+  auto it = c->prog_cache.find(key);
+  void* d;
+  if (it != c->prog_cache.end()) {
+    d = it->second;
+  } else {
+    size_t cb = pb.code().size() * sizeof(DInstr);
+    size_t bytes = round_up(cb, 32) + pb.lits().size() * sizeof(DLit) + 32;
+    TQ_CUDA(cudaMalloc(&d, bytes));
+    std::vector<uint8_t> h(bytes, 0);
+    std::memcpy(h.data(), pb.code().data(), cb);
+    std::memcpy(h.data() + round_up(cb, 32), pb.lits().data(), pb.lits().size() * sizeof(DLit));
+    TQ_CUDA(cudaMemcpy(d, h.data(), bytes, cudaMemcpyHostToDevice));
+    c->prog_cache[key] = d;
+  }
+  *code = (const DInstr*)d;
+  *lits = (const DLit*)((uint8_t*)d + round_up(pb.code().size() * sizeof(DInstr), 32));
+  return d;
+}
+
+static uint8_t out_kind_of(const Operand& o, const tq_batch* in, const ProgramBuilder& pb, uint8_t* prec,
+                           uint8_t* scale) {
+  *prec = 0;
+  *scale = 0;
+  switch (o.kind) {
+    case K_COL_I64: return TQ_INT64;
+    case K_COL_F64: return TQ_FLOAT64;
+    case K_COL_BOOL: return TQ_BOOL;
+    case K_COL_DEC: {
+      const tq_column& c = in->cols[pb.staged()[o.idx]];
+      *prec = c.precision;
+      *scale = c.scale;
+      return TQ_DECIMAL;
+    }
+    default: break;
+  }
+  switch (o.cls) {
+    case C_I: return TQ_INT64;
+    case C_D: *prec = 38; *scale = o.scale; return TQ_DECIMAL;
+    case C_F: return TQ_FLOAT64;
+    default: return TQ_BOOL;
+  }
+}
+
+// Fill program + staging part of PipeParams and the smem layout.
+struct Plan {
+  PipeParams p;
+  u32 smem = 0, grid = 0;
+};
+
+static u32 align_up(u32 x, u32 a) { return (x + a - 1) / a * a; }
+
+static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sink_bytes, cudaStream_t st) {
+  PipeParams& p = L.p;
+  std::memset(&p, 0, sizeof(p));
+  const ProgramBuilder& pb = P.pb;
+  upload_program(c, pb, &p.code, &p.lits);
+  p.rows = in->rows;
+  p.ntiles = (u32)((in->rows + kTile - 1) / kTile);
+  p.ncode = (uint16_t)pb.code().size();
+  p.npred = (uint16_t)pb.n_pred_instr();
+  p.nlits = (uint16_t)pb.lits().size();
+  p.nvslots = (uint16_t)std::max(1, pb.value_slots());
+  p.nbslots = (uint16_t)std::max(1, pb.bool_slots());
+  p.pred_kind = K_NONE;
+  if (P.has_pred) {
+    p.pred_kind = pb.root(P.pred_h).kind;
+    p.pred_idx = pb.root(P.pred_h).idx;
+  }
+  // staged columns and per-stage layout
+  p.nstaged = (uint16_t)pb.staged().size();
+  u32 off = 0;
+  for (u32 i = 0; i < p.nstaged; ++i) {
+    const tq_column& col = in->cols[pb.staged()[i]];
+    StagedCol& sc = p.cols[i];
+    sc.values = (const uint8_t*)col.values;
+    sc.validity = in->rows > 0 ? col.validity : nullptr;
+    sc.width = (u32)width_of(col.kind);
+    sc.kind = col.kind;
+    sc.bulk_ok = ((uintptr_t)col.values % 16 == 0) && (!sc.validity || (uintptr_t)sc.validity % 16 == 0);
+    off = align_up(off, 128);
+    sc.off = off;
+    off += kTile * sc.width;
+    if (sc.validity) {
+      off = align_up(off, 16);
+      sc.voff = off;
+      off += kTile / 8;
+    }
+  }
+  p.stage_bytes = align_up(std::max(off, 128u), 128);
+  // fixed regions
+  u32 o = 0;
+  p.off_code = o;
+  o += align_up(p.ncode * sizeof(DInstr), 128);
+  p.off_lits = o;
+  o += align_up(std::max<u32>(1, p.nlits) * sizeof(DLit), 128);
+  p.off_vslot = o;
+  o += kWarps * p.nvslots * kV * 32 * 16;
+  p.off_vvalid = o;
+  o += align_up(kWarps * p.nvslots * kV * 4, 16);
+  p.off_bslot = o;
+  o += align_up(kWarps * p.nbslots * kV * 8, 16);
+  p.off_sink = o;
+  o += align_up(sink_bytes, 128);
+  p.off_bar = o;
+  o += 64;
+  o = align_up(o, 128);
+  const u32 kSmemMax = 227 * 1024;
+  if (o + p.stage_bytes > kSmemMax) fail(TQ_INVALID_PLAN, "batch too wide for one pipeline tile");
+  u32 budget = kSmemMax - o;
+  // two CTAs per SM when both fit with >= 2 stages, else one CTA with up to 4 stages
+  u32 per_sm = c->ctas_per_sm;
+  u32 half = 113 * 1024;
+  if (per_sm == 0) per_sm = (o < half && (half - o) / p.stage_bytes >= 2) ? 2 : 1;
+  u32 limit = per_sm >= 2 ? (half > o ? half - o : 0) : budget;
+  u32 ns = std::min<u32>(kMaxStages, limit / p.stage_bytes);
+  if (ns == 0) { per_sm = 1; ns = std::min<u32>(kMaxStages, budget / p.stage_bytes); }
+  if (ns == 0) fail(TQ_INVALID_PLAN, "batch too wide for one pipeline tile");
+  p.nstages = ns;
+  p.off_stage = o;
+  L.smem = o + ns * p.stage_bytes;
+  L.grid = std::max<u32>(1, std::min<u32>(p.ntiles, (u32)c->sms * per_sm));
+  (void)st;
+}
+
+static void launch(tq_ctx* c, int sink, Plan& L, cudaStream_t st) {
+  if (L.p.ntiles == 0) return;
+  TQ_CUDA(launch_pipeline(sink, L.p, L.smem, L.grid, st));
+  counted_launch(c);
+}
+
+static void set_keys(PipeParams& p, const ProgramBuilder& pb, const std::vector<int>& handles) {
+  if (handles.size() > (size_t)kMaxKeys) fail(TQ_INVALID_PLAN, "too many keys");
+  p.nkeys = (u32)handles.size();
+  u32 words = 0;
+  for (size_t i = 0; i < handles.size(); ++i) {
+    const Operand& o = pb.root(handles[i]);
+    KeyOpnd& k = p.keys[i];
+    k.kind = o.kind;
+    k.idx = o.idx;
+    k.words = o.cls == C_D ? 2 : 1;
+    k.bytes = o.cls == C_D ? 16 : o.cls == C_B ? 1 : 8;
+    words += k.words;
+  }
+  if (words > (u32)kMaxKeyWords) fail(TQ_INVALID_PLAN, "keys too wide");
+  p.key_words = words;
+}
+
+// ================================================================== materializing sinks
+enum MatMode { MAT_FILTER, MAT_PARTITION, MAT_PROBE };
+
+struct MatArgs {
+  int mode = MAT_FILTER;
+  std::vector<uint32_t> key_roots;  // indices into P.outs
+  uint32_t nparts = 1;
+  const tq_join_table* table = nullptr;
+  std::vector<uint32_t> build_cols;
+};
+
+static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArgs& A, tq_batch* out,
+                            uint64_t* part_offsets, cudaStream_t st) {
+  Plan L;
+  u32 sink_bytes = kWarps * kMaxDest * 4 + kWarps * kMaxDest * 8;
+  plan_launch(c, in, P, L, sink_bytes, st);
+  PipeParams& p = L.p;
+  p.dest_kind = A.mode == MAT_FILTER ? DEST_FILTER : A.mode == MAT_PARTITION ? DEST_PARTITION : DEST_PROBE;
+  p.ndest = A.mode == MAT_PARTITION ? A.nparts : 1;
+  if (p.ndest == 0 || p.ndest > (u32)kMaxDest) fail(TQ_INVALID_PLAN, "partition count out of range (1..64)");
+  std::vector<int> kh;
+  for (uint32_t k : A.key_roots) {
+    if (k >= P.outs.size()) fail(TQ_INVALID_PLAN, "key column out of range");
+    kh.push_back(P.outs[k]);
+  }
+  set_keys(p, P.pb, kh);
+  if (A.mode == MAT_PROBE) {
+    const tq_join_table* t = A.table;
+    if (kh.size() != t->key_cls.size()) fail(TQ_INVALID_PLAN, "probe/build key count differs");
+    for (size_t i = 0; i < kh.size(); ++i) {
+      const Operand& o = P.pb.root(kh[i]);
+      if (o.cls != t->key_cls[i] || (o.cls == C_D && o.scale != t->key_scale[i]))
+        fail(TQ_INVALID_PLAN, "join key types differ");
+    }
+    p.jt = t->jt;
+  }
+  // output schema
+  std::vector<tq_column> sch;
+  std::vector<bool> wv;
+  std::vector<OutCol> outs;
+  if (A.mode == MAT_PROBE) {
+    for (uint32_t bc : A.build_cols) {
+      if (bc >= A.table->build.ncols) fail(TQ_INVALID_PLAN, "build column out of range");
+      const tq_column& col = A.table->build.cols[bc];
+      if (col.kind == TQ_UTF8) fail(TQ_INVALID_PLAN, "utf8 columns are not supported on the GPU path");
+      tq_column d{};
+      d.kind = col.kind; d.precision = col.precision; d.scale = col.scale;
+      sch.push_back(d);
+      wv.push_back(col.validity != nullptr && A.table->build.rows > 0);
+      OutCol oc{};
+      oc.src = OUT_BUILD;
+      oc.width = (uint8_t)width_of(col.kind);
+      oc.out_kind = col.kind;
+      oc.bvalues = (const uint8_t*)col.values;
+      oc.bvalidity = A.table->build.rows > 0 ? col.validity : nullptr;
+      outs.push_back(oc);
+    }
+  }
+  for (int h : P.outs) {
+    const Operand& o = P.pb.root(h);
+    tq_column d{};
+    d.kind = out_kind_of(o, in, P.pb, &d.precision, &d.scale);
+    sch.push_back(d);
+    wv.push_back(o.maybe_null);
+    OutCol oc{};
+    oc.src = OUT_OPND;
+    oc.kind = o.kind;
+    oc.idx = o.idx;
+    oc.width = (uint8_t)width_of(d.kind);
+    oc.out_kind = d.kind;
+    outs.push_back(oc);
+  }
+  if (outs.size() > (size_t)kMaxOut) fail(TQ_INVALID_PLAN, "too many output columns");
+
+  // ---- count phase (skipped for dense 1:1 projections)
+  const bool dense = A.mode == MAT_FILTER && !P.has_pred;
+  uint64_t total = dense ? in->rows : 0;
+  std::vector<uint64_t> starts(p.ndest + 1, 0);
+  u32* counts = nullptr;
+  u64* offsets = nullptr;
+  u64 ncnt = (u64)p.ndest * p.ntiles;
+  if (!dense && p.ntiles > 0) {
+    counts = (u32*)dalloc(c, ncnt * 4, st);
+    offsets = (u64*)dalloc(c, (ncnt + 1) * 8, st);
+    p.tile_counts = counts;
+    launch(c, SINK_COUNT, L, st);
+    scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      u64* pin = (u64*)c->pinned;
+      k_dest_starts<<<1, 128, 0, st>>>(offsets, p.ntiles, p.ndest, offsets + ncnt, pin);
+      counted_launch(c);
+      TQ_CUDA(cudaGetLastError());
+      TQ_CUDA(cudaStreamSynchronize(st));
+      for (u32 d = 0; d <= p.ndest; ++d) starts[d] = pin[d];
+    }
+    total = starts[p.ndest];
+    p.tile_offsets = offsets;
+  } else if (!dense) {
+    total = 0;
+  } else {
+    for (u32 d = 0; d <= p.ndest; ++d) starts[d] = d == 0 ? 0 : total;
+  }
+  if (part_offsets) {
+    for (u32 d = 0; d < p.ndest; ++d) part_offsets[d] = starts[d];
+    part_offsets[p.ndest] = total;
+  }
+  // ---- emit phase
+  try {
+    alloc_batch(c, total, sch, wv, out, st);
+  } catch (...) {
+    if (counts) dfree(c, counts, ncnt * 4, st);
+    if (offsets) dfree(c, offsets, (ncnt + 1) * 8, st);
+    throw;
+  }
+  p.nout = (u32)outs.size();
+  for (size_t i = 0; i < outs.size(); ++i) {
+    outs[i].values = (uint8_t*)out->cols[i].values;
+    outs[i].validity = out->cols[i].validity;
+    p.out[i] = outs[i];
+  }
+  if (total > 0) launch(c, SINK_EMIT, L, st);
+  if (counts) dfree(c, counts, ncnt * 4, st);
+  if (offsets) dfree(c, offsets, (ncnt + 1) * 8, st);
+}
+
+// ================================================================== join build
+static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
+                      tq_join_table** out, cudaStream_t st) {
+  Plan L;
+  plan_launch(c, in, P, L, 0, st);
+  PipeParams& p = L.p;
+  std::vector<int> kh;
+  for (uint32_t k : key_roots) {
+    if (k >= P.outs.size()) fail(TQ_INVALID_PLAN, "key column out of range");
+    kh.push_back(P.outs[k]);
+  }
+  if (kh.empty()) fail(TQ_INVALID_PLAN, "join without keys");
+  set_keys(p, P.pb, kh);
+  tq_join_table* t = new tq_join_table();
+  t->ctx = c;
+  t->stream = st;
+  for (int h : kh) {
+    const Operand& o = P.pb.root(h);
+    if (o.cls == C_F || o.cls == C_S) {
+      delete t;
+      fail(TQ_INVALID_PLAN, "unsupported join key type");
+    }
+    t->key_cls.push_back(o.cls);
+    t->key_scale.push_back(o.scale);
+  }
+  uint64_t cap = 1024;
+  while (cap < in->rows * 2) cap <<= 1;
+  t->jt.cap = cap;
+  t->jt.kw = p.key_words;
+  t->jt.stride = (u32)round_up(8 * (1 + p.key_words), 16);
+  t->bytes = cap * t->jt.stride;
+  try {
+    t->jt.entries = (uint8_t*)dalloc(c, t->bytes, st);
+  } catch (...) {
+    delete t;
+    throw;
+  }
+  TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, t->bytes, st));
+  t->build = *in;
+  t->build.owner = nullptr;
+  t->build.cols = (tq_column*)std::malloc(sizeof(tq_column) * std::max<uint32_t>(1, in->ncols));
+  std::memcpy(t->build.cols, in->cols, sizeof(tq_column) * in->ncols);
+  p.jt = t->jt;
+  p.row_base = 0;
+  launch(c, SINK_BUILD, L, st);
+  *out = t;
+}
+
+// ================================================================== aggregation
+enum AggOutKind : uint8_t {
+  AO_SUM_I64 = 0, AO_SUM_DEC, AO_SUM_F, AO_CNT, AO_AVG_I, AO_AVG_F, AO_MM_I64, AO_MM_DEC, AO_MM_BOOL, AO_MM_F
+};
+struct AggOut {
+  uint8_t kind, acc, cnt, scale;
+  uint8_t* values;
+  uint8_t* validity;
+};
+struct KeyOut {
+  uint8_t kind, word, bit, _p;
+  uint8_t* values;
+  uint8_t* validity;
+};
+struct FinalParams {
+  AggTable t;
+  u32 kwa, nacc, nkeys, naggs;
+  KeyOut keys[kMaxKeys];
+  AggOut aggs[32];
+  unsigned long long* counter;
+};
+
+__global__ void k_agg_init(AggTable t, u32 nacc, AccSpec* specs_dev_unused, u64 n_acc_words, const uint8_t* ops) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 j = i; j < t.cap; j += stride) t.state[j] = 0;
+  for (u64 j = i; j < t.cap * nacc; j += stride) {
+    u64 lo, hi;
+    uint8_t op = ops[j % nacc];
+    switch (op) {
+      case ACC_MIN_I: lo = ~0ull; hi = 0x7fffffffffffffffull; break;
+      case ACC_MAX_I: lo = 0; hi = 0x8000000000000000ull; break;
+      case ACC_MIN_F: lo = 0x7ff0000000000000ull; hi = 0; break;
+      case ACC_MAX_F: lo = 0xfff0000000000000ull; hi = 0; break;
+      default: lo = 0; hi = 0;
+    }
+    t.acc[2 * j] = lo;
+    t.acc[2 * j + 1] = hi;
+  }
+  (void)specs_dev_unused;
+  (void)n_acc_words;
+}
+
+__global__ void k_agg_final(const __grid_constant__ FinalParams f) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 s = i; s < f.t.cap; s += stride) {
+    if (f.t.state[s] != 2) continue;
+    u64 row = atomicAdd(f.counter, 1ull);
+    const u64* kw = f.t.keys + s * f.kwa;
+    u64 nullw = kw[f.kwa - 1];
+    for (u32 k = 0; k < f.nkeys; ++k) {
+      const KeyOut& ko = f.keys[k];
+      bool isnull = (nullw >> ko.bit) & 1;
+      if (ko.kind == TQ_DECIMAL) {
+        ((u64*)ko.values)[2 * row] = kw[ko.word];
+        ((u64*)ko.values)[2 * row + 1] = kw[ko.word + 1];
+      } else if (ko.kind == TQ_BOOL) {
+        ko.values[row] = (uint8_t)kw[ko.word];
+      } else {
+        ((u64*)ko.values)[row] = kw[ko.word];
+      }
+      if (ko.validity && !isnull) bm_set_atomic(ko.validity, row);
+    }
+    const u64* acc = f.t.acc + s * f.nacc * 2;
+    for (u32 a = 0; a < f.naggs; ++a) {
+      const AggOut& ao = f.aggs[a];
+      const u64* m = acc + 2 * ao.acc;
+      u64 cnt = ao.cnt != 0xff ? acc[2 * ao.cnt] : 1;
+      bool valid = cnt != 0;
+      switch (ao.kind) {
+        case AO_SUM_I64:
+        case AO_MM_I64:
+          ((u64*)ao.values)[row] = m[0];
+          break;
+        case AO_SUM_DEC:
+        case AO_MM_DEC:
+          ((u64*)ao.values)[2 * row] = m[0];
+          ((u64*)ao.values)[2 * row + 1] = m[1];
+          break;
+        case AO_MM_BOOL:
+          ao.values[row] = m[0] != 0;
+          break;
+        case AO_SUM_F:
+        case AO_MM_F:
+          ((u64*)ao.values)[row] = m[0];
+          break;
+        case AO_CNT:
+          ((u64*)ao.values)[row] = m[0];
+          valid = true;
+          break;
+        case AO_AVG_I: {
+          double d = valid ? i128_to_f64(mk128(m[0], m[1])) / pow(10.0, (double)ao.scale) / (double)cnt : 0.0;
+          ((double*)ao.values)[row] = d;
+          break;
+        }
+        case AO_AVG_F: {
+          double d = valid ? __longlong_as_double((long long)m[0]) / (double)cnt : 0.0;
+          ((double*)ao.values)[row] = d;
+          break;
+        }
+      }
+      if (ao.validity && valid) bm_set_atomic(ao.validity, row);
+    }
+  }
+}
+
+static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t* keys, uint32_t nkeys,
+                          const tq_agg* aggs, uint32_t naggs, tq_batch* out, cudaStream_t st) {
+  // ---- accumulators (deduplicated)
+  std::vector<AccSpec> acc;
+  auto acc_of = [&](uint8_t op, uint8_t kind, uint16_t idx) -> uint8_t {
+    for (size_t i = 0; i < acc.size(); ++i)
+      if (acc[i].op == op && acc[i].kind == kind && acc[i].idx == idx) return (uint8_t)i;
+    if (acc.size() >= (size_t)kMaxAcc) fail(TQ_INVALID_PLAN, "too many aggregates");
+    AccSpec a{};
+    a.op = op; a.kind = kind; a.idx = idx;
+    acc.push_back(a);
+    return (uint8_t)(acc.size() - 1);
+  };
+  if (naggs > 32) fail(TQ_INVALID_PLAN, "too many aggregates");
+  struct AggPlan { uint8_t kind, acc, cnt, scale; tq_column col; bool nullable; };
+  std::vector<AggPlan> ap;
+  for (uint32_t j = 0; j < naggs; ++j) {
+    AggPlan a{};
+    a.cnt = 0xff;
+    uint32_t fn = aggs[j].fn;
+    if (fn > TQ_AGG_AVG) fail(TQ_INVALID_PLAN, "bad aggregate");
+    if (fn == TQ_AGG_COUNT_STAR) {
+      a.kind = AO_CNT;
+      a.acc = acc_of(ACC_CNT, K_NONE, 0);
+      a.col.kind = TQ_INT64;
+      ap.push_back(a);
+      continue;
+    }
+    if (aggs[j].column >= P.outs.size()) fail(TQ_INVALID_PLAN, "aggregate column out of range");
+    const Operand& o = P.pb.root(P.outs[aggs[j].column]);
+    uint8_t prec, scale;
+    uint8_t kind = out_kind_of(o, in, P.pb, &prec, &scale);
+    uint8_t cnt_acc = o.maybe_null ? acc_of(ACC_CNT, o.kind, o.idx) : acc_of(ACC_CNT, K_NONE, 0);
+    a.nullable = o.maybe_null;
+    switch (fn) {
+      case TQ_AGG_COUNT:
+        a.kind = AO_CNT;
+        a.acc = cnt_acc;
+        a.col.kind = TQ_INT64;
+        break;
+      case TQ_AGG_SUM:
+        if (o.cls == C_B) fail(TQ_INVALID_PLAN, "sum of bool");
+        if (o.cls == C_F) { a.kind = AO_SUM_F; a.acc = acc_of(ACC_SUM_F, o.kind, o.idx); a.col.kind = TQ_FLOAT64; }
+        else if (o.cls == C_D) {
+          a.kind = AO_SUM_DEC; a.acc = acc_of(ACC_SUM_I, o.kind, o.idx);
+          a.col.kind = TQ_DECIMAL; a.col.precision = 38; a.col.scale = scale;
+        } else { a.kind = AO_SUM_I64; a.acc = acc_of(ACC_SUM_I, o.kind, o.idx); a.col.kind = TQ_INT64; }
+        a.cnt = o.maybe_null ? cnt_acc : 0xff;
+        break;
+      case TQ_AGG_AVG:
+        if (o.cls == C_B) fail(TQ_INVALID_PLAN, "avg of bool");
+        if (o.cls == C_F) { a.kind = AO_AVG_F; a.acc = acc_of(ACC_SUM_F, o.kind, o.idx); }
+        else { a.kind = AO_AVG_I; a.acc = acc_of(ACC_SUM_I, o.kind, o.idx); a.scale = o.cls == C_D ? o.scale : 0; }
+        a.cnt = cnt_acc;
+        a.col.kind = TQ_FLOAT64;
+        break;
+      default: {  // MIN / MAX
+        bool mn = fn == TQ_AGG_MIN;
+        if (o.cls == C_F) { a.kind = AO_MM_F; a.acc = acc_of(mn ? ACC_MIN_F : ACC_MAX_F, o.kind, o.idx); }
+        else {
+          a.kind = o.cls == C_D ? AO_MM_DEC : o.cls == C_B ? AO_MM_BOOL : AO_MM_I64;
+          a.acc = acc_of(mn ? ACC_MIN_I : ACC_MAX_I, o.kind, o.idx);
+        }
+        a.col.kind = kind; a.col.precision = prec; a.col.scale = scale;
+        a.cnt = o.maybe_null ? cnt_acc : 0xff;
+      }
+    }
+    ap.push_back(a);
+  }
+  // ---- keys
+  std::vector<int> kh;
+  for (uint32_t k = 0; k < nkeys; ++k) {
+    if (keys[k] >= P.outs.size()) fail(TQ_INVALID_PLAN, "key column out of range");
+    kh.push_back(P.outs[keys[k]]);
+  }
+  const u32 nacc = (u32)acc.size();
+  // local (per-CTA) group table sized to the shared-memory budget
+  u32 kwa_guess = 1;
+  for (int h : kh) kwa_guess += P.pb.root(h).cls == C_D ? 2 : 1;
+  u32 G = 64;
+  auto sink_bytes = [&](u32 g) { return align_up(g * 4, 16) + g * kwa_guess * 8 + kWarps * g * nacc * 16; };
+  while (G > 4 && sink_bytes(G) > 48 * 1024) G >>= 1;
+  Plan L;
+  plan_launch(c, in, P, L, sink_bytes(G), st);
+  PipeParams& p = L.p;
+  set_keys(p, P.pb, kh);
+  const u32 kwa = p.key_words + 1;
+  p.nacc = nacc;
+  for (u32 i = 0; i < nacc; ++i) p.acc[i] = acc[i];
+  p.local_groups = G;
+
+  // ---- global table; grows x4 and re-runs on overflow (on_oom-style retry)
+  uint64_t cap = 1024;
+  while (cap < std::min<uint64_t>(in->rows, 1 << 16) * 2) cap <<= 1;
+  uint8_t* ops_dev = (uint8_t*)dalloc(c, 64, st);
+  {
+    uint8_t ops[kMaxAcc] = {};
+    for (u32 i = 0; i < nacc; ++i) ops[i] = acc[i].op;
+    TQ_CUDA(cudaMemcpyAsync(ops_dev, ops, kMaxAcc, cudaMemcpyHostToDevice, st));
+    TQ_CUDA(cudaStreamSynchronize(st));
+  }
+  uint64_t ngroups = 0;
+  AggTable t{};
+  uint64_t tbytes = 0;
+  for (int attempt = 0;; ++attempt) {
+    tbytes = cap * 4 + cap * kwa * 8 + cap * std::max<u32>(1, nacc) * 16 + 64;
+    uint8_t* base = (uint8_t*)dalloc(c, tbytes, st);
+    t.state = (uint32_t*)base;
+    t.keys = (u64*)(base + round_up(cap * 4, 16));
+    t.acc = t.keys + cap * kwa;
+    t.cap = cap;
+    uint8_t* tail = (uint8_t*)(t.acc + cap * std::max<u32>(1, nacc) * 2);
+    t.nused = (unsigned long long*)tail;
+    t.overflow = (uint32_t*)(tail + 8);
+    TQ_CUDA(cudaMemsetAsync(tail, 0, 16, st));
+    u32 ib = (u32)std::min<uint64_t>(4096, (cap * std::max<u32>(1, nacc) + 255) / 256);
+    k_agg_init<<<ib, 256, 0, st>>>(t, nacc, nullptr, 0, ops_dev);
+    counted_launch(c);
+    TQ_CUDA(cudaGetLastError());
+    p.agg = t;
+    launch(c, SINK_AGG, L, st);
+    uint32_t ovf = 0;
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      TQ_CUDA(cudaMemcpyAsync(c->pinned, tail, 16, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaStreamSynchronize(st));
+      ngroups = ((uint64_t*)c->pinned)[0];
+      ovf = ((uint32_t*)c->pinned)[2];
+    }
+    if (!ovf) break;
+    dfree(c, base, tbytes, st);
+    if (attempt > 12) { dfree(c, ops_dev, 64, st); fail(TQ_RESERVATION_EXCEEDED, "aggregation table overflow"); }
+    cap *= 4;
+  }
+  dfree(c, ops_dev, 64, st);
+  uint8_t* tbase = (uint8_t*)t.state;
+  // ---- output batch
+  std::vector<tq_column> sch;
+  std::vector<bool> wv;
+  for (int h : kh) {
+    const Operand& o = P.pb.root(h);
+    tq_column d{};
+    d.kind = out_kind_of(o, in, P.pb, &d.precision, &d.scale);
+    sch.push_back(d);
+    wv.push_back(o.maybe_null);
+  }
+  for (auto& a : ap) {
+    sch.push_back(a.col);
+    bool can_null = a.kind != AO_CNT && a.cnt != 0xff && a.nullable;
+    wv.push_back(can_null);
+  }
+  try {
+    alloc_batch(c, ngroups, sch, wv, out, st);
+  } catch (...) {
+    dfree(c, tbase, tbytes, st);
+    throw;
+  }
+  if (ngroups > 0) {
+    FinalParams f{};
+    f.t = t;
+    f.kwa = kwa;
+    f.nacc = nacc;
+    f.nkeys = (u32)kh.size();
+    f.naggs = (u32)ap.size();
+    u32 word = 0;
+    for (u32 k = 0; k < f.nkeys; ++k) {
+      KeyOut& ko = f.keys[k];
+      ko.kind = out->cols[k].kind;
+      ko.word = (uint8_t)word;
+      ko.bit = (uint8_t)k;
+      ko.values = (uint8_t*)out->cols[k].values;
+      ko.validity = out->cols[k].validity;
+      word += p.keys[k].words;
+    }
+    for (u32 a = 0; a < f.naggs; ++a) {
+      AggOut& ao = f.aggs[a];
+      ao.kind = ap[a].kind;
+      ao.acc = ap[a].acc;
+      ao.cnt = ap[a].kind == AO_CNT ? 0xff : ap[a].cnt;
+      if (ap[a].kind == AO_AVG_I || ap[a].kind == AO_AVG_F) ao.cnt = ap[a].cnt;
+      ao.scale = ap[a].scale;
+      ao.values = (uint8_t*)out->cols[f.nkeys + a].values;
+      ao.validity = out->cols[f.nkeys + a].validity;
+    }
+    f.counter = (unsigned long long*)(t.nused + 0);  // reuse as output cursor
+    TQ_CUDA(cudaMemsetAsync(t.nused, 0, 8, st));
+    u32 nb = (u32)std::min<uint64_t>(2048, (cap + 255) / 256);
+    k_agg_final<<<nb, 256, 0, st>>>(f);
+    counted_launch(c);
+    TQ_CUDA(cudaGetLastError());
+  }
+  dfree(c, tbase, tbytes, st);
+}
+
+// ================================================================== take / concat / slice
+// dst already points at the first destination row; validity bits land at
+// dbit + i of dvalid (bitmap zeroed by the allocator).
+__global__ void k_take_fixed(const uint8_t* src, const uint8_t* svalid, const u64* ids, u64 n, u32 width,
+                             uint8_t* dst, uint8_t* dvalid, u64 id_base, u64 dbit) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    u64 r = ids ? ids[i] : id_base + i;
+    if (width == 16) ((ulonglong2*)dst)[i] = ((const ulonglong2*)src)[r];
+    else if (width == 8) ((u64*)dst)[i] = ((const u64*)src)[r];
+    else if (width == 1) dst[i] = src[r];
+    if (dvalid && (!svalid || bm_get(svalid, r))) bm_set_atomic(dvalid, dbit + i);
+  }
+}
+__global__ void k_take_utf8_len(const int32_t* soff, const u64* ids, u64 n, u32* len, u64 id_base) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    u64 r = ids ? ids[i] : id_base + i;
+    len[i] = (u32)(soff[r + 1] - soff[r]);
+  }
+}
+__global__ void k_take_utf8_copy(const uint8_t* src, const int32_t* soff, const u64* ids, u64 n, const u64* doff,
+                                 uint8_t* dst, int32_t* doff32, u64 id_base, int32_t out_base) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  u64 stride = (u64)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    u64 r = ids ? ids[i] : id_base + i;
+    int32_t a = soff[r], e = soff[r + 1];
+    u64 o = doff[i];
+    for (int32_t k = a; k < e; ++k) dst[o + (k - a)] = src[k];
+    doff32[i] = out_base + (int32_t)o;
+    if (i == n - 1) doff32[n] = out_base + (int32_t)(o + (e - a));
+  }
+}
+
+static u32 grid_for(tq_ctx* c, u64 n) { return (u32)std::max<u64>(1, std::min<u64>((n + 255) / 256, c->sms * 8)); }
+
+// gather rows (ids on device, or the contiguous range [base, base+n)) of `in` into
+// rows [dst_row, dst_row+n) of the already-allocated `out` (dst bitmaps zeroed).
+static void gather_into(tq_ctx* c, const tq_batch* in, const u64* ids, u64 n, u64 base, tq_batch* out, u64 dst_row,
+                        std::vector<int32_t>& utf8_cursor, cudaStream_t st) {
+  if (n == 0) return;
+  for (uint32_t k = 0; k < in->ncols; ++k) {
+    const tq_column& s = in->cols[k];
+    tq_column& d = out->cols[k];
+    const uint8_t* svalid = in->rows ? s.validity : nullptr;
+    if (s.kind != TQ_UTF8) {
+      u32 w = (u32)width_of(s.kind);
+      k_take_fixed<<<grid_for(c, n), 256, 0, st>>>((const uint8_t*)s.values, svalid, ids, n, w,
+                                                    (uint8_t*)d.values + dst_row * w, d.validity, base, dst_row);
+      counted_launch(c);
+    } else {
+      u32* len = (u32*)dalloc(c, n * 4, st);
+      u64* off = (u64*)dalloc(c, (n + 1) * 8, st);
+      k_take_utf8_len<<<grid_for(c, n), 256, 0, st>>>(s.offsets, ids, n, len, base);
+      counted_launch(c);
+      scan_u32(c, len, n, off, off + n, st);
+      k_take_utf8_copy<<<grid_for(c, n), 256, 0, st>>>((const uint8_t*)s.values, s.offsets, ids, n, off,
+                                                        (uint8_t*)d.values + utf8_cursor[k], d.offsets + dst_row,
+                                                        base, utf8_cursor[k]);
+      counted_launch(c);
+      if (d.validity) {
+        k_take_fixed<<<grid_for(c, n), 256, 0, st>>>(nullptr, svalid, ids, n, 0, nullptr, d.validity, base, dst_row);
+        counted_launch(c);
+      }
+      uint64_t tot = 0;
+      TQ_CUDA(cudaMemcpyAsync(&tot, off + n, 8, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaStreamSynchronize(st));
+      utf8_cursor[k] += (int32_t)tot;
+      dfree(c, len, n * 4, st);
+      dfree(c, off, (n + 1) * 8, st);
+    }
+    TQ_CUDA(cudaGetLastError());
+  }
+}
+
+// utf8 bytes of rows ids / range
+static u64 utf8_bytes_of(tq_ctx* c, const tq_column& s, const u64* ids, u64 n, u64 base, cudaStream_t st) {
+  if (n == 0) return 0;
+  if (!ids) {
+    int32_t a = 0, e = 0;
+    TQ_CUDA(cudaMemcpyAsync(&a, s.offsets + base, 4, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaMemcpyAsync(&e, s.offsets + base + n, 4, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaStreamSynchronize(st));
+    return (u64)(e - a);
+  }
+  u32* len = (u32*)dalloc(c, n * 4, st);
+  u64* off = (u64*)dalloc(c, (n + 1) * 8, st);
+  k_take_utf8_len<<<grid_for(c, n), 256, 0, st>>>(s.offsets, ids, n, len, 0);
+  counted_launch(c);
+  scan_u32(c, len, n, off, off + n, st);
+  u64 tot = 0;
+  TQ_CUDA(cudaMemcpyAsync(&tot, off + n, 8, cudaMemcpyDeviceToHost, st));
+  TQ_CUDA(cudaStreamSynchronize(st));
+  dfree(c, len, n * 4, st);
+  dfree(c, off, (n + 1) * 8, st);
+  return tot;
+}
+
+__global__ void k_set_first_offset(int32_t* off) { off[0] = 0; }
+
+static void take_impl(tq_ctx* c, const tq_batch* in, const u64* ids, u64 n, u64 base, tq_batch* out,
+                      cudaStream_t st) {
+  std::vector<tq_column> sch(in->cols, in->cols + in->ncols);
+  std::vector<bool> wv;
+  std::vector<uint64_t> ub;
+  for (uint32_t k = 0; k < in->ncols; ++k) {
+    wv.push_back(in->rows > 0 && in->cols[k].validity != nullptr);  // take: bitmap iff input had one (n>0)
+    ub.push_back(in->cols[k].kind == TQ_UTF8 ? utf8_bytes_of(c, in->cols[k], ids, n, base, st) : 0);
+  }
+  alloc_batch(c, n, sch, wv, out, st, &ub);
+  std::vector<int32_t> cur(in->ncols, 0);
+  for (uint32_t k = 0; k < in->ncols; ++k)
+    if (in->cols[k].kind == TQ_UTF8) {
+      k_set_first_offset<<<1, 1, 0, st>>>(out->cols[k].offsets);
+      counted_launch(c);
+    }
+  gather_into(c, in, ids, n, base, out, 0, cur, st);
+}
+
+}  // namespace tq
+
+using namespace tq;
+
+extern "C" {
+
+tq_status tq_take(tq_ctx* c, const tq_batch* in, const uint64_t* ids, uint64_t n, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    take_impl(c, in, (const u64*)ids, n, 0, out, pick(c, stream));
+  });
+}
+
+tq_status tq_slice(tq_ctx* c, const tq_batch* in, uint64_t start, uint64_t len, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    if (start + len > in->rows) fail(TQ_INTERNAL, "slice out of range");
+    take_impl(c, in, nullptr, len, start, out, pick(c, stream));
+  });
+}
+
+tq_status tq_concat(tq_ctx* c, const tq_batch* ins, uint32_t n, tq_batch* out, void* stream) {
+  return guard([&] {
+    if (n == 0) fail(TQ_INTERNAL, "concat of nothing");
+    cudaStream_t st = pick(c, stream);
+    const tq_batch& f = ins[0];
+    uint64_t rows = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      check_device_batch(&ins[i]);
+      if (ins[i].ncols != f.ncols) fail(TQ_SCHEMA_MISMATCH, "concat over differing schemas");
+      for (uint32_t k = 0; k < f.ncols; ++k)
+        if (ins[i].cols[k].kind != f.cols[k].kind || ins[i].cols[k].scale != f.cols[k].scale ||
+            ins[i].cols[k].precision != f.cols[k].precision)
+          fail(TQ_SCHEMA_MISMATCH, "concat over differing schemas");
+      rows += ins[i].rows;
+    }
+    std::vector<tq_column> sch(f.cols, f.cols + f.ncols);
+    std::vector<bool> wv(f.ncols, false);
+    std::vector<uint64_t> ub(f.ncols, 0);
+    for (uint32_t i = 0; i < n; ++i)
+      for (uint32_t k = 0; k < f.ncols; ++k) {
+        if (ins[i].rows > 0 && ins[i].cols[k].validity) wv[k] = true;  // bitmap if any input has one
+        if (f.cols[k].kind == TQ_UTF8) ub[k] += utf8_bytes_of(c, ins[i].cols[k], nullptr, ins[i].rows, 0, st);
+      }
+    alloc_batch(c, rows, sch, wv, out, st, &ub);
+    std::vector<int32_t> cur(f.ncols, 0);
+    for (uint32_t k = 0; k < f.ncols; ++k)
+      if (f.cols[k].kind == TQ_UTF8) {
+        k_set_first_offset<<<1, 1, 0, st>>>(out->cols[k].offsets);
+        counted_launch(c);
+      }
+    uint64_t at = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      gather_into(c, &ins[i], nullptr, ins[i].rows, 0, out, at, cur, st);
+      at += ins[i].rows;
+    }
+  });
+}
+
+}  // extern "C"
+
+// ================================================================== operator entry points
+namespace {
+using namespace tq;
+
+std::vector<uint32_t> iota_u32(uint32_t n) {
+  std::vector<uint32_t> v(n);
+  for (uint32_t i = 0; i < n; ++i) v[i] = i;
+  return v;
+}
+
+// keys given as INPUT column indices: project every input column so that
+// projected column i == input column i.
+void compile_all(Prog& P, const tq_batch* in, const tq_expr* pred) { compile_prog(P, in, pred, nullptr, 0, true); }
+}  // namespace
+
+extern "C" {
+
+tq_status tq_filter(tq_ctx* c, const tq_batch* in, tq_expr pred, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_all(P, in, &pred);
+    MatArgs A;
+    run_materialize(c, in, P, A, out, nullptr, pick(c, stream));
+  });
+}
+
+tq_status tq_project(tq_ctx* c, const tq_batch* in, const tq_expr* exprs, uint32_t n, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_prog(P, in, nullptr, exprs, n, false);
+    MatArgs A;
+    run_materialize(c, in, P, A, out, nullptr, pick(c, stream));
+  });
+}
+
+tq_status tq_pipeline_materialize(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                  uint32_t nexprs, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
+    MatArgs A;
+    run_materialize(c, in, P, A, out, nullptr, pick(c, stream));
+  });
+}
+
+tq_status tq_hash_partition(tq_ctx* c, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, uint32_t nparts,
+                            tq_batch* out, uint64_t* part_offsets, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_all(P, in, nullptr);
+    MatArgs A;
+    A.mode = MAT_PARTITION;
+    A.key_roots.assign(keys, keys + nkeys);
+    A.nparts = nparts;
+    run_materialize(c, in, P, A, out, part_offsets, pick(c, stream));
+  });
+}
+
+tq_status tq_pipeline_partition(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                uint32_t nexprs, const uint32_t* keys, uint32_t nkeys, uint32_t nparts,
+                                tq_batch* out, uint64_t* part_offsets, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
+    MatArgs A;
+    A.mode = MAT_PARTITION;
+    A.key_roots.assign(keys, keys + nkeys);
+    A.nparts = nparts;
+    run_materialize(c, in, P, A, out, part_offsets, pick(c, stream));
+  });
+}
+
+tq_status tq_join_build(tq_ctx* c, const tq_batch* build, const uint32_t* keys, uint32_t nkeys, tq_join_table** out,
+                        void* stream) {
+  return guard([&] {
+    check_device_batch(build);
+    Prog P(schema_of(build));
+    std::vector<tq_expr_node> nodes(nkeys);
+    std::vector<tq_expr> ex(nkeys);
+    for (uint32_t k = 0; k < nkeys; ++k) {
+      nodes[k] = tq_expr_node{};
+      nodes[k].tag = TQ_EX_COL;
+      nodes[k].column = keys[k];
+      ex[k] = tq_expr{&nodes[k], 1, 0};
+    }
+    compile_prog(P, build, nullptr, ex.data(), nkeys, false);
+    run_build(c, build, P, iota_u32(nkeys), out, pick(c, stream));
+  });
+}
+
+tq_status tq_pipeline_build(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const uint32_t* keys, uint32_t nkeys,
+                            tq_join_table** out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    std::vector<tq_expr_node> nodes(nkeys);
+    std::vector<tq_expr> ex(nkeys);
+    for (uint32_t k = 0; k < nkeys; ++k) {
+      nodes[k] = tq_expr_node{};
+      nodes[k].tag = TQ_EX_COL;
+      nodes[k].column = keys[k];
+      ex[k] = tq_expr{&nodes[k], 1, 0};
+    }
+    compile_prog(P, in, pred, ex.data(), nkeys, false);
+    run_build(c, in, P, iota_u32(nkeys), out, pick(c, stream));
+  });
+}
+
+tq_status tq_join_probe(tq_ctx* c, const tq_join_table* t, const tq_batch* probe, const uint32_t* keys,
+                        uint32_t nkeys, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(probe);
+    Prog P(schema_of(probe));
+    compile_all(P, probe, nullptr);
+    MatArgs A;
+    A.mode = MAT_PROBE;
+    A.key_roots.assign(keys, keys + nkeys);
+    A.table = t;
+    A.build_cols = iota_u32(t->build.ncols);
+    run_materialize(c, probe, P, A, out, nullptr, pick(c, stream));
+  });
+}
+
+tq_status tq_pipeline_probe(tq_ctx* c, const tq_join_table* t, const tq_batch* in, const tq_expr* pred,
+                            const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,
+                            const uint32_t* build_cols, uint32_t nbuild_cols, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
+    MatArgs A;
+    A.mode = MAT_PROBE;
+    A.key_roots.assign(keys, keys + nkeys);
+    A.table = t;
+    if (build_cols) A.build_cols.assign(build_cols, build_cols + nbuild_cols);
+    else A.build_cols = iota_u32(t->build.ncols);
+    run_materialize(c, in, P, A, out, nullptr, pick(c, stream));
+  });
+}
+
+void tq_join_table_destroy(tq_ctx* c, tq_join_table* t) {
+  if (!t) return;
+  (void)c;
+  dfree(t->ctx, t->jt.entries, t->bytes, t->stream);
+  std::free(t->build.cols);
+  delete t;
+}
+
+tq_status tq_aggregate(tq_ctx* c, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs,
+                       uint32_t naggs, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_all(P, in, nullptr);
+    run_aggregate(c, in, P, keys, nkeys, aggs, naggs, out, pick(c, stream));
+  });
+}
+
+tq_status tq_pipeline_aggregate(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                uint32_t nexprs, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs,
+                                uint32_t naggs, tq_batch* out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
+    run_aggregate(c, in, P, keys, nkeys, aggs, naggs, out, pick(c, stream));
+  });
+}
+
+}  // extern "C"
+
+namespace tq {
+void scan_u32_public(tq_ctx* c, const u32* in, u64 n, u64* out, u64* total_dev, cudaStream_t st) {
+  scan_u32(c, in, n, out, total_dev, st);
+}
+}  // namespace tq

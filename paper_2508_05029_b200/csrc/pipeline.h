@@ -1,0 +1,132 @@
+// pipeline.h — launch parameters of the staged tile pipeline kernels
+// (pipeline.cu).  One kernel family covers the per-batch operators of
+// SPEC.md:560-611:
+//
+//   source   : the batch, tile by tile, TMA bulk-copied into shared memory
+//   program  : the Expr register machine (program.h): predicate, projections,
+//              keys, aggregate inputs
+//   sink     : COUNT  per-tile output counts for a destination function
+//              EMIT   stable scatter of rows to their destinations
+//                     (filter = 1 destination, hash_partition = n, join probe
+//                      = k matches per row)
+//              AGG    warp-aggregated hash group-by into a global table
+//              BUILD  join build: open-addressing insert of (key, row)
+#pragma once
+#include <cstdint>
+
+#include "program.h"
+
+namespace tq {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kV = 2;                   // rows per lane per tile
+constexpr int kTile = kThreads * kV;    // rows per tile (512)
+constexpr int kMaxKeys = 4;
+constexpr int kMaxKeyWords = 8;         // + 1 null word
+constexpr int kMaxOut = 24;
+constexpr int kMaxAcc = 16;
+constexpr int kMaxDest = 64;
+constexpr int kMaxStages = 4;
+
+enum SinkKind { SINK_COUNT = 0, SINK_EMIT = 1, SINK_AGG = 2, SINK_BUILD = 3 };
+enum DestKind { DEST_FILTER = 0, DEST_PARTITION = 1, DEST_PROBE = 2 };
+
+struct StagedCol {
+  const uint8_t* values;
+  const uint8_t* validity;  // nullptr = all valid
+  uint32_t width;           // 1, 8, 16
+  uint32_t off;             // smem offset of values within a stage
+  uint32_t voff;            // smem offset of validity within a stage
+  uint8_t bulk_ok;          // base 16-B aligned -> TMA bulk copies
+  uint8_t kind;
+  uint8_t _pad[2];
+};
+
+struct KeyOpnd {
+  uint8_t kind;     // operand kind (program.h)
+  uint8_t words;    // 1 or 2 key words
+  uint8_t bytes;    // partition-hash bytes: 8, 16 or 1
+  uint8_t _pad;
+  uint16_t idx;
+  uint16_t _pad2;
+};
+
+// Join hash table: `cap` entries of `stride` bytes: int64 row (-1 empty)
+// followed by `kw` key words.
+struct JoinTable {
+  uint8_t* entries;
+  uint64_t cap;     // power of two
+  uint32_t stride;  // bytes
+  uint32_t kw;
+};
+
+enum OutSrc : uint8_t { OUT_OPND = 0, OUT_BUILD = 1 };
+struct OutCol {
+  uint8_t src;       // OUT_OPND / OUT_BUILD
+  uint8_t kind;      // operand kind for OUT_OPND
+  uint8_t width;     // output width (1, 8, 16)
+  uint8_t out_kind;  // TQ_* of the output column
+  uint16_t idx;      // operand index
+  uint16_t _pad;
+  uint8_t* values;
+  uint8_t* validity;  // nullptr = output has no bitmap
+  const uint8_t* bvalues;    // OUT_BUILD source
+  const uint8_t* bvalidity;  // OUT_BUILD source validity
+};
+
+enum AccOp : uint8_t { ACC_SUM_I = 0, ACC_SUM_F, ACC_CNT, ACC_MIN_I, ACC_MAX_I, ACC_MIN_F, ACC_MAX_F };
+struct AccSpec {
+  uint8_t op;
+  uint8_t kind;  // operand kind (K_NONE for COUNT(*))
+  uint16_t idx;
+  uint8_t scale; // F conversion scale for I operands of SUM_F/MIN_F/MAX_F (unused today)
+  uint8_t _pad[3];
+};
+
+// Global aggregation hash table.
+struct AggTable {
+  uint32_t* state;   // 0 empty, 1 writing, 2 ready
+  unsigned long long* keys;  // cap * kwa
+  unsigned long long* acc;   // cap * nacc * 2 words (16 B per accumulator)
+  uint64_t cap;      // power of two
+  unsigned long long* nused;
+  uint32_t* overflow;
+};
+
+struct PipeParams {
+  uint64_t rows;
+  uint64_t row_base;  // added to tile-relative row ids (BUILD row ids)
+  uint32_t ntiles;
+  uint32_t nstages;
+  uint32_t stage_bytes;
+  // shared-memory layout (bytes from dynamic smem base)
+  uint32_t off_code, off_lits, off_stage, off_bar, off_vslot, off_vvalid, off_bslot, off_sink;
+  // program
+  const DInstr* code;
+  const DLit* lits;
+  uint16_t ncode, npred, nlits, nstaged;
+  uint16_t nvslots, nbslots;
+  uint8_t pred_kind;
+  uint8_t _p0;
+  uint16_t pred_idx;
+  StagedCol cols[kMaxStaged];
+  // keys
+  uint32_t nkeys, key_words;
+  KeyOpnd keys[kMaxKeys];
+  // destinations
+  uint32_t dest_kind, ndest;
+  uint32_t* tile_counts;          // [ndest][ntiles]
+  const unsigned long long* tile_offsets;  // [ndest][ntiles] absolute output rows
+  JoinTable jt;
+  // emit
+  uint32_t nout;
+  OutCol out[kMaxOut];
+  // aggregate
+  uint32_t nacc;
+  uint32_t local_groups;  // per-CTA smem table slots (power of two, 0 = none)
+  AccSpec acc[kMaxAcc];
+  AggTable agg;
+};
+
+}  // namespace tq

@@ -1,0 +1,308 @@
+"""ctypes mirror of the reference operator interface over libtq_gpu.so.
+
+Names and argument meaning follow SPEC.md:560-611 (filter_execute,
+project_execute, hash_partition, join_execute, aggregate_execute) and the
+columnar substrate (take / concat / slice, transform.cpp).  Every call goes
+through the C-ABI of include/tq_gpu.h into sm_100a kernels; there is no CPU
+fallback: if the native library is missing the import of `lib()` raises.
+Errors come back as TqError carrying the reference's Errc name.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .columnar import (MEM_DEVICE, HostBatch, TqAggC, TqBatchC, TqError, TqExprC)
+from .expr import Expr
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtq_gpu.so")
+_lib = None
+
+
+class TqOptsC(C.Structure):
+    _fields_ = [("device", C.c_int), ("ctas_per_sm", C.c_uint32), ("device_budget_bytes", C.c_uint64)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() (make -C paper_2508_05029_b200/csrc)")
+        L = C.CDLL(LIB_PATH)
+        P, V = C.POINTER, C.c_void_p
+        B = P(TqBatchC)
+        L.tq_last_error.restype = C.c_char_p
+        L.tq_errc_name.restype = C.c_char_p
+        L.tq_ctx_create.argtypes = [P(TqOptsC), P(V)]
+        L.tq_ctx_destroy.argtypes = [V]
+        L.tq_sync.argtypes = [V, V]
+        L.tq_device_bytes_in_use.restype = C.c_uint64
+        L.tq_device_bytes_in_use.argtypes = [V]
+        L.tq_kernel_launches.restype = C.c_uint32
+        L.tq_kernel_launches.argtypes = [V]
+        L.tq_batch_alloc.argtypes = [V, B, C.c_uint64, B, V]
+        L.tq_batch_upload.argtypes = [V, B, B, V]
+        L.tq_batch_download.argtypes = [V, B, B, V]
+        L.tq_batch_free.argtypes = [V, B]
+        L.tq_host_batch_free.argtypes = [B]
+        L.tq_take.argtypes = [V, B, V, C.c_uint64, B, V]
+        L.tq_concat.argtypes = [V, B, C.c_uint32, B, V]
+        L.tq_slice.argtypes = [V, B, C.c_uint64, C.c_uint64, B, V]
+        L.tq_filter.argtypes = [V, B, TqExprC, B, V]
+        L.tq_project.argtypes = [V, B, P(TqExprC), C.c_uint32, B, V]
+        U32 = P(C.c_uint32)
+        L.tq_hash_partition.argtypes = [V, B, U32, C.c_uint32, C.c_uint32, B, P(C.c_uint64), V]
+        L.tq_join_build.argtypes = [V, B, U32, C.c_uint32, P(V), V]
+        L.tq_join_probe.argtypes = [V, V, B, U32, C.c_uint32, B, V]
+        L.tq_join_table_destroy.argtypes = [V, V]
+        L.tq_aggregate.argtypes = [V, B, U32, C.c_uint32, P(TqAggC), C.c_uint32, B, V]
+        E = P(TqExprC)
+        L.tq_pipeline_materialize.argtypes = [V, B, E, E, C.c_uint32, B, V]
+        L.tq_pipeline_aggregate.argtypes = [V, B, E, E, C.c_uint32, U32, C.c_uint32, P(TqAggC), C.c_uint32, B, V]
+        L.tq_pipeline_partition.argtypes = [V, B, E, E, C.c_uint32, U32, C.c_uint32, C.c_uint32, B,
+                                            P(C.c_uint64), V]
+        L.tq_pipeline_probe.argtypes = [V, V, B, E, E, C.c_uint32, U32, C.c_uint32, U32, C.c_uint32, B, V]
+        L.tq_pipeline_build.argtypes = [V, B, E, U32, C.c_uint32, P(V), V]
+        L.tq_datagen.argtypes = [V, C.c_int, C.c_double, B, V]
+        _lib = L
+    return _lib
+
+
+def _u32(xs: Sequence[int]):
+    return (C.c_uint32 * max(1, len(xs)))(*xs)
+
+
+def _exprs(exprs: Optional[Sequence[Expr]]):
+    if exprs is None:
+        return None, 0, []
+    ss = [e.serialize() for e in exprs]
+    arr = (TqExprC * max(1, len(ss)))(*[s.c() for s in ss])
+    return arr, len(ss), ss
+
+
+def _pred(pred: Optional[Expr]):
+    if pred is None:
+        return None, None
+    s = pred.serialize()
+    c = s.c()
+    return C.pointer(c), s
+
+
+class DeviceBatch:
+    """A device-resident batch owned by a Context (freed on close/GC)."""
+
+    def __init__(self, ctx: "Context", c: TqBatchC):
+        self.ctx = ctx
+        self.c = c
+
+    @property
+    def rows(self) -> int:
+        return int(self.c.rows)
+
+    @property
+    def ncols(self) -> int:
+        return int(self.c.ncols)
+
+    def to_host(self) -> HostBatch:
+        return self.ctx.download(self)
+
+    def free(self):
+        if self.c is not None and self.ctx.handle:
+            lib().tq_batch_free(self.ctx.handle, C.byref(self.c))
+            self.c = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class JoinTable:
+    def __init__(self, ctx: "Context", handle, build: DeviceBatch):
+        self.ctx, self.handle, self.build = ctx, handle, build  # keeps the build batch alive
+
+    def free(self):
+        if self.handle:
+            lib().tq_join_table_destroy(self.ctx.handle, self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Context:
+    """One tq context per GPU (tq_ctx_create)."""
+
+    def __init__(self, device: int = 0, device_budget_bytes: int = 0, ctas_per_sm: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        opts = TqOptsC(device, ctas_per_sm, device_budget_bytes)
+        self._check(L.tq_ctx_create(C.byref(opts), C.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def _check(st: int):
+        if st != 0:
+            L = lib()
+            raise TqError(st, (L.tq_last_error() or b"").decode())
+
+    def close(self):
+        if self.handle:
+            lib().tq_ctx_destroy(self.handle)
+            self.handle = None
+
+    def sync(self, stream=None):
+        self._check(lib().tq_sync(self.handle, stream))
+
+    def bytes_in_use(self) -> int:
+        return lib().tq_device_bytes_in_use(self.handle)
+
+    def kernel_launches(self) -> int:
+        return lib().tq_kernel_launches(self.handle)
+
+    # ---- movement ----------------------------------------------------------
+    def upload(self, hb: HostBatch, stream=None) -> DeviceBatch:
+        hc = hb.to_c()
+        out = TqBatchC()
+        self._check(lib().tq_batch_upload(self.handle, C.byref(hc), C.byref(out), stream))
+        self.sync(stream)
+        return DeviceBatch(self, out)
+
+    def download(self, db: DeviceBatch, stream=None) -> HostBatch:
+        out = TqBatchC()
+        self._check(lib().tq_batch_download(self.handle, C.byref(db.c), C.byref(out), stream))
+        try:
+            return HostBatch.from_c(out)
+        finally:
+            lib().tq_host_batch_free(C.byref(out))
+
+    def _wrap(self, st, out):
+        self._check(st)
+        return DeviceBatch(self, out)
+
+    def datagen(self, table: int, sf: float, stream=None) -> DeviceBatch:
+        out = TqBatchC()
+        return self._wrap(lib().tq_datagen(self.handle, table, sf, C.byref(out), stream), out)
+
+    # ---- substrate ---------------------------------------------------------
+    def take(self, b: DeviceBatch, ids: Sequence[int], stream=None) -> DeviceBatch:
+        n = len(ids)
+        dids = self.upload(HostBatch(max(n, 1), [HostBatch.col_i64(list(ids) if n else [0])]), stream)
+        out = TqBatchC()
+        r = self._wrap(lib().tq_take(self.handle, C.byref(b.c), C.c_void_p(dids.c.cols[0].values), n,
+                                     C.byref(out), stream), out)
+        self.sync(stream)
+        dids.free()
+        return r
+
+    def concat(self, bs: Sequence[DeviceBatch], stream=None) -> DeviceBatch:
+        arr = (TqBatchC * len(bs))(*[b.c for b in bs])
+        out = TqBatchC()
+        return self._wrap(lib().tq_concat(self.handle, arr, len(bs), C.byref(out), stream), out)
+
+    def slice(self, b: DeviceBatch, start: int, n: int, stream=None) -> DeviceBatch:
+        out = TqBatchC()
+        return self._wrap(lib().tq_slice(self.handle, C.byref(b.c), start, n, C.byref(out), stream), out)
+
+    # ---- operators --------------------------------------
+    def filter_execute(self, b: DeviceBatch, pred: Expr, stream=None) -> DeviceBatch:
+        s = pred.serialize()
+        out = TqBatchC()
+        return self._wrap(lib().tq_filter(self.handle, C.byref(b.c), s.c(), C.byref(out), stream), out)
+
+    def project_execute(self, b: DeviceBatch, exprs: Sequence[Expr], stream=None) -> DeviceBatch:
+        arr, n, _keep = _exprs(exprs)
+        out = TqBatchC()
+        return self._wrap(lib().tq_project(self.handle, C.byref(b.c), arr, n, C.byref(out), stream), out)
+
+    def hash_partition(self, b: DeviceBatch, keys: Sequence[int], nparts: int,
+                       stream=None) -> Tuple[DeviceBatch, List[int]]:
+        offs = (C.c_uint64 * (nparts + 1))()
+        out = TqBatchC()
+        r = self._wrap(lib().tq_hash_partition(self.handle, C.byref(b.c), _u32(keys), len(keys), nparts,
+                                               C.byref(out), offs, stream), out)
+        return r, list(offs)
+
+    def join_build(self, build: DeviceBatch, keys: Sequence[int], stream=None) -> JoinTable:
+        h = C.c_void_p()
+        self._check(lib().tq_join_build(self.handle, C.byref(build.c), _u32(keys), len(keys), C.byref(h), stream))
+        return JoinTable(self, h, build)
+
+    def join_probe(self, t: JoinTable, probe: DeviceBatch, keys: Sequence[int], stream=None) -> DeviceBatch:
+        out = TqBatchC()
+        return self._wrap(lib().tq_join_probe(self.handle, t.handle, C.byref(probe.c), _u32(keys), len(keys),
+                                              C.byref(out), stream), out)
+
+    def join_execute(self, build: DeviceBatch, probe: DeviceBatch, bkeys: Sequence[int], pkeys: Sequence[int],
+                     stream=None) -> DeviceBatch:
+        t = self.join_build(build, bkeys, stream)
+        try:
+            return self.join_probe(t, probe, pkeys, stream)
+        finally:
+            self.sync(stream)
+            t.free()
+
+    def aggregate_execute(self, b: DeviceBatch, keys: Sequence[int], aggs: Sequence[Tuple[int, int]],
+                          stream=None) -> DeviceBatch:
+        arr = (TqAggC * max(1, len(aggs)))(*[TqAggC(f, c) for f, c in aggs])
+        out = TqBatchC()
+        return self._wrap(lib().tq_aggregate(self.handle, C.byref(b.c), _u32(keys), len(keys), arr, len(aggs),
+                                             C.byref(out), stream), out)
+
+    # ---- fused pipelines ---------------------------------------------------
+    def pipeline_materialize(self, b: DeviceBatch, pred: Optional[Expr], exprs: Optional[Sequence[Expr]],
+                             stream=None) -> DeviceBatch:
+        pp, _k1 = _pred(pred)
+        arr, n, _k2 = _exprs(exprs)
+        out = TqBatchC()
+        return self._wrap(lib().tq_pipeline_materialize(self.handle, C.byref(b.c), pp, arr, n, C.byref(out),
+                                                        stream), out)
+
+    def pipeline_aggregate(self, b: DeviceBatch, pred: Optional[Expr], exprs: Optional[Sequence[Expr]],
+                           keys: Sequence[int], aggs: Sequence[Tuple[int, int]], stream=None) -> DeviceBatch:
+        pp, _k1 = _pred(pred)
+        arr, n, _k2 = _exprs(exprs)
+        ag = (TqAggC * max(1, len(aggs)))(*[TqAggC(f, c) for f, c in aggs])
+        out = TqBatchC()
+        return self._wrap(lib().tq_pipeline_aggregate(self.handle, C.byref(b.c), pp, arr, n, _u32(keys), len(keys),
+                                                      ag, len(aggs), C.byref(out), stream), out)
+
+    def pipeline_partition(self, b: DeviceBatch, pred, exprs, keys: Sequence[int], nparts: int, stream=None):
+        pp, _k1 = _pred(pred)
+        arr, n, _k2 = _exprs(exprs)
+        offs = (C.c_uint64 * (nparts + 1))()
+        out = TqBatchC()
+        r = self._wrap(lib().tq_pipeline_partition(self.handle, C.byref(b.c), pp, arr, n, _u32(keys), len(keys),
+                                                   nparts, C.byref(out), offs, stream), out)
+        return r, list(offs)
+
+    def pipeline_build(self, b: DeviceBatch, pred, keys: Sequence[int], stream=None) -> JoinTable:
+        pp, _k1 = _pred(pred)
+        h = C.c_void_p()
+        self._check(lib().tq_pipeline_build(self.handle, C.byref(b.c), pp, _u32(keys), len(keys), C.byref(h),
+                                            stream))
+        return JoinTable(self, h, b)
+
+    def pipeline_probe(self, t: JoinTable, b: DeviceBatch, pred, exprs, keys: Sequence[int],
+                       build_cols: Optional[Sequence[int]] = None, stream=None) -> DeviceBatch:
+        pp, _k1 = _pred(pred)
+        arr, n, _k2 = _exprs(exprs)
+        bc = _u32(build_cols) if build_cols is not None else None
+        nb = len(build_cols) if build_cols is not None else 0
+        out = TqBatchC()
+        return self._wrap(lib().tq_pipeline_probe(self.handle, t.handle, C.byref(b.c), pp, arr, n, _u32(keys),
+                                                  len(keys), bc, nb, C.byref(out), stream), out)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
