@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""bench.py — TPC-H Q1-style group-by over synthetic lineitem SF10 per GPU
+(BASELINE.json configs[1]) through libtq_gpu.so, plus the reference arm.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tq|reference]
+
+Prints ONE JSON line (rank 0).  Timing: CUDA events on the stream the
+pipeline kernels run on, W untimed warm-up steps, K timed steps bracketed by a
+barrier + device synchronize, max over ranks.  Inputs (5.3 GB of scanned
+columns per GPU) are larger than the 126 MB L2, so no flush is needed.
+N > 1: one process per GPU (torchrun); each rank generates and scans its own
+row-group subset of an SF(10*N) lineitem (weak scaling); the per-rank partial
+aggregates (4 groups) are merged on rank 0 after timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "query latency (ms) and input rows/sec per TPC-H-style query at 1/2/4/8 B200"
+SF_PER_GPU = 10.0
+Q1_BYTES_PER_ROW = 88  # rf 8 + ls 8 + qty 16 + ep 16 + disc 16 + tax 16 + shipdate 8
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes/launch of `kernel` from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d.get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            return None
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, x: float) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(world, x: float) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def cpu_q1_sample(sf: float, nthreads: int, reps: int):
+    """Oracle (CPU port) Q1 on a bounded lineitem sample; returns rows/s list."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    li = O.datagen(O.T_LINEITEM, sf, nthreads)
+    tabs = {O.T_LINEITEM: li}
+    O.query(1, tabs, nthreads)  # warm
+    rates = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.query(1, tabs, nthreads)
+        rates.append(li.rows / (time.perf_counter() - t0))
+    return rates, li.rows
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference path's CPU implementation (oracle port;
+    the reference ships no operator code) on this box's cores."""
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    sample_sf = 1.0
+    li = O.datagen(O.T_LINEITEM, sample_sf, nthreads)
+    tabs = {O.T_LINEITEM: li}
+    for _ in range(args.warmup):
+        O.query(1, tabs, nthreads)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.query(1, tabs, nthreads)
+        ts.append(time.perf_counter() - t0)
+    sec = sum(ts) / len(ts)
+    value = li.rows / sec
+    sample = f"lineitem SF{sample_sf:g} row-group sample ({li.rows} rows) of the SF{SF_PER_GPU:g} workload per step"
+    line = {
+        "metric": METRIC, "value": value, "unit": "rows/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int128", "data": "synthetic",
+        "config": {"workload": "TPC-H Q1-style group-by, lineitem", "query": "q1", "sf_per_gpu": SF_PER_GPU},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": nthreads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_tq(args, world, rank, local):
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_2508_05029_b200 import queries
+    from paper_2508_05029_b200.columnar import HostBatch, TqBatchC
+    from paper_2508_05029_b200.ops import Context, DeviceBatch, lib
+
+    torch.cuda.set_device(local)
+    ctx = Context(local)
+    sf_total = SF_PER_GPU * world
+    li = ctx.datagen(1, sf_total, shard=rank, nshards=world)
+    scan = li.select(queries.Q1_SCAN)
+    rows = scan.rows
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    partial = world > 1
+
+    def step():
+        out = queries.q1_scan(ctx, scan, partial=partial)
+        return out
+
+    for _ in range(args.warmup):
+        step().free()
+    ctx.sync()
+    barrier(world)
+    clocks = Clocks(local)
+    clocks.start()
+    ctx.profile(True)
+    l0 = ctx.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    outs = []
+    for _ in range(args.steps):
+        outs.append(step())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ctx.sync()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ctx.kernel_launches() - l0
+    prof = ctx.profile_report()
+    ctx.profile(False)
+    ck = clocks.stop()
+    barrier(world)
+    ms_max = max_over_ranks(world, ms)
+    total_rows = sum_over_ranks(world, float(rows))
+    result = outs[-1].to_host()
+    for o in outs:
+        o.free()
+
+    # ---- end to end through the public API: pinned host columns -> H2D ->
+    # Q1 -> D2H of the result, every step
+    host = ctx.download(scan)
+    pinned = []
+    hb = HostBatch(host.rows)
+    for c in host.cols:
+        p = C.c_void_p()
+        Context._check(lib().tq_pinned_alloc(max(1, c.values.size), C.byref(p)))
+        arr = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint8)), (max(1, c.values.size),))
+        arr[:c.values.size] = c.values
+        pinned.append(p)
+        hb.cols.append(type(c)(c.kind, arr[:c.values.size], None, None, c.precision, c.scale))
+    del host
+    hc = hb.to_c()
+    h2d = sum(c.values.size for c in hb.cols)
+
+    def e2e_step():
+        out = TqBatchC()
+        Context._check(lib().tq_batch_upload(ctx.handle, C.byref(hc), C.byref(out), None))
+        d = DeviceBatch(ctx, out)
+        r = queries.q1_scan(ctx, d, partial=partial)
+        res = r.to_host()
+        r.free()
+        d.free()
+        return res
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        e2e_step()
+    ctx.sync()
+    barrier(world)
+    ee = max(2, min(args.steps, 5))
+    e0.record(stream)
+    t0 = time.perf_counter()
+    for _ in range(ee):
+        res = e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3) / ee
+    e2e_ms = max_over_ranks(world, e2e_ms)
+    d2h = res.nbytes()
+    for p in pinned:
+        lib().tq_pinned_free(p)
+
+    # ---- correctness of what was timed vs the CPU oracle (rank 0, N=1)
+    parity = None
+    if rank == 0 and world == 1 and os.environ.get("TQ_BENCH_PARITY", "1") == "1":
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O
+            from paper_2508_05029_b200.columnar import assert_batches_equal
+            hl = O.datagen(O.T_LINEITEM, sf_total, os.cpu_count() or 1)
+            assert_batches_equal(result, O.query(1, {O.T_LINEITEM: hl}, os.cpu_count() or 1))
+            parity = "bit-exact vs oracle (float avg within 1e-9)"
+            del hl
+        except AssertionError as e:
+            parity = f"MISMATCH: {e}"
+
+    cpu = None
+    if rank == 0 and world == 1:
+        nthreads = os.cpu_count() or 1
+        rates, srows = cpu_q1_sample(1.0, nthreads, 3)
+        cpu = {"value": statistics.median(rates), "unit": "rows/s", "cores": nthreads, "kind": "port",
+               "sample": f"oracle Q1 on lineitem SF1 ({srows} rows), median of 3, {nthreads} threads"}
+
+    if rank != 0:
+        ctx.close()
+        return
+    peaks = measured_peaks()
+    peak = peaks["hbm_gbs"] if peaks else 6650.0
+    n_agg, agg_ms = prof.get("pipe_agg", (0, 0.0))
+    kern_ms = agg_ms / max(1, n_agg)
+    achieved = Q1_BYTES_PER_ROW * rows / (kern_ms * 1e-3) / 1e9 if kern_ms > 0 else None
+    value = total_rows / (ms_max * 1e-3)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "rows/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_max,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int128",
+        "data": "synthetic (counter-based SplitMix64 TPC-H-style tables, DESIGN.md §4)",
+        "config": {
+            "workload": f"TPC-H Q1-style filter+project+group-by over lineitem SF{SF_PER_GPU:g} per GPU",
+            "query": "q1", "sf_per_gpu": SF_PER_GPU, "rows_per_gpu": rows, "scan_bytes_per_row": Q1_BYTES_PER_ROW,
+            "l2": "scanned columns (%.1f GB/GPU) > 126 MB L2; no flush needed" % (rows * Q1_BYTES_PER_ROW / 1e9),
+            "parallelism": f"dp{world} (row-group subsets, partial aggregates merged)",
+        },
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic("pipe_agg"),
+            "kernel": "pipe_kernel<SINK_AGG>", "kernel_ms": kern_ms,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "B200_PROFILING.md fallback",
+            "algorithmic_bytes_per_row": Q1_BYTES_PER_ROW,
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": total_rows / (e2e_ms * 1e-3), "unit": "rows/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "kernels_ms": {k: v[1] / max(1, v[0]) for k, v in prof.items()},
+        "clocks": ck,
+        "parity": parity,
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tq", choices=["tq", "reference"])
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_tq(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -37,6 +37,14 @@ const char* tq_errc_name(tq_status status);      /* common.cpp:19-41 errc_name *
 tq_status tq_sync(tq_ctx* ctx, void* stream);
 uint64_t tq_device_bytes_in_use(tq_ctx* ctx);    /* ledger: allocated Device-tier bytes */
 uint32_t tq_kernel_launches(tq_ctx* ctx);        /* kernels this context has launched */
+void* tq_ctx_stream(tq_ctx* ctx);                /* the context's own cudaStream_t */
+/* CUDA-event timing of every pipeline kernel launch (on its launching stream);
+ * tq_profile_report writes "kernel count total_ms" lines and resets. */
+void tq_profile_enable(tq_ctx* ctx, int on);
+uint64_t tq_profile_report(tq_ctx* ctx, char* buf, uint64_t cap);
+/* page-locked, portable host memory (the Host tier of SPEC.md:236-239) */
+tq_status tq_pinned_alloc(uint64_t bytes, void** out);
+void tq_pinned_free(void* p);
 
 /* ---- batches (reference types.hpp:125-143 ColumnBatch; types.cpp:146-170) --- */
 /* Allocate an uninitialised device batch with the schema of `like`
@@ -107,6 +115,12 @@ tq_status tq_pipeline_build(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred
  * common.hpp:139-158).  table: 0 orders, 1 lineitem, 2 customer,
  * 3 supplier, 4 part, 5 partsupp, 6 nation, 7 region. */
 tq_status tq_datagen(tq_ctx* ctx, int table, double sf, tq_batch* out, void* stream);
+/* The row-group subset of worker `shard` of `nshards` (SPEC.md:661-667
+ * assign_files): orders/lineitem split by order ranges (a lineitem shard holds
+ * exactly the lines of its orders), other tables by contiguous row ranges.
+ * Values equal the corresponding rows of the full table. */
+tq_status tq_datagen_shard(tq_ctx* ctx, int table, double sf, uint32_t shard, uint32_t nshards, tq_batch* out,
+                           void* stream);
 
 #ifdef __cplusplus
 }

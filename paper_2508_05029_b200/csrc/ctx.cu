@@ -27,6 +27,22 @@ void cuda_check(cudaError_t e, const char* what) {
 
 void counted_launch(tq_ctx* c) { c->launches.fetch_add(1, std::memory_order_relaxed); }
 
+int prof_begin(tq_ctx* c, const char* name, cudaStream_t st) {
+  if (!c->profiling) return -1;
+  std::lock_guard<std::mutex> g(c->mu);
+  tq_ctx::Ev e{name, nullptr, nullptr, 0};
+  cudaEventCreate(&e.a);
+  cudaEventCreate(&e.b);
+  cudaEventRecord(e.a, st);
+  c->evs.push_back(e);
+  return (int)c->evs.size() - 1;
+}
+void prof_end(tq_ctx* c, int h, cudaStream_t st) {
+  if (h < 0) return;
+  std::lock_guard<std::mutex> g(c->mu);
+  cudaEventRecord(c->evs[h].b, st);
+}
+
 size_t width_of(uint8_t kind) {
   switch (kind) {
     case TQ_INT64: return 8;
@@ -155,6 +171,48 @@ tq_status tq_sync(tq_ctx* c, void* stream) {
 }
 
 uint64_t tq_device_bytes_in_use(tq_ctx* c) { return c->in_use.load(); }
+
+void tq_profile_enable(tq_ctx* c, int on) {
+  std::lock_guard<std::mutex> g(c->mu);
+  c->profiling = on != 0;
+}
+
+// Synchronise, then write "name count total_ms\n" lines (summed per kernel
+// name) into buf and clear the recorded events.  Returns bytes written.
+uint64_t tq_profile_report(tq_ctx* c, char* buf, uint64_t cap) {
+  cudaStreamSynchronize(c->stream);
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> g(c->mu);
+  std::map<std::string, std::pair<int, double>> agg;
+  for (auto& e : c->evs) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    auto& x = agg[e.name];
+    x.first += 1;
+    x.second += ms;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  c->evs.clear();
+  std::string out;
+  for (auto& kv : agg)
+    out += kv.first + " " + std::to_string(kv.second.first) + " " + std::to_string(kv.second.second) + "\n";
+  uint64_t n = std::min<uint64_t>(out.size(), cap ? cap - 1 : 0);
+  if (cap) {
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return n;
+}
+
+void* tq_ctx_stream(tq_ctx* c) { return (void*)c->stream; }
+
+tq_status tq_pinned_alloc(uint64_t bytes, void** out) {
+  return guard([&] { TQ_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable)); });
+}
+void tq_pinned_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
 uint32_t tq_kernel_launches(tq_ctx* c) { return c->launches.load(); }
 
 tq_status tq_batch_alloc(tq_ctx* c, const tq_batch* like, uint64_t rows, tq_batch* out, void* stream) {

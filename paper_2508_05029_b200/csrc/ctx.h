@@ -23,6 +23,15 @@ struct tq_ctx {
   void* pinned = nullptr;              // small pinned readback area (4 KiB)
   std::mutex mu;                       // guards pinned + program cache
   std::map<std::string, void*> prog_cache;  // program bytes -> device copy
+  // optional per-kernel CUDA-event timing (tq_profile_*): events recorded on
+  // the launching stream around each pipeline kernel
+  bool profiling = false;
+  struct Ev {
+    std::string name;
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::vector<Ev> evs;
 };
 
 namespace tq {
@@ -53,6 +62,9 @@ size_t width_of(uint8_t kind);
 void alloc_batch(tq_ctx* c, uint64_t rows, const std::vector<tq_column>& schema, const std::vector<bool>& want_valid,
                  tq_batch* out, cudaStream_t st, const std::vector<uint64_t>* utf8_bytes = nullptr);
 void counted_launch(tq_ctx* c);
+// begin/end an event-timed region for kernel `name` (no-op unless profiling)
+int prof_begin(tq_ctx* c, const char* name, cudaStream_t st);
+void prof_end(tq_ctx* c, int h, cudaStream_t st);
 
 extern thread_local std::string g_err;
 

@@ -41,9 +41,11 @@ struct Seeds {
 
 #define GRID_LOOP(i, n) for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (u64)gridDim.x * blockDim.x)
 
-__global__ void k_orders(u64 no, u64 nc, Seeds S, long long* ok, long long* ck, long long* od, long long* sp,
-                         long long* yr) {
-  GRID_LOOP(i, no) {
+__global__ void k_orders(u64 lo, u64 n, u64 nc, Seeds S, long long* ok0, long long* ck0, long long* od0,
+                         long long* sp0, long long* yr0) {
+  GRID_LOOP(j, n) {
+    u64 i = lo + j;
+    long long *ok = ok0 - lo, *ck = ck0 - lo, *od = od0 - lo, *sp = sp0 - lo, *yr = yr0 - lo;
     long long d = 8035 + (long long)U(S.s[1], i, 2406);
     ok[i] = (long long)i + 1;
     ck[i] = 1 + (long long)U(S.s[0], i, nc);
@@ -62,8 +64,14 @@ struct LiOut {
   ulonglong2 *qty, *ep, *disc, *tax;
 };
 
-__global__ void k_lineitem(u64 no, const u64* off, u64 np, u64 ns, Seeds S, LiOut o) {
-  GRID_LOOP(oi, no) {
+// orders [olo, olo+n); output row = global lineitem row - off[olo]
+__global__ void k_lineitem(u64 olo, u64 n, const u64* off, u64 np, u64 ns, Seeds S, LiOut o0) {
+  const u64 rbase = off[olo];
+  LiOut o = o0;
+  o.ok -= rbase; o.pk -= rbase; o.sk -= rbase; o.rf -= rbase; o.ls -= rbase; o.sd -= rbase;
+  o.qty -= rbase; o.ep -= rbase; o.disc -= rbase; o.tax -= rbase;
+  GRID_LOOP(j, n) {
+    u64 oi = olo + j;
     long long od = 8035 + (long long)U(S.s[0], oi, 2406);
     for (u64 r = off[oi]; r < off[oi + 1]; ++r) {
       long long pk = 1 + (long long)U(S.s[1], r, np);
@@ -86,8 +94,12 @@ __global__ void k_lineitem(u64 no, const u64* off, u64 np, u64 ns, Seeds S, LiOu
   }
 }
 
-__global__ void k_simple(int table, u64 n, u64 ns, Seeds S, long long* c0, long long* c1, void* c2) {
-  GRID_LOOP(i, n) {
+__global__ void k_simple(int table, u64 lo, u64 n, u64 ns, Seeds S, long long* c0_, long long* c1_, void* c2_) {
+  GRID_LOOP(j, n) {
+    u64 i = lo + j;
+    long long* c0 = c0_ - lo;
+    long long* c1 = c1_ - lo;
+    void* c2 = c2_ ? (void*)((uint8_t*)c2_ - lo * (table == 5 ? 16 : 8)) : nullptr;
     switch (table) {
       case 2:  // customer
         c0[i] = (long long)i + 1;
@@ -135,33 +147,43 @@ static tq_column colspec(uint8_t kind, uint8_t prec = 0, uint8_t scale = 0) {
   return c;
 }
 
-void datagen(tq_ctx* c, int table, double sf, tq_batch* out, cudaStream_t st) {
+void datagen(tq_ctx* c, int table, double sf, uint32_t shard, uint32_t nshards, tq_batch* out, cudaStream_t st) {
+  if (nshards == 0 || shard >= nshards) fail(TQ_INVALID_PLAN, "bad shard");
   uint64_t nc = scaled(150000, sf, 1), ns = scaled(10000, sf, 4), np = scaled(200000, sf, 1),
            no = scaled(1500000, sf, 1);
+  auto range = [&](uint64_t n, uint64_t& lo, uint64_t& hi) {
+    lo = n * shard / nshards;
+    hi = n * (shard + 1) / nshards;
+  };
   u32 grid = (u32)c->sms * 8;
   Seeds S{};
   auto I64 = colspec(TQ_INT64);
   auto DEC = colspec(TQ_DECIMAL, 11, 2);
   auto L = [&](int i) { return (long long*)out->cols[i].values; };
+  uint64_t lo, hi;
   switch (table) {
     case 0: {
-      alloc_batch(c, no, {I64, I64, I64, I64, I64}, std::vector<bool>(5, false), out, st);
+      range(no, lo, hi);
+      alloc_batch(c, hi - lo, {I64, I64, I64, I64, I64}, std::vector<bool>(5, false), out, st);
       S.s[0] = col_seed("orders.o_custkey");
       S.s[1] = col_seed("orders.o_orderdate");
-      k_orders<<<grid, 256, 0, st>>>(no, nc, S, L(0), L(1), L(2), L(3), L(4));
+      if (hi > lo) k_orders<<<grid, 256, 0, st>>>(lo, hi - lo, nc, S, L(0), L(1), L(2), L(3), L(4));
       counted_launch(c);
       break;
     }
     case 1: {
+      range(no, lo, hi);
       u32* nl = (u32*)dalloc(c, no * 4, st);
       u64* off = (u64*)dalloc(c, (no + 1) * 8, st);
       k_nlines<<<grid, 256, 0, st>>>(no, col_seed("orders.o_nlines"), nl);
       counted_launch(c);
       extern void scan_u32_public(tq_ctx*, const u32*, u64, u64*, u64*, cudaStream_t);
       scan_u32_public(c, nl, no, off, off + no, st);
-      uint64_t rows = 0;
-      TQ_CUDA(cudaMemcpyAsync(&rows, off + no, 8, cudaMemcpyDeviceToHost, st));
+      uint64_t r01[2] = {0, 0};
+      TQ_CUDA(cudaMemcpyAsync(&r01[0], off + lo, 8, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync(&r01[1], off + hi, 8, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaStreamSynchronize(st));
+      uint64_t rows = r01[1] - r01[0];
       try {
         alloc_batch(c, rows, {I64, I64, I64, DEC, DEC, DEC, DEC, I64, I64, I64}, std::vector<bool>(10, false), out,
                     st);
@@ -186,49 +208,30 @@ void datagen(tq_ctx* c, int table, double sf, tq_batch* out, cudaStream_t st) {
       o.disc = (ulonglong2*)out->cols[5].values;
       o.tax = (ulonglong2*)out->cols[6].values;
       o.rf = L(7); o.ls = L(8); o.sd = L(9);
-      k_lineitem<<<grid, 256, 0, st>>>(no, off, np, ns, S, o);
+      if (hi > lo) k_lineitem<<<grid, 256, 0, st>>>(lo, hi - lo, off, np, ns, S, o);
       counted_launch(c);
       dfree(c, nl, no * 4, st);
       dfree(c, off, (no + 1) * 8, st);
       break;
     }
-    case 2:
-      alloc_batch(c, nc, {I64, I64, I64}, std::vector<bool>(3, false), out, st);
-      S.s[0] = col_seed("customer.c_nationkey");
-      S.s[1] = col_seed("customer.c_mktsegment");
-      k_simple<<<grid, 256, 0, st>>>(2, nc, ns, S, L(0), L(1), out->cols[2].values);
+    default: {
+      uint64_t n;
+      std::vector<tq_column> sch;
+      switch (table) {
+        case 2: n = nc; sch = {I64, I64, I64}; S.s[0] = col_seed("customer.c_nationkey"); S.s[1] = col_seed("customer.c_mktsegment"); break;
+        case 3: n = ns; sch = {I64, I64}; S.s[0] = col_seed("supplier.s_nationkey"); break;
+        case 4: n = np; sch = {I64, I64}; S.s[0] = col_seed("part.p_color"); break;
+        case 5: n = 4 * np; sch = {I64, I64, DEC}; S.s[0] = col_seed("partsupp.ps_supplycost"); break;
+        case 6: n = 25; sch = {I64, I64}; break;
+        case 7: n = 5; sch = {I64, I64}; break;
+        default: fail(TQ_INVALID_PLAN, "unknown table");
+      }
+      range(n, lo, hi);
+      alloc_batch(c, hi - lo, sch, std::vector<bool>(sch.size(), false), out, st);
+      if (hi > lo)
+        k_simple<<<grid, 256, 0, st>>>(table, lo, hi - lo, ns, S, L(0), L(1), sch.size() > 2 ? out->cols[2].values : nullptr);
       counted_launch(c);
-      break;
-    case 3:
-      alloc_batch(c, ns, {I64, I64}, std::vector<bool>(2, false), out, st);
-      S.s[0] = col_seed("supplier.s_nationkey");
-      k_simple<<<grid, 256, 0, st>>>(3, ns, ns, S, L(0), L(1), nullptr);
-      counted_launch(c);
-      break;
-    case 4:
-      alloc_batch(c, np, {I64, I64}, std::vector<bool>(2, false), out, st);
-      S.s[0] = col_seed("part.p_color");
-      k_simple<<<grid, 256, 0, st>>>(4, np, ns, S, L(0), L(1), nullptr);
-      counted_launch(c);
-      break;
-    case 5:
-      alloc_batch(c, 4 * np, {I64, I64, DEC}, std::vector<bool>(3, false), out, st);
-      S.s[0] = col_seed("partsupp.ps_supplycost");
-      k_simple<<<grid, 256, 0, st>>>(5, 4 * np, ns, S, L(0), L(1), out->cols[2].values);
-      counted_launch(c);
-      break;
-    case 6:
-      alloc_batch(c, 25, {I64, I64}, std::vector<bool>(2, false), out, st);
-      k_simple<<<1, 32, 0, st>>>(6, 25, ns, S, L(0), L(1), nullptr);
-      counted_launch(c);
-      break;
-    case 7:
-      alloc_batch(c, 5, {I64, I64}, std::vector<bool>(2, false), out, st);
-      k_simple<<<1, 32, 0, st>>>(7, 5, ns, S, L(0), L(1), nullptr);
-      counted_launch(c);
-      break;
-    default:
-      fail(TQ_INVALID_PLAN, "unknown table");
+    }
   }
   TQ_CUDA(cudaGetLastError());
 }
@@ -236,5 +239,9 @@ void datagen(tq_ctx* c, int table, double sf, tq_batch* out, cudaStream_t st) {
 }  // namespace tq
 
 extern "C" tq_status tq_datagen(tq_ctx* c, int table, double sf, tq_batch* out, void* stream) {
-  return tq::guard([&] { tq::datagen(c, table, sf, out, tq::pick(c, stream)); });
+  return tq::guard([&] { tq::datagen(c, table, sf, 0, 1, out, tq::pick(c, stream)); });
+}
+extern "C" tq_status tq_datagen_shard(tq_ctx* c, int table, double sf, uint32_t shard, uint32_t nshards,
+                                      tq_batch* out, void* stream) {
+  return tq::guard([&] { tq::datagen(c, table, sf, shard, nshards, out, tq::pick(c, stream)); });
 }

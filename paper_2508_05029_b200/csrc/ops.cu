@@ -301,7 +301,10 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
 
 static void launch(tq_ctx* c, int sink, Plan& L, cudaStream_t st) {
   if (L.p.ntiles == 0) return;
+  static const char* names[] = {"pipe_count", "pipe_emit", "pipe_agg", "pipe_build"};
+  int h = prof_begin(c, names[sink], st);
   TQ_CUDA(launch_pipeline(sink, L.p, L.smem, L.grid, st));
+  prof_end(c, h, st);
   counted_launch(c);
 }
 

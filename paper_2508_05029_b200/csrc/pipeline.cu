@@ -452,7 +452,12 @@ __device__ __forceinline__ void acc_reduce(const WCtx& w, const AccSpec& as, int
   cnt = 0;
   switch (as.op) {
     case ACC_CNT: {
-      if (as.kind != K_NONE) { bool vv; (void)get_i(w, as.kind, as.idx, v, vv); valid = vv; }
+      if (as.kind != K_NONE) {
+        bool vv;
+        if (as.kind == K_COL_F64 || as.kind == K_TMP_F || as.kind == K_LIT_F) (void)get_f(w, as.kind, as.idx, v, 0, vv);
+        else (void)get_i(w, as.kind, as.idx, v, vv);
+        valid = vv;
+      }
       cnt = __popc(__ballot_sync(kFull, member && valid));
       return;
     }
@@ -672,7 +677,8 @@ __global__ void __launch_bounds__(kThreads) pipe_kernel(const __grid_constant__ 
       } else {
         // warp bases = tile offset + counts of earlier warps
         for (u32 d = threadIdx.x; d < p.ndest; d += kThreads) {
-          unsigned long long b = p.tile_offsets[(u64)d * p.ntiles + tile];
+          // dense 1:1 projection: no count phase, tile t starts at row t*kTile
+          unsigned long long b = p.tile_offsets ? p.tile_offsets[(u64)d * p.ntiles + tile] : (u64)tile * kTile;
           for (u32 ww = 0; ww < kWarps; ++ww) {
             s_base[ww * kMaxDest + d] = b;
             b += s_cnt[ww * kMaxDest + d];

@@ -15,7 +15,7 @@ from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .columnar import (MEM_DEVICE, HostBatch, TqAggC, TqBatchC, TqError, TqExprC)
+from .columnar import (MEM_DEVICE, HostBatch, TqAggC, TqBatchC, TqColumnC, TqError, TqExprC)
 from .expr import Expr
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -68,6 +68,14 @@ def lib():
         L.tq_pipeline_probe.argtypes = [V, V, B, E, E, C.c_uint32, U32, C.c_uint32, U32, C.c_uint32, B, V]
         L.tq_pipeline_build.argtypes = [V, B, E, U32, C.c_uint32, P(V), V]
         L.tq_datagen.argtypes = [V, C.c_int, C.c_double, B, V]
+        L.tq_datagen_shard.argtypes = [V, C.c_int, C.c_double, C.c_uint32, C.c_uint32, B, V]
+        L.tq_ctx_stream.restype = V
+        L.tq_ctx_stream.argtypes = [V]
+        L.tq_profile_enable.argtypes = [V, C.c_int]
+        L.tq_profile_report.restype = C.c_uint64
+        L.tq_profile_report.argtypes = [V, C.c_char_p, C.c_uint64]
+        L.tq_pinned_alloc.argtypes = [C.c_uint64, P(V)]
+        L.tq_pinned_free.argtypes = [V]
         _lib = L
     return _lib
 
@@ -93,11 +101,21 @@ def _pred(pred: Optional[Expr]):
 
 
 class DeviceBatch:
-    """A device-resident batch owned by a Context (freed on close/GC)."""
+    """A device-resident batch owned by a Context (freed on close/GC).
+    Views (`select`) borrow the parent's buffers and are never freed."""
 
-    def __init__(self, ctx: "Context", c: TqBatchC):
+    def __init__(self, ctx: "Context", c: TqBatchC, parent: "DeviceBatch" = None):
         self.ctx = ctx
         self.c = c
+        self.parent = parent
+
+    def select(self, cols: Sequence[int]) -> "DeviceBatch":
+        """Column-subset view (scan projection pushdown); no copy."""
+        arr = (TqColumnC * max(1, len(cols)))(*[self.c.cols[i] for i in cols])
+        v = TqBatchC(self.c.rows, len(cols), MEM_DEVICE, C.cast(arr, C.POINTER(TqColumnC)), None)
+        d = DeviceBatch(self.ctx, v, parent=self)
+        d._arr = arr
+        return d
 
     @property
     def rows(self) -> int:
@@ -111,6 +129,9 @@ class DeviceBatch:
         return self.ctx.download(self)
 
     def free(self):
+        if self.parent is not None:
+            self.c = None
+            return
         if self.c is not None and self.ctx.handle:
             lib().tq_batch_free(self.ctx.handle, C.byref(self.c))
             self.c = None
@@ -188,9 +209,25 @@ class Context:
         self._check(st)
         return DeviceBatch(self, out)
 
-    def datagen(self, table: int, sf: float, stream=None) -> DeviceBatch:
+    def datagen(self, table: int, sf: float, stream=None, shard: int = 0, nshards: int = 1) -> DeviceBatch:
         out = TqBatchC()
-        return self._wrap(lib().tq_datagen(self.handle, table, sf, C.byref(out), stream), out)
+        return self._wrap(lib().tq_datagen_shard(self.handle, table, sf, shard, nshards, C.byref(out), stream), out)
+
+    def stream(self):
+        return lib().tq_ctx_stream(self.handle)
+
+    def profile(self, on: bool):
+        lib().tq_profile_enable(self.handle, 1 if on else 0)
+
+    def profile_report(self) -> dict:
+        """{kernel: (launches, total_ms)} of CUDA-event-timed pipeline kernels."""
+        buf = C.create_string_buffer(1 << 16)
+        lib().tq_profile_report(self.handle, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, n, ms = line.split()
+            out[name] = (int(n), float(ms))
+        return out
 
     # ---- substrate ---------------------------------------------------------
     def take(self, b: DeviceBatch, ids: Sequence[int], stream=None) -> DeviceBatch:

@@ -38,3 +38,32 @@ def q6(ctx, lineitem, stream=None):
 
 def q1(ctx, lineitem, stream=None):
     return ctx.pipeline_aggregate(lineitem, Q1_PRED, Q1_EXPRS, Q1_KEYS, Q1_AGGS, stream)
+
+
+# Scan projection pushdown: the columns of lineitem each query reads, and the
+# same plans re-indexed over that narrower batch (what a columnar scan loads).
+Q1_SCAN = [L_RETURNFLAG, L_LINESTATUS, L_QUANTITY, L_EXTPRICE, L_DISCOUNT, L_TAX, L_SHIPDATE]
+Q6_SCAN = [L_SHIPDATE, L_QUANTITY, L_EXTPRICE, L_DISCOUNT]
+
+
+def remap(e, cols):
+    """Rewrite ColumnRef(i) -> ColumnRef(cols.index(i))."""
+    from dataclasses import replace
+    from .expr import EX_COL
+    if e.tag == EX_COL:
+        return replace(e, column=cols.index(e.column))
+    return replace(e, children=tuple(remap(c, cols) for c in e.children))
+
+
+def q1_scan(ctx, scan, stream=None, partial=False):
+    """Q1 over the pushed-down 7-column scan batch.  partial=True returns the
+    mergeable per-worker state (sums + counts) used for multi-GPU Q1."""
+    aggs = Q1_AGGS if not partial else [(AGG_SUM, 2), (AGG_SUM, 3), (AGG_SUM, 5), (AGG_SUM, 6), (AGG_SUM, 4),
+                                         (AGG_COUNT_STAR, 0)]
+    return ctx.pipeline_aggregate(scan, remap(Q1_PRED, Q1_SCAN), [remap(e, Q1_SCAN) for e in Q1_EXPRS], Q1_KEYS,
+                                  aggs, stream)
+
+
+def q6_scan(ctx, scan, stream=None):
+    return ctx.pipeline_aggregate(scan, remap(Q6_PRED, Q6_SCAN), [remap(e, Q6_SCAN) for e in Q6_EXPRS], [], Q6_AGGS,
+                                  stream)
