@@ -42,6 +42,10 @@ void* tq_ctx_stream(tq_ctx* ctx);                /* the context's own cudaStream
  * tq_profile_report writes "kernel count total_ms" lines and resets. */
 void tq_profile_enable(tq_ctx* ctx, int on);
 uint64_t tq_profile_report(tq_ctx* ctx, char* buf, uint64_t cap);
+/* Pipeline kernels are specialised per program with NVRTC (sm_100a) unless
+ * disabled here or by TQ_JIT=0; tq_jit_report writes compile/cache stats. */
+void tq_ctx_set_jit(tq_ctx* ctx, int on);
+uint64_t tq_jit_report(tq_ctx* ctx, char* buf, uint64_t cap);
 /* page-locked, portable host memory (the Host tier of SPEC.md:236-239) */
 tq_status tq_pinned_alloc(uint64_t bytes, void** out);
 void tq_pinned_free(void* p);

@@ -12,7 +12,9 @@
 #ifndef TQ_TYPES_H
 #define TQ_TYPES_H
 
+#ifndef __CUDACC_RTC__
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {

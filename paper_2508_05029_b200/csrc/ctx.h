@@ -25,6 +25,8 @@ struct tq_ctx {
   std::map<std::string, void*> prog_cache;  // program bytes -> device copy
   // optional per-kernel CUDA-event timing (tq_profile_*): events recorded on
   // the launching stream around each pipeline kernel
+  bool jit = true;                      // NVRTC-specialised pipeline kernels (jit.cu)
+  std::atomic<uint64_t> jit_launches{0};
   bool profiling = false;
   struct Ev {
     std::string name;

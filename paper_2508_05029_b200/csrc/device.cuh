@@ -3,8 +3,11 @@
 // reference common.hpp:128-136, SplitMix64 of common.hpp:139-158), and the
 // TMA bulk-copy / mbarrier primitives used to stage column tiles in smem.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
+#include "program_types.h"  // RTC builds: fixed-width integer typedefs
 
 namespace tq {
 
@@ -120,10 +123,13 @@ constexpr u64 kGamma = 0x9e3779b97f4a7c15ull;
 // k-th output of SplitMix64(seed).next(), k >= 1 (counter-based form).
 __host__ __device__ __forceinline__ u64 sm_nth(u64 seed, u64 k) { return sm_mix(seed + k * kGamma); }
 // Internal table hash (join / group tables); NOT the partition hash.
+// Multiplicative (Fibonacci) mixing per word, high bits folded down so the
+// low bits used as the slot index see every key bit.
 __device__ __forceinline__ u64 key_hash(const u64* w, int n) {
   u64 h = 0x12345678abcdefull;
-  for (int i = 0; i < n; ++i) h = sm_mix(h ^ (w[i] + kGamma));
-  return h;
+#pragma unroll
+  for (int i = 0; i < n; ++i) h = (h ^ w[i]) * kGamma;
+  return h ^ (h >> 29) ^ (h >> 47);
 }
 
 // ------------------------------------------------------------------ mbarrier + TMA bulk copy

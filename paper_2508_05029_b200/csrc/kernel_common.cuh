@@ -1,0 +1,589 @@
+// kernel_common.cuh — the staged warp-tile pipeline kernel skeleton, written
+// once against a program policy `P` and instantiated twice:
+//   * InterpP (interp.cuh, compiled into libtq_gpu.so): the generic Expr
+//     register machine interpreted per warp;
+//   * a generated policy (jit.cu): the same typed program lowered to
+//     straight-line CUDA and compiled at run time by NVRTC for sm_100a.
+//
+// Per CTA (persistent grid): thread 0 streams the referenced column slices of
+// tile t+nstages into a ring of shared-memory stages with cp.async.bulk (TMA
+// 1-D bulk copies, mbarrier complete_tx) while 8 warps process tile t (each
+// warp owns 64 rows, 2 per lane) and feed the sink:
+//   COUNT / EMIT : stable destination scatter (filter, hash_partition,
+//                  join probe) with warp ballots / match_any ranks;
+//   AGG          : per-lane private accumulators in smem for the CTA's first
+//                  groups, a global open-addressing table beyond that;
+//   BUILD        : open-addressing join-table insert (atomicCAS on the row).
+// This replaces the reference's per-row Column::*_at loops
+// (types.cpp:66-90) and take() (transform.cpp:90-120).
+#pragma once
+#include "device.cuh"
+#include "pipeline.h"
+
+namespace tq {
+
+// ------------------------------------------------------------------ per-warp context
+struct WCtx {
+  const PipeParams* p;
+  const uint8_t* stage;  // current stage base
+  const DLit* lits;      // smem copy
+  uint8_t* vslot;        // interpreter: [slot][v][32] x 16 B  (this warp)
+  u32* vvalid;           // interpreter: [slot][v]
+  u32* bslot;            // interpreter: [slot][v][2] (value, valid)
+  u32 row0;              // tile-relative first row of this warp
+  u32 nrows;             // rows in the tile
+  u32 lane;
+};
+
+__device__ __forceinline__ u32 trow(const WCtx& w, int v) { return w.row0 + (u32)v * 32u + w.lane; }
+
+// Inputs a sink reads for one row (only the used entries survive in JIT code).
+struct RowVals {
+  u64 kw[kMaxKeyWords + 1];  // key words + null word
+  i128 ai[kMaxAcc];
+  double af[kMaxAcc];
+  bool av[kMaxAcc];
+};
+
+// ------------------------------------------------------------------ join table
+__device__ __forceinline__ const long long* jt_entry(const JoinTable& t, u64 slot) {
+  return (const long long*)(t.entries + slot * t.stride);
+}
+
+template <int KW>
+__device__ __forceinline__ bool jt_key_eq(const JoinTable& t, const long long* e, const u64* kw) {
+  const u32 n = KW > 0 ? (u32)KW : t.kw;
+#pragma unroll
+  for (u32 i = 0; i < (KW > 0 ? (u32)KW : (u32)kMaxKeyWords); ++i) {
+    if (i >= n) break;
+    if ((u64)e[1 + i] != kw[i]) return false;
+  }
+  return true;
+}
+
+// Number of build rows whose keys equal kw.
+template <int KW>
+__device__ __forceinline__ u32 jt_count(const JoinTable& t, const u64* kw) {
+  const u64 mask = t.cap - 1;
+  u64 s = key_hash(kw, KW > 0 ? KW : (int)t.kw) & mask;
+  u32 n = 0;
+  for (;;) {
+    const long long* e = jt_entry(t, s);
+    if (e[0] < 0) break;
+    if (jt_key_eq<KW>(t, e, kw)) ++n;
+    s = (s + 1) & mask;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ aggregation tables
+constexpr u32 kStEmpty = 0, kStBusy = 1, kStReady = 2;
+
+// Find-or-insert `kw` (kwa words) in a state/keys open-addressing table.
+// Returns slot or -1 when `limit` probes found neither the key nor a free slot.
+template <int KWA>
+__device__ __forceinline__ long long table_find_insert(u32* state, u64* keys, u64 cap, u32 kwa_rt, const u64* kw,
+                                                       u64 h, u64 limit, unsigned long long* counter) {
+  const u32 kwa = KWA > 0 ? (u32)KWA : kwa_rt;
+  const u64 mask = cap - 1;
+  u64 s = h & mask;
+  for (u64 probe = 0; probe < limit; ++probe) {
+    volatile u32* st = state + s;
+    u32 cur = *st;
+    if (cur == kStEmpty) {
+      cur = atomicCAS(state + s, kStEmpty, kStBusy);
+      if (cur == kStEmpty) {
+        for (u32 i = 0; i < kwa; ++i) keys[s * kwa + i] = kw[i];
+        __threadfence();
+        atomicExch(state + s, kStReady);
+        if (counter) atomicAdd(counter, 1ull);
+        return (long long)s;
+      }
+    }
+    while (cur == kStBusy) cur = *st;
+    const volatile u64* k = keys + s * kwa;
+    bool eq = true;
+#pragma unroll
+    for (u32 i = 0; i < (KWA > 0 ? (u32)KWA : (u32)(kMaxKeyWords + 1)); ++i) {
+      if (i >= kwa) break;
+      eq &= k[i] == kw[i];
+    }
+    if (eq) return (long long)s;
+    s = (s + 1) & mask;
+  }
+  return -1;
+}
+
+__device__ __forceinline__ void acc_identity(uint8_t op, u64& lo, u64& hi) {
+  switch (op) {
+    case ACC_MIN_I: lo = ~0ull; hi = 0x7fffffffffffffffull; break;
+    case ACC_MAX_I: lo = 0; hi = 0x8000000000000000ull; break;
+    case ACC_MIN_F: lo = 0x7ff0000000000000ull; hi = 0; break;
+    case ACC_MAX_F: lo = 0xfff0000000000000ull; hi = 0; break;
+    default: lo = 0; hi = 0;
+  }
+}
+
+__device__ __forceinline__ void acc_apply_atomic(uint8_t op, u64* a, i128 xi, double xf, u64 cnt) {
+  switch (op) {
+    case ACC_SUM_I: if (xi != 0) atomic_add_i128(a, xi); break;
+    case ACC_SUM_F: atomicAdd((double*)a, xf); break;
+    case ACC_CNT: if (cnt) atomicAdd((unsigned long long*)a, (unsigned long long)cnt); break;
+    case ACC_MIN_I: atomic_minmax_i128((u128*)a, xi, true); break;
+    case ACC_MAX_I: atomic_minmax_i128((u128*)a, xi, false); break;
+    case ACC_MIN_F: atomic_minmax_f64((double*)a, xf, true); break;
+    case ACC_MAX_F: atomic_minmax_f64((double*)a, xf, false); break;
+  }
+}
+
+template <int KWA>
+__device__ __forceinline__ long long agg_global_slot(const PipeParams& p, const u64* kw, u32 kwa, u64 h) {
+  long long s = table_find_insert<KWA>(p.agg.state, p.agg.keys, p.agg.cap, kwa, kw, h,
+                                       p.agg.cap < 512 ? p.agg.cap : 512, p.agg.nused);
+  if (s < 0) atomicExch(p.agg.overflow, 1u);
+  return s;
+}
+
+// fnv1a64 over the LE bytes of the keys (reference common.hpp:128-136),
+// chained across key columns; a null key hashes as zero bytes.
+__device__ __forceinline__ u64 partition_hash(const PipeParams& p, const u64* kw) {
+  u64 h = kFnvBasis;
+  int pos = 0;
+  for (u32 k = 0; k < p.nkeys; ++k) {
+    const KeyOpnd& ko = p.keys[k];
+    if (ko.bytes == 16) {
+      h = fnv_bytes(h, kw[pos], 8);
+      h = fnv_bytes(h, kw[pos + 1], 8);
+    } else {
+      h = fnv_bytes(h, kw[pos], ko.bytes);
+    }
+    pos += ko.words;
+  }
+  return h;
+}
+
+// ------------------------------------------------------------------ stage loading
+__device__ __forceinline__ void issue_tile(const PipeParams& p, uint8_t* stage, uint64_t* bar, u32 tile) {
+  u64 r0 = (u64)tile * kTile;
+  u64 n = p.rows - r0;
+  bool full = n >= (u64)kTile;
+  u32 bytes = 0;
+  if (full)
+    for (u32 c = 0; c < p.nstaged; ++c)
+      if (p.cols[c].bulk_ok) bytes += kTile * p.cols[c].width + (p.cols[c].validity ? kTile / 8 : 0);
+  mbar_arrive_expect_tx(bar, bytes);
+  if (!full) return;
+  for (u32 c = 0; c < p.nstaged; ++c) {
+    const StagedCol& sc = p.cols[c];
+    if (!sc.bulk_ok) continue;
+    bulk_g2s(stage + sc.off, sc.values + r0 * sc.width, kTile * sc.width, bar);
+    if (sc.validity) bulk_g2s(stage + sc.voff, sc.validity + r0 / 8, kTile / 8, bar);
+  }
+}
+
+// Plain cooperative loads for tail tiles and misaligned columns.
+__device__ __forceinline__ void manual_tile(const PipeParams& p, uint8_t* stage, u32 tile) {
+  u64 r0 = (u64)tile * kTile;
+  u64 n = min((u64)kTile, p.rows - r0);
+  bool full = n == (u64)kTile;
+  for (u32 c = 0; c < p.nstaged; ++c) {
+    const StagedCol& sc = p.cols[c];
+    if (full && sc.bulk_ok) continue;
+    u64 bytes = n * sc.width;
+    const uint8_t* src = sc.values + r0 * sc.width;
+    for (u64 i = threadIdx.x; i < bytes; i += kThreads) stage[sc.off + i] = src[i];
+    if (sc.validity) {
+      u64 vb = (n + 7) / 8;
+      for (u64 i = threadIdx.x; i < kTile / 8; i += kThreads) stage[sc.voff + i] = i < vb ? sc.validity[r0 / 8 + i] : 0;
+    }
+  }
+}
+
+__device__ __forceinline__ bool tile_needs_manual(const PipeParams& p, u32 tile) {
+  u64 r0 = (u64)tile * kTile;
+  if (p.rows - r0 < (u64)kTile) return true;
+  for (u32 c = 0; c < p.nstaged; ++c)
+    if (!p.cols[c].bulk_ok) return true;
+  return false;
+}
+
+// ------------------------------------------------------------------ the kernel body
+template <int SINK, class P>
+__device__ __forceinline__ void pipe_body(const PipeParams& p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  DInstr* s_code = (DInstr*)(smem + p.off_code);
+  DLit* s_lits = (DLit*)(smem + p.off_lits);
+  uint64_t* bars = (uint64_t*)(smem + p.off_bar);
+  const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int KWA = P::kKwa;  // > 0 when known at compile time
+
+  if (P::kInterp) {
+    for (u32 i = threadIdx.x; i < p.ncode; i += kThreads) s_code[i] = p.code[i];
+    for (u32 i = threadIdx.x; i < p.nlits; i += kThreads) s_lits[i] = p.lits[i];
+  }
+  if (threadIdx.x == 0) {
+    for (u32 s = 0; s < p.nstages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+
+  // sink shared state
+  u32* s_cnt = (u32*)(smem + p.off_sink);                                          // [kWarps][kMaxDest]
+  unsigned long long* s_base = (unsigned long long*)(s_cnt + kWarps * kMaxDest);  // [kWarps][kMaxDest]
+  const u32 kwa = KWA > 0 ? (u32)KWA : p.key_words + 1;
+  const u32 G = p.local_groups;
+  const u32 nacc = P::nacc(p);
+  const u32 nplanes = P::nplanes(p);
+  // AGG smem: [state G u32][keys G*kwa u64][gslot G i64][planes G*nplanes*kThreads u64]
+  u32* l_state = (u32*)(smem + p.off_sink);
+  u64* l_keys = (u64*)(smem + p.off_sink + ((G * 4 + 15) & ~15u));
+  long long* l_gslot = (long long*)(l_keys + (u64)G * kwa);
+  u64* l_planes = (u64*)(l_gslot + G);
+  if (SINK == SINK_COUNT || SINK == SINK_EMIT) {
+    for (u32 i = threadIdx.x; i < kWarps * kMaxDest; i += kThreads) s_cnt[i] = 0;
+  }
+  if (SINK == SINK_AGG) {
+    for (u32 i = threadIdx.x; i < G; i += kThreads) l_state[i] = kStEmpty;
+#pragma unroll
+    for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
+      if (a >= nacc) break;
+      const uint8_t op = P::acc_op(p, a);
+      u64 lo, hi;
+      acc_identity(op, lo, hi);
+      const u32 np = (op == ACC_MIN_I || op == ACC_MAX_I) ? 2 : 1;
+      for (u32 g = 0; g < G; ++g)
+        for (u32 q = 0; q < np; ++q)
+          l_planes[((u64)g * nplanes + P::acc_plane(p, a) + q) * kThreads + threadIdx.x] = q ? hi : lo;
+    }
+  }
+  __syncthreads();
+
+  WCtx w;
+  w.p = &p;
+  w.lits = P::kInterp ? s_lits : p.lits;
+  w.vslot = smem + p.off_vslot + (size_t)warp * p.nvslots * kV * 32 * 16;
+  w.vvalid = (u32*)(smem + p.off_vvalid) + (size_t)warp * p.nvslots * kV;
+  w.bslot = (u32*)(smem + p.off_bslot) + (size_t)warp * p.nbslots * kV * 2;
+  w.row0 = warp * 32 * kV;
+  w.lane = lane;
+
+  const u32 first = blockIdx.x, step = gridDim.x;
+  if (threadIdx.x == 0) {
+    for (u32 s = 0; s < p.nstages; ++s) {
+      u32 t = first + s * step;
+      if (t < p.ntiles) issue_tile(p, smem + p.off_stage + s * p.stage_bytes, &bars[s], t);
+    }
+  }
+
+  u32 k = 0;
+  for (u32 tile = first; tile < p.ntiles; tile += step, ++k) {
+    const u32 s = k % p.nstages;
+    uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
+    mbar_wait(&bars[s], (k / p.nstages) & 1);
+    if (tile_needs_manual(p, tile)) {
+      manual_tile(p, stage, tile);
+      __syncthreads();
+    }
+    const u64 r0 = (u64)tile * kTile;
+    w.stage = stage;
+    w.nrows = (u32)min((u64)kTile, p.rows - r0);
+
+    // ---- predicate per row, then the rest of the program
+    u32 pm[kV];
+    u32 any = P::tile_begin(w, s_code, pm);
+
+    if (SINK == SINK_COUNT || SINK == SINK_EMIT) {
+      u32 dest[kV];
+      u32 mult[kV];
+#pragma unroll
+      for (int v = 0; v < kV; ++v) {
+        bool pass = (pm[v] >> lane) & 1u;
+        dest[v] = 0;
+        mult[v] = pass ? 1u : 0u;
+        if (pass && p.dest_kind != DEST_FILTER) {
+          u64 kw[kMaxKeyWords + 1];
+          bool has_null = P::keys(w, v, kw);
+          if (p.dest_kind == DEST_PARTITION) dest[v] = (u32)(partition_hash(p, kw) % p.ndest);
+          else mult[v] = has_null ? 0u : jt_count<P::kKw>(p.jt, kw);  // null keys never match
+        }
+      }
+      if (p.dest_kind == DEST_PROBE) {
+        u32 tot = 0;
+#pragma unroll
+        for (int v = 0; v < kV; ++v) tot += mult[v];
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) tot += __shfl_xor_sync(kFull, tot, m);
+        if (lane == 0) s_cnt[warp * kMaxDest] = tot;
+      } else {
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          bool pass = mult[v] != 0;
+          u32 peers = __match_any_sync(kFull, pass ? dest[v] : 0xffffffffu);
+          if (pass && (peers & lanemask_lt()) == 0) s_cnt[warp * kMaxDest + dest[v]] += __popc(peers);
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (SINK == SINK_COUNT) {
+        for (u32 d = threadIdx.x; d < p.ndest; d += kThreads) {
+          u32 t = 0;
+          for (u32 ww = 0; ww < kWarps; ++ww) {
+            t += s_cnt[ww * kMaxDest + d];
+            s_cnt[ww * kMaxDest + d] = 0;
+          }
+          p.tile_counts[(u64)d * p.ntiles + tile] = t;
+        }
+      } else {
+        // warp bases = tile offset + counts of earlier warps
+        for (u32 d = threadIdx.x; d < p.ndest; d += kThreads) {
+          // dense 1:1 projection: no count phase, tile t starts at row t*kTile
+          unsigned long long b = p.tile_offsets ? p.tile_offsets[(u64)d * p.ntiles + tile] : (u64)tile * kTile;
+          for (u32 ww = 0; ww < kWarps; ++ww) {
+            s_base[ww * kMaxDest + d] = b;
+            b += s_cnt[ww * kMaxDest + d];
+            s_cnt[ww * kMaxDest + d] = 0;
+          }
+        }
+        __syncthreads();
+        unsigned long long* wb = s_base + warp * kMaxDest;
+        if (p.dest_kind == DEST_PROBE) {
+#pragma unroll
+          for (int v = 0; v < kV; ++v) {
+            u32 m = mult[v];
+            u32 incl = m;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              u32 y = __shfl_up_sync(kFull, incl, o);
+              if (lane >= (u32)o) incl += y;
+            }
+            u32 total = __shfl_sync(kFull, incl, 31);
+            unsigned long long pos = wb[0] + (incl - m);
+            __syncwarp();
+            if (lane == 0) wb[0] += total;
+            __syncwarp();
+            if (m) {
+              u64 kw[kMaxKeyWords + 1];
+              P::keys(w, v, kw);
+              const JoinTable& t = p.jt;
+              const u64 mask = t.cap - 1;
+              u64 sl = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw) & mask;
+              for (;;) {
+                const long long* e = jt_entry(t, sl);
+                long long brow = e[0];
+                if (brow < 0) break;
+                if (jt_key_eq<P::kKw>(t, e, kw)) {
+                  P::store(w, v, pos, brow);
+                  ++pos;
+                }
+                sl = (sl + 1) & mask;
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < kV; ++v) {
+            bool pass = mult[v] != 0;
+            u32 peers = __match_any_sync(kFull, pass ? dest[v] : 0xffffffffu);
+            unsigned long long pos = 0;
+            if (pass) pos = wb[dest[v]] + __popc(peers & lanemask_lt());
+            __syncwarp();
+            if (pass && (peers & lanemask_lt()) == 0) wb[dest[v]] += __popc(peers);
+            __syncwarp();
+            if (pass) P::store(w, v, pos, -1);
+          }
+        }
+      }
+    } else if (SINK == SINK_BUILD) {
+      if (any) {
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          bool pass = (pm[v] >> lane) & 1u;
+          if (!pass) continue;
+          u64 kw[kMaxKeyWords + 1];
+          if (P::keys(w, v, kw)) continue;  // null keys never match
+          const JoinTable& t = p.jt;
+          const u64 mask = t.cap - 1;
+          u64 sl = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw) & mask;
+          long long row = (long long)(p.row_base + r0 + trow(w, v));
+          for (;;) {
+            long long* e = (long long*)(t.entries + sl * t.stride);
+            if (atomicCAS((unsigned long long*)e, (unsigned long long)-1ll, (unsigned long long)row) ==
+                (unsigned long long)-1ll) {
+#pragma unroll
+              for (u32 i = 0; i < (P::kKw > 0 ? (u32)P::kKw : (u32)kMaxKeyWords); ++i) {
+                if (i >= t.kw) break;
+                e[1 + i] = (long long)kw[i];
+              }
+              break;
+            }
+            sl = (sl + 1) & mask;
+          }
+        }
+      }
+    } else if (SINK == SINK_AGG) {
+      if (any) {
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          bool pass = (pm[v] >> lane) & 1u;
+          if (!pass) continue;
+          RowVals x;
+          P::keys(w, v, x.kw);
+          P::accs(w, v, x);
+          const u64 h = key_hash(x.kw, (int)kwa);
+          long long ls = G ? table_find_insert<KWA>(l_state, l_keys, G, kwa, x.kw, h, G, nullptr) : -1;
+          if (ls >= 0) {
+            // per-lane private accumulation (no atomics, no cross-lane traffic)
+#pragma unroll
+            for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
+              if (a >= nacc) break;
+              const uint8_t op = P::acc_op(p, a);
+              if (!x.av[a]) continue;
+              u64* pl = l_planes + ((u64)ls * nplanes + P::acc_plane(p, a)) * kThreads + threadIdx.x;
+              switch (op) {
+                case ACC_CNT: pl[0] += 1; break;
+                case ACC_SUM_I: {
+                  const i128 xi = x.ai[a];
+                  long long cur = (long long)pl[0];
+                  if (fits64(xi)) {
+                    long long y = (long long)lo64(xi);
+                    long long r = (long long)((u64)cur + (u64)y);
+                    if (((cur ^ r) & (y ^ r)) >= 0) {
+                      pl[0] = (u64)r;
+                      break;
+                    }
+                  }
+                  // escape: the exact int128 partial goes straight to the global table
+                  long long gs = agg_global_slot<KWA>(p, x.kw, kwa, h);
+                  if (gs >= 0) atomic_add_i128(p.agg.acc + ((u64)gs * nacc + a) * 2, add128((i128)cur, xi));
+                  pl[0] = 0;
+                  break;
+                }
+                case ACC_SUM_F:
+                  pl[0] = (u64)__double_as_longlong(__longlong_as_double((long long)pl[0]) + x.af[a]);
+                  break;
+                case ACC_MIN_I:
+                case ACC_MAX_I: {
+                  i128 c = mk128(pl[0], pl[kThreads]);
+                  if (op == ACC_MIN_I ? x.ai[a] < c : x.ai[a] > c) {
+                    pl[0] = lo64(x.ai[a]);
+                    pl[kThreads] = hi64(x.ai[a]);
+                  }
+                  break;
+                }
+                default: {
+                  double c = __longlong_as_double((long long)pl[0]);
+                  if (op == ACC_MIN_F ? x.af[a] < c : x.af[a] > c) pl[0] = (u64)__double_as_longlong(x.af[a]);
+                }
+              }
+            }
+          } else {
+            // local table full: this group lives only in the global table
+            long long gs = agg_global_slot<KWA>(p, x.kw, kwa, h);
+            if (gs < 0) continue;
+#pragma unroll
+            for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
+              if (a >= nacc) break;
+              if (!x.av[a]) continue;
+              acc_apply_atomic(P::acc_op(p, a), p.agg.acc + ((u64)gs * nacc + a) * 2, x.ai[a], x.af[a], 1);
+            }
+          }
+        }
+      }
+    }
+
+    __syncthreads();  // stage s fully consumed
+    if (threadIdx.x == 0) {
+      u32 nt = tile + p.nstages * step;
+      if (nt < p.ntiles) {
+        fence_proxy_async();
+        issue_tile(p, stage, &bars[s], nt);
+      }
+    }
+  }
+
+  if (SINK == SINK_AGG && G > 0) {
+    __syncthreads();
+    // 1) global slot of every local group
+    for (u32 g = warp; g < G; g += kWarps) {
+      if (lane == 0) {
+        long long gs = -1;
+        if (l_state[g] == kStReady) {
+          u64 kw[kMaxKeyWords + 1];
+          for (u32 i = 0; i < kwa; ++i) kw[i] = l_keys[(u64)g * kwa + i];
+          gs = agg_global_slot<KWA>(p, kw, kwa, key_hash(kw, (int)kwa));
+        }
+        l_gslot[g] = gs;
+      }
+    }
+    __syncthreads();
+    // 2) reduce the per-lane planes of each (group, accumulator) and apply once
+    for (u32 q = warp; q < G * nacc; q += kWarps) {
+      const u32 g = q / nacc, a = q % nacc;
+      const long long gs = l_gslot[g];
+      if (gs < 0) continue;
+      const uint8_t op = P::acc_op(p, a);
+      const u64* pl = l_planes + ((u64)g * nplanes + P::acc_plane(p, a)) * kThreads;
+      i128 xi = 0;
+      double xf = 0;
+      u64 cnt = 0;
+      switch (op) {
+        case ACC_CNT:
+          for (u32 t = lane; t < kThreads; t += 32) cnt += pl[t];
+          for (int m = 16; m > 0; m >>= 1) cnt += __shfl_xor_sync(kFull, cnt, m);
+          break;
+        case ACC_SUM_I:
+          for (u32 t = lane; t < kThreads; t += 32) xi = add128(xi, (i128)(long long)pl[t]);
+          xi = warp_sum_i128(xi);
+          break;
+        case ACC_SUM_F:
+          for (u32 t = lane; t < kThreads; t += 32) xf += __longlong_as_double((long long)pl[t]);
+          xf = warp_sum_f64(xf);
+          break;
+        case ACC_MIN_I:
+        case ACC_MAX_I: {
+          bool mn = op == ACC_MIN_I;
+          u64 lo, hi;
+          acc_identity(op, lo, hi);
+          xi = mk128(lo, hi);
+          for (u32 t = lane; t < kThreads; t += 32) {
+            i128 y = mk128(pl[t], pl[kThreads + t]);
+            xi = mn ? (y < xi ? y : xi) : (y > xi ? y : xi);
+          }
+          for (int m = 16; m > 0; m >>= 1) {
+            i128 o = shfl_xor_i128(xi, m);
+            xi = mn ? (o < xi ? o : xi) : (o > xi ? o : xi);
+          }
+          break;
+        }
+        default: {
+          bool mn = op == ACC_MIN_F;
+          xf = __longlong_as_double((long long)pl[lane]);
+          for (u32 t = lane + 32; t < kThreads; t += 32) {
+            double y = __longlong_as_double((long long)pl[t]);
+            xf = mn ? fmin(xf, y) : fmax(xf, y);
+          }
+          for (int m = 16; m > 0; m >>= 1) {
+            double o = __shfl_xor_sync(kFull, xf, m);
+            xf = mn ? fmin(xf, o) : fmax(xf, o);
+          }
+        }
+      }
+      if (lane == 0) acc_apply_atomic(op, p.agg.acc + ((u64)gs * nacc + a) * 2, xi, xf, cnt);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ output stores
+__device__ __forceinline__ void set_valid(const OutCol& o, u64 pos, bool valid) {
+  if (o.validity && valid) bm_set_atomic(o.validity, pos);
+}
+
+// Copy a build-side value (probe output) by build row id.
+__device__ __forceinline__ void store_build(const OutCol& o, u64 pos, long long brow) {
+  const uint8_t* src = o.bvalues + (u64)brow * o.width;
+  if (o.width == 16) *(ulonglong2*)(o.values + pos * 16) = *(const ulonglong2*)src;
+  else if (o.width == 8) *(u64*)(o.values + pos * 8) = *(const u64*)src;
+  else o.values[pos] = *src;
+  set_valid(o, pos, !o.bvalidity || bm_get(o.bvalidity, (u64)brow));
+}
+
+}  // namespace tq

@@ -10,6 +10,7 @@
 #include "ctx.h"
 #include "device.cuh"
 #include "pipeline.h"
+#include "program.h"
 
 struct tq_join_table {
   tq_ctx* ctx;
@@ -22,7 +23,8 @@ struct tq_join_table {
 
 namespace tq {
 
-cudaError_t launch_pipeline(int sink, const PipeParams& p, u32 smem_bytes, u32 grid, cudaStream_t st);
+cudaError_t launch_pipeline_prog(tq_ctx* c, int sink, const PipeParams& p, u32 smem, u32 grid, cudaStream_t st,
+                                 const std::vector<DInstr>& code, const std::vector<DLit>& lits);
 
 // ================================================================== scan
 constexpr int kScanItems = 8;
@@ -299,11 +301,11 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
   (void)st;
 }
 
-static void launch(tq_ctx* c, int sink, Plan& L, cudaStream_t st) {
+static void launch(tq_ctx* c, int sink, Plan& L, const Prog& P, cudaStream_t st) {
   if (L.p.ntiles == 0) return;
   static const char* names[] = {"pipe_count", "pipe_emit", "pipe_agg", "pipe_build"};
   int h = prof_begin(c, names[sink], st);
-  TQ_CUDA(launch_pipeline(sink, L.p, L.smem, L.grid, st));
+  TQ_CUDA(launch_pipeline_prog(c, sink, L.p, L.smem, L.grid, st, P.pb.code(), P.pb.lits()));
   prof_end(c, h, st);
   counted_launch(c);
 }
@@ -410,7 +412,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     counts = (u32*)dalloc(c, ncnt * 4, st);
     offsets = (u64*)dalloc(c, (ncnt + 1) * 8, st);
     p.tile_counts = counts;
-    launch(c, SINK_COUNT, L, st);
+    launch(c, SINK_COUNT, L, P, st);
     scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
     {
       std::lock_guard<std::mutex> g(c->mu);
@@ -446,7 +448,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     outs[i].validity = out->cols[i].validity;
     p.out[i] = outs[i];
   }
-  if (total > 0) launch(c, SINK_EMIT, L, st);
+  if (total > 0) launch(c, SINK_EMIT, L, P, st);
   if (counts) dfree(c, counts, ncnt * 4, st);
   if (offsets) dfree(c, offsets, (ncnt + 1) * 8, st);
 }
@@ -495,7 +497,7 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   std::memcpy(t->build.cols, in->cols, sizeof(tq_column) * in->ncols);
   p.jt = t->jt;
   p.row_base = 0;
-  launch(c, SINK_BUILD, L, st);
+  launch(c, SINK_BUILD, L, P, st);
   *out = t;
 }
 
@@ -682,19 +684,37 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
     kh.push_back(P.outs[keys[k]]);
   }
   const u32 nacc = (u32)acc.size();
-  // local (per-CTA) group table sized to the shared-memory budget
+  // local (per-CTA) group table: per-lane private accumulator planes (8 B;
+  // MIN/MAX of int128 take two) sized to the shared memory left after two stages
   u32 kwa_guess = 1;
   for (int h : kh) kwa_guess += P.pb.root(h).cls == C_D ? 2 : 1;
-  u32 G = 64;
-  auto sink_bytes = [&](u32 g) { return align_up(g * 4, 16) + g * kwa_guess * 8 + kWarps * g * nacc * 16; };
-  while (G > 4 && sink_bytes(G) > 48 * 1024) G >>= 1;
+  u32 nplanes = 0;
+  uint8_t planes[kMaxAcc] = {};
+  for (u32 i = 0; i < nacc; ++i) {
+    planes[i] = (uint8_t)nplanes;
+    nplanes += (acc[i].op == ACC_MIN_I || acc[i].op == ACC_MAX_I) ? 2 : 1;
+  }
+  auto sink_bytes = [&](u32 g) {
+    return align_up(g * 4, 16) + g * kwa_guess * 8 + g * 8 + g * std::max<u32>(1, nplanes) * kThreads * 8;
+  };
+  u32 G = 0;
+  {
+    Plan probe;
+    plan_launch(c, in, P, probe, 0, st);
+    u32 fixed = probe.smem - probe.p.nstages * probe.p.stage_bytes;  // everything but the stages
+    u32 avail = 227 * 1024 - fixed - 2 * probe.p.stage_bytes - 1024;
+    G = 64;
+    while (G > 1 && sink_bytes(G) > avail) G >>= 1;
+    if (sink_bytes(G) > avail) G = 0;
+  }
   Plan L;
-  plan_launch(c, in, P, L, sink_bytes(G), st);
+  plan_launch(c, in, P, L, G ? sink_bytes(G) : 64, st);
   PipeParams& p = L.p;
   set_keys(p, P.pb, kh);
   const u32 kwa = p.key_words + 1;
   p.nacc = nacc;
-  for (u32 i = 0; i < nacc; ++i) p.acc[i] = acc[i];
+  for (u32 i = 0; i < nacc; ++i) { p.acc[i] = acc[i]; p.acc_plane[i] = planes[i]; }
+  p.nplanes = std::max<u32>(1, nplanes);
   p.local_groups = G;
 
   // ---- global table; grows x4 and re-runs on overflow (on_oom-style retry)
@@ -726,7 +746,7 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
     counted_launch(c);
     TQ_CUDA(cudaGetLastError());
     p.agg = t;
-    launch(c, SINK_AGG, L, st);
+    launch(c, SINK_AGG, L, P, st);
     uint32_t ovf = 0;
     {
       std::lock_guard<std::mutex> g(c->mu);

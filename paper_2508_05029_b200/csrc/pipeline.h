@@ -12,9 +12,8 @@
 //              AGG    warp-aggregated hash group-by into a global table
 //              BUILD  join build: open-addressing insert of (key, row)
 #pragma once
-#include <cstdint>
-
-#include "program.h"
+#include "program_types.h"
+#include "tq_types.h"
 
 namespace tq {
 
@@ -125,6 +124,8 @@ struct PipeParams {
   // aggregate
   uint32_t nacc;
   uint32_t local_groups;  // per-CTA smem table slots (power of two, 0 = none)
+  uint32_t nplanes;       // 8-byte per-lane accumulator planes per local group
+  uint8_t acc_plane[kMaxAcc];
   AccSpec acc[kMaxAcc];
   AggTable agg;
 };

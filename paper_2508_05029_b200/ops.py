@@ -76,6 +76,9 @@ def lib():
         L.tq_profile_report.argtypes = [V, C.c_char_p, C.c_uint64]
         L.tq_pinned_alloc.argtypes = [C.c_uint64, P(V)]
         L.tq_pinned_free.argtypes = [V]
+        L.tq_ctx_set_jit.argtypes = [V, C.c_int]
+        L.tq_jit_report.restype = C.c_uint64
+        L.tq_jit_report.argtypes = [V, C.c_char_p, C.c_uint64]
         _lib = L
     return _lib
 
@@ -212,6 +215,19 @@ class Context:
     def datagen(self, table: int, sf: float, stream=None, shard: int = 0, nshards: int = 1) -> DeviceBatch:
         out = TqBatchC()
         return self._wrap(lib().tq_datagen_shard(self.handle, table, sf, shard, nshards, C.byref(out), stream), out)
+
+    def set_jit(self, on: bool):
+        """NVRTC-specialised pipeline kernels (default) vs the AOT interpreter."""
+        lib().tq_ctx_set_jit(self.handle, 1 if on else 0)
+
+    def jit_report(self) -> dict:
+        buf = C.create_string_buffer(4096)
+        lib().tq_jit_report(self.handle, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            k, _, v = line.partition(" ")
+            out[k] = v
+        return out
 
     def stream(self):
         return lib().tq_ctx_stream(self.handle)

@@ -16,11 +16,18 @@ pytestmark = pytest.mark.gpu
 AGG_SUM, AGG_COUNT, AGG_COUNT_STAR, AGG_MIN, AGG_MAX, AGG_AVG = range(6)
 
 
-@pytest.fixture(scope="module")
-def ctx():
+@pytest.fixture(scope="module", params=["jit", "interp"])
+def ctx(request):
+    """Every parity test runs twice: NVRTC-specialised kernels and the AOT
+    interpreter kernels (the same skeleton, two program policies)."""
     from paper_2508_05029_b200.ops import Context
     c = Context(0)
+    c.set_jit(request.param == "jit")
     yield c
+    if request.param == "jit":
+        rep = c.jit_report()
+        assert int(rep["failed"]) == 0, rep
+        assert int(rep["jit_launches"]) > 0, rep
     c.close()
 
 
@@ -159,3 +166,18 @@ def test_invalid_plan_errors(ctx):
     with pytest.raises(TqError) as e:
         ctx.filter_execute(b, Col(0) + 1)  # non-bool predicate
     assert e.value.errc == "InvalidPlan"
+
+
+@pytest.mark.parametrize("q", ["q1", "q6"])
+def test_query_pipelines(ctx, q):
+    """Fused Filter->Project->Aggregate pipelines vs the
+    oracle's operator-by-operator DAG, full-width and scan-pushed-down."""
+    from paper_2508_05029_b200 import queries
+    sf = 0.05
+    li = ctx.datagen(O.T_LINEITEM, sf)
+    want = O.query(int(q[1]), {O.T_LINEITEM: O.datagen(O.T_LINEITEM, sf)}, 4)
+    full = getattr(queries, q)(ctx, li).to_host()
+    assert_batches_equal(full, want)
+    scan = li.select(queries.Q1_SCAN if q == "q1" else queries.Q6_SCAN)
+    pushed = getattr(queries, q + "_scan")(ctx, scan).to_host()
+    assert_batches_equal(pushed, want)
