@@ -416,7 +416,7 @@ struct Gen {
       os << "    (void)r; (void)p; (void)pos; (void)brow;\n";
     }
     os << "  }\n};\n}  // namespace tq\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(tq::kThreads) tq_jit_main(const __grid_constant__ "
+    os << "extern \"C\" __global__ void __launch_bounds__(tq::kBlock) tq_jit_main(const __grid_constant__ "
           "tq::PipeParams p) {\n  tq::pipe_body<"
        << sink << ", tq::Gen>(p);\n}\n";
     return os.str();
@@ -515,7 +515,7 @@ cudaError_t launch_pipeline_prog(tq_ctx* c, int sink, const PipeParams& p, u32 s
         if (err != cudaSuccess) return err;
         PipeParams pp = p;
         void* args[] = {&pp};
-        err = cudaLaunchKernel((const void*)e.kern, dim3(grid), dim3(kThreads), args, smem, st);
+        err = cudaLaunchKernel((const void*)e.kern, dim3(grid), dim3(kBlock), args, smem, st);
         if (err == cudaSuccess) c->jit_launches.fetch_add(1);
         return err;
       }

@@ -181,8 +181,8 @@ __device__ __forceinline__ void issue_tile(const PipeParams& p, uint8_t* stage, 
   }
 }
 
-// Plain cooperative loads for tail tiles and misaligned columns.
-__device__ __forceinline__ void manual_tile(const PipeParams& p, uint8_t* stage, u32 tile) {
+// Plain loads (by the producer warp) for tail tiles and misaligned columns.
+__device__ __forceinline__ void manual_tile(const PipeParams& p, uint8_t* stage, u32 tile, u32 lane) {
   u64 r0 = (u64)tile * kTile;
   u64 n = min((u64)kTile, p.rows - r0);
   bool full = n == (u64)kTile;
@@ -191,21 +191,41 @@ __device__ __forceinline__ void manual_tile(const PipeParams& p, uint8_t* stage,
     if (full && sc.bulk_ok) continue;
     u64 bytes = n * sc.width;
     const uint8_t* src = sc.values + r0 * sc.width;
-    for (u64 i = threadIdx.x; i < bytes; i += kThreads) stage[sc.off + i] = src[i];
+    for (u64 i = lane; i < bytes; i += 32) stage[sc.off + i] = src[i];
     if (sc.validity) {
       u64 vb = (n + 7) / 8;
-      for (u64 i = threadIdx.x; i < kTile / 8; i += kThreads) stage[sc.voff + i] = i < vb ? sc.validity[r0 / 8 + i] : 0;
+      for (u64 i = lane; i < kTile / 8; i += 32) stage[sc.voff + i] = i < vb ? sc.validity[r0 / 8 + i] : 0;
     }
   }
 }
 
 __device__ __forceinline__ bool tile_needs_manual(const PipeParams& p, u32 tile) {
-  u64 r0 = (u64)tile * kTile;
-  if (p.rows - r0 < (u64)kTile) return true;
-  for (u32 c = 0; c < p.nstaged; ++c)
-    if (!p.cols[c].bulk_ok) return true;
-  return false;
+  return !p.all_bulk || p.rows - (u64)tile * kTile < (u64)kTile;
 }
+
+// Producer warp: keeps `nstages` tiles in flight.  Stage s is refilled once
+// every consumer warp has arrived on empty[s].
+__device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                                        u32 lane) {
+  u32 k = 0;
+  for (u32 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++k) {
+    const u32 s = k % p.nstages;
+    if (k >= p.nstages) mbar_wait(&empty[s], ((k / p.nstages) - 1) & 1);
+    uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
+    if (tile_needs_manual(p, tile)) {
+      manual_tile(p, stage, tile, lane);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      fence_proxy_async();
+      issue_tile(p, stage, &full[s], tile);
+    }
+    __syncwarp();
+  }
+}
+
+// named barrier over the consumer warps only
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
 
 // ------------------------------------------------------------------ the kernel body
 template <int SINK, class P>
@@ -213,16 +233,20 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   extern __shared__ __align__(128) uint8_t smem[];
   DInstr* s_code = (DInstr*)(smem + p.off_code);
   DLit* s_lits = (DLit*)(smem + p.off_lits);
-  uint64_t* bars = (uint64_t*)(smem + p.off_bar);
+  uint64_t* full = (uint64_t*)(smem + p.off_bar);
+  uint64_t* empty = full + kMaxStages;
   const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int KWA = P::kKwa;  // > 0 when known at compile time
 
   if (P::kInterp) {
-    for (u32 i = threadIdx.x; i < p.ncode; i += kThreads) s_code[i] = p.code[i];
-    for (u32 i = threadIdx.x; i < p.nlits; i += kThreads) s_lits[i] = p.lits[i];
+    for (u32 i = threadIdx.x; i < p.ncode; i += kBlock) s_code[i] = p.code[i];
+    for (u32 i = threadIdx.x; i < p.nlits; i += kBlock) s_lits[i] = p.lits[i];
   }
   if (threadIdx.x == 0) {
-    for (u32 s = 0; s < p.nstages; ++s) mbar_init(&bars[s], 1);
+    for (u32 s = 0; s < p.nstages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
     fence_mbar_init();
   }
 
@@ -241,7 +265,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   if (SINK == SINK_COUNT || SINK == SINK_EMIT) {
     for (u32 i = threadIdx.x; i < kWarps * kMaxDest; i += kThreads) s_cnt[i] = 0;
   }
-  if (SINK == SINK_AGG) {
+  if (SINK == SINK_AGG && threadIdx.x < kThreads) {
     for (u32 i = threadIdx.x; i < G; i += kThreads) l_state[i] = kStEmpty;
 #pragma unroll
     for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
@@ -256,6 +280,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     }
   }
   __syncthreads();
+  if (warp == kWarps) {  // producer warp
+    produce(p, smem, full, empty, lane);
+    return;
+  }
 
   WCtx w;
   w.p = &p;
@@ -267,22 +295,11 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   w.lane = lane;
 
   const u32 first = blockIdx.x, step = gridDim.x;
-  if (threadIdx.x == 0) {
-    for (u32 s = 0; s < p.nstages; ++s) {
-      u32 t = first + s * step;
-      if (t < p.ntiles) issue_tile(p, smem + p.off_stage + s * p.stage_bytes, &bars[s], t);
-    }
-  }
-
   u32 k = 0;
   for (u32 tile = first; tile < p.ntiles; tile += step, ++k) {
     const u32 s = k % p.nstages;
     uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
-    mbar_wait(&bars[s], (k / p.nstages) & 1);
-    if (tile_needs_manual(p, tile)) {
-      manual_tile(p, stage, tile);
-      __syncthreads();
-    }
+    mbar_wait(&full[s], (k / p.nstages) & 1);
     const u64 r0 = (u64)tile * kTile;
     w.stage = stage;
     w.nrows = (u32)min((u64)kTile, p.rows - r0);
@@ -322,7 +339,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           __syncwarp();
         }
       }
-      __syncthreads();
+      consumers_sync();
       if (SINK == SINK_COUNT) {
         for (u32 d = threadIdx.x; d < p.ndest; d += kThreads) {
           u32 t = 0;
@@ -343,7 +360,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
             s_cnt[ww * kMaxDest + d] = 0;
           }
         }
-        __syncthreads();
+        consumers_sync();
         unsigned long long* wb = s_base + warp * kMaxDest;
         if (p.dest_kind == DEST_PROBE) {
 #pragma unroll
@@ -490,18 +507,14 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       }
     }
 
-    __syncthreads();  // stage s fully consumed
-    if (threadIdx.x == 0) {
-      u32 nt = tile + p.nstages * step;
-      if (nt < p.ntiles) {
-        fence_proxy_async();
-        issue_tile(p, stage, &bars[s], nt);
-      }
-    }
+    // stage s consumed by this warp
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (SINK == SINK_COUNT || SINK == SINK_EMIT) consumers_sync();  // s_cnt reuse across tiles
   }
 
   if (SINK == SINK_AGG && G > 0) {
-    __syncthreads();
+    consumers_sync();
     // 1) global slot of every local group
     for (u32 g = warp; g < G; g += kWarps) {
       if (lane == 0) {
@@ -514,7 +527,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         l_gslot[g] = gs;
       }
     }
-    __syncthreads();
+    consumers_sync();
     // 2) reduce the per-lane planes of each (group, accumulator) and apply once
     for (u32 q = warp; q < G * nacc; q += kWarps) {
       const u32 g = q / nacc, a = q % nacc;

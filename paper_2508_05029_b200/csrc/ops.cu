@@ -266,6 +266,8 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
     }
   }
   p.stage_bytes = align_up(std::max(off, 128u), 128);
+  p.all_bulk = 1;
+  for (u32 i = 0; i < p.nstaged; ++i) p.all_bulk &= p.cols[i].bulk_ok;
   // fixed regions
   u32 o = 0;
   p.off_code = o;
@@ -281,7 +283,7 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
   p.off_sink = o;
   o += align_up(sink_bytes, 128);
   p.off_bar = o;
-  o += 64;
+  o += 2 * kMaxStages * 8;
   o = align_up(o, 128);
   const u32 kSmemMax = 227 * 1024;
   if (o + p.stage_bytes > kSmemMax) fail(TQ_INVALID_PLAN, "batch too wide for one pipeline tile");

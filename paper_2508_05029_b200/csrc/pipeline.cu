@@ -7,7 +7,7 @@
 namespace tq {
 
 template <int SINK>
-__global__ void __launch_bounds__(kThreads) pipe_kernel(const __grid_constant__ PipeParams p) {
+__global__ void __launch_bounds__(kBlock) pipe_kernel(const __grid_constant__ PipeParams p) {
   pipe_body<SINK, InterpP>(p);
 }
 
@@ -26,7 +26,7 @@ cudaError_t launch_interp(int sink, const PipeParams& p, u32 smem_bytes, u32 gri
   }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
   if (e != cudaSuccess) return e;
-  fn<<<grid, kThreads, smem_bytes, st>>>(p);
+  fn<<<grid, kBlock, smem_bytes, st>>>(p);
   return cudaGetLastError();
 }
 

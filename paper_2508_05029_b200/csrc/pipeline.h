@@ -17,16 +17,17 @@
 
 namespace tq {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int kV = 2;                   // rows per lane per tile
-constexpr int kTile = kThreads * kV;    // rows per tile (512)
+constexpr int kWarps = 16;                // consumer warps per CTA
+constexpr int kThreads = kWarps * 32;     // consumer threads
+constexpr int kBlock = kThreads + 32;     // + one producer (TMA) warp
+constexpr int kV = 1;                     // rows per lane per tile
+constexpr int kTile = kThreads * kV;      // rows per tile (512)
 constexpr int kMaxKeys = 4;
 constexpr int kMaxKeyWords = 8;         // + 1 null word
 constexpr int kMaxOut = 24;
 constexpr int kMaxAcc = 16;
 constexpr int kMaxDest = 64;
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 6;
 
 enum SinkKind { SINK_COUNT = 0, SINK_EMIT = 1, SINK_AGG = 2, SINK_BUILD = 3 };
 enum DestKind { DEST_FILTER = 0, DEST_PARTITION = 1, DEST_PROBE = 2 };
@@ -99,6 +100,7 @@ struct PipeParams {
   uint32_t ntiles;
   uint32_t nstages;
   uint32_t stage_bytes;
+  uint32_t all_bulk;  // every staged column is TMA-eligible (16-B aligned)
   // shared-memory layout (bytes from dynamic smem base)
   uint32_t off_code, off_lits, off_stage, off_bar, off_vslot, off_vvalid, off_bslot, off_sink;
   // program
