@@ -179,6 +179,73 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def timed(ctx, fn, reps, world, stream):
+    """median device ms of fn() over reps (after one warm-up), max over ranks."""
+    import torch
+    fn().free()
+    ctx.sync()
+    ms = []
+    for _ in range(reps):
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ctx.sync()
+        ms.append(e0.elapsed_time(e1))
+        out.free()
+    return max_over_ranks(world, statistics.median(ms))
+
+
+def run_suite(args, ctx, world, rank, stream):
+    """The other BASELINE.json configs: Q6/Q3/Q5/Q9 at SF10 on one GPU, and the
+    config-4 Q3 shuffle join (broadcast + NCCL all-to-all over NVLink) at
+    SF{shuffle_sf} total, strong scaling over the N GPUs."""
+    import torch.distributed as dist
+    from paper_2508_05029_b200 import queries
+    from paper_2508_05029_b200.ops import Comm
+    suite = {}
+    if world == 1:
+        sf = SF_PER_GPU
+        names = ["customer", "orders", "lineitem", "supplier", "part", "partsupp", "nation", "region"]
+        t = {n: ctx.datagen(queries.TABLE_IDS[n], sf) for n in names}
+        li6 = t["lineitem"].select(queries.Q6_SCAN)
+        ms = timed(ctx, lambda: queries.q6_scan(ctx, li6), 5, world, stream)
+        suite[f"q6_sf{sf:g}"] = {"ms": ms, "rows_per_s": t["lineitem"].rows / (ms * 1e-3),
+                                 "hbm_gbs": t["lineitem"].rows * queries.Q6_SCAN_BYTES_PER_ROW / (ms * 1e-3) / 1e9}
+        for q in (3, 5, 9):
+            rows = sum(t[n].rows for n in queries.QUERY_TABLES[q])
+            ms = timed(ctx, lambda: queries.run_join_query(ctx, q, t), 3, world, stream)
+            suite[f"q{q}_sf{sf:g}"] = {"ms": ms, "rows_per_s": rows / (ms * 1e-3)}
+        for v in t.values():
+            v.free()
+    # config 4: distributed shuffle join
+    uid = [Comm.unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    comm = Comm(ctx, rank, world, uid[0])
+    sf = args.shuffle_sf
+    t = {n: ctx.datagen(queries.TABLE_IDS[n], sf, shard=rank, nshards=world) for n in ("customer", "orders", "lineitem")}
+    rows = sum_over_ranks(world, float(sum(v.rows for v in t.values())))
+    b0 = comm.bytes_sent()
+    stats = {}
+    ms = timed(ctx, lambda: queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], stats),
+               3, world, stream)
+    sent = (comm.bytes_sent() - b0) / 4.0  # 1 warm-up + 3 timed runs
+    suite[f"q3_shuffle_sf{sf:g}"] = {
+        "ms": ms, "rows_per_s": rows / (ms * 1e-3), "scaling": "strong", "n_gpus": world,
+        "nvlink_bytes_sent_per_gpu": sent, "nvlink_gbs_per_gpu": sent / (ms * 1e-3) / 1e9,
+        "nvlink_frac_of_770": sent / (ms * 1e-3) / 770e9,
+        "exchange": "customer_f broadcast (allgather); orders_f, lineitem_f hash-partitioned (fnv1a64 mod N)",
+        "recv_rows_rank0": {k: v for k, v in stats.items()},
+    }
+    for v in t.values():
+        v.free()
+    comm.close()
+    return suite
+
+
 def run_tq(args, world, rank, local):
     import ctypes as C
 
@@ -295,6 +362,8 @@ def run_tq(args, world, rank, local):
         cpu = {"value": statistics.median(rates), "unit": "rows/s", "cores": nthreads, "kind": "port",
                "sample": f"oracle Q1 on lineitem SF1 ({srows} rows), median of 3, {nthreads} threads"}
 
+    del li, scan
+    suite = run_suite(args, ctx, world, rank, stream) if args.suite else None
     if rank != 0:
         ctx.close()
         return
@@ -337,6 +406,8 @@ def run_tq(args, world, rank, local):
         "kernels_ms": {k: v[1] / max(1, v[0]) for k, v in prof.items()},
         "clocks": ck,
         "parity": parity,
+        "jit": ctx.jit_report(),
+        "suite": suite,
     }
     print(json.dumps(line), flush=True)
     ctx.close()
@@ -348,6 +419,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="tq", choices=["tq", "reference"])
+    ap.add_argument("--suite", type=int, default=1, help="also time the other BASELINE configs")
+    ap.add_argument("--shuffle-sf", type=float, default=100.0, help="total SF of the config-4 shuffle join")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

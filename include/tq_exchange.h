@@ -1,0 +1,44 @@
+/*
+ * tq_exchange.h — the worker-to-worker shuffle of libtq_gpu.so: NCCL over
+ * NVLink/NVSwitch, one process (one tq_ctx) per GPU.
+ *
+ * Replaces the reference's Network Executor data path (SPEC.md:475-534:
+ * enqueue_send / send_loop / recv_loop over TCP frames) for the two
+ * AdaptiveExchange strategies of SPEC.md:580-595:
+ *   HashPartition -> tq_hash_partition / tq_pipeline_partition, then
+ *                    tq_comm_exchange (grouped ncclSend/ncclRecv all-to-allv);
+ *   Broadcast     -> tq_comm_allgather (every rank receives every rank's rows).
+ * Received parts are concatenated in source-rank order (reference concat
+ * semantics, transform.cpp:49-88: a bitmap if any part has one).
+ */
+#ifndef TQ_EXCHANGE_H
+#define TQ_EXCHANGE_H
+
+#include "tq_gpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tq_comm tq_comm;
+
+/* 128-byte NCCL unique id, created on rank 0 and shared out of band. */
+tq_status tq_comm_unique_id(uint8_t* id128);
+tq_status tq_comm_init(tq_ctx* ctx, int rank, int nranks, const uint8_t* id128, tq_comm** out);
+void tq_comm_destroy(tq_comm* comm);
+
+/* All-to-allv: rows [part_offsets[p], part_offsets[p+1]) of `partitioned` go to
+ * rank p.  `out` = concatenation of the parts received from ranks 0..n-1;
+ * recv_offsets (host, n+1) gets their boundaries.  Blocks until the receive
+ * sizes are known; the transfer itself is asynchronous on `stream`. */
+tq_status tq_comm_exchange(tq_comm* comm, const tq_batch* partitioned, const uint64_t* part_offsets, tq_batch* out,
+                           uint64_t* recv_offsets, void* stream);
+/* Broadcast join side: every rank receives all ranks' rows (rank order). */
+tq_status tq_comm_allgather(tq_comm* comm, const tq_batch* in, tq_batch* out, uint64_t* recv_offsets, void* stream);
+/* Bytes this communicator has sent to other ranks (NVLink traffic). */
+uint64_t tq_comm_bytes_sent(tq_comm* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQ_EXCHANGE_H */

@@ -1,0 +1,251 @@
+// exchange.cu — the shuffle (include/tq_exchange.h): NCCL grouped
+// ncclSend/ncclRecv all-to-allv of partitioned device batches over
+// NVLink/NVSwitch, one communicator per GPU/process.  NCCL is dlopen'd
+// (libnccl.so.2: the copy torch already loaded, else the system one), so the
+// library still loads on machines without it.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/tq_exchange.h"
+#include "ctx.h"
+#include "device.cuh"
+
+namespace tq {
+namespace {
+
+struct Nccl {
+  bool ok = false;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*);
+  ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*destroy)(ncclComm_t);
+  ncclResult_t (*group_start)();
+  ncclResult_t (*group_end)();
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+  const char* (*err)(ncclResult_t);
+};
+
+Nccl& nccl() {
+  static Nccl n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("/usr/lib/x86_64-linux-gnu/libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    n.get_unique_id = (decltype(n.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    n.init_rank = (decltype(n.init_rank))dlsym(h, "ncclCommInitRank");
+    n.destroy = (decltype(n.destroy))dlsym(h, "ncclCommDestroy");
+    n.group_start = (decltype(n.group_start))dlsym(h, "ncclGroupStart");
+    n.group_end = (decltype(n.group_end))dlsym(h, "ncclGroupEnd");
+    n.send = (decltype(n.send))dlsym(h, "ncclSend");
+    n.recv = (decltype(n.recv))dlsym(h, "ncclRecv");
+    n.all_gather = (decltype(n.all_gather))dlsym(h, "ncclAllGather");
+    n.err = (decltype(n.err))dlsym(h, "ncclGetErrorString");
+    n.ok = n.get_unique_id && n.init_rank && n.destroy && n.group_start && n.group_end && n.send && n.recv &&
+           n.all_gather && n.err;
+  });
+  if (!n.ok) fail(TQ_WORKER_FAILURE, "libnccl.so.2 not available");
+  return n;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(TQ_PEER_DISCONNECTED, std::string(what) + ": " + nccl().err(r));
+}
+
+// bitmap (or all-valid) -> one byte per row
+__global__ void k_bits_to_bytes(const uint8_t* bm, u64 n, uint8_t* out) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    out[i] = bm ? ((bm[i >> 3] >> (i & 7)) & 1) : 1;
+}
+// one byte per row -> LSB-first bitmap (8 rows per thread, whole bytes)
+__global__ void k_bytes_to_bits(const uint8_t* in, u64 n, uint8_t* bm) {
+  u64 nb = (n + 7) / 8;
+  for (u64 b = (u64)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (u64)gridDim.x * blockDim.x) {
+    uint8_t v = 0;
+    for (int k = 0; k < 8; ++k) {
+      u64 i = b * 8 + k;
+      if (i < n && in[i]) v |= (uint8_t)(1u << k);
+    }
+    bm[b] = v;
+  }
+}
+
+}  // namespace
+}  // namespace tq
+
+struct tq_comm {
+  tq_ctx* ctx;
+  ncclComm_t comm;
+  int rank, n;
+  std::atomic<uint64_t> sent{0};
+};
+
+using namespace tq;
+
+namespace {
+
+// Core all-to-allv.  send_off/send_cnt: rows of `in` for each peer (host).
+void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>& send_off,
+                   const std::vector<uint64_t>& send_cnt, tq_batch* out, uint64_t* recv_offsets, cudaStream_t st) {
+  tq_ctx* c = cm->ctx;
+  Nccl& N = nccl();
+  const int n = cm->n, me = cm->rank;
+  if (in->mem != TQ_MEM_DEVICE) fail(TQ_INTERNAL, "exchange needs a device batch");
+  for (uint32_t k = 0; k < in->ncols; ++k)
+    if (in->cols[k].kind == TQ_UTF8) fail(TQ_INVALID_PLAN, "utf8 columns are not supported on the GPU exchange");
+  if (in->ncols > 62) fail(TQ_INVALID_PLAN, "too many columns to exchange");
+  // 1) header all-gather: counts for every peer + a validity-presence mask
+  const int hw = n + 1;
+  u64* hdr = (u64*)dalloc(c, (size_t)hw * (n + 1) * 8, st);
+  std::vector<u64> mine(hw);
+  for (int p = 0; p < n; ++p) mine[p] = send_cnt[p];
+  u64 vmask = 0;
+  for (uint32_t k = 0; k < in->ncols; ++k)
+    if (in->rows > 0 && in->cols[k].validity) vmask |= 1ull << k;
+  mine[n] = vmask;
+  TQ_CUDA(cudaMemcpyAsync(hdr + (size_t)hw * n, mine.data(), hw * 8, cudaMemcpyHostToDevice, st));
+  nccl_check(N.all_gather(hdr + (size_t)hw * n, hdr, hw, ncclUint64, cm->comm, st), "ncclAllGather");
+  std::vector<u64> all((size_t)hw * n);
+  TQ_CUDA(cudaMemcpyAsync(all.data(), hdr, all.size() * 8, cudaMemcpyDeviceToHost, st));
+  TQ_CUDA(cudaStreamSynchronize(st));
+  dfree(c, hdr, (size_t)hw * (n + 1) * 8, st);
+  std::vector<uint64_t> recv_cnt(n), recv_off(n + 1, 0);
+  u64 any_valid = 0;
+  for (int s = 0; s < n; ++s) {
+    recv_cnt[s] = all[(size_t)s * hw + me];
+    recv_off[s + 1] = recv_off[s] + recv_cnt[s];
+    any_valid |= all[(size_t)s * hw + n];
+  }
+  if (recv_offsets)
+    for (int s = 0; s <= n; ++s) recv_offsets[s] = recv_off[s];
+  const uint64_t rows = recv_off[n];
+  // 2) output batch
+  std::vector<tq_column> sch(in->cols, in->cols + in->ncols);
+  std::vector<bool> wv;
+  for (uint32_t k = 0; k < in->ncols; ++k) wv.push_back((any_valid >> k) & 1);
+  alloc_batch(c, rows, sch, wv, out, st);
+  // validity travels as one byte per row
+  uint8_t* vsend = nullptr;
+  uint8_t* vrecv = nullptr;
+  const int nv = __builtin_popcountll(any_valid);
+  if (nv) {
+    vsend = (uint8_t*)dalloc(c, std::max<u64>(1, in->rows) * nv, st);
+    vrecv = (uint8_t*)dalloc(c, std::max<u64>(1, rows) * nv, st);
+    int j = 0;
+    for (uint32_t k = 0; k < in->ncols; ++k) {
+      if (!((any_valid >> k) & 1)) continue;
+      if (in->rows)
+        k_bits_to_bytes<<<std::max<u64>(1, std::min<u64>((in->rows + 255) / 256, 4096)), 256, 0, st>>>(
+            in->rows ? in->cols[k].validity : nullptr, in->rows, vsend + (u64)j * in->rows);
+      counted_launch(c);
+      ++j;
+    }
+  }
+  // 3) grouped point-to-point transfers, one per (peer, column)
+  u64 sent = 0;
+  nccl_check(N.group_start(), "ncclGroupStart");
+  for (int p = 0; p < n; ++p) {
+    int j = 0;
+    for (uint32_t k = 0; k < in->ncols; ++k) {
+      const size_t w = width_of(in->cols[k].kind);
+      const uint8_t* sv = (const uint8_t*)in->cols[k].values;
+      uint8_t* rv = (uint8_t*)out->cols[k].values;
+      if (send_cnt[p]) nccl_check(N.send(sv + send_off[p] * w, send_cnt[p] * w, ncclUint8, p, cm->comm, st), "ncclSend");
+      if (recv_cnt[p]) nccl_check(N.recv(rv + recv_off[p] * w, recv_cnt[p] * w, ncclUint8, p, cm->comm, st), "ncclRecv");
+      if (p != me) sent += send_cnt[p] * w;
+      if ((any_valid >> k) & 1) {
+        if (send_cnt[p])
+          nccl_check(N.send(vsend + (u64)j * in->rows + send_off[p], send_cnt[p], ncclUint8, p, cm->comm, st), "ncclSend");
+        if (recv_cnt[p])
+          nccl_check(N.recv(vrecv + (u64)j * rows + recv_off[p], recv_cnt[p], ncclUint8, p, cm->comm, st), "ncclRecv");
+        if (p != me) sent += send_cnt[p];
+        ++j;
+      }
+    }
+  }
+  nccl_check(N.group_end(), "ncclGroupEnd");
+  cm->sent += sent;
+  if (nv) {
+    int j = 0;
+    for (uint32_t k = 0; k < in->ncols; ++k) {
+      if (!((any_valid >> k) & 1)) continue;
+      if (rows)
+        k_bytes_to_bits<<<std::max<u64>(1, std::min<u64>((rows / 8 + 255) / 256, 4096)), 256, 0, st>>>(
+            vrecv + (u64)j * rows, rows, out->cols[k].validity);
+      counted_launch(c);
+      ++j;
+    }
+    dfree(c, vsend, std::max<u64>(1, in->rows) * nv, st);
+    dfree(c, vrecv, std::max<u64>(1, rows) * nv, st);
+  }
+  TQ_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+tq_status tq_comm_unique_id(uint8_t* id) {
+  return guard([&] {
+    ncclUniqueId u;
+    nccl_check(nccl().get_unique_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+tq_status tq_comm_init(tq_ctx* c, int rank, int nranks, const uint8_t* id, tq_comm** out) {
+  return guard([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(TQ_INVALID_PLAN, "bad rank");
+    TQ_CUDA(cudaSetDevice(c->device));
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    ncclComm_t comm;
+    nccl_check(nccl().init_rank(&comm, nranks, u, rank), "ncclCommInitRank");
+    tq_comm* cm = new tq_comm();
+    cm->ctx = c;
+    cm->comm = comm;
+    cm->rank = rank;
+    cm->n = nranks;
+    *out = cm;
+  });
+}
+
+void tq_comm_destroy(tq_comm* cm) {
+  if (!cm) return;
+  try {
+    nccl().destroy(cm->comm);
+  } catch (...) {
+  }
+  delete cm;
+}
+
+tq_status tq_comm_exchange(tq_comm* cm, const tq_batch* in, const uint64_t* part_offsets, tq_batch* out,
+                           uint64_t* recv_offsets, void* stream) {
+  return guard([&] {
+    std::vector<uint64_t> off(cm->n), cnt(cm->n);
+    for (int p = 0; p < cm->n; ++p) {
+      off[p] = part_offsets[p];
+      cnt[p] = part_offsets[p + 1] - part_offsets[p];
+    }
+    if (part_offsets[cm->n] != in->rows) fail(TQ_INVALID_PLAN, "part offsets do not cover the batch");
+    exchange_impl(cm, in, off, cnt, out, recv_offsets, pick(cm->ctx, stream));
+  });
+}
+
+tq_status tq_comm_allgather(tq_comm* cm, const tq_batch* in, tq_batch* out, uint64_t* recv_offsets, void* stream) {
+  return guard([&] {
+    std::vector<uint64_t> off(cm->n, 0), cnt(cm->n, in->rows);
+    exchange_impl(cm, in, off, cnt, out, recv_offsets, pick(cm->ctx, stream));
+  });
+}
+
+uint64_t tq_comm_bytes_sent(tq_comm* cm) { return cm->sent.load(); }
+
+}  // extern "C"

@@ -77,6 +77,13 @@ def lib():
         L.tq_pinned_alloc.argtypes = [C.c_uint64, P(V)]
         L.tq_pinned_free.argtypes = [V]
         L.tq_ctx_set_jit.argtypes = [V, C.c_int]
+        L.tq_comm_unique_id.argtypes = [C.c_char_p]
+        L.tq_comm_init.argtypes = [V, C.c_int, C.c_int, C.c_char_p, P(V)]
+        L.tq_comm_destroy.argtypes = [V]
+        L.tq_comm_exchange.argtypes = [V, B, P(C.c_uint64), B, P(C.c_uint64), V]
+        L.tq_comm_allgather.argtypes = [V, B, B, P(C.c_uint64), V]
+        L.tq_comm_bytes_sent.restype = C.c_uint64
+        L.tq_comm_bytes_sent.argtypes = [V]
         L.tq_jit_report.restype = C.c_uint64
         L.tq_jit_report.argtypes = [V, C.c_char_p, C.c_uint64]
         _lib = L
@@ -359,3 +366,40 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+class Comm:
+    """NCCL communicator over one Context per GPU (include/tq_exchange.h)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        Context._check(lib().tq_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, ctx: Context, rank: int, nranks: int, uid: bytes):
+        self.ctx, self.rank, self.n = ctx, rank, nranks
+        h = C.c_void_p()
+        Context._check(lib().tq_comm_init(ctx.handle, rank, nranks, uid, C.byref(h)))
+        self.handle = h
+
+    def exchange(self, b: DeviceBatch, part_offsets: Sequence[int], stream=None) -> Tuple[DeviceBatch, List[int]]:
+        po = (C.c_uint64 * (self.n + 1))(*part_offsets)
+        ro = (C.c_uint64 * (self.n + 1))()
+        out = TqBatchC()
+        Context._check(lib().tq_comm_exchange(self.handle, C.byref(b.c), po, C.byref(out), ro, stream))
+        return DeviceBatch(self.ctx, out), list(ro)
+
+    def allgather(self, b: DeviceBatch, stream=None) -> Tuple[DeviceBatch, List[int]]:
+        ro = (C.c_uint64 * (self.n + 1))()
+        out = TqBatchC()
+        Context._check(lib().tq_comm_allgather(self.handle, C.byref(b.c), C.byref(out), ro, stream))
+        return DeviceBatch(self.ctx, out), list(ro)
+
+    def bytes_sent(self) -> int:
+        return lib().tq_comm_bytes_sent(self.handle)
+
+    def close(self):
+        if self.handle:
+            lib().tq_comm_destroy(self.handle)
+            self.handle = None

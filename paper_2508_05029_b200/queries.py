@@ -67,3 +67,111 @@ def q1_scan(ctx, scan, stream=None, partial=False):
 def q6_scan(ctx, scan, stream=None):
     return ctx.pipeline_aggregate(scan, remap(Q6_PRED, Q6_SCAN), [remap(e, Q6_SCAN) for e in Q6_EXPRS], [], Q6_AGGS,
                                   stream)
+
+
+# ---------------------------------------------------------------- join queries
+C_CUSTKEY, C_NATIONKEY, C_MKTSEGMENT = range(3)
+S_SUPPKEY, S_NATIONKEY = range(2)
+P_PARTKEY, P_COLOR = range(2)
+PS_PARTKEY, PS_SUPPKEY, PS_SUPPLYCOST = range(3)
+N_NATIONKEY, N_REGIONKEY = range(2)
+R_REGIONKEY, R_NAME = range(2)
+REV = Col(L_EXTPRICE) * (Dec(100) - Col(L_DISCOUNT))
+
+
+def q3(ctx, customer, orders, lineitem):
+    """Q3-style: customer(BUILDING) >< orders(< 1995-03-15) >< lineitem(> 1995-03-15), group by
+    (l_orderkey, o_orderdate, o_shippriority) sum(revenue)."""
+    ct = ctx.pipeline_build(customer, Col(C_MKTSEGMENT).eq(1), [C_CUSTKEY])
+    of = ctx.pipeline_probe(ct, orders, Col(O_ORDERDATE) < 9204,
+                            [Col(O_ORDERKEY), Col(O_ORDERDATE), Col(O_SHIPPRIORITY), Col(O_CUSTKEY)], [3], [])
+    ot = ctx.join_build(of, [0])
+    j = ctx.pipeline_probe(ot, lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], [1, 2])
+    # j: [o_orderdate, o_shippriority, l_orderkey, rev]
+    out = ctx.aggregate_execute(j, [2, 0, 1], [(AGG_SUM, 3)])
+    for t in (ct, ot):
+        t.free()
+    return out
+
+
+def q5(ctx, region, nation, customer, orders, lineitem, supplier):
+    """Q5-style: ASIA nations, local supplier revenue per nation (1994)."""
+    rt = ctx.pipeline_build(region, Col(R_NAME).eq(2), [R_REGIONKEY])
+    nf = ctx.pipeline_probe(rt, nation, None, [Col(N_NATIONKEY), Col(N_REGIONKEY)], [1], [])
+    nt = ctx.join_build(nf, [0])
+    cf = ctx.pipeline_probe(nt, customer, None, [Col(C_CUSTKEY), Col(C_NATIONKEY)], [1], [])
+    ct = ctx.join_build(cf, [0])
+    of = ctx.pipeline_probe(ct, orders, (Col(O_ORDERDATE) >= 8766) & (Col(O_ORDERDATE) < 9131),
+                            [Col(O_ORDERKEY), Col(O_CUSTKEY)], [1], [1])  # [c_nationkey, o_orderkey, o_custkey]
+    ot = ctx.join_build(of, [1])
+    lj = ctx.pipeline_probe(ot, lineitem, None, [Col(L_ORDERKEY), Col(L_SUPPKEY), REV], [0], [0])
+    # lj: [c_nationkey, l_orderkey, l_suppkey, rev]
+    st = ctx.join_build(supplier, [S_SUPPKEY, S_NATIONKEY])
+    sj = ctx.pipeline_probe(st, lj, None, None, [2, 0], [S_NATIONKEY])
+    # sj: [s_nationkey, c_nationkey, l_orderkey, l_suppkey, rev]
+    out = ctx.aggregate_execute(sj, [0], [(AGG_SUM, 4)])
+    for t in (rt, nt, ct, ot, st):
+        t.free()
+    return out
+
+
+def q9(ctx, part, partsupp, lineitem, supplier, orders):
+    """Q9-style: profit of 'green' parts per (nation, year)."""
+    pt = ctx.pipeline_build(part, Col(P_COLOR) < 54, [P_PARTKEY])
+    psf = ctx.pipeline_probe(pt, partsupp, None, None, [PS_PARTKEY], [])
+    pst = ctx.join_build(psf, [PS_PARTKEY, PS_SUPPKEY])
+    lj = ctx.pipeline_probe(pst, lineitem, None,
+                            [Col(L_ORDERKEY), Col(L_PARTKEY), Col(L_SUPPKEY), Col(L_QUANTITY), Col(L_EXTPRICE),
+                             Col(L_DISCOUNT)], [1, 2], [PS_SUPPLYCOST])
+    # lj: [ps_supplycost, l_orderkey, l_partkey, l_suppkey, qty, ep, disc]
+    st = ctx.join_build(supplier, [S_SUPPKEY])
+    sj = ctx.pipeline_probe(st, lj, None, None, [3], [S_NATIONKEY])
+    # sj: [s_nationkey, ps_supplycost, l_orderkey, l_partkey, l_suppkey, qty, ep, disc]
+    ot = ctx.join_build(orders, [O_ORDERKEY])
+    amt = Col(6) * (Dec(100) - Col(7)) - Col(1) * Col(5)
+    oj = ctx.pipeline_probe(ot, sj, None, [Col(0), amt, Col(2)], [2], [O_YEAR])
+    # oj: [o_year, s_nationkey, amt, l_orderkey]
+    out = ctx.aggregate_execute(oj, [1, 0], [(AGG_SUM, 2)])
+    for t in (pt, pst, st, ot):
+        t.free()
+    return out
+
+
+QUERY_TABLES = {3: ["customer", "orders", "lineitem"],
+                5: ["region", "nation", "customer", "orders", "lineitem", "supplier"],
+                9: ["part", "partsupp", "lineitem", "supplier", "orders"]}
+TABLE_IDS = {"orders": 0, "lineitem": 1, "customer": 2, "supplier": 3, "part": 4, "partsupp": 5, "nation": 6,
+             "region": 7}
+
+
+def run_join_query(ctx, q: int, tables: dict):
+    args = [tables[n] for n in QUERY_TABLES[q]]
+    return {3: q3, 5: q5, 9: q9}[q](ctx, *args)
+
+
+# ---------------------------------------------------------------- distributed (one rank per GPU)
+def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None):
+    """Config 4: Q3-style shuffle join over each rank's row-group subset.
+    customer_f is broadcast (exchange_decide: 24 MB <= 16 MiB x N at SF100),
+    orders_f and lineitem_f are hash-partitioned on orderkey (fnv1a64 mod N)
+    and exchanged all-to-all over NVLink; the build/probe/aggregate that
+    follows is co-partitioned, so each rank's groups are final."""
+    n = comm.n
+    cf = ctx.pipeline_materialize(customer, Col(C_MKTSEGMENT).eq(1), [Col(C_CUSTKEY)])
+    cb, _ = comm.allgather(cf)
+    ct = ctx.join_build(cb, [0])
+    of = ctx.pipeline_probe(ct, orders, Col(O_ORDERDATE) < 9204,
+                            [Col(O_ORDERKEY), Col(O_ORDERDATE), Col(O_SHIPPRIORITY), Col(O_CUSTKEY)], [3], [])
+    op, ooff = ctx.hash_partition(of, [0], n)
+    orx, _ = comm.exchange(op, ooff)
+    lp, loff = ctx.pipeline_partition(lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], n)
+    lrx, _ = comm.exchange(lp, loff)
+    ot = ctx.join_build(orx, [0])
+    j = ctx.pipeline_probe(ot, lrx, None, None, [0], [1, 2])
+    out = ctx.aggregate_execute(j, [2, 0, 1], [(AGG_SUM, 3)])
+    if stats is not None:
+        stats.update({"orders_f_rows": of.rows, "lineitem_f_rows": lp.rows, "recv_orders": orx.rows,
+                      "recv_lineitem": lrx.rows})
+    for t in (ct, ot):
+        t.free()
+    return out

@@ -181,3 +181,17 @@ def test_query_pipelines(ctx, q):
     scan = li.select(queries.Q1_SCAN if q == "q1" else queries.Q6_SCAN)
     pushed = getattr(queries, q + "_scan")(ctx, scan).to_host()
     assert_batches_equal(pushed, want)
+
+
+@pytest.mark.parametrize("q", [3, 5, 9])
+def test_join_queries(ctx, q):
+    """Multi-join DAGs (build/probe pipelines + aggregate) vs the oracle."""
+    from paper_2508_05029_b200 import queries
+    sf = 0.05
+    names = queries.QUERY_TABLES[q]
+    dev = {n: ctx.datagen(queries.TABLE_IDS[n], sf) for n in names}
+    got = queries.run_join_query(ctx, q, dev).to_host()
+    host = {queries.TABLE_IDS[n]: O.datagen(queries.TABLE_IDS[n], sf) for n in names}
+    want = O.query(q, host, 4)
+    assert want.rows > 0
+    assert_batches_equal(got, want)
