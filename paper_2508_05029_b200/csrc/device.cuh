@@ -132,6 +132,23 @@ __device__ __forceinline__ u64 key_hash(const u64* w, int n) {
   return h ^ (h >> 29) ^ (h >> 47);
 }
 
+// Blocked Bloom filter: 3 bits in one 32-bit word chosen by the high hash bits.
+__device__ __forceinline__ u32 bloom_bits(u64 h) {
+  return (1u << (h & 31)) | (1u << ((h >> 5) & 31)) | (1u << ((h >> 10) & 31));
+}
+__device__ __forceinline__ u64 bloom_word(u64 h, u64 mask) { return (h >> 32) & mask; }
+
+// fnv1a64 mod 2^32 == 32-bit FNV-1a with basis 0x84222325 / prime 0x1b3
+// (low words of the 64-bit constants): exact for power-of-two part counts.
+__device__ __forceinline__ u32 fnv32_bytes(u32 h, u64 v, int nbytes) {
+#pragma unroll 8
+  for (int i = 0; i < nbytes; ++i) {
+    h ^= (u32)(v >> (8 * i)) & 0xffu;
+    h *= 0x1b3u;
+  }
+  return h;
+}
+
 // ------------------------------------------------------------------ mbarrier + TMA bulk copy
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 

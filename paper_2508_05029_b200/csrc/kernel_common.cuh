@@ -144,11 +144,26 @@ __device__ __forceinline__ long long agg_global_slot(const PipeParams& p, const 
   return s;
 }
 
-// fnv1a64 over the LE bytes of the keys (reference common.hpp:128-136),
-// chained across key columns; a null key hashes as zero bytes.
-__device__ __forceinline__ u64 partition_hash(const PipeParams& p, const u64* kw) {
-  u64 h = kFnvBasis;
+// part = fnv1a64(LE bytes of the keys) mod n (reference common.hpp:128-136),
+// chained across key columns; a null key hashes as zero bytes.  Power-of-two
+// n only needs the low 32 bits of the hash (32-bit multiplies).
+__device__ __forceinline__ u32 partition_of(const PipeParams& p, const u64* kw) {
   int pos = 0;
+  if ((p.ndest & (p.ndest - 1)) == 0) {
+    u32 h = (u32)kFnvBasis;
+    for (u32 k = 0; k < p.nkeys; ++k) {
+      const KeyOpnd& ko = p.keys[k];
+      if (ko.bytes == 16) {
+        h = fnv32_bytes(h, kw[pos], 8);
+        h = fnv32_bytes(h, kw[pos + 1], 8);
+      } else {
+        h = fnv32_bytes(h, kw[pos], ko.bytes);
+      }
+      pos += ko.words;
+    }
+    return h & (p.ndest - 1);
+  }
+  u64 h = kFnvBasis;
   for (u32 k = 0; k < p.nkeys; ++k) {
     const KeyOpnd& ko = p.keys[k];
     if (ko.bytes == 16) {
@@ -159,7 +174,44 @@ __device__ __forceinline__ u64 partition_hash(const PipeParams& p, const u64* kw
     }
     pos += ko.words;
   }
-  return h;
+  return (u32)(h % p.ndest);
+}
+
+// The single build row matching kw (unique-key tables), or -1.
+template <int KW>
+__device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u64* kw) {
+  const u64 h = key_hash(kw, KW > 0 ? KW : (int)t.kw);
+  if (t.bloom) {
+    const u32 b = bloom_bits(h);
+    if ((__ldg(t.bloom + bloom_word(h, t.bloom_mask)) & b) != b) return -1;
+  }
+  const u64 mask = t.cap - 1;
+  for (u64 s = h & mask;; s = (s + 1) & mask) {
+    const long long* e = jt_entry(t, s);
+    const long long row = e[0];
+    if (row < 0) return -1;
+    if (jt_key_eq<KW>(t, e, kw)) return row;
+  }
+}
+
+// Build rows matching kw, after the (L2-resident) Bloom filter check.
+template <int KW>
+__device__ __forceinline__ u32 jt_probe_count(const JoinTable& t, const u64* kw) {
+  const u64 h = key_hash(kw, KW > 0 ? KW : (int)t.kw);
+  if (t.bloom) {
+    const u32 b = bloom_bits(h);
+    if ((__ldg(t.bloom + bloom_word(h, t.bloom_mask)) & b) != b) return 0;
+  }
+  const u64 mask = t.cap - 1;
+  u64 s = h & mask;
+  u32 n = 0;
+  for (;;) {
+    const long long* e = jt_entry(t, s);
+    if (e[0] < 0) break;
+    if (jt_key_eq<KW>(t, e, kw)) ++n;
+    s = (s + 1) & mask;
+  }
+  return n;
 }
 
 // ------------------------------------------------------------------ stage loading
@@ -308,7 +360,29 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     u32 pm[kV];
     u32 any = P::tile_begin(w, s_code, pm);
 
-    if (SINK == SINK_COUNT || SINK == SINK_EMIT) {
+    if ((SINK == SINK_COUNT || SINK == SINK_EMIT) && p.dest_kind == DEST_PROBE1) {
+      // single pass: unique build keys -> at most one match per probe row
+#pragma unroll
+      for (int v = 0; v < kV; ++v) {
+        bool pass = (pm[v] >> lane) & 1u;
+        long long brow = -1;
+        if (pass) {
+          u64 kw[kMaxKeyWords + 1];
+          if (!P::keys(w, v, kw)) brow = jt_probe_first<P::kKw>(p.jt, kw);
+        }
+        const u32 mm = __ballot_sync(kFull, brow >= 0);
+        if (mm) {
+          unsigned long long base = 0;
+          if (lane == 0) base = atomicAdd(p.cursor, (unsigned long long)__popc(mm));
+          base = __shfl_sync(kFull, base, 0);
+          if (brow >= 0) P::store(w, v, base + __popc(mm & lanemask_lt()), brow);
+        }
+      }
+    } else if (SINK == SINK_COUNT || SINK == SINK_EMIT) {
+      // two passes, stable: COUNT writes per-warp-slice counts, EMIT scatters
+      // from the scanned per-warp-slice offsets; no cross-warp synchronisation
+      const u64 slice = (u64)tile * kWarps + warp;
+      const u64 nslices = (u64)p.ntiles * kWarps;
       u32 dest[kV];
       u32 mult[kV];
 #pragma unroll
@@ -319,49 +393,38 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (pass && p.dest_kind != DEST_FILTER) {
           u64 kw[kMaxKeyWords + 1];
           bool has_null = P::keys(w, v, kw);
-          if (p.dest_kind == DEST_PARTITION) dest[v] = (u32)(partition_hash(p, kw) % p.ndest);
-          else mult[v] = has_null ? 0u : jt_count<P::kKw>(p.jt, kw);  // null keys never match
+          if (p.dest_kind == DEST_PARTITION) dest[v] = partition_of(p, kw);
+          else mult[v] = has_null ? 0u : jt_probe_count<P::kKw>(p.jt, kw);  // null keys never match
         }
       }
-      if (p.dest_kind == DEST_PROBE) {
-        u32 tot = 0;
+      u32* wc = s_cnt + warp * kMaxDest;  // this warp's per-destination counters
+      if (SINK == SINK_COUNT) {
+        if (p.dest_kind == DEST_PROBE) {
+          u32 tot = 0;
 #pragma unroll
-        for (int v = 0; v < kV; ++v) tot += mult[v];
+          for (int v = 0; v < kV; ++v) tot += mult[v];
 #pragma unroll
-        for (int m = 16; m > 0; m >>= 1) tot += __shfl_xor_sync(kFull, tot, m);
-        if (lane == 0) s_cnt[warp * kMaxDest] = tot;
-      } else {
+          for (int m = 16; m > 0; m >>= 1) tot += __shfl_xor_sync(kFull, tot, m);
+          if (lane == 0) p.tile_counts[slice] = tot;
+        } else {
 #pragma unroll
-        for (int v = 0; v < kV; ++v) {
-          bool pass = mult[v] != 0;
-          u32 peers = __match_any_sync(kFull, pass ? dest[v] : 0xffffffffu);
-          if (pass && (peers & lanemask_lt()) == 0) s_cnt[warp * kMaxDest + dest[v]] += __popc(peers);
+          for (int v = 0; v < kV; ++v) {
+            bool pass = mult[v] != 0;
+            u32 peers = __match_any_sync(kFull, pass ? dest[v] : 0xffffffffu);
+            if (pass && (peers & lanemask_lt()) == 0) wc[dest[v]] += __popc(peers);
+            __syncwarp();
+          }
+          for (u32 d = lane; d < p.ndest; d += 32) {
+            p.tile_counts[(u64)d * nslices + slice] = wc[d];
+            wc[d] = 0;
+          }
           __syncwarp();
         }
-      }
-      consumers_sync();
-      if (SINK == SINK_COUNT) {
-        for (u32 d = threadIdx.x; d < p.ndest; d += kThreads) {
-          u32 t = 0;
-          for (u32 ww = 0; ww < kWarps; ++ww) {
-            t += s_cnt[ww * kMaxDest + d];
-            s_cnt[ww * kMaxDest + d] = 0;
-          }
-          p.tile_counts[(u64)d * p.ntiles + tile] = t;
-        }
       } else {
-        // warp bases = tile offset + counts of earlier warps
-        for (u32 d = threadIdx.x; d < p.ndest; d += kThreads) {
-          // dense 1:1 projection: no count phase, tile t starts at row t*kTile
-          unsigned long long b = p.tile_offsets ? p.tile_offsets[(u64)d * p.ntiles + tile] : (u64)tile * kTile;
-          for (u32 ww = 0; ww < kWarps; ++ww) {
-            s_base[ww * kMaxDest + d] = b;
-            b += s_cnt[ww * kMaxDest + d];
-            s_cnt[ww * kMaxDest + d] = 0;
-          }
-        }
-        consumers_sync();
         unsigned long long* wb = s_base + warp * kMaxDest;
+        for (u32 d = lane; d < p.ndest; d += 32)
+          wb[d] = p.tile_offsets ? p.tile_offsets[(u64)d * nslices + slice] : (u64)tile * kTile + w.row0;
+        __syncwarp();
         if (p.dest_kind == DEST_PROBE) {
 #pragma unroll
           for (int v = 0; v < kV; ++v) {
@@ -421,10 +484,15 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           const u64 mask = t.cap - 1;
           u64 sl = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw) & mask;
           long long row = (long long)(p.row_base + r0 + trow(w, v));
+          if (t.bloom) {
+            const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw);
+            atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
+          }
           for (;;) {
             long long* e = (long long*)(t.entries + sl * t.stride);
             if (atomicCAS((unsigned long long*)e, (unsigned long long)-1ll, (unsigned long long)row) ==
                 (unsigned long long)-1ll) {
+              if (p.cursor) atomicAdd(p.cursor, 1ull);
 #pragma unroll
               for (u32 i = 0; i < (P::kKw > 0 ? (u32)P::kKw : (u32)kMaxKeyWords); ++i) {
                 if (i >= t.kw) break;
@@ -510,7 +578,6 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     // stage s consumed by this warp
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    if (SINK == SINK_COUNT || SINK == SINK_EMIT) consumers_sync();  // s_cnt reuse across tiles
   }
 
   if (SINK == SINK_AGG && G > 0) {

@@ -118,9 +118,9 @@ static void scan_u32(tq_ctx* c, const u32* in, u64 n, u64* out, u64* total_dev, 
 }
 
 // offsets[d*ntiles] for each dest + total -> pinned[0..ndest]
-__global__ void k_dest_starts(const u64* offsets, u32 ntiles, u32 ndest, const u64* total, u64* pinned) {
+__global__ void k_dest_starts(const u64* offsets, u32 nslices, u32 ndest, const u64* total, u64* pinned) {
   u32 d = threadIdx.x;
-  if (d < ndest) pinned[d] = offsets[(u64)d * ntiles];
+  if (d < ndest) pinned[d] = offsets[(u64)d * nslices];
   if (d == 0) pinned[ndest] = *total;
 }
 
@@ -403,13 +403,47 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
   }
   if (outs.size() > (size_t)kMaxOut) fail(TQ_INVALID_PLAN, "too many output columns");
 
-  // ---- count phase (skipped for dense 1:1 projections)
+  uint64_t row_bytes = 0;
+  for (auto& sc : sch) row_bytes += width_of(sc.kind);
+  const bool probe1 = A.mode == MAT_PROBE && A.table->jt.unique && in->rows * row_bytes <= (8ull << 30);
+  if (probe1) {
+    // single pass: capacity = probe rows (<= 1 match each), exact size read back
+    p.dest_kind = DEST_PROBE1;
+    alloc_batch(c, in->rows, sch, wv, out, st);
+    u64* cursor = (u64*)dalloc(c, 8, st);
+    TQ_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
+    p.cursor = cursor;
+    p.nout = (u32)outs.size();
+    for (size_t i = 0; i < outs.size(); ++i) {
+      outs[i].values = (uint8_t*)out->cols[i].values;
+      outs[i].validity = out->cols[i].validity;
+      p.out[i] = outs[i];
+    }
+    launch(c, SINK_EMIT, L, P, st);
+    uint64_t n = 0;
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      TQ_CUDA(cudaMemcpyAsync(c->pinned, cursor, 8, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaStreamSynchronize(st));
+      n = *(uint64_t*)c->pinned;
+    }
+    dfree(c, cursor, 8, st);
+    out->rows = n;
+    for (uint32_t i = 0; i < out->ncols; ++i) {
+      out->cols[i].values_bytes = n * width_of(out->cols[i].kind);
+      if (n == 0) out->cols[i].validity = nullptr;  // a 0-row column carries no bitmap
+    }
+    return;
+  }
+
+  // ---- count phase (skipped for dense 1:1 projections), per warp-slice of a tile
   const bool dense = A.mode == MAT_FILTER && !P.has_pred;
   uint64_t total = dense ? in->rows : 0;
   std::vector<uint64_t> starts(p.ndest + 1, 0);
   u32* counts = nullptr;
   u64* offsets = nullptr;
-  u64 ncnt = (u64)p.ndest * p.ntiles;
+  const u64 nslices = (u64)p.ntiles * kWarps;
+  u64 ncnt = (u64)p.ndest * nslices;
   if (!dense && p.ntiles > 0) {
     counts = (u32*)dalloc(c, ncnt * 4, st);
     offsets = (u64*)dalloc(c, (ncnt + 1) * 8, st);
@@ -419,7 +453,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     {
       std::lock_guard<std::mutex> g(c->mu);
       u64* pin = (u64*)c->pinned;
-      k_dest_starts<<<1, 128, 0, st>>>(offsets, p.ntiles, p.ndest, offsets + ncnt, pin);
+      k_dest_starts<<<1, 128, 0, st>>>(offsets, (u32)nslices, p.ndest, offsets + ncnt, pin);
       counted_launch(c);
       TQ_CUDA(cudaGetLastError());
       TQ_CUDA(cudaStreamSynchronize(st));
@@ -456,6 +490,26 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
 }
 
 // ================================================================== join build
+// Any key stored twice?  (every occupied slot counts its key's cluster)
+__global__ void k_jt_unique(JoinTable t, u32* dup) {
+  const u64 mask = t.cap - 1;
+  for (u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x; s < t.cap; s += (u64)gridDim.x * blockDim.x) {
+    const long long* e = (const long long*)(t.entries + s * t.stride);
+    if (e[0] < 0) continue;
+    u64 kw[kMaxKeyWords + 1];
+    for (u32 i = 0; i < t.kw; ++i) kw[i] = (u64)e[1 + i];
+    u32 n = 0;
+    for (u64 q = key_hash(kw, (int)t.kw) & mask;; q = (q + 1) & mask) {
+      const long long* f = (const long long*)(t.entries + q * t.stride);
+      if (f[0] < 0) break;
+      bool eq = true;
+      for (u32 i = 0; i < t.kw; ++i) eq &= (u64)f[1 + i] == kw[i];
+      n += eq;
+    }
+    if (n > 1) atomicOr(dup, 1u);
+  }
+}
+
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
                       tq_join_table** out, cudaStream_t st) {
   Plan L;
@@ -480,19 +534,27 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
     t->key_cls.push_back(o.cls);
     t->key_scale.push_back(o.scale);
   }
+  // load factor 0.25..0.5 (linear probing: short clusters, little warp divergence)
   uint64_t cap = 1024;
   while (cap < in->rows * 2) cap <<= 1;
   t->jt.cap = cap;
   t->jt.kw = p.key_words;
   t->jt.stride = (u32)round_up(8 * (1 + p.key_words), 16);
-  t->bytes = cap * t->jt.stride;
+  // blocked Bloom filter, ~8 bits per build row: rejects non-matching probes in L2
+  uint64_t words = 1024;
+  while (words * 32 < in->rows * 8) words <<= 1;
+  t->jt.bloom_mask = words - 1;
+  uint64_t ebytes = cap * t->jt.stride;
+  t->bytes = ebytes + words * 4;
   try {
     t->jt.entries = (uint8_t*)dalloc(c, t->bytes, st);
   } catch (...) {
     delete t;
     throw;
   }
-  TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, t->bytes, st));
+  t->jt.bloom = (uint32_t*)(t->jt.entries + ebytes);
+  TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, ebytes, st));
+  TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, words * 4, st));
   t->build = *in;
   t->build.owner = nullptr;
   t->build.cols = (tq_column*)std::malloc(sizeof(tq_column) * std::max<uint32_t>(1, in->ncols));
@@ -500,6 +562,17 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   p.jt = t->jt;
   p.row_base = 0;
   launch(c, SINK_BUILD, L, P, st);
+  // unique build keys (PK side of a PK-FK join) -> single-pass probes
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    u32* dup = (u32*)c->pinned;
+    *dup = 0;
+    k_jt_unique<<<(u32)std::min<uint64_t>(4096, (cap + 255) / 256), 256, 0, st>>>(t->jt, dup);
+    counted_launch(c);
+    TQ_CUDA(cudaGetLastError());
+    TQ_CUDA(cudaStreamSynchronize(st));
+    t->jt.unique = *dup == 0;
+  }
   *out = t;
 }
 
@@ -549,9 +622,16 @@ __global__ void k_agg_init(AggTable t, u32 nacc, AccSpec* specs_dev_unused, u64 
 __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 s = i; s < f.t.cap; s += stride) {
-    if (f.t.state[s] != 2) continue;
-    u64 row = atomicAdd(f.counter, 1ull);
+  const u64 cap = (f.t.cap + 31) / 32 * 32;  // whole warps stay converged for the ballot
+  for (u64 s = i; s < cap; s += stride) {
+    const bool occ = s < f.t.cap && f.t.state[s] == 2;
+    const u32 m = __ballot_sync(0xffffffffu, occ);
+    if (!m) continue;
+    u64 base = 0;
+    if ((threadIdx.x & 31) == 0) base = atomicAdd(f.counter, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (!occ) continue;
+    u64 row = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
     const u64* kw = f.t.keys + s * f.kwa;
     u64 nullw = kw[f.kwa - 1];
     for (u32 k = 0; k < f.nkeys; ++k) {
@@ -720,8 +800,9 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
   p.local_groups = G;
 
   // ---- global table; grows x4 and re-runs on overflow (on_oom-style retry)
+  // initial table for min(rows, 1M) groups at load <= 0.5; x4 regrowth on overflow
   uint64_t cap = 1024;
-  while (cap < std::min<uint64_t>(in->rows, 1 << 16) * 2) cap <<= 1;
+  while (cap < std::min<uint64_t>(in->rows, 1ull << 20) * 2) cap <<= 1;
   uint8_t* ops_dev = (uint8_t*)dalloc(c, 64, st);
   {
     uint8_t ops[kMaxAcc] = {};

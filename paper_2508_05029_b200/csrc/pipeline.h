@@ -30,7 +30,10 @@ constexpr int kMaxDest = 64;
 constexpr int kMaxStages = 6;
 
 enum SinkKind { SINK_COUNT = 0, SINK_EMIT = 1, SINK_AGG = 2, SINK_BUILD = 3 };
-enum DestKind { DEST_FILTER = 0, DEST_PARTITION = 1, DEST_PROBE = 2 };
+// FILTER/PARTITION/PROBE: two passes (COUNT then EMIT), stable order.
+// PROBE1: single EMIT pass for unique build keys (<= 1 match per row);
+//         output rows are reserved with a warp-aggregated atomic cursor.
+enum DestKind { DEST_FILTER = 0, DEST_PARTITION = 1, DEST_PROBE = 2, DEST_PROBE1 = 3 };
 
 struct StagedCol {
   const uint8_t* values;
@@ -59,6 +62,9 @@ struct JoinTable {
   uint64_t cap;     // power of two
   uint32_t stride;  // bytes
   uint32_t kw;
+  uint32_t* bloom;  // blocked Bloom filter over the build keys (nullptr = none)
+  uint32_t unique;  // every build key occurs once (probe emits in one pass)
+  uint64_t bloom_mask;  // words - 1 (power of two)
 };
 
 enum OutSrc : uint8_t { OUT_OPND = 0, OUT_BUILD = 1 };
@@ -117,8 +123,9 @@ struct PipeParams {
   KeyOpnd keys[kMaxKeys];
   // destinations
   uint32_t dest_kind, ndest;
-  uint32_t* tile_counts;          // [ndest][ntiles]
-  const unsigned long long* tile_offsets;  // [ndest][ntiles] absolute output rows
+  uint32_t* tile_counts;          // [ndest][ntiles * kWarps] (per warp-slice of a tile)
+  const unsigned long long* tile_offsets;  // [ndest][ntiles * kWarps] absolute output rows
+  unsigned long long* cursor;     // DEST_PROBE1 output cursor; BUILD inserted-row count
   JoinTable jt;
   // emit
   uint32_t nout;
