@@ -222,12 +222,13 @@ __device__ __forceinline__ void issue_tile(const PipeParams& p, uint8_t* stage, 
   u32 bytes = 0;
   if (full)
     for (u32 c = 0; c < p.nstaged; ++c)
-      if (p.cols[c].bulk_ok) bytes += kTile * p.cols[c].width + (p.cols[c].validity ? kTile / 8 : 0);
+      if (p.cols[c].bulk_ok && ((p.load_mask >> c) & 1))
+        bytes += kTile * p.cols[c].width + (p.cols[c].validity ? kTile / 8 : 0);
   mbar_arrive_expect_tx(bar, bytes);
   if (!full) return;
   for (u32 c = 0; c < p.nstaged; ++c) {
     const StagedCol& sc = p.cols[c];
-    if (!sc.bulk_ok) continue;
+    if (!sc.bulk_ok || !((p.load_mask >> c) & 1)) continue;
     bulk_g2s(stage + sc.off, sc.values + r0 * sc.width, kTile * sc.width, bar);
     if (sc.validity) bulk_g2s(stage + sc.voff, sc.validity + r0 / 8, kTile / 8, bar);
   }
@@ -240,7 +241,7 @@ __device__ __forceinline__ void manual_tile(const PipeParams& p, uint8_t* stage,
   bool full = n == (u64)kTile;
   for (u32 c = 0; c < p.nstaged; ++c) {
     const StagedCol& sc = p.cols[c];
-    if (full && sc.bulk_ok) continue;
+    if ((full && sc.bulk_ok) || !((p.load_mask >> c) & 1)) continue;
     u64 bytes = n * sc.width;
     const uint8_t* src = sc.values + r0 * sc.width;
     for (u64 i = lane; i < bytes; i += 32) stage[sc.off + i] = src[i];

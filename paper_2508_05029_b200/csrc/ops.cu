@@ -268,6 +268,7 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
   p.stage_bytes = align_up(std::max(off, 128u), 128);
   p.all_bulk = 1;
   for (u32 i = 0; i < p.nstaged; ++i) p.all_bulk &= p.cols[i].bulk_ok;
+  p.load_mask = p.nstaged >= 32 ? 0xffffffffu : (1u << p.nstaged) - 1;
   // fixed regions
   u32 o = 0;
   p.off_code = o;
@@ -448,7 +449,15 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     counts = (u32*)dalloc(c, ncnt * 4, st);
     offsets = (u64*)dalloc(c, (ncnt + 1) * 8, st);
     p.tile_counts = counts;
-    launch(c, SINK_COUNT, L, P, st);
+    {
+      // the COUNT pass only needs the predicate and key columns
+      std::vector<int> need = kh;
+      if (P.has_pred) need.push_back(P.pred_h);
+      const u32 all = p.load_mask;
+      p.load_mask = P.pb.column_deps(need);
+      launch(c, SINK_COUNT, L, P, st);
+      p.load_mask = all;
+    }
     scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
     {
       std::lock_guard<std::mutex> g(c->mu);

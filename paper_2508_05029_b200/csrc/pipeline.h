@@ -107,6 +107,8 @@ struct PipeParams {
   uint32_t nstages;
   uint32_t stage_bytes;
   uint32_t all_bulk;  // every staged column is TMA-eligible (16-B aligned)
+  uint32_t load_mask; // staged columns this launch reads (a COUNT pass needs only
+                      // the predicate/key columns; the others are never loaded)
   // shared-memory layout (bytes from dynamic smem base)
   uint32_t off_code, off_lits, off_stage, off_bar, off_vslot, off_vvalid, off_bslot, off_sink;
   // program

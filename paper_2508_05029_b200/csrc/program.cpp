@@ -257,6 +257,27 @@ Operand ProgramBuilder::gen(int id) {
   return r;
 }
 
+uint32_t ProgramBuilder::column_deps(const std::vector<int>& roots) const {
+  uint32_t vdep[kMaxValueSlots] = {}, bdep[kMaxBoolSlots] = {};
+  auto opnd = [&](uint8_t k, uint16_t idx) -> uint32_t {
+    switch (k) {
+      case K_COL_I64: case K_COL_DEC: case K_COL_F64: case K_COL_BOOL: return 1u << idx;
+      case K_TMP_I: case K_TMP_F: return vdep[idx];
+      case K_TMP_B: return bdep[idx];
+      default: return 0;
+    }
+  };
+  for (const DInstr& in : code_) {
+    uint32_t m = opnd(in.ak, in.a) | (in.op == OP_NOT ? 0u : opnd(in.bk, in.b));
+    bool b = in.op >= OP_CMP_I;
+    if (b) bdep[in.dst] = m;
+    else vdep[in.dst] = m;
+  }
+  uint32_t out = 0;
+  for (int h : roots) out |= opnd(root_ops_[h].kind, root_ops_[h].idx);
+  return out;
+}
+
 void ProgramBuilder::finish() {
   for (auto& n : nodes_) n.uses = 0;
   for (auto& n : nodes_) {

@@ -47,6 +47,8 @@ class ProgramBuilder {
   int value_slots() const { return max_v_; }
   int bool_slots() const { return max_b_; }
   int staged_index(uint32_t col);  // stage a column, return staged slot
+  // Bitmask of staged columns that the given root handles depend on.
+  uint32_t column_deps(const std::vector<int>& roots) const;
 
  private:
   struct Node {
