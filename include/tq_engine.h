@@ -1,0 +1,66 @@
+/*
+ * tq_engine.h — the worker runtime of libtq_gpu.so: the reference's
+ * Operator / BatchHolder / executor model (SPEC.md
+ * memtier 231-335, sched 337-419, preload 421-473, engine 634-695) driving
+ * the GPU operators of tq_gpu.h on one GPU.
+ *
+ *   BatchHolder      queue of BatchHandles; push never fails — when the
+ *                    Device tier passes its high watermark, unpinned handles
+ *                    are spilled to the pinned Host pool
+ *   Memory Executor  spill (Device->Host) / load_to_device (Host->Device) of
+ *                    chunked batches, one cudaMemcpyAsync per segment on its
+ *                    own copy stream; victim selection protects the inputs of
+ *                    the compute queue's top-K tasks
+ *   Pre-loading      promotes Host-resident inputs of queued tasks to Device
+ *                    on a side stream ahead of execution
+ *   Compute Executor N threads, one CUDA stream each; priority queue
+ *                    (starvation boost, input tier, plan depth, seq); run_task
+ *                    = reserve -> load -> execute -> deposit -> stats ->
+ *                    release; ReservationExceeded -> on_oom: double the
+ *                    estimate and retry, else split, else
+ *                    OutOfMemoryUnsplittable
+ * Query DAGs for the benchmark shapes are built in C++.
+ */
+#ifndef TQ_ENGINE_H
+#define TQ_ENGINE_H
+
+#include "tq_exchange.h"
+#include "tq_memexec.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tq_engine_opts {
+  uint32_t compute_threads;     /* SPEC.md:407 default 4 */
+  uint32_t preload;             /* 1 = run the Pre-loading executor */
+  uint64_t batch_rows;          /* scan task size in rows */
+  uint64_t device_budget;       /* Device tier capacity in bytes (0 = context budget / unlimited) */
+  uint64_t pool_buffer_size;    /* Host pool buffer size (1 MiB) */
+  uint64_t pool_capacity;       /* Host pool buffers */
+  double high_watermark;        /* 0.90 */
+  double low_watermark;         /* 0.70 */
+  uint32_t protect_top_k;       /* 8 */
+  uint32_t tables_on_host;      /* 1 = scan inputs start in the Host tier (config 5) */
+} tq_engine_opts;
+
+/* Input tables: tables[t] (t = 0 orders, 1 lineitem, 2 customer, 3 supplier,
+ * 4 part, 5 partsupp, 6 nation, 7 region) are DEVICE batches; unused entries
+ * may be zero.  With tables_on_host the engine first moves each scan batch to
+ * the pinned Host pool so every scan task goes through load_to_device.
+ * comm may be NULL (single worker); with a communicator the query runs as one
+ * worker of a distributed plan (exchanges over NCCL).  The result is a HOST
+ * batch (free with tq_host_batch_free); metrics_json (may be NULL) receives
+ * a JSON object of executor metrics. */
+tq_status tq_engine_run_query(tq_ctx* ctx, tq_comm* comm, int query, const tq_batch* tables,
+                              const tq_engine_opts* opts, tq_batch* result, char* metrics_json, uint64_t cap);
+
+/* max(ema_peak, ema_ratio*input) * safety, or multiplier *
+ * input without history; never below input_bytes. */
+uint64_t tq_estimate_reservation(uint64_t samples, double ema_peak, double ema_ratio, uint64_t input_bytes,
+                                 double default_multiplier, double safety);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQ_ENGINE_H */

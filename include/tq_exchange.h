@@ -37,6 +37,8 @@ tq_status tq_comm_exchange(tq_comm* comm, const tq_batch* partitioned, const uin
 tq_status tq_comm_allgather(tq_comm* comm, const tq_batch* in, tq_batch* out, uint64_t* recv_offsets, void* stream);
 /* Bytes this communicator has sent to other ranks (NVLink traffic). */
 uint64_t tq_comm_bytes_sent(tq_comm* comm);
+int tq_comm_size(tq_comm* comm);
+int tq_comm_rank(tq_comm* comm);
 
 #ifdef __cplusplus
 }

@@ -96,6 +96,17 @@ void tq_join_table_destroy(tq_ctx* ctx, tq_join_table* t);
 tq_status tq_aggregate(tq_ctx* ctx, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs,
                        uint32_t naggs, tq_batch* out, void* stream);
 
+/* Streaming aggregation state (agg_update / agg_finalize of SURVEY §8b):
+ * every batch is aggregated on the GPU into partial accumulators; finalize
+ * merges them and emits the aggregate_execute outputs.  Operator state is
+ * serialised by the caller. */
+typedef struct tq_agg_state tq_agg_state;
+tq_status tq_agg_create(tq_ctx* ctx, const tq_expr* pred, const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys,
+                        uint32_t nkeys, const tq_agg* aggs, uint32_t naggs, tq_agg_state** out);
+tq_status tq_agg_update(tq_agg_state* state, const tq_batch* in, void* stream);
+tq_status tq_agg_finalize(tq_agg_state* state, tq_batch* out, void* stream);
+void tq_agg_destroy(tq_agg_state* state);
+
 /* ---- fused pipelines: Filter -> Project -> sink in one pass over the batch
  * (the per-batch operator chain of one compute task).
  * pred may be NULL; keys/aggs index the PROJECTED columns. ------------- */

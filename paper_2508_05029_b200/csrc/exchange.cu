@@ -247,5 +247,7 @@ tq_status tq_comm_allgather(tq_comm* cm, const tq_batch* in, tq_batch* out, uint
 }
 
 uint64_t tq_comm_bytes_sent(tq_comm* cm) { return cm->sent.load(); }
+int tq_comm_size(tq_comm* cm) { return cm->n; }
+int tq_comm_rank(tq_comm* cm) { return cm->rank; }
 
 }  // extern "C"

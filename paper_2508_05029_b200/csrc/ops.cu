@@ -699,10 +699,20 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
   }
 }
 
-static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t* keys, uint32_t nkeys,
-                          const tq_agg* aggs, uint32_t naggs, tq_batch* out, cudaStream_t st) {
-  // ---- accumulators (deduplicated)
-  std::vector<AccSpec> acc;
+struct AggPlan {
+  uint8_t kind, acc, cnt, scale;
+  tq_column col;
+  bool nullable;
+};
+struct AggSpec {
+  std::vector<AccSpec> acc;   // deduplicated accumulators
+  std::vector<AggPlan> ap;    // one output per aggregate, referencing acc
+};
+
+// Aggregates -> accumulators + output plans.
+static AggSpec plan_aggs(const tq_batch* in, Prog& P, const tq_agg* aggs, uint32_t naggs) {
+  AggSpec S;
+  std::vector<AccSpec>& acc = S.acc;
   auto acc_of = [&](uint8_t op, uint8_t kind, uint16_t idx) -> uint8_t {
     for (size_t i = 0; i < acc.size(); ++i)
       if (acc[i].op == op && acc[i].kind == kind && acc[i].idx == idx) return (uint8_t)i;
@@ -713,8 +723,6 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
     return (uint8_t)(acc.size() - 1);
   };
   if (naggs > 32) fail(TQ_INVALID_PLAN, "too many aggregates");
-  struct AggPlan { uint8_t kind, acc, cnt, scale; tq_column col; bool nullable; };
-  std::vector<AggPlan> ap;
   for (uint32_t j = 0; j < naggs; ++j) {
     AggPlan a{};
     a.cnt = 0xff;
@@ -724,7 +732,7 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
       a.kind = AO_CNT;
       a.acc = acc_of(ACC_CNT, K_NONE, 0);
       a.col.kind = TQ_INT64;
-      ap.push_back(a);
+      S.ap.push_back(a);
       continue;
     }
     if (aggs[j].column >= P.outs.size()) fail(TQ_INVALID_PLAN, "aggregate column out of range");
@@ -766,14 +774,16 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
         a.cnt = o.maybe_null ? cnt_acc : 0xff;
       }
     }
-    ap.push_back(a);
+    S.ap.push_back(a);
   }
-  // ---- keys
-  std::vector<int> kh;
-  for (uint32_t k = 0; k < nkeys; ++k) {
-    if (keys[k] >= P.outs.size()) fail(TQ_INVALID_PLAN, "key column out of range");
-    kh.push_back(P.outs[keys[k]]);
-  }
+  return S;
+}
+
+// One hash group-by pass over `in`.  ap == nullptr -> PARTIAL output: the key
+// columns then one column per raw accumulator (int128 accumulators as
+// Decimal(38,0), counts Int64, float accumulators Float64) for a later merge.
+static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<int>& kh,
+                     const std::vector<AccSpec>& acc, const std::vector<AggPlan>* ap, tq_batch* out, cudaStream_t st) {
   const u32 nacc = (u32)acc.size();
   // local (per-CTA) group table: per-lane private accumulator planes (8 B;
   // MIN/MAX of int128 take two) sized to the shared memory left after two stages
@@ -809,7 +819,7 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
   p.local_groups = G;
 
   // ---- global table; grows x4 and re-runs on overflow (on_oom-style retry)
-  // initial table for min(rows, 1M) groups at load <= 0.5; x4 regrowth on overflow
+  // initial table for min(rows, 1M) groups at load <= 0.5
   uint64_t cap = 1024;
   while (cap < std::min<uint64_t>(in->rows, 1ull << 20) * 2) cap <<= 1;
   uint8_t* ops_dev = (uint8_t*)dalloc(c, 64, st);
@@ -864,7 +874,22 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
     sch.push_back(d);
     wv.push_back(o.maybe_null);
   }
-  for (auto& a : ap) {
+  std::vector<AggPlan> raw;
+  if (!ap) {  // PARTIAL: raw accumulators
+    for (u32 i = 0; i < nacc; ++i) {
+      AggPlan a{};
+      a.acc = (uint8_t)i;
+      a.cnt = 0xff;
+      switch (acc[i].op) {
+        case ACC_SUM_I: case ACC_MIN_I: case ACC_MAX_I: a.kind = AO_SUM_DEC; a.col.kind = TQ_DECIMAL; a.col.precision = 38; break;
+        case ACC_CNT: a.kind = AO_SUM_I64; a.col.kind = TQ_INT64; break;
+        default: a.kind = AO_SUM_F; a.col.kind = TQ_FLOAT64;
+      }
+      raw.push_back(a);
+    }
+    ap = &raw;
+  }
+  for (auto& a : *ap) {
     sch.push_back(a.col);
     bool can_null = a.kind != AO_CNT && a.cnt != 0xff && a.nullable;
     wv.push_back(can_null);
@@ -881,7 +906,7 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
     f.kwa = kwa;
     f.nacc = nacc;
     f.nkeys = (u32)kh.size();
-    f.naggs = (u32)ap.size();
+    f.naggs = (u32)ap->size();
     u32 word = 0;
     for (u32 k = 0; k < f.nkeys; ++k) {
       KeyOut& ko = f.keys[k];
@@ -893,12 +918,13 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
       word += p.keys[k].words;
     }
     for (u32 a = 0; a < f.naggs; ++a) {
+      const AggPlan& pl = (*ap)[a];
       AggOut& ao = f.aggs[a];
-      ao.kind = ap[a].kind;
-      ao.acc = ap[a].acc;
-      ao.cnt = ap[a].kind == AO_CNT ? 0xff : ap[a].cnt;
-      if (ap[a].kind == AO_AVG_I || ap[a].kind == AO_AVG_F) ao.cnt = ap[a].cnt;
-      ao.scale = ap[a].scale;
+      ao.kind = pl.kind;
+      ao.acc = pl.acc;
+      ao.cnt = pl.kind == AO_CNT ? 0xff : pl.cnt;
+      if (pl.kind == AO_AVG_I || pl.kind == AO_AVG_F) ao.cnt = pl.cnt;
+      ao.scale = pl.scale;
       ao.values = (uint8_t*)out->cols[f.nkeys + a].values;
       ao.validity = out->cols[f.nkeys + a].validity;
     }
@@ -910,6 +936,21 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
     TQ_CUDA(cudaGetLastError());
   }
   dfree(c, tbase, tbytes, st);
+}
+
+static std::vector<int> key_handles(Prog& P, const uint32_t* keys, uint32_t nkeys) {
+  std::vector<int> kh;
+  for (uint32_t k = 0; k < nkeys; ++k) {
+    if (keys[k] >= P.outs.size()) fail(TQ_INVALID_PLAN, "key column out of range");
+    kh.push_back(P.outs[keys[k]]);
+  }
+  return kh;
+}
+
+static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t* keys, uint32_t nkeys,
+                          const tq_agg* aggs, uint32_t naggs, tq_batch* out, cudaStream_t st) {
+  AggSpec S = plan_aggs(in, P, aggs, naggs);
+  agg_core(c, in, P, key_handles(P, keys, nkeys), S.acc, &S.ap, out, st);
 }
 
 // ================================================================== take / concat / slice
@@ -1276,3 +1317,120 @@ void scan_u32_public(tq_ctx* c, const u32* in, u64 n, u64* out, u64* total_dev, 
   scan_u32(c, in, n, out, total_dev, st);
 }
 }  // namespace tq
+
+// ================================================================== streaming aggregation state
+// tq_agg_update aggregates each batch into a PARTIAL (keys + raw accumulators);
+// tq_agg_finalize merges the partials (sums of sums / counts, min of mins, ...)
+// and produces the SPEC.md:604-611 outputs.  Exact: int128 sums are
+// associative, so the result does not depend on how rows were batched.
+struct tq_agg_state {
+  tq_ctx* ctx = nullptr;
+  bool has_pred = false, has_exprs = false;
+  std::vector<tq_expr_node> pred;
+  std::vector<std::vector<tq_expr_node>> exprs;
+  std::vector<uint32_t> keys;
+  std::vector<tq_agg> aggs;
+  bool planned = false;
+  std::vector<tq::AggPlan> ap;
+  std::vector<uint8_t> acc_ops;
+  std::vector<tq_batch> partials;
+};
+
+namespace {
+tq_expr as_expr(const std::vector<tq_expr_node>& v) { return tq_expr{v.data(), (uint32_t)v.size(), 0}; }
+}  // namespace
+
+extern "C" {
+
+tq_status tq_agg_create(tq_ctx* c, const tq_expr* pred, const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys,
+                        uint32_t nkeys, const tq_agg* aggs, uint32_t naggs, tq_agg_state** out) {
+  return guard([&] {
+    tq_agg_state* s = new tq_agg_state();
+    s->ctx = c;
+    if (pred) {
+      s->has_pred = true;
+      s->pred.assign(pred->nodes, pred->nodes + pred->len);
+    }
+    if (exprs) {
+      s->has_exprs = true;
+      for (uint32_t i = 0; i < nexprs; ++i) s->exprs.emplace_back(exprs[i].nodes, exprs[i].nodes + exprs[i].len);
+    }
+    s->keys.assign(keys, keys + nkeys);
+    s->aggs.assign(aggs, aggs + naggs);
+    *out = s;
+  });
+}
+
+tq_status tq_agg_update(tq_agg_state* s, const tq_batch* in, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    tq_ctx* c = s->ctx;
+    cudaStream_t st = pick(c, stream);
+    Prog P(schema_of(in));
+    tq_expr pe = as_expr(s->pred);
+    std::vector<tq_expr> ex;
+    for (auto& e : s->exprs) ex.push_back(as_expr(e));
+    compile_prog(P, in, s->has_pred ? &pe : nullptr, s->has_exprs ? ex.data() : nullptr, (uint32_t)ex.size(),
+                 !s->has_exprs);
+    AggSpec S = plan_aggs(in, P, s->aggs.data(), (uint32_t)s->aggs.size());
+    if (!s->planned) {
+      s->ap = S.ap;
+      for (auto& a : S.acc) s->acc_ops.push_back(a.op);
+      s->planned = true;
+    } else if (S.acc.size() != s->acc_ops.size()) {
+      fail(TQ_SCHEMA_MISMATCH, "aggregate input schema changed between batches");
+    }
+    if (in->rows == 0) return;
+    tq_batch part{};
+    agg_core(c, in, P, key_handles(P, s->keys.data(), (uint32_t)s->keys.size()), S.acc, nullptr, &part, st);
+    s->partials.push_back(part);
+  });
+}
+
+tq_status tq_agg_finalize(tq_agg_state* s, tq_batch* out, void* stream) {
+  return guard([&] {
+    tq_ctx* c = s->ctx;
+    cudaStream_t st = pick(c, stream);
+    const uint32_t nk = (uint32_t)s->keys.size();
+    if (s->partials.empty()) {
+      // empty input -> empty output
+      alloc_batch(c, 0, {}, {}, out, st);
+      return;
+    }
+    tq_batch merged{};
+    const tq_batch* src = &s->partials[0];
+    if (s->partials.size() > 1) {
+      tq_status r = tq_concat(c, s->partials.data(), (uint32_t)s->partials.size(), &merged, st);
+      if (r != TQ_OK) fail(r, g_err);
+      src = &merged;
+    }
+    Prog P(schema_of(src));
+    compile_prog(P, src, nullptr, nullptr, 0, true);
+    std::vector<int> kh;
+    for (uint32_t k = 0; k < nk; ++k) kh.push_back(P.outs[k]);
+    std::vector<AccSpec> macc;
+    for (size_t i = 0; i < s->acc_ops.size(); ++i) {
+      const Operand& o = P.pb.root(P.outs[nk + i]);
+      AccSpec a{};
+      a.op = s->acc_ops[i] == ACC_CNT ? (uint8_t)ACC_SUM_I : s->acc_ops[i];
+      a.kind = o.kind;
+      a.idx = o.idx;
+      macc.push_back(a);
+    }
+    try {
+      agg_core(c, src, P, kh, macc, &s->ap, out, st);
+    } catch (...) {
+      if (src == &merged) tq_batch_free(c, &merged);
+      throw;
+    }
+    if (src == &merged) tq_batch_free(c, &merged);
+  });
+}
+
+void tq_agg_destroy(tq_agg_state* s) {
+  if (!s) return;
+  for (auto& b : s->partials) tq_batch_free(s->ctx, &b);
+  delete s;
+}
+
+}  // extern "C"

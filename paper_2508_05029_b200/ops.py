@@ -23,6 +23,13 @@ LIB_PATH = os.path.join(HERE, "libtq_gpu.so")
 _lib = None
 
 
+class TqEngineOptsC(C.Structure):
+    _fields_ = [("compute_threads", C.c_uint32), ("preload", C.c_uint32), ("batch_rows", C.c_uint64),
+                ("device_budget", C.c_uint64), ("pool_buffer_size", C.c_uint64), ("pool_capacity", C.c_uint64),
+                ("high_watermark", C.c_double), ("low_watermark", C.c_double), ("protect_top_k", C.c_uint32),
+                ("tables_on_host", C.c_uint32)]
+
+
 class TqOptsC(C.Structure):
     _fields_ = [("device", C.c_int), ("ctas_per_sm", C.c_uint32), ("device_budget_bytes", C.c_uint64)]
 
@@ -84,6 +91,32 @@ def lib():
         L.tq_comm_allgather.argtypes = [V, B, B, P(C.c_uint64), V]
         L.tq_comm_bytes_sent.restype = C.c_uint64
         L.tq_comm_bytes_sent.argtypes = [V]
+        L.tq_comm_size.argtypes = [V]
+        L.tq_comm_rank.argtypes = [V]
+        # memory tier (include/tq_memexec.h)
+        L.tq_pool_create.argtypes = [C.c_uint64, C.c_uint64, P(V)]
+        L.tq_pool_destroy.argtypes = [V]
+        L.tq_pool_free_count.restype = C.c_uint64
+        L.tq_pool_free_count.argtypes = [V]
+        L.tq_pool_buffer_size.restype = C.c_uint64
+        L.tq_pool_buffer_size.argtypes = [V]
+        L.tq_pool_acquire.argtypes = [V, C.c_uint64, P(C.c_uint32)]
+        L.tq_pool_release.argtypes = [V, P(C.c_uint32), C.c_uint64]
+        L.tq_pool_buffer.restype = C.c_void_p
+        L.tq_pool_buffer.argtypes = [V, C.c_uint32]
+        L.tq_chunked_encode.argtypes = [V, B, P(V)]
+        L.tq_chunked_decode.argtypes = [V, B]
+        L.tq_spill.argtypes = [V, V, B, P(V), V]
+        L.tq_load.argtypes = [V, V, B, V]
+        L.tq_chunked_layout.restype = C.c_uint32
+        L.tq_chunked_layout.argtypes = [V, P(C.c_uint64), P(C.c_uint64), P(C.c_uint64), P(C.c_uint32), C.c_uint32]
+        L.tq_chunked_rows.restype = C.c_uint64
+        L.tq_chunked_rows.argtypes = [V]
+        L.tq_chunked_release.argtypes = [V]
+        # engine (include/tq_engine.h)
+        L.tq_engine_run_query.argtypes = [V, V, C.c_int, P(TqBatchC), P(TqEngineOptsC), B, C.c_char_p, C.c_uint64]
+        L.tq_estimate_reservation.restype = C.c_uint64
+        L.tq_estimate_reservation.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double]
         L.tq_jit_report.restype = C.c_uint64
         L.tq_jit_report.argtypes = [V, C.c_char_p, C.c_uint64]
         _lib = L
@@ -403,3 +436,105 @@ class Comm:
         if self.handle:
             lib().tq_comm_destroy(self.handle)
             self.handle = None
+
+
+class Pool:
+    """Pinned FixedBufferPool (reference pool.hpp:29-56) — the Host tier."""
+
+    def __init__(self, buffer_size: int, capacity: int):
+        h = C.c_void_p()
+        Context._check(lib().tq_pool_create(buffer_size, capacity, C.byref(h)))
+        self.handle = h
+
+    def free_count(self) -> int:
+        return lib().tq_pool_free_count(self.handle)
+
+    def acquire(self, n: int) -> List[int]:
+        ids = (C.c_uint32 * max(1, n))()
+        Context._check(lib().tq_pool_acquire(self.handle, n, ids))
+        return list(ids)[:n]
+
+    def release(self, ids: Sequence[int]):
+        arr = (C.c_uint32 * max(1, len(ids)))(*ids)
+        Context._check(lib().tq_pool_release(self.handle, arr, len(ids)))
+
+    def encode(self, hb: HostBatch) -> "Chunked":
+        hc = hb.to_c()
+        h = C.c_void_p()
+        Context._check(lib().tq_chunked_encode(self.handle, C.byref(hc), C.byref(h)))
+        return Chunked(h)
+
+    def spill(self, ctx: Context, db: DeviceBatch, stream=None) -> "Chunked":
+        h = C.c_void_p()
+        Context._check(lib().tq_spill(ctx.handle, self.handle, C.byref(db.c), C.byref(h), stream))
+        ctx.sync(stream)
+        return Chunked(h)
+
+    def close(self):
+        if self.handle:
+            lib().tq_pool_destroy(self.handle)
+            self.handle = None
+
+
+class Chunked:
+    """ChunkedBatch (reference chunked.hpp:22-53) in a Pool."""
+
+    def __init__(self, h):
+        self.handle = h
+
+    def layout(self):
+        nbuf, tail, total = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        n = lib().tq_chunked_layout(self.handle, C.byref(nbuf), C.byref(tail), C.byref(total), None, 0)
+        segs = (C.c_uint32 * (3 * max(1, n)))()
+        lib().tq_chunked_layout(self.handle, None, None, None, segs, n)
+        return nbuf.value, tail.value, total.value, [tuple(segs[3 * i:3 * i + 3]) for i in range(n)]
+
+    def decode(self) -> HostBatch:
+        out = TqBatchC()
+        Context._check(lib().tq_chunked_decode(self.handle, C.byref(out)))
+        try:
+            return HostBatch.from_c(out)
+        finally:
+            lib().tq_host_batch_free(C.byref(out))
+
+    def load(self, ctx: Context, stream=None) -> DeviceBatch:
+        out = TqBatchC()
+        Context._check(lib().tq_load(ctx.handle, self.handle, C.byref(out), stream))
+        ctx.sync(stream)
+        return DeviceBatch(ctx, out)
+
+    def release(self):
+        if self.handle:
+            lib().tq_chunked_release(self.handle)
+            self.handle = None
+
+
+def estimate_reservation(samples, ema_peak, ema_ratio, input_bytes, multiplier, safety=1.25) -> int:
+    return lib().tq_estimate_reservation(samples, ema_peak, ema_ratio, input_bytes, multiplier, safety)
+
+
+def engine_run_query(ctx: Context, query: int, tables: dict, comm: "Comm" = None, **opts):
+    """Run a benchmark query DAG on the C++ worker runtime (include/tq_engine.h).
+    tables: {table_id: DeviceBatch or HostBatch}.  Returns (HostBatch, metrics)."""
+    import json
+    arr = (TqBatchC * 8)()
+    keep = []
+    for t, b in tables.items():
+        if isinstance(b, DeviceBatch):
+            arr[t] = b.c
+        else:
+            c = b.to_c()
+            keep.append(c)
+            arr[t] = c
+    o = TqEngineOptsC()
+    for k, v in opts.items():
+        setattr(o, k, v)
+    out = TqBatchC()
+    buf = C.create_string_buffer(1 << 16)
+    Context._check(lib().tq_engine_run_query(ctx.handle, comm.handle if comm else None, query, arr, C.byref(o),
+                                             C.byref(out), buf, len(buf)))
+    try:
+        res = HostBatch.from_c(out)
+    finally:
+        lib().tq_host_batch_free(C.byref(out))
+    return res, json.loads(buf.value.decode() or "{}")

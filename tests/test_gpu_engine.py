@@ -1,0 +1,58 @@
+"""GPU: Device<->Host tier moves and the C++ worker runtime (BatchHolders,
+Memory / Pre-loading / Compute executors, run_task lifecycle) running the
+benchmark query DAGs vs the oracle — with resident tables, with Host-tier
+tables under a Device budget (spill / load_to_device / preload), and through
+the on_oom retry path."""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import rand_batch
+from paper_2508_05029_b200.columnar import BOOL, DECIMAL, FLOAT64, INT64, assert_batches_equal
+from paper_2508_05029_b200.ops import Context, Pool, engine_run_query
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_spill_load_roundtrip(ctx, seed):
+    b = rand_batch(seed, [0, 7, 5000, 123457][seed], (INT64, DECIMAL, BOOL, FLOAT64), null_frac=0.1 * (seed % 2))
+    p = Pool([64, 4096, 1 << 20, 1 << 16][seed], 4096)
+    d = ctx.upload(b)
+    cb = p.spill(ctx, d)                       # one cudaMemcpyAsync per segment, D2H
+    assert_batches_equal(cb.decode(), b, ordered=True)
+    back = cb.load(ctx)                        # load_to_device, H2D
+    assert_batches_equal(back.to_host(), b, ordered=True)
+    cb.release()
+    p.close()
+
+
+@pytest.mark.parametrize("q", [1, 3, 5, 6, 9])
+def test_engine_queries_resident(ctx, q):
+    sf = 0.05
+    tabs = {t: ctx.datagen(t, sf) for t in O.QUERY_TABLES[q]}
+    got, m = engine_run_query(ctx, q, tabs, compute_threads=4, batch_rows=64 * 1024)
+    want = O.query(q, {t: O.datagen(t, sf) for t in O.QUERY_TABLES[q]}, 8)
+    assert_batches_equal(got, want)
+    assert m["tasks"] > 0
+
+
+@pytest.mark.parametrize("q", [3, 9])
+def test_engine_host_tables_under_budget(ctx, q):
+    """Config-5 path: tables start in the pinned Host tier, a Device budget
+    forces spills; results stay identical."""
+    sf = 0.05
+    host = {t: O.datagen(t, sf) for t in O.QUERY_TABLES[q]}
+    total = sum(b.nbytes() for b in host.values())
+    got, m = engine_run_query(ctx, q, host, compute_threads=4, batch_rows=32 * 1024, preload=1,
+                              device_budget=max(total // 3, 48 << 20))
+    want = O.query(q, host, 8)
+    assert_batches_equal(got, want)
+    assert m["loads"] + m["preloads"] > 0, m
