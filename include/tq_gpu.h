@@ -118,7 +118,8 @@ tq_status tq_pipeline_aggregate(tq_ctx* ctx, const tq_batch* in, const tq_expr* 
 tq_status tq_pipeline_partition(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
                                 uint32_t nexprs, const uint32_t* keys, uint32_t nkeys, uint32_t nparts,
                                 tq_batch* out, uint64_t* part_offsets, void* stream);
-/* probe output = build columns listed in build_cols, then projected probe columns */
+/* probe output = build columns listed in build_cols (NULL = all build
+ * columns; a non-NULL array with nbuild_cols = 0 = none), then projected probe columns */
 tq_status tq_pipeline_probe(tq_ctx* ctx, const tq_join_table* table, const tq_batch* in, const tq_expr* pred,
                             const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,
                             const uint32_t* build_cols, uint32_t nbuild_cols, tq_batch* out, void* stream);

@@ -285,8 +285,11 @@ tq_status tq_batch_download(tq_ctx* c, const tq_batch* d, tq_batch* out, void* s
 void tq_batch_free(tq_ctx* c, tq_batch* b) {
   if (!b) return;
   if (b->owner) {
+    // Released in the context stream's order: work on other streams that
+    // still reads the batch must be synchronised by the caller first (the
+    // producing stream may be gone by now, e.g. an executor thread's).
     Owner* o = (Owner*)b->owner;
-    for (auto& pb : o->bufs) dfree(o->ctx, pb.first, pb.second, o->stream);
+    for (auto& pb : o->bufs) dfree(o->ctx, pb.first, pb.second, o->ctx->stream);
     delete o;
   }
   (void)c;

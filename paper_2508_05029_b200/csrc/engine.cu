@@ -73,6 +73,7 @@ void check(tq_status s) {
 struct OpStat {
   uint64_t tasks = 0;
   double ms = 0;
+  std::atomic<uint64_t> rows_out{0};
 };
 
 class Runtime;
@@ -585,6 +586,7 @@ class PipeOp : public Op {
       check(tq_pipeline_materialize(rt->ctx, &h->dev, has_pred ? &pe : nullptr, ex.empty() ? nullptr : ex.data(),
                                     (uint32_t)ex.size(), &o, st));
       cudaStreamSynchronize(st);
+      stat.rows_out += o.rows;
       out->push(rt->adopt(o, false));
       if (!h->view) rt->free_handle(h);
     }
@@ -676,10 +678,13 @@ class ProbeOp : public Op {
       for (auto& e : exprs) ex.push_back(e.e());
       tq_expr pe = pred.e();
       tq_batch o{};
+      static const uint32_t none = 0;  // NULL build_cols would mean "all build columns"
+      const uint32_t* bcols = build_cols.empty() ? &none : build_cols.data();
       check(tq_pipeline_probe(rt->ctx, b->table, &h->dev, has_pred ? &pe : nullptr, ex.empty() ? nullptr : ex.data(),
-                              (uint32_t)ex.size(), keys.data(), (uint32_t)keys.size(), build_cols.data(),
+                              (uint32_t)ex.size(), keys.data(), (uint32_t)keys.size(), bcols,
                               (uint32_t)build_cols.size(), &o, st));
       cudaStreamSynchronize(st);
+      stat.rows_out += o.rows;
       out->push(rt->adopt(o, false));
       if (!h->view) rt->free_handle(h);
     }
@@ -739,6 +744,7 @@ class AggOp : public Op {
     tq_batch o{};
     check(tq_agg_finalize(state, &o, st));
     cudaStreamSynchronize(st);
+    stat.rows_out += o.rows;
     out->push(rt->adopt(o, false));
     std::lock_guard<std::mutex> g(rt->mu);
     done = true;
@@ -1096,7 +1102,7 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
       for (auto& op : rt.ops) {
         if (!op->stat.tasks) continue;
         js << (first ? "" : ", ") << "\"" << op->name << "\": {\"tasks\": " << op->stat.tasks << ", \"ms\": " << op->stat.ms
-           << "}";
+           << ", \"rows_out\": " << op->stat.rows_out.load() << "}";
         first = false;
       }
       js << "}}";

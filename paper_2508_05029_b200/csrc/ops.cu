@@ -1284,7 +1284,7 @@ tq_status tq_pipeline_probe(tq_ctx* c, const tq_join_table* t, const tq_batch* i
 void tq_join_table_destroy(tq_ctx* c, tq_join_table* t) {
   if (!t) return;
   (void)c;
-  dfree(t->ctx, t->jt.entries, t->bytes, t->stream);
+  dfree(t->ctx, t->jt.entries, t->bytes, t->ctx->stream);  // see tq_batch_free
   std::free(t->build.cols);
   delete t;
 }

@@ -115,6 +115,10 @@ def lib():
         L.tq_chunked_release.argtypes = [V]
         # engine (include/tq_engine.h)
         L.tq_engine_run_query.argtypes = [V, V, C.c_int, P(TqBatchC), P(TqEngineOptsC), B, C.c_char_p, C.c_uint64]
+        L.tq_agg_create.argtypes = [V, E, E, C.c_uint32, U32, C.c_uint32, P(TqAggC), C.c_uint32, P(V)]
+        L.tq_agg_update.argtypes = [V, B, V]
+        L.tq_agg_finalize.argtypes = [V, B, V]
+        L.tq_agg_destroy.argtypes = [V]
         L.tq_estimate_reservation.restype = C.c_uint64
         L.tq_estimate_reservation.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double]
         L.tq_jit_report.restype = C.c_uint64
@@ -367,6 +371,23 @@ class Context:
         out = TqBatchC()
         return self._wrap(lib().tq_pipeline_aggregate(self.handle, C.byref(b.c), pp, arr, n, _u32(keys), len(keys),
                                                       ag, len(aggs), C.byref(out), stream), out)
+
+    def agg_stream(self, batches: Sequence[DeviceBatch], pred: Optional[Expr], exprs: Optional[Sequence[Expr]],
+                   keys: Sequence[int], aggs: Sequence[Tuple[int, int]], stream=None) -> DeviceBatch:
+        """Streaming aggregation state: tq_agg_create / update per batch / finalize."""
+        pp, _k1 = _pred(pred)
+        arr, n, _k2 = _exprs(exprs)
+        ag = (TqAggC * max(1, len(aggs)))(*[TqAggC(f, c) for f, c in aggs])
+        h = C.c_void_p()
+        self._check(lib().tq_agg_create(self.handle, pp, arr, n, _u32(keys), len(keys), ag, len(aggs), C.byref(h)))
+        try:
+            for b in batches:
+                self._check(lib().tq_agg_update(h, C.byref(b.c), stream))
+            out = TqBatchC()
+            self._check(lib().tq_agg_finalize(h, C.byref(out), stream))
+            return DeviceBatch(self, out)
+        finally:
+            lib().tq_agg_destroy(h)
 
     def pipeline_partition(self, b: DeviceBatch, pred, exprs, keys: Sequence[int], nparts: int, stream=None):
         pp, _k1 = _pred(pred)

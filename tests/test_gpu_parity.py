@@ -195,3 +195,17 @@ def test_join_queries(ctx, q):
     want = O.query(q, host, 4)
     assert want.rows > 0
     assert_batches_equal(got, want)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_streaming_aggregate_state(ctx, seed):
+    """tq_agg_update over row-group slices + tq_agg_finalize == one aggregate."""
+    kinds = (INT64, DECIMAL, FLOAT64, BOOL, INT64)
+    b = rand_batch(seed, 20000, kinds, null_frac=0.1 if seed % 2 else 0.0)
+    keys = [[0], [3], [0, 3], [], [1, 4], [0, 1, 3]][seed]
+    aggs = [(AGG_SUM, 1), (AGG_SUM, 0), (AGG_SUM, 2), (AGG_COUNT, 1), (AGG_COUNT_STAR, 0), (AGG_MIN, 1),
+            (AGG_MAX, 2), (AGG_AVG, 1), (AGG_AVG, 0), (AGG_MIN, 3), (AGG_MAX, 0), (AGG_AVG, 2)]
+    d = ctx.upload(b)
+    parts = [ctx.slice(d, s, min(3000, b.rows - s)) for s in range(0, b.rows, 3000)]
+    got = ctx.agg_stream(parts, None, None, keys, aggs).to_host()
+    assert_batches_equal(got, O.aggregate_execute(b, keys, aggs))
