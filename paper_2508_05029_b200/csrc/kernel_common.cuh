@@ -474,46 +474,62 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         }
       }
     } else if (SINK == SINK_BUILD) {
-      if (any) {
+      // read keys into registers, release the stage, then insert
+      u64 kws[kV][kMaxKeyWords + 1];
+      bool ok[kV];
 #pragma unroll
-        for (int v = 0; v < kV; ++v) {
-          bool pass = (pm[v] >> lane) & 1u;
-          if (!pass) continue;
-          u64 kw[kMaxKeyWords + 1];
-          if (P::keys(w, v, kw)) continue;  // null keys never match
-          const JoinTable& t = p.jt;
-          const u64 mask = t.cap - 1;
-          u64 sl = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw) & mask;
-          long long row = (long long)(p.row_base + r0 + trow(w, v));
-          if (t.bloom) {
-            const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw);
-            atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
-          }
-          for (;;) {
-            long long* e = (long long*)(t.entries + sl * t.stride);
-            if (atomicCAS((unsigned long long*)e, (unsigned long long)-1ll, (unsigned long long)row) ==
-                (unsigned long long)-1ll) {
-              if (p.cursor) atomicAdd(p.cursor, 1ull);
+      for (int v = 0; v < kV; ++v) {
+        ok[v] = ((pm[v] >> lane) & 1u) && !P::keys(w, v, kws[v]);  // null keys never match
+      }
+      if (!P::kInterp) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
 #pragma unroll
-              for (u32 i = 0; i < (P::kKw > 0 ? (u32)P::kKw : (u32)kMaxKeyWords); ++i) {
-                if (i >= t.kw) break;
-                e[1 + i] = (long long)kw[i];
-              }
-              break;
+      for (int v = 0; v < kV; ++v) {
+        if (!ok[v]) continue;
+        const u64* kw = kws[v];
+        const JoinTable& t = p.jt;
+        const u64 mask = t.cap - 1;
+        const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw);
+        u64 sl = hb & mask;
+        long long row = (long long)(p.row_base + r0 + trow(w, v));
+        if (t.bloom) atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
+        for (;;) {
+          long long* e = (long long*)(t.entries + sl * t.stride);
+          if (atomicCAS((unsigned long long*)e, (unsigned long long)-1ll, (unsigned long long)row) ==
+              (unsigned long long)-1ll) {
+            if (p.cursor) atomicAdd(p.cursor, 1ull);
+#pragma unroll
+            for (u32 i = 0; i < (P::kKw > 0 ? (u32)P::kKw : (u32)kMaxKeyWords); ++i) {
+              if (i >= t.kw) break;
+              e[1 + i] = (long long)kw[i];
             }
-            sl = (sl + 1) & mask;
+            break;
           }
+          sl = (sl + 1) & mask;
         }
       }
     } else if (SINK == SINK_AGG) {
+      // read every input of the row into registers, release the stage, then
+      // do the hash-table / accumulator work (keeps more tiles in flight)
+      RowVals xs[kV];
+#pragma unroll
+      for (int v = 0; v < kV; ++v)
+        if ((pm[v] >> lane) & 1u) {
+          P::keys(w, v, xs[v].kw);
+          P::accs(w, v, xs[v]);
+        }
+      if (!P::kInterp) {  // the interpreter keeps the stage until the end of the tile
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+      }
       if (any) {
 #pragma unroll
         for (int v = 0; v < kV; ++v) {
           bool pass = (pm[v] >> lane) & 1u;
           if (!pass) continue;
-          RowVals x;
-          P::keys(w, v, x.kw);
-          P::accs(w, v, x);
+          RowVals& x = xs[v];
           const u64 h = key_hash(x.kw, (int)kwa);
           long long ls = G ? table_find_insert<KWA>(l_state, l_keys, G, kwa, x.kw, h, G, nullptr) : -1;
           if (ls >= 0) {
@@ -576,9 +592,11 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       }
     }
 
-    // stage s consumed by this warp
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
+    // stage s consumed by this warp (JIT AGG / BUILD released it above)
+    if (SINK == SINK_COUNT || SINK == SINK_EMIT || P::kInterp) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
   }
 
   if (SINK == SINK_AGG && G > 0) {
