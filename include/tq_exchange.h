@@ -35,6 +35,8 @@ tq_status tq_comm_exchange(tq_comm* comm, const tq_batch* partitioned, const uin
                            uint64_t* recv_offsets, void* stream);
 /* Broadcast join side: every rank receives all ranks' rows (rank order). */
 tq_status tq_comm_allgather(tq_comm* comm, const tq_batch* in, tq_batch* out, uint64_t* recv_offsets, void* stream);
+/* OR a Bloom filter across all ranks (allgather + OR), for LIP before a shuffle. */
+tq_status tq_comm_bloom_union(tq_comm* comm, tq_bloom* bloom, void* stream);
 /* Bytes this communicator has sent to other ranks (NVLink traffic). */
 uint64_t tq_comm_bytes_sent(tq_comm* comm);
 int tq_comm_size(tq_comm* comm);

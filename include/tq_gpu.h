@@ -126,6 +126,23 @@ tq_status tq_pipeline_probe(tq_ctx* ctx, const tq_join_table* table, const tq_ba
 tq_status tq_pipeline_build(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
                             uint32_t nkeys, tq_join_table** out, void* stream);
 
+/* ---- Lookahead Information Passing: a Bloom filter over
+ * build-side keys (~10 bits/key, blocked), applied to the probe side BEFORE
+ * it is hash-partitioned and shuffled, so rows that cannot join never cross
+ * NVLink.  Results are unchanged (a semi-join reduction).  Union across
+ * workers: tq_comm_bloom_union (tq_exchange.h). */
+typedef struct tq_bloom tq_bloom;
+tq_status tq_bloom_build(tq_ctx* ctx, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, uint64_t expected_keys,
+                         tq_bloom** out, void* stream);
+void tq_bloom_destroy(tq_bloom* b);
+uint64_t tq_bloom_words(const tq_bloom* b);
+uint32_t* tq_bloom_data(tq_bloom* b);
+/* OR nranks gathered copies (nranks x words, device) into b */
+tq_status tq_bloom_or_gathered(tq_bloom* b, const uint32_t* gathered, int nranks, void* stream);
+tq_status tq_pipeline_partition_semi(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                     uint32_t nexprs, const uint32_t* keys, uint32_t nkeys, uint32_t nparts,
+                                     const tq_bloom* semi, tq_batch* out, uint64_t* part_offsets, void* stream);
+
 /* ---- synthetic TPC-H-style tables generated on the device,
  * bit-identical to the CPU generator (counter-based SplitMix64,
  * common.hpp:139-158).  table: 0 orders, 1 lineitem, 2 customer,

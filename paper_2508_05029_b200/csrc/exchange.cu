@@ -247,6 +247,21 @@ tq_status tq_comm_allgather(tq_comm* cm, const tq_batch* in, tq_batch* out, uint
 }
 
 uint64_t tq_comm_bytes_sent(tq_comm* cm) { return cm->sent.load(); }
+
+tq_status tq_comm_bloom_union(tq_comm* cm, tq_bloom* b, void* stream) {
+  return guard([&] {
+    if (cm->n == 1) return;
+    tq_ctx* c = cm->ctx;
+    cudaStream_t st = pick(c, stream);
+    const uint64_t nw = tq_bloom_words(b);
+    uint32_t* all = (uint32_t*)dalloc(c, nw * 4 * cm->n, st);
+    nccl_check(nccl().all_gather(tq_bloom_data(b), all, nw, ncclUint32, cm->comm, st), "ncclAllGather");
+    cm->sent += nw * 4 * (cm->n - 1);
+    tq_status r = tq_bloom_or_gathered(b, all, cm->n, st);
+    dfree(c, all, nw * 4 * cm->n, st);
+    if (r != TQ_OK) fail(r, g_err);
+  });
+}
 int tq_comm_size(tq_comm* cm) { return cm->n; }
 int tq_comm_rank(tq_comm* cm) { return cm->rank; }
 

@@ -394,6 +394,13 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (pass && p.dest_kind != DEST_FILTER) {
           u64 kw[kMaxKeyWords + 1];
           bool has_null = P::keys(w, v, kw);
+          if (p.dest_kind == DEST_PARTITION && p.semi_bloom) {
+            // Lookahead Information Passing: a key absent from the (global)
+            // build-side Bloom filter cannot join -> never shipped
+            const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)p.key_words);
+            const u32 bb = bloom_bits(hb);
+            if (has_null || (__ldg(p.semi_bloom + bloom_word(hb, p.semi_mask)) & bb) != bb) mult[v] = 0;
+          }
           if (p.dest_kind == DEST_PARTITION) dest[v] = partition_of(p, kw);
           else mult[v] = has_null ? 0u : jt_probe_count<P::kKw>(p.jt, kw);  // null keys never match
         }
@@ -495,6 +502,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         u64 sl = hb & mask;
         long long row = (long long)(p.row_base + r0 + trow(w, v));
         if (t.bloom) atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
+        if (!t.entries) continue;  // Bloom-only build (LIP filter)
         for (;;) {
           long long* e = (long long*)(t.entries + sl * t.stride);
           if (atomicCAS((unsigned long long*)e, (unsigned long long)-1ll, (unsigned long long)row) ==

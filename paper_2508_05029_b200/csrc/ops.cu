@@ -333,7 +333,10 @@ static void set_keys(PipeParams& p, const ProgramBuilder& pb, const std::vector<
 // ================================================================== materializing sinks
 enum MatMode { MAT_FILTER, MAT_PARTITION, MAT_PROBE };
 
+struct tq_bloom_impl;
 struct MatArgs {
+  const uint32_t* semi_words = nullptr;  // LIP Bloom filter on the partition keys
+  uint64_t semi_mask = 0;
   int mode = MAT_FILTER;
   std::vector<uint32_t> key_roots;  // indices into P.outs
   uint32_t nparts = 1;
@@ -356,6 +359,8 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     kh.push_back(P.outs[k]);
   }
   set_keys(p, P.pb, kh);
+  p.semi_bloom = A.semi_words;
+  p.semi_mask = A.semi_mask;
   if (A.mode == MAT_PROBE) {
     const tq_join_table* t = A.table;
     if (kh.size() != t->key_cls.size()) fail(TQ_INVALID_PLAN, "probe/build key count differs");
@@ -1431,6 +1436,119 @@ void tq_agg_destroy(tq_agg_state* s) {
   if (!s) return;
   for (auto& b : s->partials) tq_batch_free(s->ctx, &b);
   delete s;
+}
+
+}  // extern "C"
+
+
+// ================================================================== LIP Bloom filters
+struct tq_bloom {
+  tq_ctx* ctx;
+  uint32_t* words;
+  uint64_t nwords;  // power of two
+  uint32_t kw;
+  std::vector<uint8_t> key_cls, key_scale;
+};
+
+namespace {
+__global__ void k_bloom_or(uint32_t* dst, const uint32_t* all, uint64_t nwords, int n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t v = 0;
+    for (int r = 0; r < n; ++r) v |= all[(uint64_t)r * nwords + i];
+    dst[i] = v;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+tq_status tq_bloom_build(tq_ctx* c, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, uint64_t expected_keys,
+                         tq_bloom** out, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    cudaStream_t st = pick(c, stream);
+    Prog P(schema_of(in));
+    std::vector<tq_expr_node> nodes(nkeys);
+    std::vector<tq_expr> ex(nkeys);
+    for (uint32_t k = 0; k < nkeys; ++k) {
+      nodes[k] = tq_expr_node{};
+      nodes[k].tag = TQ_EX_COL;
+      nodes[k].column = keys[k];
+      ex[k] = tq_expr{&nodes[k], 1, 0};
+    }
+    compile_prog(P, in, nullptr, ex.data(), nkeys, false);
+    Plan L;
+    plan_launch(c, in, P, L, 0, st);
+    PipeParams& p = L.p;
+    std::vector<int> kh(P.outs.begin(), P.outs.end());
+    if (kh.empty()) fail(TQ_INVALID_PLAN, "bloom filter without keys");
+    set_keys(p, P.pb, kh);
+    tq_bloom* b = new tq_bloom();
+    b->ctx = c;
+    b->kw = p.key_words;
+    for (int h : kh) {
+      b->key_cls.push_back(P.pb.root(h).cls);
+      b->key_scale.push_back(P.pb.root(h).scale);
+    }
+    uint64_t words = 1024;
+    while (words * 32 < std::max<uint64_t>(expected_keys, in->rows) * 10) words <<= 1;  // ~10 bits per key
+    b->nwords = words;
+    b->words = (uint32_t*)dalloc(c, words * 4, st);
+    TQ_CUDA(cudaMemsetAsync(b->words, 0, words * 4, st));
+    p.jt = JoinTable{};
+    p.jt.entries = nullptr;  // Bloom-only build
+    p.jt.kw = p.key_words;
+    p.jt.cap = 1;
+    p.jt.bloom = b->words;
+    p.jt.bloom_mask = words - 1;
+    launch(c, SINK_BUILD, L, P, st);
+    *out = b;
+  });
+}
+
+void tq_bloom_destroy(tq_bloom* b) {
+  if (!b) return;
+  dfree(b->ctx, b->words, b->nwords * 4, b->ctx->stream);
+  delete b;
+}
+
+uint64_t tq_bloom_words(const tq_bloom* b) { return b->nwords; }
+uint32_t* tq_bloom_data(tq_bloom* b) { return b->words; }
+
+tq_status tq_bloom_or_gathered(tq_bloom* b, const uint32_t* gathered, int nranks, void* stream) {
+  return guard([&] {
+    cudaStream_t st = pick(b->ctx, stream);
+    k_bloom_or<<<(u32)std::min<uint64_t>(4096, (b->nwords + 255) / 256), 256, 0, st>>>(b->words, gathered, b->nwords,
+                                                                                      nranks);
+    counted_launch(b->ctx);
+    TQ_CUDA(cudaGetLastError());
+  });
+}
+
+tq_status tq_pipeline_partition_semi(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                     uint32_t nexprs, const uint32_t* keys, uint32_t nkeys, uint32_t nparts,
+                                     const tq_bloom* semi, tq_batch* out, uint64_t* part_offsets, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
+    MatArgs A;
+    A.mode = MAT_PARTITION;
+    A.key_roots.assign(keys, keys + nkeys);
+    A.nparts = nparts;
+    if (semi) {
+      if (semi->key_cls.size() != nkeys) fail(TQ_INVALID_PLAN, "semi-join key count differs");
+      for (uint32_t k = 0; k < nkeys; ++k) {
+        if (keys[k] >= P.outs.size()) fail(TQ_INVALID_PLAN, "key column out of range");
+        const Operand& o = P.pb.root(P.outs[keys[k]]);
+        if (o.cls != semi->key_cls[k] || (o.cls == C_D && o.scale != semi->key_scale[k]))
+          fail(TQ_INVALID_PLAN, "semi-join key types differ");
+      }
+      A.semi_words = semi->words;
+      A.semi_mask = semi->nwords - 1;
+    }
+    run_materialize(c, in, P, A, out, part_offsets, pick(c, stream));
+  });
 }
 
 }  // extern "C"

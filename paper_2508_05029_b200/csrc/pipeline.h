@@ -129,6 +129,10 @@ struct PipeParams {
   const unsigned long long* tile_offsets;  // [ndest][ntiles * kWarps] absolute output rows
   unsigned long long* cursor;     // DEST_PROBE1 output cursor; BUILD inserted-row count
   JoinTable jt;
+  // LIP semi-join filter on the key words (dest PARTITION): rows whose keys
+  // miss this Bloom filter are dropped before they are partitioned / shipped
+  const uint32_t* semi_bloom;
+  uint64_t semi_mask;
   // emit
   uint32_t nout;
   OutCol out[kMaxOut];

@@ -119,6 +119,11 @@ def lib():
         L.tq_agg_update.argtypes = [V, B, V]
         L.tq_agg_finalize.argtypes = [V, B, V]
         L.tq_agg_destroy.argtypes = [V]
+        L.tq_bloom_build.argtypes = [V, B, U32, C.c_uint32, C.c_uint64, P(V), V]
+        L.tq_bloom_destroy.argtypes = [V]
+        L.tq_pipeline_partition_semi.argtypes = [V, B, E, E, C.c_uint32, U32, C.c_uint32, C.c_uint32, V, B,
+                                                 P(C.c_uint64), V]
+        L.tq_comm_bloom_union.argtypes = [V, V, V]
         L.tq_estimate_reservation.restype = C.c_uint64
         L.tq_estimate_reservation.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double]
         L.tq_jit_report.restype = C.c_uint64
@@ -398,6 +403,24 @@ class Context:
                                                    nparts, C.byref(out), offs, stream), out)
         return r, list(offs)
 
+    def bloom_build(self, b: DeviceBatch, keys: Sequence[int], expected_keys: int = 0, stream=None) -> "Bloom":
+        """LIP Bloom filter over the key columns of a build side."""
+        h = C.c_void_p()
+        self._check(lib().tq_bloom_build(self.handle, C.byref(b.c), _u32(keys), len(keys), expected_keys, C.byref(h),
+                                         stream))
+        return Bloom(self, h)
+
+    def pipeline_partition_semi(self, b: DeviceBatch, pred, exprs, keys: Sequence[int], nparts: int, semi: "Bloom",
+                                stream=None):
+        pp, _k1 = _pred(pred)
+        arr, n, _k2 = _exprs(exprs)
+        offs = (C.c_uint64 * (nparts + 1))()
+        out = TqBatchC()
+        r = self._wrap(lib().tq_pipeline_partition_semi(self.handle, C.byref(b.c), pp, arr, n, _u32(keys), len(keys),
+                                                        nparts, semi.handle if semi else None, C.byref(out), offs,
+                                                        stream), out)
+        return r, list(offs)
+
     def pipeline_build(self, b: DeviceBatch, pred, keys: Sequence[int], stream=None) -> JoinTable:
         pp, _k1 = _pred(pred)
         h = C.c_void_p()
@@ -418,6 +441,22 @@ class Context:
     def __del__(self):
         try:
             self.close()
+        except Exception:
+            pass
+
+
+class Bloom:
+    def __init__(self, ctx, h):
+        self.ctx, self.handle = ctx, h
+
+    def free(self):
+        if self.handle:
+            lib().tq_bloom_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
         except Exception:
             pass
 
@@ -449,6 +488,9 @@ class Comm:
         out = TqBatchC()
         Context._check(lib().tq_comm_allgather(self.handle, C.byref(b.c), C.byref(out), ro, stream))
         return DeviceBatch(self.ctx, out), list(ro)
+
+    def bloom_union(self, bloom: "Bloom", stream=None):
+        Context._check(lib().tq_comm_bloom_union(self.handle, bloom.handle, stream))
 
     def bytes_sent(self) -> int:
         return lib().tq_comm_bytes_sent(self.handle)

@@ -24,7 +24,7 @@ def main():
     sf = float(os.environ.get("TQ_SF", "0.1"))
     t = {name: ctx.datagen(queries.TABLE_IDS[name], sf, shard=rank, nshards=world)
          for name in ("customer", "orders", "lineitem")}
-    out = queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"]).to_host()
+    out = queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], lip=os.environ.get("TQ_LIP", "1") == "1").to_host()
     parts = [None] * world
     dist.all_gather_object(parts, out)
     rc = 0

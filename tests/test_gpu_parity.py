@@ -209,3 +209,25 @@ def test_streaming_aggregate_state(ctx, seed):
     parts = [ctx.slice(d, s, min(3000, b.rows - s)) for s in range(0, b.rows, 3000)]
     got = ctx.agg_stream(parts, None, None, keys, aggs).to_host()
     assert_batches_equal(got, O.aggregate_execute(b, keys, aggs))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_partition_semi_bloom(ctx, seed):
+    """LIP: partition with a build-side Bloom filter keeps every row whose key
+    is in the build set (no false negatives), drops most others, and the join
+    result is unchanged."""
+    rng = np.random.default_rng(seed)
+    build = HostBatch(2000, [HostBatch.col_i64(rng.integers(0, 100000, 2000))])
+    probe = HostBatch(50000, [HostBatch.col_i64(rng.integers(0, 100000, 50000)),
+                              HostBatch.col_dec(rng.integers(0, 10**6, 50000))])
+    db, dp = ctx.upload(build), ctx.upload(probe)
+    bloom = ctx.bloom_build(db, [0])
+    part, offs = ctx.pipeline_partition_semi(dp, None, None, [0], 4, bloom)
+    got = part.to_host()
+    keys = set(build.cols[0].i64().tolist())
+    kept = got.cols[0].i64().tolist()
+    must = [k for k in probe.cols[0].i64().tolist() if k in keys]
+    assert set(must) <= set(kept) and len([k for k in kept if k in keys]) == len(must)
+    assert len(kept) < 0.2 * probe.rows            # most non-joining rows dropped
+    j1 = O.join_execute(build, got, [0], [0])
+    assert_batches_equal(j1, O.join_execute(build, probe, [0], [0]))
