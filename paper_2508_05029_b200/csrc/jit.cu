@@ -487,28 +487,65 @@ Entry compile(const std::string& src) {
 cudaError_t launch_pipeline_prog(tq_ctx* c, int sink, const PipeParams& p, u32 smem, u32 grid, cudaStream_t st,
                                  const std::vector<DInstr>& code, const std::vector<DLit>& lits) {
   if (c->jit && jit_env_enabled()) {
-    std::string src;
-    try {
-      Gen g(p, code, lits);
-      src = g.source(sink);
-    } catch (const Fail&) {
-      src.clear();
+    // cache key: every launch parameter the generator bakes into the source
+    std::string key;
+    key.reserve(1024);
+    auto put = [&](const void* d, size_t n) { key.append((const char*)d, n); };
+    put(&sink, sizeof sink);
+    put(code.data(), code.size() * sizeof(DInstr));
+    put(lits.data(), lits.size() * sizeof(DLit));
+    put(&p.npred, sizeof p.npred);
+    put(&p.pred_kind, 1);
+    put(&p.pred_idx, 2);
+    for (u32 c2 = 0; c2 < p.nstaged; ++c2) {
+      const StagedCol& sc = p.cols[c2];
+      uint32_t f[4] = {sc.off, sc.voff, sc.width, (uint32_t)(sc.validity != nullptr)};
+      put(f, sizeof f);
     }
-    if (!src.empty()) {
-      Entry e;
-      {
-        std::lock_guard<std::mutex> lk(g_mu);
-        auto it = g_cache.find(src);
-        if (it != g_cache.end()) {
-          e = it->second;
-          g_stats.hits++;
-        } else {
-          e = compile(src);
-          g_cache[src] = e;
-          if (e.ok) g_stats.compiled++;
-          else g_stats.failed++;
-        }
+    put(&p.nkeys, 4);
+    put(&p.key_words, 4);
+    put(p.keys, sizeof(KeyOpnd) * p.nkeys);
+    put(&p.nacc, 4);
+    put(&p.nplanes, 4);
+    put(p.acc, sizeof(AccSpec) * p.nacc);
+    put(p.acc_plane, p.nacc);
+    put(&p.nout, 4);
+    for (u32 o = 0; o < p.nout; ++o) {
+      const OutCol& oc = p.out[o];
+      uint32_t f[6] = {oc.src, oc.kind, oc.width, oc.out_kind, oc.idx, (uint32_t)(oc.validity != nullptr)};
+      put(f, sizeof f);
+    }
+    Entry e;
+    bool have = false;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto it = g_cache.find(key);
+      if (it != g_cache.end()) {
+        e = it->second;
+        g_stats.hits++;
+        have = true;
       }
+    }
+    if (!have) {
+      std::string src;
+      try {
+        Gen g(p, code, lits);
+        src = g.source(sink);
+      } catch (const Fail&) {
+        src.clear();
+      }
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto it = g_cache.find(key);
+      if (it != g_cache.end()) {
+        e = it->second;
+      } else {
+        e = src.empty() ? Entry{} : compile(src);
+        g_cache[key] = e;
+        if (e.ok) g_stats.compiled++;
+        else g_stats.failed++;
+      }
+    }
+    {
       if (e.ok) {
         cudaError_t err = cudaFuncSetAttribute((const void*)e.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)smem);

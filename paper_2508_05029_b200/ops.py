@@ -136,20 +136,35 @@ def _u32(xs: Sequence[int]):
     return (C.c_uint32 * max(1, len(xs)))(*xs)
 
 
+_SER = {}  # id(expr or list) -> (object, prepared ctypes args): repeated plans skip re-serialisation
+
+
 def _exprs(exprs: Optional[Sequence[Expr]]):
     if exprs is None:
         return None, 0, []
+    hit = _SER.get(id(exprs))
+    if hit is not None and hit[0] is exprs:
+        return hit[1]
     ss = [e.serialize() for e in exprs]
     arr = (TqExprC * max(1, len(ss)))(*[s.c() for s in ss])
-    return arr, len(ss), ss
+    res = (arr, len(ss), ss)
+    if isinstance(exprs, tuple) or len(_SER) < 4096:
+        _SER[id(exprs)] = (exprs, res)
+    return res
 
 
 def _pred(pred: Optional[Expr]):
     if pred is None:
         return None, None
+    hit = _SER.get(id(pred))
+    if hit is not None and hit[0] is pred:
+        return hit[1]
     s = pred.serialize()
     c = s.c()
-    return C.pointer(c), s
+    res = (C.pointer(c), (s, c))
+    if len(_SER) < 4096:
+        _SER[id(pred)] = (pred, res)
+    return res
 
 
 class DeviceBatch:

@@ -55,18 +55,22 @@ def remap(e, cols):
     return replace(e, children=tuple(remap(c, cols) for c in e.children))
 
 
+_Q1_SCAN_PRED = remap(Q1_PRED, Q1_SCAN)
+_Q1_SCAN_EXPRS = [remap(e, Q1_SCAN) for e in Q1_EXPRS]
+_Q1_PARTIAL_AGGS = [(AGG_SUM, 2), (AGG_SUM, 3), (AGG_SUM, 5), (AGG_SUM, 6), (AGG_SUM, 4), (AGG_COUNT_STAR, 0)]
+_Q6_SCAN_PRED = remap(Q6_PRED, Q6_SCAN)
+_Q6_SCAN_EXPRS = [remap(e, Q6_SCAN) for e in Q6_EXPRS]
+
+
 def q1_scan(ctx, scan, stream=None, partial=False):
     """Q1 over the pushed-down 7-column scan batch.  partial=True returns the
     mergeable per-worker state (sums + counts) used for multi-GPU Q1."""
-    aggs = Q1_AGGS if not partial else [(AGG_SUM, 2), (AGG_SUM, 3), (AGG_SUM, 5), (AGG_SUM, 6), (AGG_SUM, 4),
-                                         (AGG_COUNT_STAR, 0)]
-    return ctx.pipeline_aggregate(scan, remap(Q1_PRED, Q1_SCAN), [remap(e, Q1_SCAN) for e in Q1_EXPRS], Q1_KEYS,
-                                  aggs, stream)
+    return ctx.pipeline_aggregate(scan, _Q1_SCAN_PRED, _Q1_SCAN_EXPRS, Q1_KEYS,
+                                  _Q1_PARTIAL_AGGS if partial else Q1_AGGS, stream)
 
 
 def q6_scan(ctx, scan, stream=None):
-    return ctx.pipeline_aggregate(scan, remap(Q6_PRED, Q6_SCAN), [remap(e, Q6_SCAN) for e in Q6_EXPRS], [], Q6_AGGS,
-                                  stream)
+    return ctx.pipeline_aggregate(scan, _Q6_SCAN_PRED, _Q6_SCAN_EXPRS, [], Q6_AGGS, stream)
 
 
 # ---------------------------------------------------------------- join queries
