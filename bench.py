@@ -223,6 +223,34 @@ def run_suite(args, ctx, world, rank, stream):
             suite[f"q{q}_sf{sf:g}"] = {"ms": ms, "rows_per_s": rows / (ms * 1e-3)}
         for v in t.values():
             v.free()
+        # config 5 (one worker's share: SF100 / 8 GPUs): Q5 / Q9 on the C++ worker
+        # runtime with the tables in the pinned Host tier and a Device budget of a
+        # quarter of the data, so scans go through load_to_device / preload and
+        # holders spill (PCIe-bound by design)
+        from paper_2508_05029_b200.ops import engine_run_query
+        sf5 = args.spill_sf
+        for q in (5, 9):
+            names = queries.QUERY_TABLES[q]
+            host = {}
+            for n in names:
+                d = ctx.datagen(queries.TABLE_IDS[n], sf5)
+                host[queries.TABLE_IDS[n]] = d.to_host()
+                d.free()
+            data_bytes = sum(b.nbytes() for b in host.values())
+            rows = sum(b.rows for b in host.values())
+            runs = []
+            for _ in range(2):
+                _, m = engine_run_query(ctx, q, host, compute_threads=4, preload=1, batch_rows=4 << 20,
+                                        device_budget=max(data_bytes // 4, 1 << 30))
+                runs.append(m)
+            m = runs[-1]
+            suite[f"q{q}_engine_hosttier_sf{sf5:g}"] = {
+                "ms": m["run_ms"], "rows_per_s": rows / (m["run_ms"] * 1e-3), "host_tier_bytes": data_bytes,
+                "device_budget": m["device_capacity"], "loads": m["loads"], "preloads": m["preloads"],
+                "spills": m["spills"], "spill_bytes": m["spill_bytes"], "h2d_bytes": m["load_bytes"],
+                "h2d_gbs": m["load_bytes"] / (m["run_ms"] * 1e-3) / 1e9, "oom_retries": m["oom_retries"],
+                "tasks": m["tasks"], "timing": "host wall clock of tq_engine_run_query's run phase"}
+            del host
     # config 4: distributed shuffle join
     uid = [Comm.unique_id() if rank == 0 else None]
     if world > 1:
@@ -424,6 +452,7 @@ def main():
     ap.add_argument("--impl", default="tq", choices=["tq", "reference"])
     ap.add_argument("--suite", type=int, default=1, help="also time the other BASELINE configs")
     ap.add_argument("--shuffle-sf", type=float, default=100.0, help="total SF of the config-4 shuffle join")
+    ap.add_argument("--spill-sf", type=float, default=12.5, help="SF of the config-5 Host-tier engine runs")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

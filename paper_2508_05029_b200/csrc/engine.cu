@@ -1074,6 +1074,8 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
       s->out->close();
     }
     if (rt.capacity) c->budget = rt.capacity;
+    const auto t_run = Clock::now();
+    const double setup_ms = std::chrono::duration<double, std::milli>(t_run - t0).count();
     try {
       rt.run();
     } catch (...) {
@@ -1092,9 +1094,10 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
     rt.load(r, c->stream, false);
     check(tq_batch_download(c, &r->dev, result, nullptr));
     double wall = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+    double run_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_run).count();
     if (metrics_json && cap) {
       std::ostringstream js;
-      js << "{\"wall_ms\": " << wall << ", \"tasks\": " << rt.m_tasks << ", \"oom_retries\": " << rt.m_retries
+      js << "{\"wall_ms\": " << wall << ", \"setup_ms\": " << setup_ms << ", \"run_ms\": " << run_ms << ", \"tasks\": " << rt.m_tasks << ", \"oom_retries\": " << rt.m_retries
          << ", \"splits\": " << rt.m_splits << ", \"spills\": " << rt.m_spills << ", \"spill_bytes\": " << rt.m_spill_bytes
          << ", \"loads\": " << rt.m_loads << ", \"preloads\": " << rt.m_preloads << ", \"load_bytes\": " << rt.m_load_bytes
          << ", \"peak_device_bytes\": " << rt.m_peak << ", \"device_capacity\": " << rt.capacity << ", \"ops\": {";

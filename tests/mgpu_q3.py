@@ -24,7 +24,14 @@ def main():
     sf = float(os.environ.get("TQ_SF", "0.1"))
     t = {name: ctx.datagen(queries.TABLE_IDS[name], sf, shard=rank, nshards=world)
          for name in ("customer", "orders", "lineitem")}
-    out = queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], lip=os.environ.get("TQ_LIP", "1") == "1").to_host()
+    if os.environ.get("TQ_ENGINE") == "1":
+        # the C++ worker runtime with ExchangeOps (broadcast customer_f, hash orders_f / lineitem_f)
+        from paper_2508_05029_b200.ops import engine_run_query
+        out, m = engine_run_query(ctx, 3, {queries.TABLE_IDS[k]: v for k, v in t.items()}, comm=comm,
+                                  compute_threads=4, batch_rows=256 * 1024)
+    else:
+        out = queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"],
+                                     lip=os.environ.get("TQ_LIP", "1") == "1").to_host()
     parts = [None] * world
     dist.all_gather_object(parts, out)
     rc = 0
