@@ -241,7 +241,7 @@ def run_suite(args, ctx, world, rank, stream):
             runs = []
             for _ in range(2):
                 _, m = engine_run_query(ctx, q, host, compute_threads=4, preload=1, batch_rows=4 << 20,
-                                        device_budget=max(data_bytes // 4, 1 << 30))
+                                        device_budget=max(int(data_bytes / 2.5), 1 << 30))
                 runs.append(m)
             m = runs[-1]
             suite[f"q{q}_engine_hosttier_sf{sf5:g}"] = {

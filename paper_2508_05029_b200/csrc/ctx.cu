@@ -161,6 +161,7 @@ void tq_ctx_destroy(tq_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (auto& kv : c->prog_cache) cudaFree(kv.second);
+  if (c->host_pool && c->host_pool_free) c->host_pool_free(c->host_pool);
   cudaFreeHost(c->pinned);
   cudaStreamDestroy(c->stream);
   delete c;

@@ -26,6 +26,10 @@ struct tq_ctx {
   // optional per-kernel CUDA-event timing (tq_profile_*): events recorded on
   // the launching stream around each pipeline kernel
   bool jit = true;                      // NVRTC-specialised pipeline kernels (jit.cu)
+  // Host tier kept across engine runs (pinning GBs of memory takes seconds)
+  void* host_pool = nullptr;
+  uint64_t host_pool_buffers = 0, host_pool_buffer_size = 0;
+  void (*host_pool_free)(void*) = nullptr;
   std::atomic<uint64_t> jit_launches{0};
   bool profiling = false;
   struct Ev {

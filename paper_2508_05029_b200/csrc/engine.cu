@@ -223,6 +223,7 @@ class Runtime {
   std::vector<std::weak_ptr<Handle>> registry;
   uint64_t next_id = 0, next_seq = 0, reserved = 0;
   int running_tasks = 0;
+  int executing = 0;  // tasks past their reservation (the ones that can free memory)
   bool stop = false;
   std::exception_ptr error;
   int exchange_turn = 0;  // collectives run in DAG order on every worker
@@ -321,15 +322,17 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
     if (capacity) {
       while (device_in_use() + reserved + want > capacity) {
         if (make_room(reserved + want, capacity)) break;
-        if (running_tasks <= 1) break;  // nobody else will free memory: try, on_oom on failure
+        if (executing == 0) break;  // nobody can free memory: try it, on_oom on failure
         cv.wait_for(g, std::chrono::milliseconds(2));
       }
     }
     reserved += want;
+    executing++;
     for (HP& h : t.inputs) h->pins++;
   }
   auto release = [&] {
     std::lock_guard<std::mutex> g(mu);
+    executing--;
     reserved -= want;
     for (HP& h : t.inputs) h->pins--;
     cv.notify_all();
@@ -346,6 +349,9 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
       std::lock_guard<std::mutex> g(mu);
       Task r = t;
       r.estimate = t.estimate * 2;
+      // the Device may be full of other operators' data: spill what we can first
+      make_room(capacity, capacity);
+      if (r.estimate > capacity && t.attempt <= 3 && executing > 0) r.estimate = capacity;  // wait for others
       if (capacity == 0 || r.estimate <= capacity) {
         r.attempt++;
         m_retries++;
@@ -495,7 +501,7 @@ Runtime::~Runtime() {
       h->host = nullptr;
       h->dev.cols = nullptr;
     }
-  if (pool) tq_pool_destroy(pool);
+  // the pool belongs to the context (reused by the next query)
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (preload_stream) cudaStreamDestroy(preload_stream);
 }
@@ -504,8 +510,21 @@ void Runtime::setup() {
   cudaSetDevice(ctx->device);
   cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&preload_stream, cudaStreamNonBlocking);
-  if (opts.pool_capacity) check(tq_pool_create(opts.pool_buffer_size ? opts.pool_buffer_size : (1 << 20),
-                                               opts.pool_capacity, &pool));
+  if (opts.pool_capacity) {
+    const uint64_t bs = opts.pool_buffer_size ? opts.pool_buffer_size : (1 << 20);
+    if (ctx->host_pool && ctx->host_pool_buffer_size == bs && ctx->host_pool_buffers >= opts.pool_capacity &&
+        tq_pool_free_count((tq_pool*)ctx->host_pool) == ctx->host_pool_buffers) {
+      pool = (tq_pool*)ctx->host_pool;  // reuse the context's pinned Host tier
+    } else {
+      if (ctx->host_pool) ctx->host_pool_free(ctx->host_pool);
+      ctx->host_pool = nullptr;
+      check(tq_pool_create(bs, opts.pool_capacity, &pool));
+      ctx->host_pool = pool;
+      ctx->host_pool_buffers = opts.pool_capacity;
+      ctx->host_pool_buffer_size = bs;
+      ctx->host_pool_free = [](void* p) { tq_pool_destroy((tq_pool*)p); };
+    }
+  }
 }
 
 // ------------------------------------------------------------------ operators

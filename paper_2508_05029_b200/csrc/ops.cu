@@ -411,7 +411,11 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
 
   uint64_t row_bytes = 0;
   for (auto& sc : sch) row_bytes += width_of(sc.kind);
-  const bool probe1 = A.mode == MAT_PROBE && A.table->jt.unique && in->rows * row_bytes <= (8ull << 30);
+  // single-pass probe needs a worst-case (one match per probe row) output buffer:
+  // only when it is small against the Device budget left
+  uint64_t cap_bytes = in->rows * row_bytes;
+  uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
+  const bool probe1 = A.mode == MAT_PROBE && A.table->jt.unique && cap_bytes <= (8ull << 30) && cap_bytes * 4 <= room;
   if (probe1) {
     // single pass: capacity = probe rows (<= 1 match each), exact size read back
     p.dest_kind = DEST_PROBE1;
