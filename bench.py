@@ -50,52 +50,64 @@ def ncu_traffic(kernel: str):
 
 
 class Clocks:
-    """SM clocks and throttle reasons sampled DURING the timed region (NVML in a
-    background thread every 2 ms; the B200_PROFILING.md clocks line)."""
+    """SM clocks and throttle reasons sampled DURING the timed region by an
+    nvidia-smi subprocess (B200_PROFILING.md clocks line), started by rank 0
+    only and covering every GPU of the job: in-process NVML polling from each
+    rank stalls the other ranks' CUDA calls."""
 
-    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
-        self.device = device
-        self.samples, self.reasons, self.max = [], set(), None
-        self._stop = None
-        self._t = None
+    def __init__(self, devices, period_ms: int = 20):
+        self.devices = devices
+        self.period = period_ms
+        self.proc = None
 
     def start(self):
-        import threading
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
-            self.max = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-        except Exception:
+        if os.environ.get("TQ_BENCH_CLOCKS", "1") == "0":
             return
-        self._stop = threading.Event()
-
-        def loop():
-            while not self._stop.is_set():
+        try:
+            import torch
+            ids = []
+            for d in self.devices:  # UUIDs: CUDA_VISIBLE_DEVICES ordinals are not nvidia-smi indices
                 try:
-                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
-                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    for n, bit in self.REASONS.items():
-                        if r & bit:
-                            self.reasons.add(n)
+                    ids.append("GPU-" + str(torch.cuda.get_device_properties(d).uuid))
                 except Exception:
-                    pass
-                self._stop.wait(0.002)
-
-        self._t = threading.Thread(target=loop, daemon=True)
-        self._t.start()
+                    ids.append(str(d))
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", ",".join(ids), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", str(self.period)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
 
     def stop(self):
-        if not self._t:
+        if not self.proc:
             return None
-        self._stop.set()
-        self._t.join()
-        if not self.samples:
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
             return None
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
-                "samples": len(self.samples), "source": "nvml"}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": f"nvidia-smi -lms {self.period} (rank 0, all GPUs)"}
 
 
 def dist_setup():
@@ -123,6 +135,16 @@ def max_over_ranks(world, x: float) -> float:
     t = torch.tensor([x], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_ranks(world, x: float) -> list:
+    if world == 1:
+        return [x]
+    import torch
+    import torch.distributed as dist
+    out = [None] * world
+    dist.all_gather_object(out, x)
+    return out
 
 
 def sum_over_ranks(world, x: float) -> float:
@@ -304,8 +326,10 @@ def run_tq(args, world, rank, local):
         step().free()
     ctx.sync()
     barrier(world)
-    clocks = Clocks(local)
-    clocks.start()
+    clocks = Clocks(list(range(world)) if world > 1 else [local])
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)  # nvidia-smi start-up, so samples land inside the timed region
     ctx.profile(True)
     l0 = ctx.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -324,6 +348,7 @@ def run_tq(args, world, rank, local):
     ck = clocks.stop()
     barrier(world)
     ms_max = max_over_ranks(world, ms)
+    ms_ranks = gather_ranks(world, round(ms, 4))
     total_rows = sum_over_ranks(world, float(rows))
     result = outs[-1].to_host()
     for o in outs:
@@ -412,6 +437,7 @@ def run_tq(args, world, rank, local):
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_max,
+        "ms_per_step_by_rank": ms_ranks,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,

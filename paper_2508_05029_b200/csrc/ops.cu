@@ -616,13 +616,17 @@ struct FinalParams {
   unsigned long long* counter;
 };
 
-__global__ void k_agg_init(AggTable t, u32 nacc, AccSpec* specs_dev_unused, u64 n_acc_words, const uint8_t* ops) {
+struct AccOps {
+  uint8_t op[kMaxAcc];
+};
+
+__global__ void k_agg_init(AggTable t, u32 nacc, AccOps ops) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 j = i; j < t.cap; j += stride) t.state[j] = 0;
   for (u64 j = i; j < t.cap * nacc; j += stride) {
     u64 lo, hi;
-    uint8_t op = ops[j % nacc];
+    uint8_t op = ops.op[j % nacc];
     switch (op) {
       case ACC_MIN_I: lo = ~0ull; hi = 0x7fffffffffffffffull; break;
       case ACC_MAX_I: lo = 0; hi = 0x8000000000000000ull; break;
@@ -633,8 +637,6 @@ __global__ void k_agg_init(AggTable t, u32 nacc, AccSpec* specs_dev_unused, u64 
     t.acc[2 * j] = lo;
     t.acc[2 * j + 1] = hi;
   }
-  (void)specs_dev_unused;
-  (void)n_acc_words;
 }
 
 __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
@@ -831,13 +833,8 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
   // initial table for min(rows, 1M) groups at load <= 0.5
   uint64_t cap = 1024;
   while (cap < std::min<uint64_t>(in->rows, 1ull << 20) * 2) cap <<= 1;
-  uint8_t* ops_dev = (uint8_t*)dalloc(c, 64, st);
-  {
-    uint8_t ops[kMaxAcc] = {};
-    for (u32 i = 0; i < nacc; ++i) ops[i] = acc[i].op;
-    TQ_CUDA(cudaMemcpyAsync(ops_dev, ops, kMaxAcc, cudaMemcpyHostToDevice, st));
-    TQ_CUDA(cudaStreamSynchronize(st));
-  }
+  AccOps ops{};  // by value: no host sync before the pipeline launch
+  for (u32 i = 0; i < nacc; ++i) ops.op[i] = acc[i].op;
   uint64_t ngroups = 0;
   AggTable t{};
   uint64_t tbytes = 0;
@@ -853,7 +850,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     t.overflow = (uint32_t*)(tail + 8);
     TQ_CUDA(cudaMemsetAsync(tail, 0, 16, st));
     u32 ib = (u32)std::min<uint64_t>(4096, (cap * std::max<u32>(1, nacc) + 255) / 256);
-    k_agg_init<<<ib, 256, 0, st>>>(t, nacc, nullptr, 0, ops_dev);
+    k_agg_init<<<ib, 256, 0, st>>>(t, nacc, ops);
     counted_launch(c);
     TQ_CUDA(cudaGetLastError());
     p.agg = t;
@@ -868,10 +865,9 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     }
     if (!ovf) break;
     dfree(c, base, tbytes, st);
-    if (attempt > 12) { dfree(c, ops_dev, 64, st); fail(TQ_RESERVATION_EXCEEDED, "aggregation table overflow"); }
+    if (attempt > 12) fail(TQ_RESERVATION_EXCEEDED, "aggregation table overflow");
     cap *= 4;
   }
-  dfree(c, ops_dev, 64, st);
   uint8_t* tbase = (uint8_t*)t.state;
   // ---- output batch
   std::vector<tq_column> sch;
