@@ -310,7 +310,9 @@ struct InterpP {
   __device__ __forceinline__ static uint8_t acc_op(const PipeParams& p, u32 a) { return p.acc[a].op; }
   __device__ __forceinline__ static u32 acc_plane(const PipeParams& p, u32 a) { return p.acc_plane[a]; }
 
-  __device__ __forceinline__ static u32 tile_begin(WCtx& w, const DInstr* code, u32* pm) {
+  struct Raw {};  // the interpreter reads the stage directly (held until the tile ends)
+  __device__ __forceinline__ static void load(const WCtx&, int, Raw&) {}
+  __device__ __forceinline__ static u32 tile_begin(WCtx& w, const DInstr* code, u32* pm, const Raw*) {
     const PipeParams& p = *w.p;
     run_code(w, code, 0, p.npred);
     u32 any = 0;
@@ -322,8 +324,10 @@ struct InterpP {
     if (any) run_code(w, code, p.npred, p.ncode);
     return any;
   }
-  __device__ __forceinline__ static bool keys(const WCtx& w, int v, u64* kw) { return key_words(w, v, kw); }
-  __device__ __forceinline__ static void accs(const WCtx& w, int v, RowVals& x) {
+  __device__ __forceinline__ static bool keys(const WCtx& w, int v, u64* kw, const Raw&) {
+    return key_words(w, v, kw);
+  }
+  __device__ __forceinline__ static void accs(const WCtx& w, int v, RowVals& x, const Raw&) {
     const PipeParams& p = *w.p;
     for (u32 a = 0; a < p.nacc; ++a) {
       const AccSpec& as = p.acc[a];
@@ -343,7 +347,7 @@ struct InterpP {
       x.av[a] = valid;
     }
   }
-  __device__ __forceinline__ static void store(const WCtx& w, int v, u64 pos, long long brow) {
+  __device__ __forceinline__ static void store(const WCtx& w, int v, u64 pos, long long brow, const Raw&) {
     const PipeParams& p = *w.p;
     for (u32 c = 0; c < p.nout; ++c) store_out(p.out[c], pos, w, v, brow);
   }

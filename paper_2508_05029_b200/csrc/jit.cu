@@ -111,10 +111,19 @@ struct Gen {
 
   Gen(const PipeParams& p_, const std::vector<DInstr>& c_, const std::vector<DLit>& l_) : p(p_), code(c_), lits(l_) {}
 
-  std::string col_base(int c) { return "(w.stage + " + std::to_string(p.cols[c].off) + "u)"; }
+  // staged column c of the current row, already in registers (struct Raw)
+  std::string col_val(int c) { return "R.c" + std::to_string(c); }
   std::string col_valid(int c) {
     if (!p.cols[c].validity) return "true";
-    return "((((const u32*)(w.stage + " + std::to_string(p.cols[c].voff) + "u))[(w.row0 >> 5) + v] >> w.lane) & 1u)";
+    return "R.v" + std::to_string(c);
+  }
+  static const char* raw_type(uint8_t kind) {
+    switch (kind) {
+      case TQ_FLOAT64: return "double";
+      case TQ_BOOL: return "uint8_t";
+      case TQ_DECIMAL: return "i128";
+      default: return "long long";
+    }
   }
   std::string lit_i(int i) { return "mk128(" + hex64(lits[i].lo) + ", " + hex64(lits[i].hi) + ")"; }
   bool lit_fits64(int i) {
@@ -127,11 +136,11 @@ struct Gen {
     is64 = false;
     switch (k) {
       case K_COL_I64: valid = col_valid(idx); is64 = true;
-        return "((const long long*)" + col_base(idx) + ")[r]";
+        return col_val(idx);
       case K_COL_DEC: valid = col_valid(idx);
-        return "ld_dec(" + col_base(idx) + ", r)";
+        return col_val(idx);
       case K_COL_BOOL: valid = col_valid(idx); is64 = true;
-        return "(long long)(" + col_base(idx) + "[r] != 0)";
+        return "(long long)(" + col_val(idx) + " != 0)";
       case K_TMP_I: valid = vn[idx]; is64 = v64[idx]; return vv[idx];
       case K_TMP_B: valid = bn[idx]; is64 = true; return "(long long)" + bv[idx];
       case K_LIT_I: case K_LIT_B:
@@ -144,7 +153,7 @@ struct Gen {
   std::string as128(const std::string& e, bool is64) { return is64 ? "((i128)(" + e + "))" : e; }
   std::string opnd_f(uint8_t k, uint16_t idx, uint8_t scale, std::string& valid) {
     switch (k) {
-      case K_COL_F64: valid = col_valid(idx); return "((const double*)" + col_base(idx) + ")[r]";
+      case K_COL_F64: valid = col_valid(idx); return col_val(idx);
       case K_TMP_F: valid = vn[idx]; return vv[idx];
       case K_LIT_F: {
         valid = lits[idx].valid ? "true" : "false";
@@ -293,9 +302,34 @@ struct Gen {
     for (int a = 0; a < nacc; ++a) os << " case " << a << ": return " << (int)p.acc_plane[a] << ";";
     os << " default: return 0; }\n  }\n";
     // ---- predicate
-    os << "  __device__ __forceinline__ static u32 tile_begin(WCtx& w, const DInstr*, u32* pm) {\n"
+    // ---- the row's staged columns, copied out of the stage into registers
+    os << "  struct Raw {";
+    for (u32 c = 0; c < p.nstaged; ++c) {
+      os << " " << raw_type(p.cols[c].kind) << " c" << c << ";";
+      if (p.cols[c].validity) os << " bool v" << c << ";";
+    }
+    os << " };\n";
+    os << "  __device__ __forceinline__ static void load(const WCtx& w, int v, Raw& R) {\n"
+          "    const u32 r = trow(w, v);\n    (void)r;\n";
+    for (u32 c = 0; c < p.nstaged; ++c) {
+      const std::string base = "(w.stage + " + std::to_string(p.cols[c].off) + "u)";
+      const std::string f = "R.c" + std::to_string(c);
+      if (!((p.load_mask >> c) & 1)) {  // not loaded by this launch: dead in the generated code
+        os << "    " << f << " = 0;\n";
+        if (p.cols[c].validity) os << "    R.v" << c << " = false;\n";
+        continue;
+      }
+      if (p.cols[c].kind == TQ_DECIMAL) os << "    " << f << " = ld_dec(" << base << ", r);\n";
+      else
+        os << "    " << f << " = ((const " << raw_type(p.cols[c].kind) << "*)" << base << ")[r];\n";
+      if (p.cols[c].validity)
+        os << "    R.v" << c << " = (((const u32*)(w.stage + " << p.cols[c].voff
+           << "u))[(w.row0 >> 5) + v] >> w.lane) & 1u;\n";
+    }
+    os << "  }\n";
+    os << "  __device__ __forceinline__ static u32 tile_begin(WCtx& w, const DInstr*, u32* pm, const Raw* Rs) {\n"
           "    u32 any = 0;\n#pragma unroll\n    for (int v = 0; v < kV; ++v) {\n      const u32 r = trow(w, v);\n"
-          "      bool pass = r < w.nrows;\n";
+          "      const Raw& R = Rs[v];\n      (void)R;\n      bool pass = r < w.nrows;\n";
     if (p.pred_kind != K_NONE) {
       os << "      if (pass) {\n";
       Gen g(p, code, lits);
@@ -307,7 +341,8 @@ struct Gen {
     }
     os << "      pm[v] = __ballot_sync(kFull, pass);\n      any |= pm[v];\n    }\n    return any;\n  }\n";
     // ---- keys
-    os << "  __device__ __forceinline__ static bool keys(const WCtx& w, int v, u64* kw) {\n    const u32 r = trow(w, v);\n";
+    os << "  __device__ __forceinline__ static bool keys(const WCtx& w, int v, u64* kw, const Raw& R) {\n"
+          "    const u32 r = trow(w, v);\n    (void)r; (void)R;\n";
     if (p.nkeys) {
       Gen g(p, code, lits);
       g.body((int)code.size());
@@ -335,7 +370,8 @@ struct Gen {
       os << "    (void)r; kw[0] = 0; return false;\n  }\n";
     }
     // ---- aggregate inputs
-    os << "  __device__ __forceinline__ static void accs(const WCtx& w, int v, RowVals& x) {\n    const u32 r = trow(w, v);\n";
+    os << "  __device__ __forceinline__ static void accs(const WCtx& w, int v, RowVals& x, const Raw& R) {\n"
+          "    const u32 r = trow(w, v);\n    (void)R;\n";
     if (sink == SINK_AGG && nacc) {
       Gen g(p, code, lits);
       g.body((int)code.size());
@@ -363,8 +399,8 @@ struct Gen {
     }
     os << "  }\n";
     // ---- materialised outputs
-    os << "  __device__ __forceinline__ static void store(const WCtx& w, int v, u64 pos, long long brow) {\n"
-          "    const u32 r = trow(w, v);\n    const PipeParams& p = *w.p;\n";
+    os << "  __device__ __forceinline__ static void store(const WCtx& w, int v, u64 pos, long long brow, const Raw& R) "
+          "{\n    const u32 r = trow(w, v);\n    const PipeParams& p = *w.p;\n    (void)R;\n";
     if (sink == SINK_EMIT && p.nout) {
       Gen g(p, code, lits);
       g.body((int)code.size());
@@ -378,18 +414,23 @@ struct Gen {
         }
         std::string valid;
         switch (o.kind) {
-          case K_COL_I64: case K_COL_F64:
+          case K_COL_I64:
             valid = g.col_valid(o.idx);
-            os << "    *(u64*)(" << oc << ".values + pos * 8) = ((const u64*)" << g.col_base(o.idx) << ")[r];\n";
+            os << "    *(u64*)(" << oc << ".values + pos * 8) = (u64)" << g.col_val(o.idx) << ";\n";
+            break;
+          case K_COL_F64:
+            valid = g.col_valid(o.idx);
+            os << "    *(u64*)(" << oc << ".values + pos * 8) = (u64)__double_as_longlong(" << g.col_val(o.idx)
+               << ");\n";
             break;
           case K_COL_DEC:
             valid = g.col_valid(o.idx);
-            os << "    *(ulonglong2*)(" << oc << ".values + pos * 16) = ((const ulonglong2*)" << g.col_base(o.idx)
-               << ")[r];\n";
+            os << "    *(ulonglong2*)(" << oc << ".values + pos * 16) = make_ulonglong2(lo64(" << g.col_val(o.idx)
+               << "), hi64(" << g.col_val(o.idx) << "));\n";
             break;
           case K_COL_BOOL:
             valid = g.col_valid(o.idx);
-            os << "    " << oc << ".values[pos] = " << g.col_base(o.idx) << "[r];\n";
+            os << "    " << oc << ".values[pos] = " << g.col_val(o.idx) << ";\n";
             break;
           case K_TMP_F: case K_LIT_F: {
             std::string e = g.opnd_f(o.kind, o.idx, 0, valid);

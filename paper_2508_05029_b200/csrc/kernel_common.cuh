@@ -79,6 +79,18 @@ __device__ __forceinline__ u32 jt_count(const JoinTable& t, const u64* kw) {
 // ------------------------------------------------------------------ aggregation tables
 constexpr u32 kStEmpty = 0, kStBusy = 1, kStReady = 2;
 
+// 32-bit multiplicative hash for the small per-CTA group tables (full keys
+// are compared on every hit, so only the spread matters here).
+__device__ __forceinline__ u64 local_hash(const u64* kw, int n) {
+  u32 x = 0;
+#pragma unroll
+  for (int i = 0; i < kMaxKeyWords + 1; ++i) {
+    if (i >= n) break;
+    x = (x ^ (u32)kw[i] ^ (u32)(kw[i] >> 32)) * 0x9E3779B1u;
+  }
+  return x ^ (x >> 15);
+}
+
 // Find-or-insert `kw` (kwa words) in a state/keys open-addressing table.
 // Returns slot or -1 when `limit` probes found neither the key nor a free slot.
 template <int KWA>
@@ -260,10 +272,9 @@ __device__ __forceinline__ bool tile_needs_manual(const PipeParams& p, u32 tile)
 // every consumer warp has arrived on empty[s].
 __device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint64_t* full, uint64_t* empty,
                                         u32 lane) {
-  u32 k = 0;
+  u32 k = 0, s = 0, ph = 0;
   for (u32 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++k) {
-    const u32 s = k % p.nstages;
-    if (k >= p.nstages) mbar_wait(&empty[s], ((k / p.nstages) - 1) & 1);
+    if (k >= p.nstages) mbar_wait(&empty[s], ph ^ 1u);
     uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
     if (tile_needs_manual(p, tile)) {
       manual_tile(p, stage, tile, lane);
@@ -274,6 +285,7 @@ __device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint
       issue_tile(p, stage, &full[s], tile);
     }
     __syncwarp();
+    if (++s == p.nstages) { s = 0; ph ^= 1u; }
   }
 }
 
@@ -348,18 +360,28 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   w.lane = lane;
 
   const u32 first = blockIdx.x, step = gridDim.x;
-  u32 k = 0;
-  for (u32 tile = first; tile < p.ntiles; tile += step, ++k) {
-    const u32 s = k % p.nstages;
+  u32 s = 0, ph = 0;
+  for (u32 tile = first; tile < p.ntiles; tile += step) {
     uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
-    mbar_wait(&full[s], (k / p.nstages) & 1);
+    mbar_wait(&full[s], ph);
     const u64 r0 = (u64)tile * kTile;
     w.stage = stage;
     w.nrows = (u32)min((u64)kTile, p.rows - r0);
 
+    // ---- generated programs copy the row's staged columns into registers
+    // and hand the stage back at once (the next tile's copy overlaps all of
+    // this tile's work); the interpreter reads the stage until the tile ends
+    typename P::Raw raw[kV];
+    if (!P::kInterp) {
+#pragma unroll
+      for (int v = 0; v < kV; ++v) P::load(w, v, raw[v]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
     // ---- predicate per row, then the rest of the program
     u32 pm[kV];
-    u32 any = P::tile_begin(w, s_code, pm);
+    u32 any = P::tile_begin(w, s_code, pm, raw);
 
     if ((SINK == SINK_COUNT || SINK == SINK_EMIT) && p.dest_kind == DEST_PROBE1) {
       // single pass: unique build keys -> at most one match per probe row
@@ -369,14 +391,14 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         long long brow = -1;
         if (pass) {
           u64 kw[kMaxKeyWords + 1];
-          if (!P::keys(w, v, kw)) brow = jt_probe_first<P::kKw>(p.jt, kw);
+          if (!P::keys(w, v, kw, raw[v])) brow = jt_probe_first<P::kKw>(p.jt, kw);
         }
         const u32 mm = __ballot_sync(kFull, brow >= 0);
         if (mm) {
           unsigned long long base = 0;
           if (lane == 0) base = atomicAdd(p.cursor, (unsigned long long)__popc(mm));
           base = __shfl_sync(kFull, base, 0);
-          if (brow >= 0) P::store(w, v, base + __popc(mm & lanemask_lt()), brow);
+          if (brow >= 0) P::store(w, v, base + __popc(mm & lanemask_lt()), brow, raw[v]);
         }
       }
     } else if (SINK == SINK_COUNT || SINK == SINK_EMIT) {
@@ -393,7 +415,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         mult[v] = pass ? 1u : 0u;
         if (pass && p.dest_kind != DEST_FILTER) {
           u64 kw[kMaxKeyWords + 1];
-          bool has_null = P::keys(w, v, kw);
+          bool has_null = P::keys(w, v, kw, raw[v]);
           if (p.dest_kind == DEST_PARTITION && p.semi_bloom) {
             // Lookahead Information Passing: a key absent from the (global)
             // build-side Bloom filter cannot join -> never shipped
@@ -450,7 +472,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
             __syncwarp();
             if (m) {
               u64 kw[kMaxKeyWords + 1];
-              P::keys(w, v, kw);
+              P::keys(w, v, kw, raw[v]);
               const JoinTable& t = p.jt;
               const u64 mask = t.cap - 1;
               u64 sl = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw) & mask;
@@ -459,7 +481,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
                 long long brow = e[0];
                 if (brow < 0) break;
                 if (jt_key_eq<P::kKw>(t, e, kw)) {
-                  P::store(w, v, pos, brow);
+                  P::store(w, v, pos, brow, raw[v]);
                   ++pos;
                 }
                 sl = (sl + 1) & mask;
@@ -476,7 +498,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
             __syncwarp();
             if (pass && (peers & lanemask_lt()) == 0) wb[dest[v]] += __popc(peers);
             __syncwarp();
-            if (pass) P::store(w, v, pos, -1);
+            if (pass) P::store(w, v, pos, -1, raw[v]);
           }
         }
       }
@@ -486,11 +508,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       bool ok[kV];
 #pragma unroll
       for (int v = 0; v < kV; ++v) {
-        ok[v] = ((pm[v] >> lane) & 1u) && !P::keys(w, v, kws[v]);  // null keys never match
-      }
-      if (!P::kInterp) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        ok[v] = ((pm[v] >> lane) & 1u) && !P::keys(w, v, kws[v], raw[v]);  // null keys never match
       }
 #pragma unroll
       for (int v = 0; v < kV; ++v) {
@@ -525,21 +543,20 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
 #pragma unroll
       for (int v = 0; v < kV; ++v)
         if ((pm[v] >> lane) & 1u) {
-          P::keys(w, v, xs[v].kw);
-          P::accs(w, v, xs[v]);
+          P::keys(w, v, xs[v].kw, raw[v]);
+          P::accs(w, v, xs[v], raw[v]);
         }
-      if (!P::kInterp) {  // the interpreter keeps the stage until the end of the tile
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-      }
       if (any) {
 #pragma unroll
         for (int v = 0; v < kV; ++v) {
           bool pass = (pm[v] >> lane) & 1u;
           if (!pass) continue;
           RowVals& x = xs[v];
-          const u64 h = key_hash(x.kw, (int)kwa);
-          long long ls = G ? table_find_insert<KWA>(l_state, l_keys, G, kwa, x.kw, h, G, nullptr) : -1;
+          // cheap 32-bit hash for the CTA-local table; the global table's
+          // key_hash is only computed on the (rare) paths that reach it
+          long long ls = G ? table_find_insert<KWA>(l_state, l_keys, G, kwa, x.kw, local_hash(x.kw, (int)kwa), G,
+                                                    nullptr)
+                           : -1;
           if (ls >= 0) {
             // per-lane private accumulation (no atomics, no cross-lane traffic)
 #pragma unroll
@@ -562,7 +579,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
                     }
                   }
                   // escape: the exact int128 partial goes straight to the global table
-                  long long gs = agg_global_slot<KWA>(p, x.kw, kwa, h);
+                  long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa));
                   if (gs >= 0) atomic_add_i128(p.agg.acc + ((u64)gs * nacc + a) * 2, add128((i128)cur, xi));
                   pl[0] = 0;
                   break;
@@ -587,7 +604,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
             }
           } else {
             // local table full: this group lives only in the global table
-            long long gs = agg_global_slot<KWA>(p, x.kw, kwa, h);
+            long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa));
             if (gs < 0) continue;
 #pragma unroll
             for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
@@ -600,11 +617,12 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       }
     }
 
-    // stage s consumed by this warp (JIT AGG / BUILD released it above)
-    if (SINK == SINK_COUNT || SINK == SINK_EMIT || P::kInterp) {
+    // stage s consumed by this warp (generated programs released it above)
+    if (P::kInterp) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
+    if (++s == p.nstages) { s = 0; ph ^= 1u; }
   }
 
   if (SINK == SINK_AGG && G > 0) {

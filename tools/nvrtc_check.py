@@ -2,6 +2,7 @@
 the CPU build box, so codegen errors are caught without a GPU.
 
     python tools/nvrtc_check.py gpurun_out/jitdump/tq_jit_0.cu
+    CUBIN_OUT=/tmp/k.cubin python tools/nvrtc_check.py x.cu && cuobjdump -sass /tmp/k.cubin
 """
 import ctypes as C
 import os
@@ -25,14 +26,22 @@ def compile_src(src: str):
     L.nvrtcGetProgramLogSize(prog, C.byref(n))
     log = C.create_string_buffer(n.value)
     L.nvrtcGetProgramLog(prog, log)
-    return rc, log.value.decode(errors="replace")
+    cubin = None
+    if rc == 0:
+        L.nvrtcGetCUBINSize(prog, C.byref(n))
+        buf = C.create_string_buffer(n.value)
+        L.nvrtcGetCUBIN(prog, buf)
+        cubin = buf.raw
+    return rc, log.value.decode(errors="replace"), cubin
 
 
 if __name__ == "__main__":
     for path in sys.argv[1:]:
         src = open(path).read()
         src = re.sub(r"/\* NVRTC LOG:.*\*/\s*$", "", src, flags=re.S)
-        rc, log = compile_src(src)
+        rc, log, cubin = compile_src(src)
+        if cubin and os.environ.get("CUBIN_OUT"):
+            open(os.environ["CUBIN_OUT"], "wb").write(cubin)
         errs = [l for l in log.splitlines() if "error" in l]
         print(path, "rc", rc, "errors", len(errs))
         for l in errs[:10]:
