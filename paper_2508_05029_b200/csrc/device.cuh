@@ -26,7 +26,12 @@ __device__ __forceinline__ bool fits64(i128 v) { return hi64(v) == (u64)((long l
 
 // Wrapping 128-bit multiply with a 64x64->128 fast path (decimal(11,2)
 // operands and their products almost always fit).
+__device__ __forceinline__ bool fits32(i128 v) {
+  const long long l = (long long)lo64(v);
+  return hi64(v) == (u64)(l >> 63) && l == (long long)(int)l;
+}
 __device__ __forceinline__ i128 mul128(i128 a, i128 b) {
+  if (fits32(a) && fits32(b)) return (i128)((long long)(int)lo64(a) * (long long)(int)lo64(b));
   if (fits64(a) && fits64(b)) {
     long long x = (long long)lo64(a), y = (long long)lo64(b);
     u64 lo = (u64)x * (u64)y;

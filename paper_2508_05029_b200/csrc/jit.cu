@@ -109,6 +109,8 @@ struct Gen {
   std::string vv[kMaxValueSlots], vn[kMaxValueSlots], bv[kMaxBoolSlots], bn[kMaxBoolSlots];
   bool v64[kMaxValueSlots] = {};  // slot value known to fit int64
 
+  int min_blocks = 1;  // resident CTAs per SM the launch plans for (__launch_bounds__)
+
   Gen(const PipeParams& p_, const std::vector<DInstr>& c_, const std::vector<DLit>& l_) : p(p_), code(c_), lits(l_) {}
 
   // staged column c of the current row, already in registers (struct Raw)
@@ -457,7 +459,8 @@ struct Gen {
       os << "    (void)r; (void)p; (void)pos; (void)brow;\n";
     }
     os << "  }\n};\n}  // namespace tq\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(tq::kBlock) tq_jit_main(const __grid_constant__ "
+    os << "extern \"C\" __global__ void __launch_bounds__(tq::kBlock, " << min_blocks
+       << ") tq_jit_main(const __grid_constant__ "
           "tq::PipeParams p) {\n  tq::pipe_body<"
        << sink << ", tq::Gen>(p);\n}\n";
     return os.str();
@@ -540,9 +543,12 @@ cudaError_t launch_pipeline_prog(tq_ctx* c, int sink, const PipeParams& p, u32 s
     put(&p.pred_idx, 2);
     for (u32 c2 = 0; c2 < p.nstaged; ++c2) {
       const StagedCol& sc = p.cols[c2];
-      uint32_t f[4] = {sc.off, sc.voff, sc.width, (uint32_t)(sc.validity != nullptr)};
+      uint32_t f[5] = {sc.off, sc.voff, sc.width, (uint32_t)(sc.validity != nullptr), sc.kind};
       put(f, sizeof f);
     }
+    put(&p.load_mask, 4);
+    const int min_blocks = grid > (u32)c->sms ? 2 : 1;
+    put(&min_blocks, 4);
     put(&p.nkeys, 4);
     put(&p.key_words, 4);
     put(p.keys, sizeof(KeyOpnd) * p.nkeys);
@@ -571,6 +577,7 @@ cudaError_t launch_pipeline_prog(tq_ctx* c, int sink, const PipeParams& p, u32 s
       std::string src;
       try {
         Gen g(p, code, lits);
+        g.min_blocks = min_blocks;
         src = g.source(sink);
       } catch (const Fail&) {
         src.clear();

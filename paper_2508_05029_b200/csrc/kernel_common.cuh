@@ -81,14 +81,61 @@ constexpr u32 kStEmpty = 0, kStBusy = 1, kStReady = 2;
 
 // 32-bit multiplicative hash for the small per-CTA group tables (full keys
 // are compared on every hit, so only the spread matters here).
-__device__ __forceinline__ u64 local_hash(const u64* kw, int n) {
+__device__ __forceinline__ u32 local_hash(const u64* kw, int n) {
   u32 x = 0;
 #pragma unroll
   for (int i = 0; i < kMaxKeyWords + 1; ++i) {
     if (i >= n) break;
     x = (x ^ (u32)kw[i] ^ (u32)(kw[i] >> 32)) * 0x9E3779B1u;
   }
-  return x ^ (x >> 15);
+  return x;
+}
+
+// |v| <= 2^46: 2^16 such values sum to within int64 (per-lane plane bound)
+// (non-zero bits of (v + 2^46) above bit 46, OR-able across values)
+__device__ __forceinline__ u64 plane_excess(i128 v) {
+  const u128 t = (u128)v + ((u128)1 << 46);
+  return (u64)(t >> 64) | ((u64)t >> 47);
+}
+__device__ __forceinline__ bool fits_plane(i128 v) { return plane_excess(v) == 0; }
+
+// Find-or-insert in the per-CTA (shared-memory) group table.  A ready slot's
+// state holds the key's 32-bit hash with bit 1 set (never Empty/Busy), so a
+// probe past a different group costs one shared load; keys are compared only
+// when the tags agree.  Returns the slot or -1 when the table is full.
+template <int KWA>
+__device__ __forceinline__ long long local_find_insert(u32* state, u64* keys, u32 cap, u32 kwa_rt, const u64* kw,
+                                                       u32 h) {
+  const u32 kwa = KWA > 0 ? (u32)KWA : kwa_rt;
+  const u32 tag = h | 2u;
+  const u32 mask = cap - 1;
+  u32 s = (h >> 16) & mask;  // top bits of the multiplicative hash
+  for (u32 probe = 0; probe < cap; ++probe) {
+    volatile u32* st = state + s;
+    u32 cur = *st;
+    if (cur == kStEmpty) {
+      cur = atomicCAS(state + s, kStEmpty, kStBusy);
+      if (cur == kStEmpty) {
+        for (u32 i = 0; i < kwa; ++i) keys[s * kwa + i] = kw[i];
+        __threadfence_block();
+        atomicExch(state + s, tag);
+        return (long long)s;
+      }
+    }
+    while (cur == kStBusy) cur = *st;
+    if (cur == tag) {
+      const volatile u64* k = keys + s * kwa;
+      bool eq = true;
+#pragma unroll
+      for (u32 i = 0; i < (KWA > 0 ? (u32)KWA : (u32)(kMaxKeyWords + 1)); ++i) {
+        if (i >= kwa) break;
+        eq &= k[i] == kw[i];
+      }
+      if (eq) return (long long)s;
+    }
+    s = (s + 1) & mask;
+  }
+  return -1;
 }
 
 // Find-or-insert `kw` (kwa words) in a state/keys open-addressing table.
@@ -320,6 +367,8 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   unsigned long long* s_base = (unsigned long long*)(s_cnt + kWarps * kMaxDest);  // [kWarps][kMaxDest]
   const u32 kwa = KWA > 0 ? (u32)KWA : p.key_words + 1;
   const u32 G = p.local_groups;
+  // rows one lane can add to one accumulator plane in this launch
+  const bool bounded = ((p.ntiles + gridDim.x - 1) / gridDim.x) * (u32)kV <= (1u << 16);
   const u32 nacc = P::nacc(p);
   const u32 nplanes = P::nplanes(p);
   // AGG smem: [state G u32][keys G*kwa u64][gslot G i64][planes G*nplanes*kThreads u64]
@@ -541,11 +590,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       // do the hash-table / accumulator work (keeps more tiles in flight)
       RowVals xs[kV];
 #pragma unroll
-      for (int v = 0; v < kV; ++v)
-        if ((pm[v] >> lane) & 1u) {
-          P::keys(w, v, xs[v].kw, raw[v]);
-          P::accs(w, v, xs[v], raw[v]);
-        }
+      for (int v = 0; v < kV; ++v) {  // for every row: no divergent merge of the values
+        P::keys(w, v, xs[v].kw, raw[v]);
+        P::accs(w, v, xs[v], raw[v]);
+      }
       if (any) {
 #pragma unroll
         for (int v = 0; v < kV; ++v) {
@@ -554,10 +602,46 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           RowVals& x = xs[v];
           // cheap 32-bit hash for the CTA-local table; the global table's
           // key_hash is only computed on the (rare) paths that reach it
-          long long ls = G ? table_find_insert<KWA>(l_state, l_keys, G, kwa, x.kw, local_hash(x.kw, (int)kwa), G,
-                                                    nullptr)
-                           : -1;
-          if (ls >= 0) {
+          long long ls = G ? local_find_insert<KWA>(l_state, l_keys, G, kwa, x.kw, local_hash(x.kw, (int)kwa)) : -1;
+          // bounded planes: when every integer input of the row is within
+          // +-2^46, plain 64-bit adds cannot overflow a plane (<= 2^16 rows per lane)
+          u64 excess = 0;
+#pragma unroll
+          for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
+            if (a >= nacc) break;
+            if (P::acc_op(p, a) == ACC_SUM_I && x.av[a]) excess |= plane_excess(x.ai[a]);
+          }
+          const bool fast = bounded && excess == 0;
+          if (ls >= 0 && fast) {
+            u64* pl0 = l_planes + (u64)ls * nplanes * kThreads + threadIdx.x;
+#pragma unroll
+            for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
+              if (a >= nacc) break;
+              const uint8_t op = P::acc_op(p, a);
+              if (!x.av[a]) continue;
+              u64* pl = pl0 + (u64)P::acc_plane(p, a) * kThreads;
+              switch (op) {
+                case ACC_CNT: pl[0] += 1; break;
+                case ACC_SUM_I: pl[0] += lo64(x.ai[a]); break;
+                case ACC_SUM_F:
+                  pl[0] = (u64)__double_as_longlong(__longlong_as_double((long long)pl[0]) + x.af[a]);
+                  break;
+                case ACC_MIN_I:
+                case ACC_MAX_I: {
+                  i128 c = mk128(pl[0], pl[kThreads]);
+                  if (op == ACC_MIN_I ? x.ai[a] < c : x.ai[a] > c) {
+                    pl[0] = lo64(x.ai[a]);
+                    pl[kThreads] = hi64(x.ai[a]);
+                  }
+                  break;
+                }
+                default: {
+                  double c = __longlong_as_double((long long)pl[0]);
+                  if (op == ACC_MIN_F ? x.af[a] < c : x.af[a] > c) pl[0] = (u64)__double_as_longlong(x.af[a]);
+                }
+              }
+            }
+          } else if (ls >= 0) {
             // per-lane private accumulation (no atomics, no cross-lane traffic)
 #pragma unroll
             for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
@@ -569,6 +653,15 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
                 case ACC_CNT: pl[0] += 1; break;
                 case ACC_SUM_I: {
                   const i128 xi = x.ai[a];
+                  if (bounded) {  // keep the plane bound: large inputs go to the global table exactly
+                    if (fits_plane(xi)) {
+                      pl[0] += lo64(xi);
+                    } else {
+                      long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa));
+                      if (gs >= 0) atomic_add_i128(p.agg.acc + ((u64)gs * nacc + a) * 2, xi);
+                    }
+                    break;
+                  }
                   long long cur = (long long)pl[0];
                   if (fits64(xi)) {
                     long long y = (long long)lo64(xi);
@@ -631,7 +724,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     for (u32 g = warp; g < G; g += kWarps) {
       if (lane == 0) {
         long long gs = -1;
-        if (l_state[g] == kStReady) {
+        if (l_state[g] > kStBusy) {  // ready (holds the key's tag)
           u64 kw[kMaxKeyWords + 1];
           for (u32 i = 0; i < kwa; ++i) kw[i] = l_keys[(u64)g * kwa + i];
           gs = agg_global_slot<KWA>(p, kw, kwa, key_hash(kw, (int)kwa));

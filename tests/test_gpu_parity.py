@@ -138,6 +138,24 @@ def test_aggregate_many_groups(ctx):
     assert_batches_equal(got, want)
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_aggregate_mixed_magnitudes(ctx, seed):
+    """Mostly small sums with rare values beyond 2^46 in the same groups: the
+    per-lane 64-bit planes take the small ones, the large ones go to the
+    global int128 table; sums must still be exact (and wrap like the oracle)."""
+    rng = np.random.default_rng(100 + seed)
+    n = 300000
+    big = rng.random(n) < 0.01
+    iv = np.where(big, rng.integers(-(1 << 62), 1 << 62, n), rng.integers(-1000, 1000, n))
+    dv = np.where(big, rng.integers(-(1 << 62), 1 << 62, n), rng.integers(-10**6, 10**6, n))
+    b = HostBatch(n, [HostBatch.col_i64(rng.integers(0, 6, n)), HostBatch.col_i64(iv),
+                      HostBatch.col_dec(dv.astype(np.int64), 11, 2)])
+    aggs = [(AGG_SUM, 1), (AGG_SUM, 2), (AGG_COUNT_STAR, 0), (AGG_AVG, 2), (AGG_MIN, 2), (AGG_MAX, 1)]
+    got = ctx.aggregate_execute(ctx.upload(b), [0], aggs).to_host()
+    want = O.aggregate_execute(b, [0], aggs)
+    assert_batches_equal(got, want)
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_take_concat_slice_parity(ctx, seed):
     rng = np.random.default_rng(seed)
