@@ -195,6 +195,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, 
       : "memory");
 }
 
+// Bulk prefetch global -> L2 (no shared memory, no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, u32 bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ u32 lanemask_lt() {
   u32 m;

@@ -494,9 +494,11 @@ Entry compile(const std::string& src) {
   }
   std::string dir = csrc_dir();
   std::string inc1 = "-I" + dir, inc2 = "-I" + dir + "/../../include";
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DTQ_JIT=1", "--device-int128", inc1.c_str(),
-                        inc2.c_str()};
-  int rc = n.compile(prog, 7, opts);
+  // the tile geometry this library was built with (pipeline.h)
+  std::string dw = "-DTQ_KWARPS=" + std::to_string(kWarps), dv = "-DTQ_KV=" + std::to_string(kV);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DTQ_JIT=1", "--device-int128",
+                        inc1.c_str(), inc2.c_str(), dw.c_str(), dv.c_str()};
+  int rc = n.compile(prog, 9, opts);
   if (rc != 0) {
     size_t ls = 0;
     n.log_size(prog, &ls);

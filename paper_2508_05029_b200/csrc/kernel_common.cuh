@@ -140,9 +140,16 @@ __device__ __forceinline__ long long local_find_insert(u32* state, u64* keys, u3
 
 // Find-or-insert `kw` (kwa words) in a state/keys open-addressing table.
 // Returns slot or -1 when `limit` probes found neither the key nor a free slot.
-template <int KWA>
+struct NoClaimInit {
+  __device__ __forceinline__ void operator()(u64) const {}
+};
+
+// `init(slot)` runs once, by the claiming thread, before the slot is published
+// (lazy per-slot initialisation: the table needs only its state words zeroed).
+template <int KWA, class Init = NoClaimInit>
 __device__ __forceinline__ long long table_find_insert(u32* state, u64* keys, u64 cap, u32 kwa_rt, const u64* kw,
-                                                       u64 h, u64 limit, unsigned long long* counter) {
+                                                       u64 h, u64 limit, unsigned long long* counter,
+                                                       const Init& init = Init()) {
   const u32 kwa = KWA > 0 ? (u32)KWA : kwa_rt;
   const u64 mask = cap - 1;
   u64 s = h & mask;
@@ -153,6 +160,7 @@ __device__ __forceinline__ long long table_find_insert(u32* state, u64* keys, u6
       cur = atomicCAS(state + s, kStEmpty, kStBusy);
       if (cur == kStEmpty) {
         for (u32 i = 0; i < kwa; ++i) keys[s * kwa + i] = kw[i];
+        init(s);
         __threadfence();
         atomicExch(state + s, kStReady);
         if (counter) atomicAdd(counter, 1ull);
@@ -195,10 +203,23 @@ __device__ __forceinline__ void acc_apply_atomic(uint8_t op, u64* a, i128 xi, do
   }
 }
 
+// a claimed global slot starts from the accumulators' identities
+struct AccClaimInit {
+  const PipeParams& p;
+  __device__ __forceinline__ void operator()(u64 s) const {
+    for (u32 a = 0; a < p.nacc; ++a) {
+      u64 lo, hi;
+      acc_identity(p.acc[a].op, lo, hi);
+      p.agg.acc[(s * p.nacc + a) * 2] = lo;
+      p.agg.acc[(s * p.nacc + a) * 2 + 1] = hi;
+    }
+  }
+};
+
 template <int KWA>
 __device__ __forceinline__ long long agg_global_slot(const PipeParams& p, const u64* kw, u32 kwa, u64 h) {
   long long s = table_find_insert<KWA>(p.agg.state, p.agg.keys, p.agg.cap, kwa, kw, h,
-                                       p.agg.cap < 512 ? p.agg.cap : 512, p.agg.nused);
+                                       p.agg.cap < 512 ? p.agg.cap : 512, p.agg.nused, AccClaimInit{p});
   if (s < 0) atomicExch(p.agg.overflow, 1u);
   return s;
 }
@@ -293,6 +314,19 @@ __device__ __forceinline__ void issue_tile(const PipeParams& p, uint8_t* stage, 
   }
 }
 
+// Warm L2 with a future full tile of this CTA: more bytes in flight than the
+// shared-memory ring holds, so the ring's bulk copies mostly hit L2.
+__device__ __forceinline__ void prefetch_tile(const PipeParams& p, u32 tile) {
+  if (tile >= p.ntiles || p.rows - (u64)tile * kTile < (u64)kTile) return;
+  const u64 r0 = (u64)tile * kTile;
+  for (u32 c = 0; c < p.nstaged; ++c) {
+    const StagedCol& sc = p.cols[c];
+    if (!sc.bulk_ok || !((p.load_mask >> c) & 1)) continue;
+    bulk_prefetch_l2(sc.values + r0 * sc.width, kTile * sc.width);
+    if (sc.validity) bulk_prefetch_l2(sc.validity + r0 / 8, kTile / 8);
+  }
+}
+
 // Plain loads (by the producer warp) for tail tiles and misaligned columns.
 __device__ __forceinline__ void manual_tile(const PipeParams& p, uint8_t* stage, u32 tile, u32 lane) {
   u64 r0 = (u64)tile * kTile;
@@ -320,7 +354,10 @@ __device__ __forceinline__ bool tile_needs_manual(const PipeParams& p, u32 tile)
 __device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint64_t* full, uint64_t* empty,
                                         u32 lane) {
   u32 k = 0, s = 0, ph = 0;
+  if (lane == 0)
+    for (u32 j = p.nstages; j < p.nstages + p.pf_dist; ++j) prefetch_tile(p, blockIdx.x + j * gridDim.x);
   for (u32 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++k) {
+    if (p.pf_dist && lane == 0) prefetch_tile(p, tile + (p.nstages + p.pf_dist) * gridDim.x);
     if (k >= p.nstages) mbar_wait(&empty[s], ph ^ 1u);
     uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
     if (tile_needs_manual(p, tile)) {

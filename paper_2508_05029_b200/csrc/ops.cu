@@ -298,6 +298,13 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
   if (ns == 0) { per_sm = 1; ns = std::min<u32>(kMaxStages, budget / p.stage_bytes); }
   if (ns == 0) fail(TQ_INVALID_PLAN, "batch too wide for one pipeline tile");
   p.nstages = ns;
+  {  // L2 prefetch distance (tiles beyond the ring); TQ_PF overrides
+    static const int pf_env = [] {
+      const char* e = getenv("TQ_PF");
+      return e ? atoi(e) : -1;
+    }();
+    p.pf_dist = pf_env >= 0 ? (u32)pf_env : 0;  // measured slower when on (TMA queue contention)
+  }
   p.off_stage = o;
   L.smem = o + ns * p.stage_bytes;
   L.grid = std::max<u32>(1, std::min<u32>(p.ntiles, (u32)c->sms * per_sm));
@@ -616,29 +623,6 @@ struct FinalParams {
   unsigned long long* counter;
 };
 
-struct AccOps {
-  uint8_t op[kMaxAcc];
-};
-
-__global__ void k_agg_init(AggTable t, u32 nacc, AccOps ops) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 j = i; j < t.cap; j += stride) t.state[j] = 0;
-  for (u64 j = i; j < t.cap * nacc; j += stride) {
-    u64 lo, hi;
-    uint8_t op = ops.op[j % nacc];
-    switch (op) {
-      case ACC_MIN_I: lo = ~0ull; hi = 0x7fffffffffffffffull; break;
-      case ACC_MAX_I: lo = 0; hi = 0x8000000000000000ull; break;
-      case ACC_MIN_F: lo = 0x7ff0000000000000ull; hi = 0; break;
-      case ACC_MAX_F: lo = 0xfff0000000000000ull; hi = 0; break;
-      default: lo = 0; hi = 0;
-    }
-    t.acc[2 * j] = lo;
-    t.acc[2 * j + 1] = hi;
-  }
-}
-
 __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   u64 stride = (u64)gridDim.x * blockDim.x;
@@ -833,8 +817,6 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
   // initial table for min(rows, 1M) groups at load <= 0.5
   uint64_t cap = 1024;
   while (cap < std::min<uint64_t>(in->rows, 1ull << 20) * 2) cap <<= 1;
-  AccOps ops{};  // by value: no host sync before the pipeline launch
-  for (u32 i = 0; i < nacc; ++i) ops.op[i] = acc[i].op;
   uint64_t ngroups = 0;
   AggTable t{};
   uint64_t tbytes = 0;
@@ -849,10 +831,9 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     t.nused = (unsigned long long*)tail;
     t.overflow = (uint32_t*)(tail + 8);
     TQ_CUDA(cudaMemsetAsync(tail, 0, 16, st));
-    u32 ib = (u32)std::min<uint64_t>(4096, (cap * std::max<u32>(1, nacc) + 255) / 256);
-    k_agg_init<<<ib, 256, 0, st>>>(t, nacc, ops);
-    counted_launch(c);
-    TQ_CUDA(cudaGetLastError());
+    // only the state words: a slot's accumulators are initialised by the
+    // thread that claims it (AccClaimInit, kernel_common.cuh)
+    TQ_CUDA(cudaMemsetAsync(t.state, 0, cap * 4, st));
     p.agg = t;
     launch(c, SINK_AGG, L, P, st);
     uint32_t ovf = 0;

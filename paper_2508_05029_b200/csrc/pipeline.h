@@ -17,10 +17,16 @@
 
 namespace tq {
 
-constexpr int kWarps = 16;                // consumer warps per CTA
+#ifndef TQ_KWARPS
+#define TQ_KWARPS 16
+#endif
+#ifndef TQ_KV
+#define TQ_KV 1
+#endif
+constexpr int kWarps = TQ_KWARPS;         // consumer warps per CTA
 constexpr int kThreads = kWarps * 32;     // consumer threads
 constexpr int kBlock = kThreads + 32;     // + one producer (TMA) warp
-constexpr int kV = 1;                     // rows per lane per tile
+constexpr int kV = TQ_KV;                 // rows per lane per tile
 constexpr int kTile = kThreads * kV;      // rows per tile (512)
 constexpr int kMaxKeys = 4;
 constexpr int kMaxKeyWords = 8;         // + 1 null word
@@ -109,6 +115,7 @@ struct PipeParams {
   uint32_t all_bulk;  // every staged column is TMA-eligible (16-B aligned)
   uint32_t load_mask; // staged columns this launch reads (a COUNT pass needs only
                       // the predicate/key columns; the others are never loaded)
+  uint32_t pf_dist;   // L2 prefetch distance in tiles of this CTA (0 = off)
   // shared-memory layout (bytes from dynamic smem base)
   uint32_t off_code, off_lits, off_stage, off_bar, off_vslot, off_vvalid, off_bslot, off_sink;
   // program

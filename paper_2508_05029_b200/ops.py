@@ -19,7 +19,7 @@ from .columnar import (MEM_DEVICE, HostBatch, TqAggC, TqBatchC, TqColumnC, TqErr
 from .expr import Expr
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtq_gpu.so")
+LIB_PATH = os.environ.get("TQ_LIB") or os.path.join(HERE, "libtq_gpu.so")  # TQ_LIB: build-variant experiments
 _lib = None
 
 

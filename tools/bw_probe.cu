@@ -46,7 +46,7 @@ struct Cols {
 };
 
 template <int W>
-__global__ void __launch_bounds__((W + 1) * 32) staged(Cols c, u64 rows, u32 tile, u32 stages, u64* sink) {
+__global__ void __launch_bounds__((W + 1) * 32, 1) staged(Cols c, u64 rows, u32 tile, u32 stages, u64* sink, u32 work) {
   extern __shared__ __align__(128) uint8_t sm[];
   uint64_t* full = (uint64_t*)sm;
   uint64_t* empty = full + 8;
@@ -87,6 +87,10 @@ __global__ void __launch_bounds__((W + 1) * 32) staged(Cols c, u64 rows, u32 til
     for (u32 r = warp * 32 + lane; r < tile; r += W * 32) acc ^= ((const u64*)st)[r];
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    // synthetic per-tile compute after the release (models the aggregation work)
+    u64 x = acc | 1;
+    for (u32 i = 0; i < work; ++i) x = x * 0x9E3779B97F4A7C15ull + i;
+    acc ^= x;
     if (++s == stages) { s = 0; ph ^= 1; }
   }
   if (acc == 0x1234567) sink[0] = acc;
@@ -147,6 +151,7 @@ int main() {
     printf("plain LDG.128 one 16B column: %.3f ms  %.0f GB/s\n", r.first, rows * 16.0 / r.first / 1e6);
     (void)n16;
   }
+  u32 work = 0;
   auto run = [&](auto kern, int W, u32 tile, u32 stages, int cpsm) {
     size_t smem = 128 + (size_t)stages * tile * 88;
     if (smem > 227 * 1024) return;
@@ -154,17 +159,16 @@ int main() {
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (W + 1) * 32, smem);
     if (occ < cpsm) return;
-    auto r = timeit([&] { kern<<<sms * cpsm, (W + 1) * 32, smem>>>(c, rows, tile, stages, sink); });
+    auto r = timeit([&] { kern<<<sms * cpsm, (W + 1) * 32, smem>>>(c, rows, tile, stages, sink, work); });
     cudaError_t e = cudaGetLastError();
-    printf("W=%2d tile=%5u stages=%u ctas/sm=%d smem=%6zu  best %.3f ms avg %.3f ms  %.0f GB/s (avg %.0f) %s\n", W,
-           tile, stages, cpsm, smem, r.first, r.second, bytes / r.first / 1e6, bytes / r.second / 1e6,
+    printf("work=%4u W=%2d tile=%5u stages=%u ctas/sm=%d smem=%6zu  best %.3f ms avg %.3f ms  %.0f GB/s (avg %.0f) %s\n", W,
+           work, tile, stages, cpsm, smem, r.first, r.second, bytes / r.first / 1e6, bytes / r.second / 1e6,
            e ? cudaGetErrorString(e) : "");
   };
-  for (u32 tile : {256u, 512u, 1024u, 2048u})
-    for (u32 stages : {2u, 3u, 4u, 6u, 8u})
-      for (int cpsm : {1, 2}) {
-        run(staged<16>, 16, tile, stages, cpsm);
-        if (cpsm == 2) run(staged<8>, 8, tile, stages, cpsm);
-      }
+  for (u32 wk : {0u, 40u, 80u, 120u, 160u}) {
+    work = wk;
+    for (u32 stages : {2u, 3u, 4u}) run(staged<16>, 16, 512, stages, 1);
+    for (u32 stages : {4u, 6u, 8u}) run(staged<16>, 16, 256, stages, 1);
+  }
   return 0;
 }
