@@ -295,25 +295,6 @@ __device__ __forceinline__ u32 jt_probe_count(const JoinTable& t, const u64* kw)
 }
 
 // ------------------------------------------------------------------ stage loading
-__device__ __forceinline__ void issue_tile(const PipeParams& p, uint8_t* stage, uint64_t* bar, u32 tile) {
-  u64 r0 = (u64)tile * kTile;
-  u64 n = p.rows - r0;
-  bool full = n >= (u64)kTile;
-  u32 bytes = 0;
-  if (full)
-    for (u32 c = 0; c < p.nstaged; ++c)
-      if (p.cols[c].bulk_ok && ((p.load_mask >> c) & 1))
-        bytes += kTile * p.cols[c].width + (p.cols[c].validity ? kTile / 8 : 0);
-  mbar_arrive_expect_tx(bar, bytes);
-  if (!full) return;
-  for (u32 c = 0; c < p.nstaged; ++c) {
-    const StagedCol& sc = p.cols[c];
-    if (!sc.bulk_ok || !((p.load_mask >> c) & 1)) continue;
-    bulk_g2s(stage + sc.off, sc.values + r0 * sc.width, kTile * sc.width, bar);
-    if (sc.validity) bulk_g2s(stage + sc.voff, sc.validity + r0 / 8, kTile / 8, bar);
-  }
-}
-
 // Warm L2 with a future full tile of this CTA: more bytes in flight than the
 // shared-memory ring holds, so the ring's bulk copies mostly hit L2.
 __device__ __forceinline__ void prefetch_tile(const PipeParams& p, u32 tile) {
@@ -345,14 +326,38 @@ __device__ __forceinline__ void manual_tile(const PipeParams& p, uint8_t* stage,
   }
 }
 
-__device__ __forceinline__ bool tile_needs_manual(const PipeParams& p, u32 tile) {
-  return !p.all_bulk || p.rows - (u64)tile * kTile < (u64)kTile;
+// One bulk copy of the producer warp: a staged column's values or validity
+// slice of a full tile.  Lane j owns copies j and j + 32, so a tile's copies
+// issue in parallel with no per-tile parameter walking (the producer shares
+// its scheduler with busy consumer warps; its per-tile latency gates the ring).
+struct BulkCopy {
+  const uint8_t* src;  // tile t starts at src + t * bytes
+  u32 bytes, dst;      // bytes per tile, offset within a stage
+  bool on;
+};
+__device__ __forceinline__ BulkCopy bulk_copy_of(const PipeParams& p, u32 j) {
+  BulkCopy b{nullptr, 0, 0, false};
+  const u32 c = j >> 1;
+  if (c >= p.nstaged) return b;
+  const StagedCol& sc = p.cols[c];
+  if (!sc.bulk_ok || !((p.load_mask >> c) & 1)) return b;
+  if (j & 1) {
+    if (!sc.validity) return b;
+    b = BulkCopy{sc.validity, (u32)(kTile / 8), sc.voff, true};
+  } else {
+    b = BulkCopy{sc.values, (u32)kTile * sc.width, sc.off, true};
+  }
+  return b;
 }
 
 // Producer warp: keeps `nstages` tiles in flight.  Stage s is refilled once
 // every consumer warp has arrived on empty[s].
 __device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint64_t* full, uint64_t* empty,
                                         u32 lane) {
+  const BulkCopy c0 = bulk_copy_of(p, lane), c1 = bulk_copy_of(p, lane + 32);
+  u32 tile_bytes = (c0.on ? c0.bytes : 0) + (c1.on ? c1.bytes : 0);
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) tile_bytes += __shfl_xor_sync(kFull, tile_bytes, m);
   u32 k = 0, s = 0, ph = 0;
   if (lane == 0)
     for (u32 j = p.nstages; j < p.nstages + p.pf_dist; ++j) prefetch_tile(p, blockIdx.x + j * gridDim.x);
@@ -360,15 +365,20 @@ __device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint
     if (p.pf_dist && lane == 0) prefetch_tile(p, tile + (p.nstages + p.pf_dist) * gridDim.x);
     if (k >= p.nstages) mbar_wait(&empty[s], ph ^ 1u);
     uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
-    if (tile_needs_manual(p, tile)) {
+    const bool full_tile = p.rows - (u64)tile * kTile >= (u64)kTile;
+    if (!p.all_bulk || !full_tile) {
       manual_tile(p, stage, tile, lane);
       __syncwarp();
     }
     if (lane == 0) {
       fence_proxy_async();
-      issue_tile(p, stage, &full[s], tile);
+      mbar_arrive_expect_tx(&full[s], full_tile ? tile_bytes : 0);
     }
     __syncwarp();
+    if (full_tile) {
+      if (c0.on) bulk_g2s(stage + c0.dst, c0.src + (u64)tile * c0.bytes, c0.bytes, &full[s]);
+      if (c1.on) bulk_g2s(stage + c1.dst, c1.src + (u64)tile * c1.bytes, c1.bytes, &full[s]);
+    }
     if (++s == p.nstages) { s = 0; ph ^= 1u; }
   }
 }

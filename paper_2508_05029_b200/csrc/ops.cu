@@ -294,7 +294,11 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
   u32 half = 113 * 1024;
   if (per_sm == 0) per_sm = (o < half && (half - o) / p.stage_bytes >= 2) ? 2 : 1;
   u32 limit = per_sm >= 2 ? (half > o ? half - o : 0) : budget;
-  u32 ns = std::min<u32>(kMaxStages, limit / p.stage_bytes);
+  static const u32 max_stages = [] {  // TQ_MAXSTAGES: experiments only
+    const char* e = getenv("TQ_MAXSTAGES");
+    return e ? (u32)std::max(1, std::min(atoi(e), kMaxStages)) : (u32)kMaxStages;
+  }();
+  u32 ns = std::min<u32>(max_stages, limit / p.stage_bytes);
   if (ns == 0) { per_sm = 1; ns = std::min<u32>(kMaxStages, budget / p.stage_bytes); }
   if (ns == 0) fail(TQ_INVALID_PLAN, "batch too wide for one pipeline tile");
   p.nstages = ns;
@@ -799,7 +803,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     plan_launch(c, in, P, probe, 0, st);
     u32 fixed = probe.smem - probe.p.nstages * probe.p.stage_bytes;  // everything but the stages
     u32 avail = 227 * 1024 - fixed - 2 * probe.p.stage_bytes - 1024;
-    G = 64;
+    G = kh.empty() ? 1 : 64;  // a global aggregate has exactly one group
     while (G > 1 && sink_bytes(G) > avail) G >>= 1;
     if (sink_bytes(G) > avail) G = 0;
   }
@@ -816,7 +820,8 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
   // ---- global table; grows x4 and re-runs on overflow (on_oom-style retry)
   // initial table for min(rows, 1M) groups at load <= 0.5
   uint64_t cap = 1024;
-  while (cap < std::min<uint64_t>(in->rows, 1ull << 20) * 2) cap <<= 1;
+  if (!kh.empty())
+    while (cap < std::min<uint64_t>(in->rows, 1ull << 20) * 2) cap <<= 1;
   uint64_t ngroups = 0;
   AggTable t{};
   uint64_t tbytes = 0;
