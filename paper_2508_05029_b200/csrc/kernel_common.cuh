@@ -383,6 +383,47 @@ __device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint
   }
 }
 
+// ---- DEST_PROBE1 output slots: a CTA hands out rows of its current kChunk-row
+// chunk through one 32-bit shared word {generation:21 | used:11}; the warp
+// whose reservation crosses the chunk end allocates the next chunk with one
+// global atomic (so the global cursor sees ~rows/kChunk atomics, not one per
+// warp and tile).  Each CTA's last chunk may stay partly unused: the holes are
+// closed after the kernel (k_chunk_plan / k_chunk_move, ops.cu).
+struct ChunkCursor {
+  u32 word;
+  u32 _pad;
+  unsigned long long base[16];  // chunk start by generation (mod 16)
+};
+constexpr u32 kChunkUsedBits = 11;  // used <= kChunk + kThreads < 2^11
+static_assert(kChunk + kThreads < (1 << kChunkUsedBits), "chunk word layout");
+
+// Reserve m (1..32) slots for the calling lane-0: [a, a+k1) in the current
+// chunk, the rest [b, b + m - k1) in a newly allocated one.
+__device__ __forceinline__ void chunk_reserve(ChunkCursor* cc, u32 m, unsigned long long* gcursor, u64& a, u32& k1,
+                                              u64& b) {
+  for (;;) {
+    const u32 old = atomicAdd(&cc->word, m);
+    const u32 gen = old >> kChunkUsedBits, off = old & ((1u << kChunkUsedBits) - 1);
+    if (off + m <= (u32)kChunk) {
+      a = cc->base[gen & 15] + off;
+      k1 = m;
+      b = 0;
+      return;
+    }
+    if (off <= (u32)kChunk) {  // this reservation crosses the chunk end
+      k1 = (u32)kChunk - off;
+      a = cc->base[gen & 15] + off;
+      b = atomicAdd(gcursor, (unsigned long long)kChunk);
+      ((volatile unsigned long long*)cc->base)[(gen + 1) & 15] = b;
+      __threadfence_block();
+      atomicExch(&cc->word, ((gen + 1) << kChunkUsedBits) | (m - k1));
+      return;
+    }
+    while ((((volatile u32*)&cc->word)[0] >> kChunkUsedBits) == gen) {
+    }
+  }
+}
+
 // named barrier over the consumer warps only
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
 
@@ -426,6 +467,8 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   if (SINK == SINK_COUNT || SINK == SINK_EMIT) {
     for (u32 i = threadIdx.x; i < kWarps * kMaxDest; i += kThreads) s_cnt[i] = 0;
   }
+  ChunkCursor* s_chunk = (ChunkCursor*)s_base;  // DEST_PROBE1 only (s_base unused there)
+  if (SINK == SINK_EMIT && threadIdx.x == 0) s_chunk->word = (u32)kChunk;  // generation 0, full: first use allocates
   if (SINK == SINK_AGG && threadIdx.x < kThreads) {
     for (u32 i = threadIdx.x; i < G; i += kThreads) l_state[i] = kStEmpty;
 #pragma unroll
@@ -491,10 +534,14 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         }
         const u32 mm = __ballot_sync(kFull, brow >= 0);
         if (mm) {
-          unsigned long long base = 0;
-          if (lane == 0) base = atomicAdd(p.cursor, (unsigned long long)__popc(mm));
-          base = __shfl_sync(kFull, base, 0);
-          if (brow >= 0) P::store(w, v, base + __popc(mm & lanemask_lt()), brow, raw[v]);
+          u64 a = 0, b = 0;
+          u32 k1 = 0;
+          if (lane == 0) chunk_reserve(s_chunk, (u32)__popc(mm), p.cursor, a, k1, b);
+          a = __shfl_sync(kFull, a, 0);
+          b = __shfl_sync(kFull, b, 0);
+          k1 = __shfl_sync(kFull, k1, 0);
+          const u32 rank = __popc(mm & lanemask_lt());
+          if (brow >= 0) P::store(w, v, rank < k1 ? a + rank : b + (rank - k1), brow, raw[v]);
         }
       }
     } else if (SINK == SINK_COUNT || SINK == SINK_EMIT) {
@@ -765,6 +812,15 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     if (++s == p.nstages) { s = 0; ph ^= 1u; }
   }
 
+  if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1) {
+    consumers_sync();
+    if (threadIdx.x == 0) {
+      const u32 word = s_chunk->word;
+      const u32 used = min(word & ((1u << kChunkUsedBits) - 1), (u32)kChunk);
+      p.chunk_tail[2 * blockIdx.x] = s_chunk->base[(word >> kChunkUsedBits) & 15];
+      p.chunk_tail[2 * blockIdx.x + 1] = used;  // kChunk: no hole (also a CTA that never emitted)
+    }
+  }
   if (SINK == SINK_AGG && G > 0) {
     consumers_sync();
     // 1) global slot of every local group

@@ -355,6 +355,107 @@ struct MatArgs {
   std::vector<uint32_t> build_cols;
 };
 
+// ---- closing the holes of DEST_PROBE1's chunked output (kernel_common.cuh,
+// chunk_reserve).  Rows were written to [0, R) in kChunk-row chunks; each CTA's
+// last chunk may be partly unused, so n = R - holes rows exist.  The used rows
+// at positions >= n are moved into the holes below n (any bijection will do:
+// join output order is unspecified), then bitmap bits >= n are cleared.
+struct ChunkOut {
+  uint8_t* values[kMaxOut];
+  uint8_t* validity[kMaxOut];
+  uint32_t width[kMaxOut];
+  uint32_t ncols;
+};
+// plan: [0] n, [1] moves, [2] hole ranges, [3] source ranges, then
+// hole start[nh], hole prefix[nh + 1], source start[ns], source prefix[ns + 1]
+__global__ void k_chunk_plan(const u64* tails, u32 nctas, const u64* gcursor, u64* plan) {
+  extern __shared__ u64 sm_chunk[];
+  u64* tb = sm_chunk;          // [nctas] last-chunk base
+  u64* tu = tb + nctas;        // [nctas] used rows
+  u64* uj = tu + nctas;        // [nctas + 2] used rows of the chunks at/after floor(n / kChunk)
+  __shared__ unsigned long long holes_total;
+  if (threadIdx.x == 0) holes_total = 0;
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < nctas; i += blockDim.x) {
+    tb[i] = tails[2 * i];
+    tu[i] = tails[2 * i + 1];
+    if (tu[i] < (u64)kChunk) atomicAdd(&holes_total, (unsigned long long)(kChunk - tu[i]));
+  }
+  __syncthreads();
+  const u64 R = *gcursor, n = R - holes_total;
+  const u64 j0 = n / kChunk, nj = R / kChunk - j0;
+  for (u64 i = threadIdx.x; i < nj; i += blockDim.x) uj[i] = kChunk;
+  __syncthreads();
+  for (u32 i = threadIdx.x; i < nctas; i += blockDim.x)
+    if (tu[i] < (u64)kChunk && tb[i] >= j0 * kChunk) uj[tb[i] / kChunk - j0] = tu[i];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  u64* hs = plan + 4;
+  u64* hp = hs + nctas;
+  u64* ss = hp + nctas + 1;
+  u64* sp = ss + nctas + 2;
+  u64 nh = 0, tot = 0;
+  hp[0] = 0;
+  for (u32 i = 0; i < nctas; ++i) {
+    if (tu[i] >= (u64)kChunk || tb[i] >= n) continue;
+    const u64 a = tb[i] + tu[i], e = min(tb[i] + (u64)kChunk, n);
+    if (a >= e) continue;
+    hs[nh] = a;
+    tot += e - a;
+    hp[++nh] = tot;
+  }
+  u64 ns = 0, tot2 = 0;
+  sp[0] = 0;
+  for (u64 j = 0; j < nj; ++j) {
+    const u64 s0 = (j0 + j) * kChunk, a = max(s0, n), e = s0 + uj[j];
+    if (a >= e) continue;
+    ss[ns] = a;
+    tot2 += e - a;
+    sp[++ns] = tot2;
+  }
+  plan[0] = n;
+  plan[1] = tot == tot2 ? tot : ~0ull;  // (equal by construction)
+  plan[2] = nh;
+  plan[3] = ns;
+}
+
+__device__ __forceinline__ u64 range_at(const u64* start, const u64* pref, u64 nr, u64 k) {
+  u64 lo = 0, hi = nr;  // last range with pref <= k
+  while (hi - lo > 1) {
+    const u64 mid = (lo + hi) / 2;
+    if (pref[mid] <= k) lo = mid;
+    else hi = mid;
+  }
+  return start[lo] + (k - pref[lo]);
+}
+
+__global__ void k_chunk_move(const u64* plan, u32 nctas, const __grid_constant__ ChunkOut o) {
+  const u64 moves = plan[1];
+  if (moves == ~0ull) return;
+  const u64 nh = plan[2], ns = plan[3];
+  const u64* hs = plan + 4;
+  const u64* hp = hs + nctas;
+  const u64* ss = hp + nctas + 1;
+  const u64* sp = ss + nctas + 2;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < moves; k += (u64)gridDim.x * blockDim.x) {
+    const u64 dst = range_at(hs, hp, nh, k), src = range_at(ss, sp, ns, k);
+    for (u32 c = 0; c < o.ncols; ++c) {
+      const u32 w = o.width[c];
+      if (w == 16) ((ulonglong2*)o.values[c])[dst] = ((const ulonglong2*)o.values[c])[src];
+      else if (w == 8) ((u64*)o.values[c])[dst] = ((const u64*)o.values[c])[src];
+      else o.values[c][dst] = o.values[c][src];
+      if (o.validity[c] && bm_get(o.validity[c], src)) bm_set_atomic(o.validity[c], dst);
+    }
+  }
+}
+
+__global__ void k_chunk_clear_tail(const u64* plan, const __grid_constant__ ChunkOut o) {
+  const u64 n = plan[0];
+  const u32 c = threadIdx.x;
+  if (c >= o.ncols || !o.validity[c] || (n & 7) == 0) return;
+  o.validity[c][n >> 3] &= (uint8_t)((1u << (n & 7)) - 1);
+}
+
 static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArgs& A, tq_batch* out,
                             uint64_t* part_offsets, cudaStream_t st) {
   Plan L;
@@ -430,25 +531,47 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
   if (probe1) {
     // single pass: capacity = probe rows (<= 1 match each), exact size read back
     p.dest_kind = DEST_PROBE1;
-    alloc_batch(c, in->rows, sch, wv, out, st);
-    u64* cursor = (u64*)dalloc(c, 8, st);
+    // rows land in kChunk-row chunks: room for one partly used chunk per CTA
+    const uint64_t cap_rows = in->rows + (uint64_t)L.grid * kChunk;
+    alloc_batch(c, cap_rows, sch, wv, out, st);
+    const uint64_t scratch = 8 + L.grid * 16 + (10 + 4 * (uint64_t)L.grid) * 8;  // cursor, tails, plan
+    uint8_t* sb = (uint8_t*)dalloc(c, scratch, st);
+    u64* cursor = (u64*)sb;
+    u64* tails = cursor + 1;
+    u64* plan = tails + 2 * L.grid;
     TQ_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
     p.cursor = cursor;
+    p.chunk_tail = tails;
     p.nout = (u32)outs.size();
+    ChunkOut co{};
+    co.ncols = p.nout;
     for (size_t i = 0; i < outs.size(); ++i) {
       outs[i].values = (uint8_t*)out->cols[i].values;
       outs[i].validity = out->cols[i].validity;
       p.out[i] = outs[i];
+      co.values[i] = outs[i].values;
+      co.validity[i] = outs[i].validity;
+      co.width[i] = (u32)width_of(out->cols[i].kind);
     }
     launch(c, SINK_EMIT, L, P, st);
+    if (p.ntiles == 0) {
+      TQ_CUDA(cudaMemsetAsync(plan, 0, 8, st));
+    } else {
+      k_chunk_plan<<<1, 1024, (3 * L.grid + 2) * 8, st>>>(tails, L.grid, cursor, plan);
+      k_chunk_move<<<c->sms * 2, 256, 0, st>>>(plan, L.grid, co);
+      k_chunk_clear_tail<<<1, 32, 0, st>>>(plan, co);
+      for (int k = 0; k < 3; ++k) counted_launch(c);
+      TQ_CUDA(cudaGetLastError());
+    }
     uint64_t n = 0;
     {
       std::lock_guard<std::mutex> g(c->mu);
-      TQ_CUDA(cudaMemcpyAsync(c->pinned, cursor, 8, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync(c->pinned, plan, 16, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaStreamSynchronize(st));
-      n = *(uint64_t*)c->pinned;
+      n = ((uint64_t*)c->pinned)[0];
+      if (p.ntiles && ((uint64_t*)c->pinned)[1] == ~0ull) fail(TQ_INTERNAL, "probe output chunk plan inconsistent");
     }
-    dfree(c, cursor, 8, st);
+    dfree(c, sb, scratch, st);
     out->rows = n;
     for (uint32_t i = 0; i < out->ncols; ++i) {
       out->cols[i].values_bytes = n * width_of(out->cols[i].kind);

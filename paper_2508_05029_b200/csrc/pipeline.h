@@ -34,6 +34,7 @@ constexpr int kMaxOut = 24;
 constexpr int kMaxAcc = 16;
 constexpr int kMaxDest = 64;
 constexpr int kMaxStages = 6;
+constexpr int kChunk = 512;  // DEST_PROBE1 output rows a CTA reserves per global atomic
 
 enum SinkKind { SINK_COUNT = 0, SINK_EMIT = 1, SINK_AGG = 2, SINK_BUILD = 3 };
 // FILTER/PARTITION/PROBE: two passes (COUNT then EMIT), stable order.
@@ -134,7 +135,8 @@ struct PipeParams {
   uint32_t dest_kind, ndest;
   uint32_t* tile_counts;          // [ndest][ntiles * kWarps] (per warp-slice of a tile)
   const unsigned long long* tile_offsets;  // [ndest][ntiles * kWarps] absolute output rows
-  unsigned long long* cursor;     // DEST_PROBE1 output cursor; BUILD inserted-row count
+  unsigned long long* cursor;     // DEST_PROBE1 chunk cursor (rows, kChunk units); BUILD inserted-row count
+  unsigned long long* chunk_tail; // DEST_PROBE1: per CTA {base, used} of its last output chunk
   JoinTable jt;
   // LIP semi-join filter on the key words (dest PARTITION): rows whose keys
   // miss this Bloom filter are dropped before they are partitioned / shipped

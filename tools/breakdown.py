@@ -17,11 +17,43 @@ from paper_2508_05029_b200 import queries  # noqa: E402
 from paper_2508_05029_b200.ops import Context  # noqa: E402
 
 
+def q3_stages(ctx, st, t):
+    from paper_2508_05029_b200.expr import Col
+    Q = queries
+    for rep in range(3):
+        marks = []
+
+        def mark(name):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(st)
+            marks.append((name, e))
+        mark("start")
+        ct = ctx.pipeline_build(t["customer"], Col(Q.C_MKTSEGMENT).eq(1), [Q.C_CUSTKEY])
+        mark("customer filter+build")
+        of = ctx.pipeline_probe(ct, t["orders"], Col(Q.O_ORDERDATE) < 9204,
+                                [Col(Q.O_ORDERKEY), Col(Q.O_ORDERDATE), Col(Q.O_SHIPPRIORITY), Col(Q.O_CUSTKEY)], [3], [])
+        mark(f"orders filter+probe -> {of.rows} rows")
+        ot = ctx.join_build(of, [0])
+        mark("orders_f build")
+        j = ctx.pipeline_probe(ot, t["lineitem"], Col(Q.L_SHIPDATE) > 9204, [Col(Q.L_ORDERKEY), Q.REV], [0], [1, 2])
+        mark(f"lineitem filter+probe -> {j.rows} rows")
+        out = ctx.aggregate_execute(j, [2, 0, 1], [(Q.AGG_SUM, 3)])
+        mark(f"aggregate -> {out.rows} groups")
+        torch.cuda.synchronize()
+        if rep == 2:
+            for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
+                print(f"  {n1:45s} {e0.elapsed_time(e1):7.3f} ms")
+            print(f"  total {marks[0][1].elapsed_time(marks[-1][1]):.3f} ms", flush=True)
+        for x in (ct, of, ot, j, out):
+            x.free()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sf", type=float, default=10.0)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--queries", default="q1,q6,q3,q5,q9")
+    ap.add_argument("--stages", action="store_true", help="Q3 operator-by-operator timing")
     a = ap.parse_args()
     ctx = Context(0)
     st = torch.cuda.ExternalStream(ctx.stream())
@@ -32,6 +64,9 @@ def main():
     fns = {"q1": lambda: queries.q1_scan(ctx, li1), "q6": lambda: queries.q6_scan(ctx, li6)}
     for q in (3, 5, 9):
         fns[f"q{q}"] = (lambda q=q: queries.run_join_query(ctx, q, t))
+    if a.stages:
+        q3_stages(ctx, st, t)
+        return
     for name in a.queries.split(","):
         fn = fns[name]
         for _ in range(3):
