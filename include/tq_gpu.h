@@ -46,6 +46,9 @@ uint64_t tq_profile_report(tq_ctx* ctx, char* buf, uint64_t cap);
  * disabled here or by TQ_JIT=0; tq_jit_report writes compile/cache stats. */
 void tq_ctx_set_jit(tq_ctx* ctx, int on);
 uint64_t tq_jit_report(tq_ctx* ctx, char* buf, uint64_t cap);
+/* Host-side phase timings accumulated since the last call when the process
+ * runs with TQ_HOST_TIMING=1 (one line per phase); returns the length. */
+uint64_t tq_host_timing_report(char* buf, uint64_t cap);
 /* page-locked, portable host memory (the Host tier of SPEC.md:236-239) */
 tq_status tq_pinned_alloc(uint64_t bytes, void** out);
 void tq_pinned_free(void* p);

@@ -7,14 +7,65 @@
 // MemoryLedger / alloc_within); exceeding the configured Device capacity
 // returns ReservationExceeded, the signal the Compute Executor's on_oom
 // retry path consumes.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 
 #include "ctx.h"
 
 namespace tq {
 
 thread_local std::string g_err;
+
+namespace {
+struct HostTiming {
+  std::mutex mu;
+  std::map<std::string, std::pair<uint64_t, double>> acc;
+  bool on = false;
+  HostTiming() {
+    const char* e = getenv("TQ_HOST_TIMING");
+    on = e && e[0] == '1';
+  }
+  std::string report() {
+    std::lock_guard<std::mutex> g(mu);
+    std::string r;
+    char line[160];
+    for (auto& kv : acc) {
+      snprintf(line, sizeof line, "%-28s %8llu calls %10.1f us total %8.2f us/call\n", kv.first.c_str(),
+               (unsigned long long)kv.second.first, kv.second.second,
+               kv.second.second / std::max<uint64_t>(1, kv.second.first));
+      r += line;
+    }
+    acc.clear();
+    return r;
+  }
+};
+HostTiming& host_timing() {
+  static HostTiming* h = new HostTiming;  // never destroyed: frees can run during interpreter teardown
+  return *h;
+}
+long long now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+}  // namespace
+
+bool host_timing_on() { return host_timing().on; }
+std::string host_timing_report() { return host_timing().report(); }
+void host_timing_add(const char* name, double us) {
+  HostTiming& h = host_timing();
+  std::lock_guard<std::mutex> g(h.mu);
+  auto& e = h.acc[name];
+  e.first++;
+  e.second += us;
+}
+HostTimer::HostTimer(const char* n) : name(n), t0(host_timing_on() ? now_ns() : 0) {}
+HostTimer::~HostTimer() {
+  if (t0) host_timing_add(name, (now_ns() - t0) / 1e3);
+}
 
 void fail(int status, const std::string& msg) { throw Fail{status, msg}; }
 
@@ -54,6 +105,7 @@ size_t width_of(uint8_t kind) {
 }
 
 void* dalloc(tq_ctx* c, uint64_t bytes, cudaStream_t st) {
+  TQ_HT("dalloc");
   uint64_t b = round_up(bytes ? bytes : 1, 256) + 256;  // tail pad: 16-B bulk copies never run off the end
   uint64_t now = c->in_use.fetch_add(b) + b;
   if (c->budget && now > c->budget) {
@@ -72,6 +124,7 @@ void* dalloc(tq_ctx* c, uint64_t bytes, cudaStream_t st) {
 }
 
 void dfree(tq_ctx* c, void* p, uint64_t bytes, cudaStream_t st) {
+  TQ_HT("dfree");
   if (!p) return;
   uint64_t b = round_up(bytes ? bytes : 1, 256) + 256;
   cudaFreeAsync(p, st);
@@ -313,3 +366,13 @@ void tq_host_batch_free(tq_batch* b) {
 }
 
 }  // extern "C"
+
+extern "C" uint64_t tq_host_timing_report(char* buf, uint64_t cap) {
+  std::string r = tq::host_timing_report();
+  uint64_t n = std::min<uint64_t>(r.size(), cap ? cap - 1 : 0);
+  if (cap) {
+    std::memcpy(buf, r.data(), n);
+    buf[n] = 0;
+  }
+  return n;
+}

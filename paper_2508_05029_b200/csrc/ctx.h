@@ -74,6 +74,19 @@ void prof_end(tq_ctx* c, int h, cudaStream_t st);
 
 extern thread_local std::string g_err;
 
+// Host-side phase timing (TQ_HOST_TIMING=1: totals printed at exit).
+bool host_timing_on();
+void host_timing_add(const char* name, double us);
+struct HostTimer {
+  const char* name;
+  long long t0;
+  explicit HostTimer(const char* n);
+  ~HostTimer();
+};
+#define TQ_HT_CAT2(a, b) a##b
+#define TQ_HT_CAT(a, b) TQ_HT_CAT2(a, b)
+#define TQ_HT(name) ::tq::HostTimer TQ_HT_CAT(_ht_, __LINE__)(name)
+
 template <typename F>
 tq_status guard(F&& f) {
   try {

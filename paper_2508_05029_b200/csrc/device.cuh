@@ -195,6 +195,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, 
       : "memory");
 }
 
+// Same, with an L2 cache policy (streamed column tiles: evict_first, so
+// hash tables and Bloom filters the kernel probes stay resident in L2).
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, u32 bytes, uint64_t* bar, u64 policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ u64 l2_policy_evict_first() {
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 // Bulk prefetch global -> L2 (no shared memory, no completion tracking).
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, u32 bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

@@ -533,6 +533,7 @@ Entry compile(const std::string& src) {
 cudaError_t launch_pipeline_prog(tq_ctx* c, int sink, const PipeParams& p, u32 smem, u32 grid, cudaStream_t st,
                                  const std::vector<DInstr>& code, const std::vector<DLit>& lits) {
   if (c->jit && jit_env_enabled()) {
+    TQ_HT("jit key+lookup+launch");
     // cache key: every launch parameter the generator bakes into the source
     std::string key;
     key.reserve(1024);

@@ -355,6 +355,7 @@ __device__ __forceinline__ BulkCopy bulk_copy_of(const PipeParams& p, u32 j) {
 __device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint64_t* full, uint64_t* empty,
                                         u32 lane) {
   const BulkCopy c0 = bulk_copy_of(p, lane), c1 = bulk_copy_of(p, lane + 32);
+  const u64 pol = l2_policy_evict_first();  // column tiles are read once
   u32 tile_bytes = (c0.on ? c0.bytes : 0) + (c1.on ? c1.bytes : 0);
 #pragma unroll
   for (int m = 16; m > 0; m >>= 1) tile_bytes += __shfl_xor_sync(kFull, tile_bytes, m);
@@ -376,8 +377,8 @@ __device__ __forceinline__ void produce(const PipeParams& p, uint8_t* smem, uint
     }
     __syncwarp();
     if (full_tile) {
-      if (c0.on) bulk_g2s(stage + c0.dst, c0.src + (u64)tile * c0.bytes, c0.bytes, &full[s]);
-      if (c1.on) bulk_g2s(stage + c1.dst, c1.src + (u64)tile * c1.bytes, c1.bytes, &full[s]);
+      if (c0.on) bulk_g2s_hint(stage + c0.dst, c0.src + (u64)tile * c0.bytes, c0.bytes, &full[s], pol);
+      if (c1.on) bulk_g2s_hint(stage + c1.dst, c1.src + (u64)tile * c1.bytes, c1.bytes, &full[s], pol);
     }
     if (++s == p.nstages) { s = 0; ph ^= 1u; }
   }

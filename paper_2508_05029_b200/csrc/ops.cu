@@ -154,6 +154,7 @@ static void check_device_batch(const tq_batch* b) {
 // pred may be null; exprs==null && all_cols -> every input column passes through
 static void compile_prog(Prog& P, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs, uint32_t nexprs,
                          bool all_cols) {
+  TQ_HT("compile_prog");
   try {
     if (pred) {
       P.pred_h = P.pb.add_root(*pred);
@@ -229,6 +230,7 @@ struct Plan {
 static u32 align_up(u32 x, u32 a) { return (x + a - 1) / a * a; }
 
 static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sink_bytes, cudaStream_t st) {
+  TQ_HT("plan_launch");
   PipeParams& p = L.p;
   std::memset(&p, 0, sizeof(p));
   const ProgramBuilder& pb = P.pb;
@@ -316,6 +318,7 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
 }
 
 static void launch(tq_ctx* c, int sink, Plan& L, const Prog& P, cudaStream_t st) {
+  TQ_HT("launch(pipeline)");
   if (L.p.ntiles == 0) return;
   static const char* names[] = {"pipe_count", "pipe_emit", "pipe_agg", "pipe_build"};
   int h = prof_begin(c, names[sink], st);
@@ -567,7 +570,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     {
       std::lock_guard<std::mutex> g(c->mu);
       TQ_CUDA(cudaMemcpyAsync(c->pinned, plan, 16, cudaMemcpyDeviceToHost, st));
-      TQ_CUDA(cudaStreamSynchronize(st));
+      { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
       n = ((uint64_t*)c->pinned)[0];
       if (p.ntiles && ((uint64_t*)c->pinned)[1] == ~0ull) fail(TQ_INTERNAL, "probe output chunk plan inconsistent");
     }
@@ -608,7 +611,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
       k_dest_starts<<<1, 128, 0, st>>>(offsets, (u32)nslices, p.ndest, offsets + ncnt, pin);
       counted_launch(c);
       TQ_CUDA(cudaGetLastError());
-      TQ_CUDA(cudaStreamSynchronize(st));
+      { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
       for (u32 d = 0; d <= p.ndest; ++d) starts[d] = pin[d];
     }
     total = starts[p.ndest];
@@ -722,7 +725,7 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
     k_jt_unique<<<(u32)std::min<uint64_t>(4096, (cap + 255) / 256), 256, 0, st>>>(t->jt, dup);
     counted_launch(c);
     TQ_CUDA(cudaGetLastError());
-    TQ_CUDA(cudaStreamSynchronize(st));
+    { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
     t->jt.unique = *dup == 0;
   }
   *out = t;
@@ -968,7 +971,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     {
       std::lock_guard<std::mutex> g(c->mu);
       TQ_CUDA(cudaMemcpyAsync(c->pinned, tail, 16, cudaMemcpyDeviceToHost, st));
-      TQ_CUDA(cudaStreamSynchronize(st));
+      { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
       ngroups = ((uint64_t*)c->pinned)[0];
       ovf = ((uint32_t*)c->pinned)[2];
     }
@@ -1136,7 +1139,7 @@ static void gather_into(tq_ctx* c, const tq_batch* in, const u64* ids, u64 n, u6
       }
       uint64_t tot = 0;
       TQ_CUDA(cudaMemcpyAsync(&tot, off + n, 8, cudaMemcpyDeviceToHost, st));
-      TQ_CUDA(cudaStreamSynchronize(st));
+      { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
       utf8_cursor[k] += (int32_t)tot;
       dfree(c, len, n * 4, st);
       dfree(c, off, (n + 1) * 8, st);
@@ -1152,7 +1155,7 @@ static u64 utf8_bytes_of(tq_ctx* c, const tq_column& s, const u64* ids, u64 n, u
     int32_t a = 0, e = 0;
     TQ_CUDA(cudaMemcpyAsync(&a, s.offsets + base, 4, cudaMemcpyDeviceToHost, st));
     TQ_CUDA(cudaMemcpyAsync(&e, s.offsets + base + n, 4, cudaMemcpyDeviceToHost, st));
-    TQ_CUDA(cudaStreamSynchronize(st));
+    { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
     return (u64)(e - a);
   }
   u32* len = (u32*)dalloc(c, n * 4, st);
@@ -1162,7 +1165,7 @@ static u64 utf8_bytes_of(tq_ctx* c, const tq_column& s, const u64* ids, u64 n, u
   scan_u32(c, len, n, off, off + n, st);
   u64 tot = 0;
   TQ_CUDA(cudaMemcpyAsync(&tot, off + n, 8, cudaMemcpyDeviceToHost, st));
-  TQ_CUDA(cudaStreamSynchronize(st));
+  { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
   dfree(c, len, n * 4, st);
   dfree(c, off, (n + 1) * 8, st);
   return tot;
@@ -1417,6 +1420,7 @@ tq_status tq_pipeline_aggregate(tq_ctx* c, const tq_batch* in, const tq_expr* pr
                                 uint32_t nexprs, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs,
                                 uint32_t naggs, tq_batch* out, void* stream) {
   return guard([&] {
+    TQ_HT("tq_pipeline_aggregate");
     check_device_batch(in);
     Prog P(schema_of(in));
     compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);

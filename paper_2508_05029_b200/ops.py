@@ -9,8 +9,10 @@ Errors come back as TqError carrying the reference's Errc name.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
+import weakref
 from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
@@ -21,6 +23,21 @@ from .expr import Expr
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TQ_LIB") or os.path.join(HERE, "libtq_gpu.so")  # TQ_LIB: build-variant experiments
 _lib = None
+# Contexts still open at interpreter exit are closed by an atexit hook while
+# the CUDA runtime is alive; frees that run later (finalizers) become no-ops.
+_LIVE = weakref.WeakSet()
+_SHUTDOWN = False
+
+
+@atexit.register
+def _close_all():
+    global _SHUTDOWN
+    _SHUTDOWN = True
+    for ctx in list(_LIVE):
+        try:
+            ctx.close()
+        except Exception:
+            pass
 
 
 class TqEngineOptsC(C.Structure):
@@ -128,6 +145,8 @@ def lib():
         L.tq_estimate_reservation.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double]
         L.tq_jit_report.restype = C.c_uint64
         L.tq_jit_report.argtypes = [V, C.c_char_p, C.c_uint64]
+        L.tq_host_timing_report.restype = C.c_uint64
+        L.tq_host_timing_report.argtypes = [C.c_char_p, C.c_uint64]
         _lib = L
     return _lib
 
@@ -199,7 +218,7 @@ class DeviceBatch:
         if self.parent is not None:
             self.c = None
             return
-        if self.c is not None and self.ctx.handle:
+        if self.c is not None and self.ctx.handle and not _SHUTDOWN:
             lib().tq_batch_free(self.ctx.handle, C.byref(self.c))
             self.c = None
 
@@ -215,7 +234,7 @@ class JoinTable:
         self.ctx, self.handle, self.build = ctx, handle, build  # keeps the build batch alive
 
     def free(self):
-        if self.handle:
+        if self.handle and self.ctx.handle and not _SHUTDOWN:
             lib().tq_join_table_destroy(self.ctx.handle, self.handle)
             self.handle = None
 
@@ -235,6 +254,7 @@ class Context:
         opts = TqOptsC(device, ctas_per_sm, device_budget_bytes)
         self._check(L.tq_ctx_create(C.byref(opts), C.byref(h)))
         self.handle = h
+        _LIVE.add(self)
 
     @staticmethod
     def _check(st: int):
@@ -465,7 +485,7 @@ class Bloom:
         self.ctx, self.handle = ctx, h
 
     def free(self):
-        if self.handle:
+        if self.handle and not _SHUTDOWN:
             lib().tq_bloom_destroy(self.handle)
             self.handle = None
 
