@@ -220,6 +220,8 @@ def timed(ctx, fn, reps, world, stream):
         ctx.sync()
         ms.append(e0.elapsed_time(e1))
         out.free()
+    if os.environ.get("TQ_BENCH_VERBOSE"):
+        print(f"[timed rank{os.environ.get('RANK', '0')}] {[round(x, 3) for x in ms]}", file=sys.stderr, flush=True)
     return max_over_ranks(world, statistics.median(ms))
 
 
