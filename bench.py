@@ -454,7 +454,8 @@ def run_tq(args, world, rank, local):
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic("pipe_agg"),
-            "kernel": "pipe_kernel<SINK_AGG>", "kernel_ms": kern_ms,
+            "traffic_unit": "bytes/launch (dram read+write, ncu)",
+            "kernel": "tq_jit_main = pipe_body<SINK_AGG> (NVRTC-specialised)", "kernel_ms": kern_ms,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "B200_PROFILING.md fallback",
             "algorithmic_bytes_per_row": Q1_BYTES_PER_ROW,
         },
