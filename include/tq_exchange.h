@@ -37,6 +37,17 @@ tq_status tq_comm_exchange(tq_comm* comm, const tq_batch* partitioned, const uin
 tq_status tq_comm_allgather(tq_comm* comm, const tq_batch* in, tq_batch* out, uint64_t* recv_offsets, void* stream);
 /* OR a Bloom filter across all ranks (allgather + OR), for LIP before a shuffle. */
 tq_status tq_comm_bloom_union(tq_comm* comm, tq_bloom* bloom, void* stream);
+/* Fused hash-partition + shuffle over NVLink peer memory (replaces
+ * tq_pipeline_partition[_semi] + tq_comm_exchange, SPEC.md:589-595 + 475-534):
+ * evaluate pred / exprs over `in` (as tq_pipeline_partition), drop rows whose
+ * keys miss `semi` (LIP; may be NULL), and write every remaining row straight
+ * into the receive window of rank fnv1a64(keys) mod n — CUDA IPC mappings of
+ * the peers' windows, no partitioned staging batch, no NCCL payload copy.
+ * `out` = the rows all ranks sent to this one, in unspecified order.
+ * Collective: every rank calls it, in the same order as its other collectives. */
+tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, const tq_expr* pred,
+                                         const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,
+                                         const tq_bloom* semi, tq_batch* out, void* stream);
 /* Bytes this communicator has sent to other ranks (NVLink traffic). */
 uint64_t tq_comm_bytes_sent(tq_comm* comm);
 int tq_comm_size(tq_comm* comm);

@@ -14,6 +14,7 @@
 #include "../../include/tq_exchange.h"
 #include "ctx.h"
 #include "device.cuh"
+#include "peer.h"
 
 namespace tq {
 namespace {
@@ -85,9 +86,95 @@ struct tq_comm {
   ncclComm_t comm;
   int rank, n;
   std::atomic<uint64_t> sent{0};
+  // receive window for the fused partition + NVLink scatter (peer.h): one
+  // cudaMalloc'd buffer per rank, mapped into every other rank with CUDA IPC
+  uint8_t* win = nullptr;
+  uint64_t win_bytes = 0;
+  std::vector<uint8_t*> win_peer;  // [n]; win_peer[rank] == win
+  uint64_t win_cap_rows = 0;       // last capacity that sufficed (next call's first guess)
 };
 
 using namespace tq;
+
+// ---- peer windows (peer.h)
+namespace tq {
+
+tq_ctx* comm_ctx(tq_comm* cm) { return cm->ctx; }
+int comm_rank(tq_comm* cm) { return cm->rank; }
+int comm_size(tq_comm* cm) { return cm->n; }
+uint64_t& comm_window_rows(tq_comm* cm) { return cm->win_cap_rows; }
+void comm_add_sent(tq_comm* cm, uint64_t bytes) { cm->sent += bytes; }
+
+void comm_allgather_u64(tq_comm* cm, const unsigned long long* dev_in, unsigned long long* dev_out, uint64_t count, cudaStream_t st) {
+  nccl_check(nccl().all_gather(dev_in, dev_out, count, ncclUint64, cm->comm, st), "ncclAllGather");
+}
+
+void peer_barrier(tq_comm* cm, cudaStream_t st) {
+  if (cm->n == 1) return;
+  // stream-ordered: work after this point starts only once every rank's prior
+  // stream work (their scatter kernels) has completed
+  tq_ctx* c = cm->ctx;
+  u64* b = (u64*)dalloc(c, 8 * (cm->n + 1), st);
+  TQ_CUDA(cudaMemsetAsync(b, 0, 8, st));
+  comm_allgather_u64(cm, b, b + 1, 1, st);
+  dfree(c, b, 8 * (cm->n + 1), st);
+}
+
+PeerView peer_window(tq_comm* cm, uint64_t bytes, cudaStream_t st) {
+  tq_ctx* c = cm->ctx;
+  const int n = cm->n;
+  // every rank must see the same size: take the max over ranks
+  u64* g = (u64*)dalloc(c, 8 * (n + 1), st);
+  TQ_CUDA(cudaMemcpyAsync(g, &bytes, 8, cudaMemcpyHostToDevice, st));
+  comm_allgather_u64(cm, g, g + 1, 1, st);
+  std::vector<u64> all(n);
+  TQ_CUDA(cudaMemcpyAsync(all.data(), g + 1, 8 * n, cudaMemcpyDeviceToHost, st));
+  TQ_CUDA(cudaStreamSynchronize(st));
+  dfree(c, g, 8 * (n + 1), st);
+  for (u64 v : all) bytes = std::max<u64>(bytes, v);
+  if (cm->win_bytes < bytes) {
+    // drop the old mappings and buffer (every peer finished with them: the
+    // previous scatter ended with a barrier and its copy-out is stream-ordered)
+    TQ_CUDA(cudaStreamSynchronize(st));
+    peer_barrier(cm, st);
+    TQ_CUDA(cudaStreamSynchronize(st));
+    for (int p = 0; p < (int)cm->win_peer.size(); ++p)
+      if (p != cm->rank && cm->win_peer[p]) cudaIpcCloseMemHandle(cm->win_peer[p]);
+    if (cm->win) cudaFree(cm->win);
+    cm->win = nullptr;
+    cm->win_peer.assign(n, nullptr);
+    const u64 alloc = round_up(std::max<u64>(bytes, 1ull << 20) * 5 / 4, 1ull << 21);
+    TQ_CUDA(cudaMalloc(&cm->win, alloc));  // plain cudaMalloc: exportable with cudaIpcGetMemHandle
+    cm->win_bytes = alloc;
+    cudaIpcMemHandle_t h;
+    TQ_CUDA(cudaIpcGetMemHandle(&h, cm->win));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+    u64* hd = (u64*)dalloc(c, 64 * (n + 1), st);
+    TQ_CUDA(cudaMemcpyAsync(hd, &h, 64, cudaMemcpyHostToDevice, st));
+    comm_allgather_u64(cm, hd, hd + 8, 8, st);
+    std::vector<cudaIpcMemHandle_t> hs(n);
+    TQ_CUDA(cudaMemcpyAsync(hs.data(), hd + 8, 64 * n, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaStreamSynchronize(st));
+    dfree(c, hd, 64 * (n + 1), st);
+    for (int p = 0; p < n; ++p) {
+      if (p == cm->rank) {
+        cm->win_peer[p] = cm->win;
+        continue;
+      }
+      void* ptr = nullptr;
+      TQ_CUDA(cudaIpcOpenMemHandle(&ptr, hs[p], cudaIpcMemLazyEnablePeerAccess));
+      cm->win_peer[p] = (uint8_t*)ptr;
+    }
+  }
+  PeerView v;
+  v.local = cm->win;
+  v.peer = cm->win_peer;
+  v.rank = cm->rank;
+  v.n = n;
+  return v;
+}
+
+}  // namespace tq
 
 namespace {
 
@@ -219,6 +306,9 @@ tq_status tq_comm_init(tq_ctx* c, int rank, int nranks, const uint8_t* id, tq_co
 
 void tq_comm_destroy(tq_comm* cm) {
   if (!cm) return;
+  for (int p = 0; p < (int)cm->win_peer.size(); ++p)
+    if (p != cm->rank && cm->win_peer[p]) cudaIpcCloseMemHandle(cm->win_peer[p]);
+  if (cm->win) cudaFree(cm->win);
   try {
     nccl().destroy(cm->comm);
   } catch (...) {

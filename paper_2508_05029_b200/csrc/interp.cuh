@@ -255,50 +255,51 @@ __device__ __forceinline__ bool key_words(const WCtx& w, int v, u64* kw) {
 // ------------------------------------------------------------------ emit helpers
 __device__ __forceinline__ void store_out(const OutCol& o, u64 pos, const WCtx& w, int v, long long brow) {
   bool valid = true;
+  uint8_t* dst = o.values + w.out_delta;
   if (o.src == OUT_BUILD) {
-    store_build(o, pos, brow);
+    store_build(o, pos, brow, w.out_delta);
     return;
   } else {
     switch (o.kind) {
       case K_COL_I64:
       case K_COL_F64: {
         const StagedCol& sc = w.p->cols[o.idx];
-        *(u64*)(o.values + pos * 8) = ((const u64*)(w.stage + sc.off))[trow(w, v)];
+        *(u64*)(dst + pos * 8) = ((const u64*)(w.stage + sc.off))[trow(w, v)];
         valid = col_valid(w, o.idx, v);
         break;
       }
       case K_COL_DEC: {
         const StagedCol& sc = w.p->cols[o.idx];
-        *(ulonglong2*)(o.values + pos * 16) = ((const ulonglong2*)(w.stage + sc.off))[trow(w, v)];
+        *(ulonglong2*)(dst + pos * 16) = ((const ulonglong2*)(w.stage + sc.off))[trow(w, v)];
         valid = col_valid(w, o.idx, v);
         break;
       }
       case K_COL_BOOL: {
         const StagedCol& sc = w.p->cols[o.idx];
-        o.values[pos] = w.stage[sc.off + trow(w, v)];
+        dst[pos] = w.stage[sc.off + trow(w, v)];
         valid = col_valid(w, o.idx, v);
         break;
       }
       case K_TMP_F:
       case K_LIT_F: {
         double d = get_f(w, o.kind, o.idx, v, 0, valid);
-        *(double*)(o.values + pos * 8) = d;
+        *(double*)(dst + pos * 8) = d;
         break;
       }
       case K_TMP_B:
       case K_LIT_B: {
         bool b = get_b(w, o.kind, o.idx, v, valid);
-        o.values[pos] = b ? 1 : 0;
+        dst[pos] = b ? 1 : 0;
         break;
       }
       default: {  // K_TMP_I / K_LIT_I
         i128 x = get_i(w, o.kind, o.idx, v, valid);
-        if (o.width == 16) *(ulonglong2*)(o.values + pos * 16) = make_ulonglong2(lo64(x), hi64(x));
-        else *(u64*)(o.values + pos * 8) = lo64(x);
+        if (o.width == 16) *(ulonglong2*)(dst + pos * 16) = make_ulonglong2(lo64(x), hi64(x));
+        else *(u64*)(dst + pos * 8) = lo64(x);
       }
     }
   }
-  if (o.validity && valid) bm_set_atomic(o.validity, pos);
+  if (o.validity && valid) bm_set_atomic(o.validity + w.out_delta, pos);
 }
 
 

@@ -411,49 +411,49 @@ struct Gen {
         const OutCol& o = p.out[c];
         std::string oc = "p.out[" + std::to_string(c) + "]";
         if (o.src == OUT_BUILD) {
-          os << "    store_build(" << oc << ", pos, brow);\n";
+          os << "    store_build(" << oc << ", pos, brow, w.out_delta);\n";
           continue;
         }
         std::string valid;
         switch (o.kind) {
           case K_COL_I64:
             valid = g.col_valid(o.idx);
-            os << "    *(u64*)(" << oc << ".values + pos * 8) = (u64)" << g.col_val(o.idx) << ";\n";
+            os << "    *(u64*)(" << oc << ".values + w.out_delta + pos * 8) = (u64)" << g.col_val(o.idx) << ";\n";
             break;
           case K_COL_F64:
             valid = g.col_valid(o.idx);
-            os << "    *(u64*)(" << oc << ".values + pos * 8) = (u64)__double_as_longlong(" << g.col_val(o.idx)
+            os << "    *(u64*)(" << oc << ".values + w.out_delta + pos * 8) = (u64)__double_as_longlong(" << g.col_val(o.idx)
                << ");\n";
             break;
           case K_COL_DEC:
             valid = g.col_valid(o.idx);
-            os << "    *(ulonglong2*)(" << oc << ".values + pos * 16) = make_ulonglong2(lo64(" << g.col_val(o.idx)
+            os << "    *(ulonglong2*)(" << oc << ".values + w.out_delta + pos * 16) = make_ulonglong2(lo64(" << g.col_val(o.idx)
                << "), hi64(" << g.col_val(o.idx) << "));\n";
             break;
           case K_COL_BOOL:
             valid = g.col_valid(o.idx);
-            os << "    " << oc << ".values[pos] = " << g.col_val(o.idx) << ";\n";
+            os << "    (" << oc << ".values + w.out_delta)[pos] = " << g.col_val(o.idx) << ";\n";
             break;
           case K_TMP_F: case K_LIT_F: {
             std::string e = g.opnd_f(o.kind, o.idx, 0, valid);
-            os << "    *(double*)(" << oc << ".values + pos * 8) = " << e << ";\n";
+            os << "    *(double*)(" << oc << ".values + w.out_delta + pos * 8) = " << e << ";\n";
             break;
           }
           case K_TMP_B: case K_LIT_B: {
             std::string e = g.opnd_b(o.kind, o.idx, valid);
-            os << "    " << oc << ".values[pos] = (" << e << ") ? 1 : 0;\n";
+            os << "    (" << oc << ".values + w.out_delta)[pos] = (" << e << ") ? 1 : 0;\n";
             break;
           }
           default: {
             std::string e = g.root_i(o.kind, o.idx, valid);
             if (o.width == 16)
               os << "    { const i128 ox = " << e << "; *(ulonglong2*)(" << oc
-                 << ".values + pos * 16) = make_ulonglong2(lo64(ox), hi64(ox)); }\n";
+                 << ".values + w.out_delta + pos * 16) = make_ulonglong2(lo64(ox), hi64(ox)); }\n";
             else
-              os << "    *(u64*)(" << oc << ".values + pos * 8) = lo64(" << e << ");\n";
+              os << "    *(u64*)(" << oc << ".values + w.out_delta + pos * 8) = lo64(" << e << ");\n";
           }
         }
-        if (o.validity) os << "    set_valid(" << oc << ", pos, " << valid << ");\n";
+        if (o.validity) os << "    set_valid(" << oc << ", pos, " << valid << ", w.out_delta);\n";
       }
     } else {
       os << "    (void)r; (void)p; (void)pos; (void)brow;\n";

@@ -33,6 +33,7 @@ struct WCtx {
   u32 row0;              // tile-relative first row of this warp
   u32 nrows;             // rows in the tile
   u32 lane;
+  long long out_delta;   // added to output addresses (DEST_PEER: the destination rank's window)
 };
 
 __device__ __forceinline__ u32 trow(const WCtx& w, int v) { return w.row0 + (u32)v * 32u + w.lane; }
@@ -400,6 +401,7 @@ static_assert(kChunk + kThreads < (1 << kChunkUsedBits), "chunk word layout");
 
 // Reserve m (1..32) slots for the calling lane-0: [a, a+k1) in the current
 // chunk, the rest [b, b + m - k1) in a newly allocated one.
+template <bool kSystem = false>
 __device__ __forceinline__ void chunk_reserve(ChunkCursor* cc, u32 m, unsigned long long* gcursor, u64& a, u32& k1,
                                               u64& b) {
   for (;;) {
@@ -414,7 +416,7 @@ __device__ __forceinline__ void chunk_reserve(ChunkCursor* cc, u32 m, unsigned l
     if (off <= (u32)kChunk) {  // this reservation crosses the chunk end
       k1 = (u32)kChunk - off;
       a = cc->base[gen & 15] + off;
-      b = atomicAdd(gcursor, (unsigned long long)kChunk);
+      b = kSystem ? atomicAdd_system(gcursor, (unsigned long long)kChunk) : atomicAdd(gcursor, (unsigned long long)kChunk);
       ((volatile unsigned long long*)cc->base)[(gen + 1) & 15] = b;
       __threadfence_block();
       atomicExch(&cc->word, ((gen + 1) << kChunkUsedBits) | (m - k1));
@@ -470,6 +472,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   }
   ChunkCursor* s_chunk = (ChunkCursor*)s_base;  // DEST_PROBE1 only (s_base unused there)
   if (SINK == SINK_EMIT && threadIdx.x == 0) s_chunk->word = (u32)kChunk;  // generation 0, full: first use allocates
+  if (SINK == SINK_EMIT && p.dest_kind == DEST_PEER && threadIdx.x < p.ndest) s_chunk[threadIdx.x].word = (u32)kChunk;
   if (SINK == SINK_AGG && threadIdx.x < kThreads) {
     for (u32 i = threadIdx.x; i < G; i += kThreads) l_state[i] = kStEmpty;
 #pragma unroll
@@ -498,6 +501,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   w.bslot = (u32*)(smem + p.off_bslot) + (size_t)warp * p.nbslots * kV * 2;
   w.row0 = warp * 32 * kV;
   w.lane = lane;
+  w.out_delta = 0;
 
   const u32 first = blockIdx.x, step = gridDim.x;
   u32 s = 0, ph = 0;
@@ -523,7 +527,47 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     u32 pm[kV];
     u32 any = P::tile_begin(w, s_code, pm, raw);
 
-    if ((SINK == SINK_COUNT || SINK == SINK_EMIT) && p.dest_kind == DEST_PROBE1) {
+    if (SINK == SINK_EMIT && p.dest_kind == DEST_PEER) {
+      // fused partition + NVLink scatter: every passing row goes straight into
+      // its destination rank's receive window (peer memory via CUDA IPC)
+#pragma unroll
+      for (int v = 0; v < kV; ++v) {
+        bool pass = (pm[v] >> lane) & 1u;
+        u32 dest = 0;
+        if (pass) {
+          u64 kw[kMaxKeyWords + 1];
+          const bool has_null = P::keys(w, v, kw, raw[v]);
+          if (p.semi_bloom) {  // LIP: keys absent from the build side's Bloom filter cannot join
+            const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)p.key_words);
+            const u32 bb = bloom_bits(hb);
+            if (has_null || (__ldg(p.semi_bloom + bloom_word(hb, p.semi_mask)) & bb) != bb) pass = false;
+          }
+          dest = partition_of(p, kw);
+        }
+        u32 todo = __ballot_sync(kFull, pass);
+        while (todo) {
+          const u32 leader = __ffs(todo) - 1;
+          const u32 d = __shfl_sync(kFull, dest, leader);
+          const u32 grp = __ballot_sync(kFull, pass && dest == d);
+          todo &= ~grp;
+          u64 a = 0, b = 0;
+          u32 k1 = 0;
+          if (lane == leader) chunk_reserve<true>(s_chunk + d, (u32)__popc(grp), p.peer_counter[d], a, k1, b);
+          a = __shfl_sync(kFull, a, leader);
+          b = __shfl_sync(kFull, b, leader);
+          k1 = __shfl_sync(kFull, k1, leader);
+          if (pass && dest == d) {
+            const u32 rank = __popc(grp & lanemask_lt());
+            const u64 pos = rank < k1 ? a + rank : b + (rank - k1);
+            if (pos < p.peer_cap) {  // beyond: counted, not written (the host grows the window and re-runs)
+              w.out_delta = p.peer_delta[d];
+              P::store(w, v, pos, -1, raw[v]);
+              w.out_delta = 0;
+            }
+          }
+        }
+      }
+    } else if ((SINK == SINK_COUNT || SINK == SINK_EMIT) && p.dest_kind == DEST_PROBE1) {
       // single pass: unique build keys -> at most one match per probe row
 #pragma unroll
       for (int v = 0; v < kV; ++v) {
@@ -813,6 +857,17 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     if (++s == p.nstages) { s = 0; ph ^= 1u; }
   }
 
+  if (SINK == SINK_EMIT && p.dest_kind == DEST_PEER) {
+    consumers_sync();
+    if (threadIdx.x < p.ndest) {
+      const u32 d = threadIdx.x;
+      const u32 word = s_chunk[d].word;
+      const u32 used = min(word & ((1u << kChunkUsedBits) - 1), (u32)kChunk);
+      unsigned long long* t = p.peer_tails[d] + 2ull * (p.tail_slot0 + blockIdx.x);
+      t[0] = s_chunk[d].base[(word >> kChunkUsedBits) & 15];
+      t[1] = used;
+    }
+  }
   if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1) {
     consumers_sync();
     if (threadIdx.x == 0) {
@@ -895,17 +950,18 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
 }
 
 // ------------------------------------------------------------------ output stores
-__device__ __forceinline__ void set_valid(const OutCol& o, u64 pos, bool valid) {
-  if (o.validity && valid) bm_set_atomic(o.validity, pos);
+__device__ __forceinline__ void set_valid(const OutCol& o, u64 pos, bool valid, long long delta = 0) {
+  if (o.validity && valid) bm_set_atomic(o.validity + delta, pos);
 }
 
 // Copy a build-side value (probe output) by build row id.
-__device__ __forceinline__ void store_build(const OutCol& o, u64 pos, long long brow) {
+__device__ __forceinline__ void store_build(const OutCol& o, u64 pos, long long brow, long long delta = 0) {
   const uint8_t* src = o.bvalues + (u64)brow * o.width;
-  if (o.width == 16) *(ulonglong2*)(o.values + pos * 16) = *(const ulonglong2*)src;
-  else if (o.width == 8) *(u64*)(o.values + pos * 8) = *(const u64*)src;
-  else o.values[pos] = *src;
-  set_valid(o, pos, !o.bvalidity || bm_get(o.bvalidity, (u64)brow));
+  uint8_t* dst = o.values + delta;
+  if (o.width == 16) *(ulonglong2*)(dst + pos * 16) = *(const ulonglong2*)src;
+  else if (o.width == 8) *(u64*)(dst + pos * 8) = *(const u64*)src;
+  else dst[pos] = *src;
+  set_valid(o, pos, !o.bvalidity || bm_get(o.bvalidity, (u64)brow), delta);
 }
 
 }  // namespace tq

@@ -11,6 +11,7 @@
 #include "device.cuh"
 #include "pipeline.h"
 #include "program.h"
+#include "peer.h"
 
 struct tq_join_table {
   tq_ctx* ctx;
@@ -663,6 +664,169 @@ __global__ void k_jt_unique(JoinTable t, u32* dup) {
     }
     if (n > 1) atomicOr(dup, 1u);
   }
+}
+
+// ================================================================== fused partition + NVLink scatter
+// Every rank scans its rows once; each row that passes the predicate (and the
+// LIP Bloom filter) is written straight into the receive window of the rank
+// its key hashes to (fnv1a64 mod n, as tq_hash_partition), through CUDA IPC
+// mappings of the peers' windows over NVLink — the partitioned staging batch
+// and the NCCL payload copy of partition + tq_comm_exchange disappear.
+// Receivers then close the holes of the chunked layout and copy their rows out.
+__global__ void k_tail_reset(u64* tails, u64 nslots) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nslots; i += (u64)gridDim.x * blockDim.x) {
+    tails[2 * i] = 0;
+    tails[2 * i + 1] = kChunk;  // "full": no hole unless a CTA writes its tail here
+  }
+}
+
+static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, Prog& P,
+                                   const std::vector<uint32_t>& key_roots, const uint32_t* semi_words,
+                                   uint64_t semi_mask, tq_batch* out, uint64_t* rows_sent, cudaStream_t st) {
+  const int n = comm_size(cm), me = comm_rank(cm);
+  if (n > kMaxPeers) fail(TQ_INVALID_PLAN, "too many ranks for the fused exchange");
+  Plan L;
+  u32 sink_bytes = kWarps * kMaxDest * 4 + kWarps * kMaxDest * 8;
+  plan_launch(c, in, P, L, sink_bytes, st);
+  PipeParams& p = L.p;
+  if (L.grid > (u32)kMaxTailCtas) L.grid = kMaxTailCtas;
+  p.dest_kind = DEST_PEER;
+  p.ndest = (u32)n;
+  std::vector<int> kh;
+  for (uint32_t k : key_roots) {
+    if (k >= P.outs.size()) fail(TQ_INVALID_PLAN, "key column out of range");
+    kh.push_back(P.outs[k]);
+  }
+  set_keys(p, P.pb, kh);
+  p.semi_bloom = semi_words;
+  p.semi_mask = semi_mask;
+  std::vector<tq_column> sch;
+  std::vector<bool> wv;
+  std::vector<OutCol> outs;
+  for (int h : P.outs) {
+    const Operand& o = P.pb.root(h);
+    tq_column d{};
+    d.kind = out_kind_of(o, in, P.pb, &d.precision, &d.scale);
+    sch.push_back(d);
+    wv.push_back(o.maybe_null);
+    OutCol oc{};
+    oc.src = OUT_OPND;
+    oc.kind = o.kind;
+    oc.idx = o.idx;
+    oc.width = (uint8_t)width_of(d.kind);
+    oc.out_kind = d.kind;
+    outs.push_back(oc);
+  }
+  if (outs.size() > (size_t)kMaxOut) fail(TQ_INVALID_PLAN, "too many output columns");
+  p.nout = (u32)outs.size();
+
+  // window capacity (rows): every rank's guess, max over ranks; grown and
+  // re-run when a receiver's counter passed it (rows beyond were not written)
+  const bool filtered = P.has_pred || semi_words;
+  u64 guess = std::max<u64>(filtered ? in->rows / n / 4 : in->rows * 5 / 4 / n, 1ull << 16);
+  const u64 nslots = (u64)n * kMaxTailCtas;
+  const u64 data0 = round_up(256 + nslots * 16, 256);
+  u64* scratch = (u64*)dalloc(c, 8 * (2 * n + 8), st);  // [0..n) allgather out, [n] in, [n+1..] sent counter
+  u64* sent_dev = scratch + n + 1;
+  {
+    TQ_CUDA(cudaMemcpyAsync(scratch + n, &guess, 8, cudaMemcpyHostToDevice, st));
+    comm_allgather_u64(cm, scratch + n, scratch, 1, st);
+    std::vector<u64> g(n);
+    TQ_CUDA(cudaMemcpyAsync(g.data(), scratch, 8 * n, cudaMemcpyDeviceToHost, st));
+    { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+    for (u64 x : g) guess = std::max(guess, x);
+  }
+  u64 cap = guess;
+  const u64 plan_words = 4 + 4 * nslots + 6;
+  u64* plan = (u64*)dalloc(c, plan_words * 8, st);
+  static bool smem_set = false;
+  const u32 plan_smem = (u32)((3 * nslots + 2) * 8);
+  if (!smem_set || plan_smem > 48 * 1024) {
+    TQ_CUDA(cudaFuncSetAttribute(k_chunk_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    smem_set = true;
+  }
+  for (int attempt = 0;; ++attempt) {
+    // layout of the data region (same on every rank)
+    std::vector<u64> voff(outs.size()), boff(outs.size(), 0);
+    u64 end = data0;
+    for (size_t k = 0; k < outs.size(); ++k) {
+      voff[k] = end;
+      end = round_up(end + cap * outs[k].width, 256);
+      if (wv[k]) {
+        boff[k] = end;
+        end = round_up(end + (cap + 7) / 8, 256);
+      }
+    }
+    PeerView v = peer_window(cm, end, st);
+    u64* counter = (u64*)v.local;
+    u64* tails = (u64*)(v.local + 256);
+    TQ_CUDA(cudaMemsetAsync(counter, 0, 8, st));
+    TQ_CUDA(cudaMemsetAsync(sent_dev, 0, 8, st));
+    k_tail_reset<<<(u32)std::min<u64>(1024, (nslots + 255) / 256), 256, 0, st>>>(tails, nslots);
+    counted_launch(c);
+    for (size_t k = 0; k < outs.size(); ++k)
+      if (wv[k]) TQ_CUDA(cudaMemsetAsync(v.local + boff[k], 0, (cap + 7) / 8, st));
+    peer_barrier(cm, st);  // every window reset before anyone writes into it
+    for (int d = 0; d < n; ++d) {
+      p.peer_delta[d] = (long long)(v.peer[d] - v.local);
+      p.peer_counter[d] = (unsigned long long*)v.peer[d];
+      p.peer_tails[d] = (unsigned long long*)(v.peer[d] + 256);
+    }
+    p.peer_cap = cap;
+    p.tail_slot0 = (u32)me * kMaxTailCtas;
+    p.cursor = sent_dev;
+    ChunkOut co{};
+    co.ncols = p.nout;
+    for (size_t k = 0; k < outs.size(); ++k) {
+      outs[k].values = v.local + voff[k];
+      outs[k].validity = wv[k] ? v.local + boff[k] : nullptr;
+      p.out[k] = outs[k];
+      co.values[k] = outs[k].values;
+      co.validity[k] = outs[k].validity;
+      co.width[k] = outs[k].width;
+    }
+    launch(c, SINK_EMIT, L, P, st);
+    peer_barrier(cm, st);  // every rank's scatter into this window has completed
+    k_chunk_plan<<<1, 1024, plan_smem, st>>>(tails, (u32)nslots, counter, plan);
+    counted_launch(c);
+    TQ_CUDA(cudaMemcpyAsync(scratch + n, counter, 8, cudaMemcpyDeviceToDevice, st));
+    comm_allgather_u64(cm, scratch + n, scratch, 1, st);
+    u64 n_rows = 0, moves = 0, rmax = 0, sent_rows = 0;
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      u64* pin = (u64*)c->pinned;
+      TQ_CUDA(cudaMemcpyAsync(pin, plan, 16, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync(pin + 2, scratch, 8 * n, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync(pin + 2 + n, sent_dev, 8, cudaMemcpyDeviceToHost, st));
+      { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+      n_rows = pin[0];
+      moves = pin[1];
+      for (int d = 0; d < n; ++d) rmax = std::max(rmax, pin[2 + d]);
+      sent_rows = pin[2 + n];
+    }
+    if (rmax > cap) {  // some receiver overflowed: every rank sees the same rmax and re-runs
+      if (attempt > 4) fail(TQ_INTERNAL, "fused exchange window did not converge");
+      cap = rmax + rmax / 8 + (u64)kChunk * 64;
+      continue;
+    }
+    if (moves == ~0ull) fail(TQ_INTERNAL, "fused exchange chunk plan inconsistent");
+    k_chunk_move<<<c->sms * 2, 256, 0, st>>>(plan, (u32)nslots, co);
+    k_chunk_clear_tail<<<1, 32, 0, st>>>(plan, co);
+    counted_launch(c);
+    counted_launch(c);
+    TQ_CUDA(cudaGetLastError());
+    alloc_batch(c, n_rows, sch, wv, out, st);
+    for (size_t k = 0; k < outs.size(); ++k) {
+      if (n_rows) TQ_CUDA(cudaMemcpyAsync(out->cols[k].values, co.values[k], n_rows * outs[k].width,
+                                          cudaMemcpyDeviceToDevice, st));
+      if (wv[k] && n_rows)
+        TQ_CUDA(cudaMemcpyAsync(out->cols[k].validity, co.validity[k], (n_rows + 7) / 8, cudaMemcpyDeviceToDevice, st));
+    }
+    if (rows_sent) *rows_sent = sent_rows;
+    break;
+  }
+  dfree(c, plan, plan_words * 8, st);
+  dfree(c, scratch, 8 * (2 * n + 8), st);
 }
 
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
@@ -1661,6 +1825,36 @@ tq_status tq_pipeline_partition_semi(tq_ctx* c, const tq_batch* in, const tq_exp
       A.semi_mask = semi->nwords - 1;
     }
     run_materialize(c, in, P, A, out, part_offsets, pick(c, stream));
+  });
+}
+
+tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, const tq_expr* pred,
+                                         const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,
+                                         const tq_bloom* semi, tq_batch* out, void* stream) {
+  return guard([&] {
+    tq_ctx* c = comm_ctx(comm);
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
+    std::vector<uint32_t> kr(keys, keys + nkeys);
+    const uint32_t* sw = nullptr;
+    uint64_t sm = 0;
+    if (semi) {
+      if (semi->key_cls.size() != nkeys) fail(TQ_INVALID_PLAN, "semi-join key count differs");
+      for (uint32_t k = 0; k < nkeys; ++k) {
+        if (keys[k] >= P.outs.size()) fail(TQ_INVALID_PLAN, "key column out of range");
+        const Operand& o = P.pb.root(P.outs[keys[k]]);
+        if (o.cls != semi->key_cls[k] || (o.cls == C_D && o.scale != semi->key_scale[k]))
+          fail(TQ_INVALID_PLAN, "semi-join key types differ");
+      }
+      sw = semi->words;
+      sm = semi->nwords - 1;
+    }
+    uint64_t sent_rows = 0;
+    run_partition_exchange(c, comm, in, P, kr, sw, sm, out, &sent_rows, pick(c, stream));
+    uint64_t row_bytes = 0;
+    for (uint32_t k = 0; k < out->ncols; ++k) row_bytes += width_of(out->cols[k].kind);
+    comm_add_sent(comm, sent_rows * row_bytes);
   });
 }
 

@@ -40,7 +40,9 @@ enum SinkKind { SINK_COUNT = 0, SINK_EMIT = 1, SINK_AGG = 2, SINK_BUILD = 3 };
 // FILTER/PARTITION/PROBE: two passes (COUNT then EMIT), stable order.
 // PROBE1: single EMIT pass for unique build keys (<= 1 match per row);
 //         output rows are reserved with a warp-aggregated atomic cursor.
-enum DestKind { DEST_FILTER = 0, DEST_PARTITION = 1, DEST_PROBE = 2, DEST_PROBE1 = 3 };
+enum DestKind { DEST_FILTER = 0, DEST_PARTITION = 1, DEST_PROBE = 2, DEST_PROBE1 = 3, DEST_PEER = 4 };
+constexpr int kMaxPeers = 16;       // DEST_PEER: ranks of one communicator
+constexpr int kMaxTailCtas = 512;   // DEST_PEER: per-source-rank tail slots in a receive window
 
 struct StagedCol {
   const uint8_t* values;
@@ -137,6 +139,15 @@ struct PipeParams {
   const unsigned long long* tile_offsets;  // [ndest][ntiles * kWarps] absolute output rows
   unsigned long long* cursor;     // DEST_PROBE1 chunk cursor (rows, kChunk units); BUILD inserted-row count
   unsigned long long* chunk_tail; // DEST_PROBE1: per CTA {base, used} of its last output chunk
+  // DEST_PEER (fused partition + NVLink scatter): destination d's receive
+  // window is this rank's window + peer_delta[d] (CUDA IPC mapping); rows are
+  // reserved in kChunk-row chunks from the receiver's counter and each CTA
+  // leaves its last chunk {base, used} in the receiver's tail slots.
+  long long peer_delta[kMaxPeers];
+  unsigned long long* peer_counter[kMaxPeers];
+  unsigned long long* peer_tails[kMaxPeers];
+  uint64_t peer_cap;     // rows of every receive window
+  uint32_t tail_slot0;   // this rank's first tail slot (rank * kMaxTailCtas)
   JoinTable jt;
   // LIP semi-join filter on the key words (dest PARTITION): rows whose keys
   // miss this Bloom filter are dropped before they are partitioned / shipped

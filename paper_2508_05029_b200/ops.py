@@ -140,6 +140,7 @@ def lib():
         L.tq_bloom_destroy.argtypes = [V]
         L.tq_pipeline_partition_semi.argtypes = [V, B, E, E, C.c_uint32, U32, C.c_uint32, C.c_uint32, V, B,
                                                  P(C.c_uint64), V]
+        L.tq_pipeline_partition_exchange.argtypes = [V, B, E, E, C.c_uint32, U32, C.c_uint32, V, B, V]
         L.tq_comm_bloom_union.argtypes = [V, V, V]
         L.tq_estimate_reservation.restype = C.c_uint64
         L.tq_estimate_reservation.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double]
@@ -517,6 +518,19 @@ class Comm:
         out = TqBatchC()
         Context._check(lib().tq_comm_exchange(self.handle, C.byref(b.c), po, C.byref(out), ro, stream))
         return DeviceBatch(self.ctx, out), list(ro)
+
+    def partition_exchange(self, b: DeviceBatch, pred, exprs, keys: Sequence[int], semi: "Bloom" = None,
+                           stream=None) -> DeviceBatch:
+        """Fused hash-partition + shuffle over NVLink peer memory
+        (tq_pipeline_partition_exchange): the rows every rank sends to this one,
+        in unspecified order.  Collective."""
+        pp, _k1 = _pred(pred)
+        arr, n, _k2 = _exprs(exprs)
+        out = TqBatchC()
+        Context._check(lib().tq_pipeline_partition_exchange(self.handle, C.byref(b.c), pp, arr, n, _u32(keys),
+                                                            len(keys), semi.handle if semi else None,
+                                                            C.byref(out), stream))
+        return DeviceBatch(self.ctx, out)
 
     def allgather(self, b: DeviceBatch, stream=None) -> Tuple[DeviceBatch, List[int]]:
         ro = (C.c_uint64 * (self.n + 1))()

@@ -154,7 +154,7 @@ def run_join_query(ctx, q: int, tables: dict):
 
 
 # ---------------------------------------------------------------- distributed (one rank per GPU)
-def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True):
+def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True, fused=False):
     """Config 4: Q3-style shuffle join over each rank's row-group subset.
     customer_f is broadcast (exchange_decide: 24 MB <= 16 MiB x N at SF100),
     orders_f and lineitem_f are hash-partitioned on orderkey (fnv1a64 mod N)
@@ -162,7 +162,10 @@ def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True):
     follows is co-partitioned, so each rank's groups are final.
     lip=True adds Lookahead Information Passing: a Bloom filter
     of the orders_f keys, OR-ed across ranks, drops lineitem rows that cannot
-    join before they are partitioned and shipped (same result)."""
+    join before they are partitioned and shipped (same result).
+    fused=True replaces each partition + all-to-all pair with the fused
+    partition/scatter over NVLink peer memory (tq_pipeline_partition_exchange):
+    rows are written once, straight into their destination rank's window."""
     n = comm.n
     cf = ctx.pipeline_materialize(customer, Col(C_MKTSEGMENT).eq(1), [Col(C_CUSTKEY)])
     cb, _ = comm.allgather(cf)
@@ -173,19 +176,25 @@ def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True):
     if lip:
         bloom = ctx.bloom_build(of, [0], expected_keys=of.rows * n)
         comm.bloom_union(bloom)
-    op, ooff = ctx.hash_partition(of, [0], n)
-    orx, _ = comm.exchange(op, ooff)
-    if lip:
-        lp, loff = ctx.pipeline_partition_semi(lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], n, bloom)
+    if fused:
+        orx = comm.partition_exchange(of, None, None, [0])
+        lrx = comm.partition_exchange(lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], bloom)
+        lp = lrx
     else:
-        lp, loff = ctx.pipeline_partition(lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], n)
-    lrx, _ = comm.exchange(lp, loff)
+        op, ooff = ctx.hash_partition(of, [0], n)
+        orx, _ = comm.exchange(op, ooff)
+        if lip:
+            lp, loff = ctx.pipeline_partition_semi(lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], n,
+                                                   bloom)
+        else:
+            lp, loff = ctx.pipeline_partition(lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], n)
+        lrx, _ = comm.exchange(lp, loff)
     ot = ctx.join_build(orx, [0])
     j = ctx.pipeline_probe(ot, lrx, None, None, [0], [1, 2])
     out = ctx.aggregate_execute(j, [2, 0, 1], [(AGG_SUM, 3)])
     if stats is not None:
-        stats.update({"orders_f_rows": of.rows, "lineitem_shipped_rows": lp.rows, "recv_orders": orx.rows,
-                      "recv_lineitem": lrx.rows, "lip": lip})
+        stats.update({"orders_f_rows": of.rows, "lineitem_shipped_rows": None if fused else lp.rows,
+                      "recv_orders": orx.rows, "recv_lineitem": lrx.rows, "lip": lip, "fused": fused})
     for t in (ct, ot):
         t.free()
     if bloom is not None:

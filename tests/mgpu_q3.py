@@ -31,7 +31,8 @@ def main():
                                   compute_threads=4, batch_rows=256 * 1024)
     else:
         out = queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"],
-                                     lip=os.environ.get("TQ_LIP", "1") == "1").to_host()
+                                     lip=os.environ.get("TQ_LIP", "1") == "1",
+                                     fused=os.environ.get("TQ_FUSED", "0") == "1").to_host()
     parts = [None] * world
     dist.all_gather_object(parts, out)
     rc = 0
