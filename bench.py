@@ -283,18 +283,23 @@ def run_suite(args, ctx, world, rank, stream):
     sf = args.shuffle_sf
     t = {n: ctx.datagen(queries.TABLE_IDS[n], sf, shard=rank, nshards=world) for n in ("customer", "orders", "lineitem")}
     rows = sum_over_ranks(world, float(sum(v.rows for v in t.values())))
-    b0 = comm.bytes_sent()
-    stats = {}
-    ms = timed(ctx, lambda: queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], stats),
-               3, world, stream)
-    sent = (comm.bytes_sent() - b0) / 4.0  # 1 warm-up + 3 timed runs
-    suite[f"q3_shuffle_sf{sf:g}"] = {
-        "ms": ms, "rows_per_s": rows / (ms * 1e-3), "scaling": "strong", "n_gpus": world,
-        "nvlink_bytes_sent_per_gpu": sent, "nvlink_gbs_per_gpu": sent / (ms * 1e-3) / 1e9,
-        "nvlink_frac_of_770": sent / (ms * 1e-3) / 770e9,
-        "exchange": "customer_f broadcast (allgather); orders_f, lineitem_f hash-partitioned (fnv1a64 mod N)",
-        "recv_rows_rank0": {k: v for k, v in stats.items()},
-    }
+    for fused in (True, False):
+        b0 = comm.bytes_sent()
+        stats = {}
+        ms = timed(ctx, lambda: queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], stats,
+                                                       fused=fused), 3, world, stream)
+        sent = (comm.bytes_sent() - b0) / 4.0  # 1 warm-up + 3 timed runs
+        key = f"q3_shuffle_sf{sf:g}" if fused else f"q3_shuffle_nccl_sf{sf:g}"
+        suite[key] = {
+            "ms": ms, "rows_per_s": rows / (ms * 1e-3), "scaling": "strong", "n_gpus": world,
+            "nvlink_bytes_sent_per_gpu": sent, "nvlink_gbs_per_gpu": sent / (ms * 1e-3) / 1e9,
+            "nvlink_frac_of_770": sent / (ms * 1e-3) / 770e9,
+            "exchange": ("customer_f broadcast (allgather); orders_f, lineitem_f: fused partition + scatter into "
+                         "the destination rank's CUDA-IPC window over NVLink (fnv1a64 mod N)") if fused else
+                        ("customer_f broadcast (allgather); orders_f, lineitem_f hash-partitioned (fnv1a64 mod N) "
+                         "then NCCL grouped send/recv"),
+            "recv_rows_rank0": {k: v for k, v in stats.items()},
+        }
     for v in t.values():
         v.free()
     comm.close()

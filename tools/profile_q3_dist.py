@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--sf", type=float, default=100)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nolip", action="store_true")
+    ap.add_argument("--fused", action="store_true", help="fused partition + NVLink scatter")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -69,19 +70,28 @@ def main():
             mark("LIP bloom build")
             comm.bloom_union(bloom)
             mark("LIP bloom union")
-        op, ooff = ctx.hash_partition(of, [0], n)
-        mark("orders partition")
-        orx, _ = comm.exchange(op, ooff)
-        mark("orders exchange")
-        if lip:
-            lp, loff = ctx.pipeline_partition_semi(t["lineitem"], Col(Q.L_SHIPDATE) > 9204, [Col(Q.L_ORDERKEY), Q.REV],
-                                                   [0], n, bloom)
+        if a.fused:
+            orx = comm.partition_exchange(of, None, None, [0])
+            op = orx
+            mark("orders fused partition+scatter")
+            lrx = comm.partition_exchange(t["lineitem"], Col(Q.L_SHIPDATE) > 9204, [Col(Q.L_ORDERKEY), Q.REV], [0],
+                                          bloom)
+            lp = lrx
+            mark("lineitem fused filter+semi+partition+scatter")
         else:
-            lp, loff = ctx.pipeline_partition(t["lineitem"], Col(Q.L_SHIPDATE) > 9204, [Col(Q.L_ORDERKEY), Q.REV], [0],
-                                              n)
-        mark("lineitem filter+partition")
-        lrx, _ = comm.exchange(lp, loff)
-        mark("lineitem exchange")
+            op, ooff = ctx.hash_partition(of, [0], n)
+            mark("orders partition")
+            orx, _ = comm.exchange(op, ooff)
+            mark("orders exchange")
+            if lip:
+                lp, loff = ctx.pipeline_partition_semi(t["lineitem"], Col(Q.L_SHIPDATE) > 9204,
+                                                       [Col(Q.L_ORDERKEY), Q.REV], [0], n, bloom)
+            else:
+                lp, loff = ctx.pipeline_partition(t["lineitem"], Col(Q.L_SHIPDATE) > 9204, [Col(Q.L_ORDERKEY), Q.REV],
+                                                  [0], n)
+            mark("lineitem filter+partition")
+            lrx, _ = comm.exchange(lp, loff)
+            mark("lineitem exchange")
         ot = ctx.join_build(orx, [0])
         mark("orders_f build")
         j = ctx.pipeline_probe(ot, lrx, None, None, [0], [1, 2])
@@ -97,7 +107,7 @@ def main():
         else:
             allt = [times]
         if rank == 0 and rep == a.reps - 1:
-            print(f"world={world} sf={a.sf:g} lip={lip}")
+            print(f"world={world} sf={a.sf:g} lip={lip} fused={a.fused}")
             for i, (name, ms) in enumerate(times):
                 mx = max(r[i][1] for r in allt)
                 print(f"  {name:28s} rank0 {ms:8.3f} ms   max {mx:8.3f} ms", flush=True)
@@ -105,7 +115,7 @@ def main():
             print(f"  total rank0 {tot[0]:.3f} ms  max {max(tot):.3f} ms", flush=True)
             prof = ctx.profile_report()
             print("  kernels (rank0): " + ", ".join(f"{k} {v[0]}x {v[1]:.3f} ms" for k, v in sorted(prof.items())))
-        for x in (cf, cb, of, op, orx, lp, lrx, j, out):
+        for x in {id(x): x for x in (cf, cb, of, op, orx, lp, lrx, j, out)}.values():
             x.free()
         for x in (ct, ot):
             x.free()
