@@ -723,7 +723,8 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
   // window capacity (rows): every rank's guess, max over ranks; grown and
   // re-run when a receiver's counter passed it (rows beyond were not written)
   const bool filtered = P.has_pred || semi_words;
-  u64 guess = std::max<u64>(filtered ? in->rows / n / 4 : in->rows * 5 / 4 / n, 1ull << 16);
+  // a receiver gets ~ (all ranks' rows) / n ~ this rank's rows when balanced
+  u64 guess = std::max<u64>(filtered ? in->rows / 4 : in->rows * 5 / 4, 1ull << 16);
   const u64 nslots = (u64)n * kMaxTailCtas;
   const u64 data0 = round_up(256 + nslots * 16, 256);
   u64* scratch = (u64*)dalloc(c, 8 * (2 * n + 8), st);  // [0..n) allgather out, [n] in, [n+1..] sent counter
@@ -757,7 +758,11 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
         end = round_up(end + (cap + 7) / 8, 256);
       }
     }
-    PeerView v = peer_window(cm, end, st);
+    TQ_HT("pex total attempt");
+    PeerView v = [&] {
+      TQ_HT("pex window");
+      return peer_window(cm, end, st);
+    }();
     u64* counter = (u64*)v.local;
     u64* tails = (u64*)(v.local + 256);
     TQ_CUDA(cudaMemsetAsync(counter, 0, 8, st));
@@ -766,7 +771,10 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     counted_launch(c);
     for (size_t k = 0; k < outs.size(); ++k)
       if (wv[k]) TQ_CUDA(cudaMemsetAsync(v.local + boff[k], 0, (cap + 7) / 8, st));
-    peer_barrier(cm, st);  // every window reset before anyone writes into it
+    {
+      TQ_HT("pex barrier1");
+      peer_barrier(cm, st);  // every window reset before anyone writes into it
+    }
     for (int d = 0; d < n; ++d) {
       p.peer_delta[d] = (long long)(v.peer[d] - v.local);
       p.peer_counter[d] = (unsigned long long*)v.peer[d];
@@ -786,7 +794,10 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
       co.width[k] = outs[k].width;
     }
     launch(c, SINK_EMIT, L, P, st);
-    peer_barrier(cm, st);  // every rank's scatter into this window has completed
+    {
+      TQ_HT("pex barrier2");
+      peer_barrier(cm, st);  // every rank's scatter into this window has completed
+    }
     k_chunk_plan<<<1, 1024, plan_smem, st>>>(tails, (u32)nslots, counter, plan);
     counted_launch(c);
     TQ_CUDA(cudaMemcpyAsync(scratch + n, counter, 8, cudaMemcpyDeviceToDevice, st));
@@ -798,7 +809,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
       TQ_CUDA(cudaMemcpyAsync(pin, plan, 16, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaMemcpyAsync(pin + 2, scratch, 8 * n, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaMemcpyAsync(pin + 2 + n, sent_dev, 8, cudaMemcpyDeviceToHost, st));
-      { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+      { TQ_HT("pex sync after plan"); TQ_CUDA(cudaStreamSynchronize(st)); }
       n_rows = pin[0];
       moves = pin[1];
       for (int d = 0; d < n; ++d) rmax = std::max(rmax, pin[2 + d]);

@@ -48,6 +48,10 @@ def main():
             dist.barrier()
         marks = []
         ctx.profile(rep == a.reps - 1)
+        if rep == a.reps - 1 and os.environ.get("TQ_HOST_TIMING") == "1":
+            import ctypes as C
+            from paper_2508_05029_b200.ops import lib
+            lib().tq_host_timing_report(C.create_string_buffer(1 << 16), 1 << 16)  # only the last rep
 
         def mark(name):
             e = torch.cuda.Event(enable_timing=True)
@@ -113,6 +117,12 @@ def main():
                 print(f"  {name:28s} rank0 {ms:8.3f} ms   max {mx:8.3f} ms", flush=True)
             tot = [sum(x[1] for x in r) for r in allt]
             print(f"  total rank0 {tot[0]:.3f} ms  max {max(tot):.3f} ms", flush=True)
+            if os.environ.get("TQ_HOST_TIMING") == "1":
+                import ctypes as C
+                from paper_2508_05029_b200.ops import lib
+                buf = C.create_string_buffer(1 << 16)
+                lib().tq_host_timing_report(buf, len(buf))
+                print(buf.value.decode())
             prof = ctx.profile_report()
             print("  kernels (rank0): " + ", ".join(f"{k} {v[0]}x {v[1]:.3f} ms" for k, v in sorted(prof.items())))
         for x in {id(x): x for x in (cf, cb, of, op, orx, lp, lrx, j, out)}.values():
