@@ -50,64 +50,75 @@ def ncu_traffic(kernel: str):
 
 
 class Clocks:
-    """SM clocks and throttle reasons sampled DURING the timed region by an
-    nvidia-smi subprocess (B200_PROFILING.md clocks line), started by rank 0
-    only and covering every GPU of the job: in-process NVML polling from each
-    rank stalls the other ranks' CUDA calls."""
+    """SM clocks and throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line). Each rank polls NVML for its OWN GPU
+    from a background thread that runs from just before the opening event to
+    just after the closing synchronize (ctypes NVML calls release the GIL, so
+    the launching thread is not held up); rank 0 merges every rank's samples. (An nvidia-smi -lms subprocess block-buffers its
+    output and produced no samples inside a ~10 ms timed region.)"""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, devices, period_ms: int = 20):
-        self.devices = devices
-        self.period = period_ms
-        self.proc = None
-
-    def start(self):
+    def __init__(self, device: int):
+        self.h = None
+        self.sm, self.mx, self.bits = [], None, 0
         if os.environ.get("TQ_BENCH_CLOCKS", "1") == "0":
             return
         try:
+            import pynvml
             import torch
-            ids = []
-            for d in self.devices:  # UUIDs: CUDA_VISIBLE_DEVICES ordinals are not nvidia-smi indices
-                try:
-                    ids.append("GPU-" + str(torch.cuda.get_device_properties(d).uuid))
-                except Exception:
-                    ids.append(str(d))
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", ",".join(ids), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", str(self.period)],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(device).uuid))
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
         except Exception:
-            self.proc = None
+            self.h = None
+
+    def sample(self):
+        if self.h is None:
+            return
+        try:
+            self.sm.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
+            self.bits |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+        except Exception:
+            pass
+
+    def start(self, period_s: float = 0.001):
+        """Background sampler thread for the timed region (NVML calls release the GIL)."""
+        import threading
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                self.sample()
+                time.sleep(period_s)
+        self._thr = threading.Thread(target=run, daemon=True)
+        self._thr.start()
 
     def stop(self):
-        if not self.proc:
-            return None
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            return None
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
+        if getattr(self, "_thr", None):
+            self._stop.set()
+            self._thr.join()
+            self._thr = None
+
+    def report(self, world: int):
+        mine = {"sm": self.sm, "mx": self.mx, "bits": self.bits}
+        alls = [mine]
+        if world > 1:
+            import torch.distributed as dist
+            alls = [None] * world
+            dist.all_gather_object(alls, mine)
+        sm = [x for a in alls for x in a["sm"]]
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
-                "source": f"nvidia-smi -lms {self.period} (rank 0, all GPUs)"}
+        bits = 0
+        for a in alls:
+            bits |= a["bits"]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(a["mx"] or 0 for a in alls),
+                "reasons": sorted(n for n, b in self.REASONS.items() if bits & b), "samples": len(sm),
+                "samples_by_rank": [len(a["sm"]) for a in alls],
+                "source": "NVML clocks/event reasons polled by every rank for its own GPU inside the timed region"}
 
 
 def dist_setup():
@@ -333,10 +344,8 @@ def run_tq(args, world, rank, local):
         step().free()
     ctx.sync()
     barrier(world)
-    clocks = Clocks(list(range(world)) if world > 1 else [local])
-    if rank == 0:
-        clocks.start()
-        time.sleep(0.3)  # nvidia-smi start-up, so samples land inside the timed region
+    clocks = Clocks(local)
+    clocks.start()
     ctx.profile(True)
     l0 = ctx.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -348,11 +357,12 @@ def run_tq(args, world, rank, local):
     e1.record(stream)
     torch.cuda.synchronize()
     ctx.sync()
+    clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     launches = ctx.kernel_launches() - l0
     prof = ctx.profile_report()
     ctx.profile(False)
-    ck = clocks.stop()
+    ck = clocks.report(world)
     barrier(world)
     ms_max = max_over_ranks(world, ms)
     ms_ranks = gather_ranks(world, round(ms, 4))
