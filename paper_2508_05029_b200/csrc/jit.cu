@@ -496,9 +496,14 @@ Entry compile(const std::string& src) {
   std::string inc1 = "-I" + dir, inc2 = "-I" + dir + "/../../include";
   // the tile geometry this library was built with (pipeline.h)
   std::string dw = "-DTQ_KWARPS=" + std::to_string(kWarps), dv = "-DTQ_KV=" + std::to_string(kV);
+  // TQ_JIT_DEFS: one extra -D for experiments (e.g. TQ_PB=4)
+  static const std::string xdef = [] {
+    const char* e = getenv("TQ_JIT_DEFS");
+    return e && *e ? std::string("-D") + e : std::string("-DTQ_JIT_NOEXTRA=1");
+  }();
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DTQ_JIT=1", "--device-int128",
-                        inc1.c_str(), inc2.c_str(), dw.c_str(), dv.c_str()};
-  int rc = n.compile(prog, 9, opts);
+                        inc1.c_str(), inc2.c_str(), dw.c_str(), dv.c_str(), xdef.c_str()};
+  int rc = n.compile(prog, 10, opts);
   if (rc != 0) {
     size_t ls = 0;
     n.log_size(prog, &ls);

@@ -259,19 +259,28 @@ __device__ __forceinline__ u32 partition_of(const PipeParams& p, const u64* kw) 
 }
 
 // The single build row matching kw (unique-key tables), or -1.
+// First build row matching kw (-1: none); the rest of the cluster is walked
+// too, and a second match sets *dup (non-unique build keys).
 template <int KW>
-__device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u64* kw) {
+__device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u64* kw, bool& dup) {
   const u64 h = key_hash(kw, KW > 0 ? KW : (int)t.kw);
   if (t.bloom) {
     const u32 b = bloom_bits(h);
     if ((__ldg(t.bloom + bloom_word(h, t.bloom_mask)) & b) != b) return -1;
   }
   const u64 mask = t.cap - 1;
+  long long found = -1;
   for (u64 s = h & mask;; s = (s + 1) & mask) {
     const long long* e = jt_entry(t, s);
     const long long row = e[0];
-    if (row < 0) return -1;
-    if (jt_key_eq<KW>(t, e, kw)) return row;
+    if (row < 0) return found;
+    if (jt_key_eq<KW>(t, e, kw)) {
+      if (found >= 0) {
+        dup = true;
+        return found;
+      }
+      found = row;
+    }
   }
 }
 
@@ -575,7 +584,9 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         long long brow = -1;
         if (pass) {
           u64 kw[kMaxKeyWords + 1];
-          if (!P::keys(w, v, kw, raw[v])) brow = jt_probe_first<P::kKw>(p.jt, kw);
+          bool dup = false;
+          if (!P::keys(w, v, kw, raw[v])) brow = jt_probe_first<P::kKw>(p.jt, kw, dup);
+          if (dup && *(volatile u32*)p.dup_flag == 0) *(volatile u32*)p.dup_flag = 1;
         }
         const u32 mm = __ballot_sync(kFull, brow >= 0);
         if (mm) {

@@ -372,19 +372,63 @@ struct ChunkOut {
 };
 // plan: [0] n, [1] moves, [2] hole ranges, [3] source ranges, then
 // hole start[nh], hole prefix[nh + 1], source start[ns], source prefix[ns + 1]
+//
+// Block-wide exclusive scan of (count, length) pairs over 1024 threads;
+// returns the exclusive prefixes and leaves the block totals in *tc / *tl.
+__device__ __forceinline__ void block_scan2(u32 c, u64 l, u32& ec, u64& el, u32* tc, u64* tl) {
+  __shared__ u32 wc[32];
+  __shared__ u64 wl[32];
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u32 ic = c;
+  u64 il = l;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 yc = __shfl_up_sync(0xffffffffu, ic, o);
+    const u64 yl = __shfl_up_sync(0xffffffffu, il, o);
+    if (lane >= (u32)o) { ic += yc; il += yl; }
+  }
+  if (lane == 31) { wc[warp] = ic; wl[warp] = il; }
+  __syncthreads();
+  if (warp == 0) {
+    const u32 nw = blockDim.x >> 5;
+    u32 xc = lane < nw ? wc[lane] : 0;
+    u64 xl = lane < nw ? wl[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 yc = __shfl_up_sync(0xffffffffu, xc, o);
+      const u64 yl = __shfl_up_sync(0xffffffffu, xl, o);
+      if (lane >= (u32)o) { xc += yc; xl += yl; }
+    }
+    if (lane < nw) { wc[lane] = xc; wl[lane] = xl; }
+    if (lane == nw - 1) { *tc = xc; *tl = xl; }
+  }
+  __syncthreads();
+  ec = ic - c + (warp ? wc[warp - 1] : 0);
+  el = il - l + (warp ? wl[warp - 1] : 0);
+  __syncthreads();
+}
+
+// One block; every loop is a parallel pass (a serial single-thread plan cost
+// ~45 us for 296 CTAs).  Ranges are listed in CTA / chunk order.
 __global__ void k_chunk_plan(const u64* tails, u32 nctas, const u64* gcursor, u64* plan) {
   extern __shared__ u64 sm_chunk[];
   u64* tb = sm_chunk;          // [nctas] last-chunk base
   u64* tu = tb + nctas;        // [nctas] used rows
   u64* uj = tu + nctas;        // [nctas + 2] used rows of the chunks at/after floor(n / kChunk)
   __shared__ unsigned long long holes_total;
+  __shared__ u32 tot_c;
+  __shared__ u64 tot_l;
   if (threadIdx.x == 0) holes_total = 0;
   __syncthreads();
+  unsigned long long my_holes = 0;
   for (u32 i = threadIdx.x; i < nctas; i += blockDim.x) {
     tb[i] = tails[2 * i];
     tu[i] = tails[2 * i + 1];
-    if (tu[i] < (u64)kChunk) atomicAdd(&holes_total, (unsigned long long)(kChunk - tu[i]));
+    if (tu[i] < (u64)kChunk) my_holes += kChunk - tu[i];
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) my_holes += __shfl_xor_sync(0xffffffffu, my_holes, o);
+  if ((threadIdx.x & 31) == 0 && my_holes) atomicAdd(&holes_total, my_holes);
   __syncthreads();
   const u64 R = *gcursor, n = R - holes_total;
   const u64 j0 = n / kChunk, nj = R / kChunk - j0;
@@ -393,30 +437,57 @@ __global__ void k_chunk_plan(const u64* tails, u32 nctas, const u64* gcursor, u6
   for (u32 i = threadIdx.x; i < nctas; i += blockDim.x)
     if (tu[i] < (u64)kChunk && tb[i] >= j0 * kChunk) uj[tb[i] / kChunk - j0] = tu[i];
   __syncthreads();
-  if (threadIdx.x != 0) return;
   u64* hs = plan + 4;
   u64* hp = hs + nctas;
   u64* ss = hp + nctas + 1;
   u64* sp = ss + nctas + 2;
-  u64 nh = 0, tot = 0;
+  // holes: the unused tail of every partly used chunk below n
+  u32 nh = 0;
+  u64 tot = 0;
+  for (u32 base = 0; base < nctas; base += blockDim.x) {
+    const u32 i = base + threadIdx.x;
+    u64 a = 0, len = 0;
+    if (i < nctas && tu[i] < (u64)kChunk && tb[i] < n) {
+      a = tb[i] + tu[i];
+      const u64 e = min(tb[i] + (u64)kChunk, n);
+      len = a < e ? e - a : 0;
+    }
+    u32 ec;
+    u64 el;
+    block_scan2(len ? 1u : 0u, len, ec, el, &tot_c, &tot_l);
+    if (len) {
+      hs[nh + ec] = a;
+      hp[nh + ec + 1] = tot + el + len;
+    }
+    nh += tot_c;
+    tot += tot_l;
+    __syncthreads();
+  }
+  // sources: the used rows at/after n
+  u32 ns = 0;
+  u64 tot2 = 0;
+  for (u64 base = 0; base < nj; base += blockDim.x) {
+    const u64 j = base + threadIdx.x;
+    u64 a = 0, len = 0;
+    if (j < nj) {
+      const u64 s0 = (j0 + j) * kChunk, e = s0 + uj[j];
+      a = max(s0, n);
+      len = a < e ? e - a : 0;
+    }
+    u32 ec;
+    u64 el;
+    block_scan2(len ? 1u : 0u, len, ec, el, &tot_c, &tot_l);
+    if (len) {
+      ss[ns + ec] = a;
+      sp[ns + ec + 1] = tot2 + el + len;
+    }
+    ns += tot_c;
+    tot2 += tot_l;
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
   hp[0] = 0;
-  for (u32 i = 0; i < nctas; ++i) {
-    if (tu[i] >= (u64)kChunk || tb[i] >= n) continue;
-    const u64 a = tb[i] + tu[i], e = min(tb[i] + (u64)kChunk, n);
-    if (a >= e) continue;
-    hs[nh] = a;
-    tot += e - a;
-    hp[++nh] = tot;
-  }
-  u64 ns = 0, tot2 = 0;
   sp[0] = 0;
-  for (u64 j = 0; j < nj; ++j) {
-    const u64 s0 = (j0 + j) * kChunk, a = max(s0, n), e = s0 + uj[j];
-    if (a >= e) continue;
-    ss[ns] = a;
-    tot2 += e - a;
-    sp[++ns] = tot2;
-  }
   plan[0] = n;
   plan[1] = tot == tot2 ? tot : ~0ull;  // (equal by construction)
   plan[2] = nh;
@@ -538,14 +609,17 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     // rows land in kChunk-row chunks: room for one partly used chunk per CTA
     const uint64_t cap_rows = in->rows + (uint64_t)L.grid * kChunk;
     alloc_batch(c, cap_rows, sch, wv, out, st);
-    const uint64_t scratch = 8 + L.grid * 16 + (10 + 4 * (uint64_t)L.grid) * 8;  // cursor, tails, plan
+    // cursor, dup flag, tails, plan
+    const uint64_t scratch = 16 + L.grid * 16 + (10 + 4 * (uint64_t)L.grid) * 8;
     uint8_t* sb = (uint8_t*)dalloc(c, scratch, st);
     u64* cursor = (u64*)sb;
-    u64* tails = cursor + 1;
+    u32* dup = (u32*)(cursor + 1);
+    u64* tails = cursor + 2;
     u64* plan = tails + 2 * L.grid;
-    TQ_CUDA(cudaMemsetAsync(cursor, 0, 8, st));
+    TQ_CUDA(cudaMemsetAsync(cursor, 0, 16, st));
     p.cursor = cursor;
     p.chunk_tail = tails;
+    p.dup_flag = dup;
     p.nout = (u32)outs.size();
     ChunkOut co{};
     co.ncols = p.nout;
@@ -568,14 +642,29 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
       TQ_CUDA(cudaGetLastError());
     }
     uint64_t n = 0;
+    bool dup_keys = false;
     {
       std::lock_guard<std::mutex> g(c->mu);
       TQ_CUDA(cudaMemcpyAsync(c->pinned, plan, 16, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync((uint8_t*)c->pinned + 16, dup, 4, cudaMemcpyDeviceToHost, st));
       { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
       n = ((uint64_t*)c->pinned)[0];
-      if (p.ntiles && ((uint64_t*)c->pinned)[1] == ~0ull) fail(TQ_INTERNAL, "probe output chunk plan inconsistent");
+      dup_keys = ((uint32_t*)c->pinned)[4] != 0;
+      if (!dup_keys && p.ntiles && ((uint64_t*)c->pinned)[1] == ~0ull)
+        fail(TQ_INTERNAL, "probe output chunk plan inconsistent");
     }
     dfree(c, sb, scratch, st);
+    if (dup_keys) {
+      // a probe key matched two build rows: the build side is not unique on
+      // this key -> drop this pass, remember it on the table, probe two-pass
+      tq_batch_free(c, out);
+      const_cast<tq_join_table*>(A.table)->jt.unique = 0;  // a cached hint; every writer stores 0
+      p.dest_kind = DEST_PROBE;
+      p.cursor = nullptr;
+      p.chunk_tail = nullptr;
+      p.dup_flag = nullptr;
+      goto two_pass;
+    }
     out->rows = n;
     for (uint32_t i = 0; i < out->ncols; ++i) {
       out->cols[i].values_bytes = n * width_of(out->cols[i].kind);
@@ -584,6 +673,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     return;
   }
 
+two_pass:
   // ---- count phase (skipped for dense 1:1 projections), per warp-slice of a tile
   const bool dense = A.mode == MAT_FILTER && !P.has_pred;
   uint64_t total = dense ? in->rows : 0;
@@ -646,25 +736,6 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
 }
 
 // ================================================================== join build
-// Any key stored twice?  (every occupied slot counts its key's cluster)
-__global__ void k_jt_unique(JoinTable t, u32* dup) {
-  const u64 mask = t.cap - 1;
-  for (u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x; s < t.cap; s += (u64)gridDim.x * blockDim.x) {
-    const long long* e = (const long long*)(t.entries + s * t.stride);
-    if (e[0] < 0) continue;
-    u64 kw[kMaxKeyWords + 1];
-    for (u32 i = 0; i < t.kw; ++i) kw[i] = (u64)e[1 + i];
-    u32 n = 0;
-    for (u64 q = key_hash(kw, (int)t.kw) & mask;; q = (q + 1) & mask) {
-      const long long* f = (const long long*)(t.entries + q * t.stride);
-      if (f[0] < 0) break;
-      bool eq = true;
-      for (u32 i = 0; i < t.kw; ++i) eq &= (u64)f[1 + i] == kw[i];
-      n += eq;
-    }
-    if (n > 1) atomicOr(dup, 1u);
-  }
-}
 
 // ================================================================== fused partition + NVLink scatter
 // Every rank scans its rows once; each row that passes the predicate (and the
@@ -885,6 +956,10 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   t->jt.bloom = (uint32_t*)(t->jt.entries + ebytes);
   TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, ebytes, st));
   TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, words * 4, st));
+  {  // TQ_BLOOM=0: experiments only (probe without the Bloom pre-check)
+    static const bool no_bloom = [] { const char* e = getenv("TQ_BLOOM"); return e && e[0] == '0'; }();
+    if (no_bloom) t->jt.bloom = nullptr;
+  }
   t->build = *in;
   t->build.owner = nullptr;
   t->build.cols = (tq_column*)std::malloc(sizeof(tq_column) * std::max<uint32_t>(1, in->ncols));
@@ -892,17 +967,11 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   p.jt = t->jt;
   p.row_base = 0;
   launch(c, SINK_BUILD, L, P, st);
-  // unique build keys (PK side of a PK-FK join) -> single-pass probes
-  {
-    std::lock_guard<std::mutex> g(c->mu);
-    u32* dup = (u32*)c->pinned;
-    *dup = 0;
-    k_jt_unique<<<(u32)std::min<uint64_t>(4096, (cap + 255) / 256), 256, 0, st>>>(t->jt, dup);
-    counted_launch(c);
-    TQ_CUDA(cudaGetLastError());
-    { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
-    t->jt.unique = *dup == 0;
-  }
+  // No uniqueness pass and no host sync: a probe first assumes unique build
+  // keys (the PK side of a PK-FK join) and runs in one pass; that pass flags a
+  // probe key with a second match, and the probe then re-runs two-pass and
+  // marks the table (jt.unique = 0) for later probes.
+  t->jt.unique = 1;
   *out = t;
 }
 

@@ -163,6 +163,9 @@ struct PipeParams {
   uint8_t acc_plane[kMaxAcc];
   AccSpec acc[kMaxAcc];
   AggTable agg;
+  // DEST_PROBE1: set when a probe key matches a second build row (the build
+  // keys are not unique; the single-pass output is discarded)
+  uint32_t* dup_flag;
 };
 
 }  // namespace tq

@@ -114,6 +114,28 @@ def test_join_parity(ctx, seed):
     assert_batches_equal(got, want)
 
 
+@pytest.mark.parametrize("dups_probed", [False, True])
+def test_probe_unique_then_duplicate_keys(ctx, dups_probed):
+    """A probe assumes unique build keys and runs single-pass; a probe key with
+    a second build match makes it discard that pass and re-run two-pass (and
+    the table remembers it).  Duplicates no probe key reaches keep one pass."""
+    rng = np.random.default_rng(7)
+    nb = 50000
+    bkeys = rng.permutation(np.arange(1, 4 * nb, 4))[:nb].astype(np.int64)  # unique
+    bkeys[:20] = bkeys[20:40] if dups_probed else -bkeys[:20]              # 20 duplicated keys / unreachable negatives
+    if not dups_probed:
+        bkeys[20:40] = bkeys[:20]                                          # duplicates among the negatives
+    build = HostBatch(nb, [HostBatch.col_i64(bkeys), HostBatch.col_i64(rng.integers(0, 100, nb))])
+    npr = 200000
+    probe = HostBatch(npr, [HostBatch.col_i64(rng.integers(0, 4 * nb, npr)), HostBatch.col_dec(rng.integers(0, 999, npr))])
+    want = O.join_execute(build, probe, [0], [0])
+    t = ctx.join_build(ctx.upload(build), [0])
+    dp = ctx.upload(probe)
+    for _ in range(2):  # the second probe reuses the table (and its uniqueness hint)
+        assert_batches_equal(ctx.join_probe(t, dp, [0]).to_host(), want)
+    t.free()
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_aggregate_parity(ctx, seed):
     kinds = (INT64, DECIMAL, FLOAT64, BOOL, INT64)

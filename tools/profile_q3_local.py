@@ -59,15 +59,28 @@ def main():
             x.free()
         ct.free()
         ot.free()
-    # whole query, events around queries.q3
-    for rep in range(3):
+    # whole query, events around queries.q3; host phase timers on the last rep
+    import ctypes as C
+    import time
+    from paper_2508_05029_b200.ops import lib
+    ht = os.environ.get("TQ_HOST_TIMING") == "1"
+    for rep in range(4):
+        if ht and rep == 3:
+            lib().tq_host_timing_report(C.create_string_buffer(1 << 16), 1 << 16)  # drop earlier reps
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(st)
+        h0 = time.perf_counter()
         r = Q.q3(ctx, t["customer"], t["orders"], t["lineitem"])
         e1.record(st)
+        h1 = time.perf_counter()
         torch.cuda.synchronize()
-        print("q3 whole:", round(e0.elapsed_time(e1), 3), "ms")
+        print("q3 whole:", round(e0.elapsed_time(e1), 3), "ms device;", round((h1 - h0) * 1e3, 3), "ms host")
         r.free()
+    if ht:
+        buf = C.create_string_buffer(1 << 16)
+        lib().tq_host_timing_report(buf, len(buf))
+        print(buf.value.decode())
+    print("jit:", ctx.jit_report())
     ctx.close()
 
 
