@@ -51,6 +51,18 @@ __device__ __forceinline__ const long long* jt_entry(const JoinTable& t, u64 slo
   return (const long long*)(t.entries + slot * t.stride);
 }
 
+// 128-bit compare-and-swap of a 16-B table entry {row, key} (sm_90+):
+// returns the entry's previous contents
+__device__ __forceinline__ void cas128(long long* addr, u64 cmp_lo, u64 cmp_hi, u64 new_lo, u64 new_hi, u64& old_lo,
+                                      u64& old_hi) {
+  asm volatile(
+      "{\n .reg .b128 d, c, n;\n mov.b128 c, {%2, %3};\n mov.b128 n, {%4, %5};\n"
+      " atom.global.cas.b128 d, [%6], c, n;\n mov.b128 {%0, %1}, d;\n}"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(new_lo), "l"(new_hi), "l"(addr)
+      : "memory");
+}
+
 template <int KW>
 __device__ __forceinline__ bool jt_key_eq(const JoinTable& t, const long long* e, const u64* kw) {
   const u32 n = KW > 0 ? (u32)KW : t.kw;
@@ -259,10 +271,10 @@ __device__ __forceinline__ u32 partition_of(const PipeParams& p, const u64* kw) 
 }
 
 // The single build row matching kw (unique-key tables), or -1.
-// First build row matching kw (-1: none); the rest of the cluster is walked
-// too, and a second match sets *dup (non-unique build keys).
+// First build row matching kw (-1: none).  With `walk` the rest of the
+// cluster is walked too, and a second match sets dup (non-unique build keys).
 template <int KW>
-__device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u64* kw, bool& dup) {
+__device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u64* kw, bool walk, bool& dup) {
   const u64 h = key_hash(kw, KW > 0 ? KW : (int)t.kw);
   if (t.bloom) {
     const u32 b = bloom_bits(h);
@@ -275,6 +287,7 @@ __device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u6
     const long long row = e[0];
     if (row < 0) return found;
     if (jt_key_eq<KW>(t, e, kw)) {
+      if (!walk) return row;
       if (found >= 0) {
         dup = true;
         return found;
@@ -514,6 +527,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
 
   const u32 first = blockIdx.x, step = gridDim.x;
   u32 s = 0, ph = 0;
+  // single-pass probe: walk clusters for a duplicate match only when the build
+  // did not prove its keys unique
+  bool walk_dups = true;
+  if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 && p.jt.dup_dev) walk_dups = *p.jt.dup_dev != 0;
   for (u32 tile = first; tile < p.ntiles; tile += step) {
     uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
     mbar_wait(&full[s], ph);
@@ -585,7 +602,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (pass) {
           u64 kw[kMaxKeyWords + 1];
           bool dup = false;
-          if (!P::keys(w, v, kw, raw[v])) brow = jt_probe_first<P::kKw>(p.jt, kw, dup);
+          if (!P::keys(w, v, kw, raw[v])) brow = jt_probe_first<P::kKw>(p.jt, kw, walk_dups, dup);
           if (dup && *(volatile u32*)p.dup_flag == 0) *(volatile u32*)p.dup_flag = 1;
         }
         const u32 mm = __ballot_sync(kFull, brow >= 0);
@@ -720,6 +737,22 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         long long row = (long long)(p.row_base + r0 + trow(w, v));
         if (t.bloom) atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
         if (!t.entries) continue;  // Bloom-only build (LIP filter)
+        if ((P::kKw == 1 || (P::kKw == 0 && t.kw == 1)) && t.dup_dev) {
+          // {row, key} claimed in one 128-bit CAS against the empty pattern
+          // (all ones): an equal key already present is seen atomically
+          bool dup = false;
+          for (;;) {
+            long long* e = (long long*)(t.entries + sl * t.stride);
+            u64 olo, ohi;
+            cas128(e, ~0ull, ~0ull, (u64)row, kw[0], olo, ohi);
+            if (olo == ~0ull && ohi == ~0ull) break;
+            dup |= ohi == kw[0];
+            sl = (sl + 1) & mask;
+          }
+          if (dup && *(volatile u32*)t.dup_dev == 0) *(volatile u32*)t.dup_dev = 1;
+          if (p.cursor) atomicAdd(p.cursor, 1ull);
+          continue;
+        }
         for (;;) {
           long long* e = (long long*)(t.entries + sl * t.stride);
           if (atomicCAS((unsigned long long*)e, (unsigned long long)-1ll, (unsigned long long)row) ==

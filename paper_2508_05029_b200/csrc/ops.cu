@@ -946,7 +946,7 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   while (words * 32 < in->rows * 8) words <<= 1;
   t->jt.bloom_mask = words - 1;
   uint64_t ebytes = cap * t->jt.stride;
-  t->bytes = ebytes + words * 4;
+  t->bytes = ebytes + words * 4 + 16;  // + the build's duplicate-key flag
   try {
     t->jt.entries = (uint8_t*)dalloc(c, t->bytes, st);
   } catch (...) {
@@ -955,7 +955,8 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   }
   t->jt.bloom = (uint32_t*)(t->jt.entries + ebytes);
   TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, ebytes, st));
-  TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, words * 4, st));
+  TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, words * 4 + 16, st));
+  t->jt.dup_dev = t->jt.kw == 1 && t->jt.stride == 16 ? (uint32_t*)(t->jt.bloom + words) : nullptr;
   {  // TQ_BLOOM=0: experiments only (probe without the Bloom pre-check)
     static const bool no_bloom = [] { const char* e = getenv("TQ_BLOOM"); return e && e[0] == '0'; }();
     if (no_bloom) t->jt.bloom = nullptr;
@@ -968,9 +969,10 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   p.row_base = 0;
   launch(c, SINK_BUILD, L, P, st);
   // No uniqueness pass and no host sync: a probe first assumes unique build
-  // keys (the PK side of a PK-FK join) and runs in one pass; that pass flags a
-  // probe key with a second match, and the probe then re-runs two-pass and
-  // marks the table (jt.unique = 0) for later probes.
+  // keys (the PK side of a PK-FK join) and runs in one pass.  One-word keys
+  // are proven unique (or not) by the build itself (jt.dup_dev); otherwise the
+  // pass walks each matched cluster for a second match.  A probe that finds
+  // one re-runs two-pass and marks the table (jt.unique = 0) for later probes.
   t->jt.unique = 1;
   *out = t;
 }

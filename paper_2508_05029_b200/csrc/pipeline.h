@@ -72,7 +72,12 @@ struct JoinTable {
   uint32_t stride;  // bytes
   uint32_t kw;
   uint32_t* bloom;  // blocked Bloom filter over the build keys (nullptr = none)
-  uint32_t unique;  // every build key occurs once (probe emits in one pass)
+  uint32_t unique;  // host hint: probe single-pass first (cleared when a probe found a duplicate)
+  // device flag written by the build: 0 = build keys proven unique (16-B
+  // entries are claimed with one 128-bit CAS of {row, key}, so an equal key is
+  // seen atomically), 1 = a key was inserted twice; nullptr = not tracked
+  // (wider keys): single-pass probes then walk each cluster to check
+  uint32_t* dup_dev;
   uint64_t bloom_mask;  // words - 1 (power of two)
 };
 

@@ -35,6 +35,18 @@ def main():
     for name, fn in (("orders_probe", lambda: ctx.pipeline_probe(ct, t["orders"], Col(Q.O_ORDERDATE) < 9204,
                                                                   [Col(Q.O_ORDERKEY), Col(Q.O_ORDERDATE),
                                                                    Col(Q.O_SHIPPRIORITY), Col(Q.O_CUSTKEY)], [3], [])),
+                     ("no_pass", lambda: ctx.pipeline_probe(ct, t["orders"], Col(Q.O_ORDERDATE) < 0,
+                                                            [Col(Q.O_ORDERKEY), Col(Q.O_ORDERDATE),
+                                                             Col(Q.O_SHIPPRIORITY), Col(Q.O_CUSTKEY)], [3], [])),
+                     ("one_out_col", lambda: ctx.pipeline_probe(ct, t["orders"], Col(Q.O_ORDERDATE) < 9204,
+                                                                [Col(Q.O_CUSTKEY)], [0], [])),
+                     ("orderkey_probe(miss)", lambda: ctx.pipeline_probe(ct, t["orders"], Col(Q.O_ORDERDATE) < 9204,
+                                                                          [Col(Q.O_ORDERKEY), Col(Q.O_ORDERDATE),
+                                                                           Col(Q.O_SHIPPRIORITY), Col(Q.O_CUSTKEY)],
+                                                                          [0], [])),
+                     ("no_pred", lambda: ctx.pipeline_probe(ct, t["orders"], None,
+                                                            [Col(Q.O_ORDERKEY), Col(Q.O_ORDERDATE),
+                                                             Col(Q.O_SHIPPRIORITY), Col(Q.O_CUSTKEY)], [3], [])),
                      ("orders_probe_small_table", lambda: ctx.pipeline_probe(
                          ct2, t["orders"], Col(Q.O_ORDERDATE) < 9204,
                          [Col(Q.O_ORDERKEY), Col(Q.O_ORDERDATE), Col(Q.O_SHIPPRIORITY), Col(Q.O_CUSTKEY)], [3], [])),
@@ -49,7 +61,9 @@ def main():
         prof = ctx.profile_report()
         ctx.profile(False)
         n, ms = prof["pipe_emit"]
-        res[name] = round(ms / n * 1e3, 1)
+        r = fn()
+        res[name] = (round(ms / n * 1e3, 1), r.rows)
+        r.free()
     print(os.environ.get("TQ_JIT_DEFS", "-"), os.environ.get("TQ_MAXSTAGES", "-"), a.ctas, res, ctx.jit_report()["failed"])
     ctx.close()
 
