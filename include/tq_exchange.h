@@ -48,6 +48,15 @@ tq_status tq_comm_bloom_union(tq_comm* comm, tq_bloom* bloom, void* stream);
 tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, const tq_expr* pred,
                                          const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,
                                          const tq_bloom* semi, tq_batch* out, void* stream);
+/* Partitioned LIP filter (PAPER.md:394 Lookahead Information Passing, after
+ * the build side's shuffle): all-gather every rank's join-table Bloom filter
+ * (equal sizes: tq_join_build_sized) into one filter whose part d is rank d's.
+ * Passed as `semi` to tq_pipeline_partition_exchange, a row is checked only
+ * against the part of the rank it is sent to.  Collective. */
+tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* table, tq_bloom** out, void* stream);
+/* Row capacity of the last tq_pipeline_partition_exchange's receive windows:
+ * identical on every rank, >= the rows any rank received. */
+uint64_t tq_comm_last_exchange_capacity(tq_comm* comm);
 /* Bytes this communicator has sent to other ranks (NVLink traffic). */
 uint64_t tq_comm_bytes_sent(tq_comm* comm);
 int tq_comm_size(tq_comm* comm);

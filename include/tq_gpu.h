@@ -90,6 +90,12 @@ tq_status tq_hash_partition(tq_ctx* ctx, const tq_batch* in, const uint32_t* key
  * build batch (which must stay alive until the table is destroyed). */
 tq_status tq_join_build(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
                         tq_join_table** out, void* stream);
+/* tq_join_build with the table's Bloom filter sized for max(build rows,
+ * bloom_keys) keys: ranks that pass the same bloom_keys (e.g. the capacity of
+ * the fused exchange that delivered the build side) get equal-size filters,
+ * which tq_comm_gather_table_blooms (tq_exchange.h) can all-gather. */
+tq_status tq_join_build_sized(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
+                              uint64_t bloom_keys, tq_join_table** out, void* stream);
 /* join_execute probe side: inner equi-join, null keys never match; output =
  * build columns then probe columns. */
 tq_status tq_join_probe(tq_ctx* ctx, const tq_join_table* table, const tq_batch* probe, const uint32_t* keys,

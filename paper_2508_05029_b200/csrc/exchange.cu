@@ -91,7 +91,7 @@ struct tq_comm {
   uint8_t* win = nullptr;
   uint64_t win_bytes = 0;
   std::vector<uint8_t*> win_peer;  // [n]; win_peer[rank] == win
-  uint64_t win_cap_rows = 0;       // last capacity that sufficed (next call's first guess)
+  uint64_t win_cap_rows = 0;       // capacity (rows) of the last fused exchange (identical on every rank)
 };
 
 using namespace tq;
@@ -102,7 +102,7 @@ namespace tq {
 tq_ctx* comm_ctx(tq_comm* cm) { return cm->ctx; }
 int comm_rank(tq_comm* cm) { return cm->rank; }
 int comm_size(tq_comm* cm) { return cm->n; }
-uint64_t& comm_window_rows(tq_comm* cm) { return cm->win_cap_rows; }
+uint64_t& comm_last_cap(tq_comm* cm) { return cm->win_cap_rows; }
 void comm_add_sent(tq_comm* cm, uint64_t bytes) { cm->sent += bytes; }
 
 void comm_allgather_u64(tq_comm* cm, const unsigned long long* dev_in, unsigned long long* dev_out, uint64_t count, cudaStream_t st) {
@@ -120,18 +120,24 @@ void peer_barrier(tq_comm* cm, cudaStream_t st) {
   dfree(c, b, 8 * (cm->n + 1), st);
 }
 
-PeerView peer_window(tq_comm* cm, uint64_t bytes, cudaStream_t st) {
+uint64_t comm_window_bytes(tq_comm* cm) { return cm->win_bytes; }
+
+PeerView peer_window(tq_comm* cm, uint64_t bytes, cudaStream_t st, bool agreed) {
   tq_ctx* c = cm->ctx;
   const int n = cm->n;
-  // every rank must see the same size: take the max over ranks
-  u64* g = (u64*)dalloc(c, 8 * (n + 1), st);
-  TQ_CUDA(cudaMemcpyAsync(g, &bytes, 8, cudaMemcpyHostToDevice, st));
-  comm_allgather_u64(cm, g, g + 1, 1, st);
-  std::vector<u64> all(n);
-  TQ_CUDA(cudaMemcpyAsync(all.data(), g + 1, 8 * n, cudaMemcpyDeviceToHost, st));
-  TQ_CUDA(cudaStreamSynchronize(st));
-  dfree(c, g, 8 * (n + 1), st);
-  for (u64 v : all) bytes = std::max<u64>(bytes, v);
+  if (!agreed) {
+    // every rank must see the same size: take the max over ranks
+    u64* g = (u64*)dalloc(c, 8 * (n + 1), st);
+    TQ_CUDA(cudaMemcpyAsync(g, &bytes, 8, cudaMemcpyHostToDevice, st));
+    comm_allgather_u64(cm, g, g + 1, 1, st);
+    std::vector<u64> all(n);
+    TQ_CUDA(cudaMemcpyAsync(all.data(), g + 1, 8 * n, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaStreamSynchronize(st));
+    dfree(c, g, 8 * (n + 1), st);
+    for (u64 v : all) bytes = std::max<u64>(bytes, v);
+  }
+  // (agreed: every rank passes the same `bytes`, so every rank takes the same
+  // grow / no-grow branch and the collectives below stay matched)
   if (cm->win_bytes < bytes) {
     // drop the old mappings and buffer (every peer finished with them: the
     // previous scatter ended with a barrier and its copy-out is stream-ordered)

@@ -230,10 +230,19 @@ struct AccClaimInit {
 };
 
 template <int KWA>
-__device__ __forceinline__ long long agg_global_slot(const PipeParams& p, const u64* kw, u32 kwa, u64 h) {
+__device__ __forceinline__ long long agg_global_slot(const PipeParams& p, const u64* kw, u32 kwa, u64 h,
+                                                    unsigned long long* cta_groups) {
+  // new groups are counted per CTA in shared memory (one global atomic per
+  // CTA at the end, not one per group); a probe run of kAggProbeLimit slots
+  // flags overflow (the host grows the table x4 and re-runs)
+  constexpr u64 kAggProbeLimit = 128;
+  // after an overflow this launch's result is discarded (the host re-runs
+  // with a larger table): stop walking the full table
+  if (*(volatile u32*)p.agg.overflow) return -1;
   long long s = table_find_insert<KWA>(p.agg.state, p.agg.keys, p.agg.cap, kwa, kw, h,
-                                       p.agg.cap < 512 ? p.agg.cap : 512, p.agg.nused, AccClaimInit{p});
-  if (s < 0) atomicExch(p.agg.overflow, 1u);
+                                       p.agg.cap < kAggProbeLimit ? p.agg.cap : kAggProbeLimit, cta_groups,
+                                       AccClaimInit{p});
+  if (s < 0 && *(volatile u32*)p.agg.overflow == 0) atomicExch(p.agg.overflow, 1u);
   return s;
 }
 
@@ -467,12 +476,15 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     for (u32 i = threadIdx.x; i < p.ncode; i += kBlock) s_code[i] = p.code[i];
     for (u32 i = threadIdx.x; i < p.nlits; i += kBlock) s_lits[i] = p.lits[i];
   }
+  // AGG: new global groups of this CTA (in the padding after the barriers)
+  unsigned long long* s_groups = (unsigned long long*)(smem + p.off_bar + 2 * kMaxStages * 8);
   if (threadIdx.x == 0) {
     for (u32 s = 0; s < p.nstages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kWarps);
     }
     fence_mbar_init();
+    *s_groups = 0;
   }
 
   // sink shared state
@@ -563,12 +575,13 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (pass) {
           u64 kw[kMaxKeyWords + 1];
           const bool has_null = P::keys(w, v, kw, raw[v]);
+          dest = partition_of(p, kw);
           if (p.semi_bloom) {  // LIP: keys absent from the build side's Bloom filter cannot join
             const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)p.key_words);
             const u32 bb = bloom_bits(hb);
-            if (has_null || (__ldg(p.semi_bloom + bloom_word(hb, p.semi_mask)) & bb) != bb) pass = false;
+            const uint32_t* sb = p.semi_bloom + (u64)dest * p.semi_part_words;
+            if (has_null || (__ldg(sb + bloom_word(hb, p.semi_mask)) & bb) != bb) pass = false;
           }
-          dest = partition_of(p, kw);
         }
         u32 todo = __ballot_sync(kFull, pass);
         while (todo) {
@@ -632,15 +645,17 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (pass && p.dest_kind != DEST_FILTER) {
           u64 kw[kMaxKeyWords + 1];
           bool has_null = P::keys(w, v, kw, raw[v]);
+          if (p.dest_kind == DEST_PARTITION) dest[v] = partition_of(p, kw);
           if (p.dest_kind == DEST_PARTITION && p.semi_bloom) {
-            // Lookahead Information Passing: a key absent from the (global)
-            // build-side Bloom filter cannot join -> never shipped
+            // Lookahead Information Passing: a key absent from the (global or
+            // destination part's) build-side Bloom filter cannot join -> never shipped
             const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)p.key_words);
             const u32 bb = bloom_bits(hb);
-            if (has_null || (__ldg(p.semi_bloom + bloom_word(hb, p.semi_mask)) & bb) != bb) mult[v] = 0;
+            const uint32_t* sb = p.semi_bloom + (u64)dest[v] * p.semi_part_words;
+            if (has_null || (__ldg(sb + bloom_word(hb, p.semi_mask)) & bb) != bb) mult[v] = 0;
           }
-          if (p.dest_kind == DEST_PARTITION) dest[v] = partition_of(p, kw);
-          else mult[v] = has_null ? 0u : jt_probe_count<P::kKw>(p.jt, kw);  // null keys never match
+          if (p.dest_kind != DEST_PARTITION)
+            mult[v] = has_null ? 0u : jt_probe_count<P::kKw>(p.jt, kw);  // null keys never match
         }
       }
       u32* wc = s_cnt + warp * kMaxDest;  // this warp's per-destination counters
@@ -840,7 +855,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
                     if (fits_plane(xi)) {
                       pl[0] += lo64(xi);
                     } else {
-                      long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa));
+                      long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa), s_groups);
                       if (gs >= 0) atomic_add_i128(p.agg.acc + ((u64)gs * nacc + a) * 2, xi);
                     }
                     break;
@@ -855,7 +870,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
                     }
                   }
                   // escape: the exact int128 partial goes straight to the global table
-                  long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa));
+                  long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa), s_groups);
                   if (gs >= 0) atomic_add_i128(p.agg.acc + ((u64)gs * nacc + a) * 2, add128((i128)cur, xi));
                   pl[0] = 0;
                   break;
@@ -880,7 +895,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
             }
           } else {
             // local table full: this group lives only in the global table
-            long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa));
+            long long gs = agg_global_slot<KWA>(p, x.kw, kwa, key_hash(x.kw, (int)kwa), s_groups);
             if (gs < 0) continue;
 #pragma unroll
             for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
@@ -930,7 +945,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (l_state[g] > kStBusy) {  // ready (holds the key's tag)
           u64 kw[kMaxKeyWords + 1];
           for (u32 i = 0; i < kwa; ++i) kw[i] = l_keys[(u64)g * kwa + i];
-          gs = agg_global_slot<KWA>(p, kw, kwa, key_hash(kw, (int)kwa));
+          gs = agg_global_slot<KWA>(p, kw, kwa, key_hash(kw, (int)kwa), s_groups);
         }
         l_gslot[g] = gs;
       }
@@ -990,6 +1005,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       }
       if (lane == 0) acc_apply_atomic(op, p.agg.acc + ((u64)gs * nacc + a) * 2, xi, xf, cnt);
     }
+  }
+  if (SINK == SINK_AGG) {
+    consumers_sync();
+    if (threadIdx.x == 0 && *s_groups) atomicAdd(p.agg.nused, *s_groups);
   }
 }
 

@@ -287,7 +287,7 @@ static void plan_launch(tq_ctx* c, const tq_batch* in, Prog& P, Plan& L, u32 sin
   p.off_sink = o;
   o += align_up(sink_bytes, 128);
   p.off_bar = o;
-  o += 2 * kMaxStages * 8;
+  o += 2 * kMaxStages * 8 + 8;  // full / empty barriers + the AGG sink's per-CTA new-group count
   o = align_up(o, 128);
   const u32 kSmemMax = 227 * 1024;
   if (o + p.stage_bytes > kSmemMax) fail(TQ_INVALID_PLAN, "batch too wide for one pipeline tile");
@@ -352,6 +352,7 @@ struct tq_bloom_impl;
 struct MatArgs {
   const uint32_t* semi_words = nullptr;  // LIP Bloom filter on the partition keys
   uint64_t semi_mask = 0;
+  uint64_t semi_part_words = 0;  // partitioned filter: part d at d * semi_part_words
   int mode = MAT_FILTER;
   std::vector<uint32_t> key_roots;  // indices into P.outs
   uint32_t nparts = 1;
@@ -548,6 +549,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
   set_keys(p, P.pb, kh);
   p.semi_bloom = A.semi_words;
   p.semi_mask = A.semi_mask;
+  p.semi_part_words = A.semi_part_words;
   if (A.mode == MAT_PROBE) {
     const tq_join_table* t = A.table;
     if (kh.size() != t->key_cls.size()) fail(TQ_INVALID_PLAN, "probe/build key count differs");
@@ -753,7 +755,8 @@ __global__ void k_tail_reset(u64* tails, u64 nslots) {
 
 static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, Prog& P,
                                    const std::vector<uint32_t>& key_roots, const uint32_t* semi_words,
-                                   uint64_t semi_mask, tq_batch* out, uint64_t* rows_sent, cudaStream_t st) {
+                                   uint64_t semi_mask, uint64_t semi_part_words, tq_batch* out, uint64_t* rows_sent,
+                                   cudaStream_t st) {
   const int n = comm_size(cm), me = comm_rank(cm);
   if (n > kMaxPeers) fail(TQ_INVALID_PLAN, "too many ranks for the fused exchange");
   Plan L;
@@ -771,6 +774,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
   set_keys(p, P.pb, kh);
   p.semi_bloom = semi_words;
   p.semi_mask = semi_mask;
+  p.semi_part_words = semi_part_words;
   std::vector<tq_column> sch;
   std::vector<bool> wv;
   std::vector<OutCol> outs;
@@ -791,24 +795,45 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
   if (outs.size() > (size_t)kMaxOut) fail(TQ_INVALID_PLAN, "too many output columns");
   p.nout = (u32)outs.size();
 
-  // window capacity (rows): every rank's guess, max over ranks; grown and
-  // re-run when a receiver's counter passed it (rows beyond were not written)
-  const bool filtered = P.has_pred || semi_words;
-  // a receiver gets ~ (all ranks' rows) / n ~ this rank's rows when balanced
-  u64 guess = std::max<u64>(filtered ? in->rows / 4 : in->rows * 5 / 4, 1ull << 16);
+  // window capacity (rows).  The data-region layout is a function of the
+  // capacity, and the capacity a function of the window size, which every
+  // rank holds identically (windows only grow collectively) -> no per-call
+  // agreement and no host sync.  The first exchange on a communicator agrees
+  // on a first size (all-gather of every rank's guess); a receiver whose
+  // counter passed the capacity makes every rank grow the window and re-run.
   const u64 nslots = (u64)n * kMaxTailCtas;
   const u64 data0 = round_up(256 + nslots * 16, 256);
+  auto layout_end = [&](u64 cap) {
+    u64 end = data0;
+    for (size_t k = 0; k < outs.size(); ++k) {
+      end = round_up(end + cap * outs[k].width, 256);
+      if (wv[k]) end = round_up(end + (cap + 7) / 8, 256);
+    }
+    return end;
+  };
   u64* scratch = (u64*)dalloc(c, 8 * (2 * n + 8), st);  // [0..n) allgather out, [n] in, [n+1..] sent counter
   u64* sent_dev = scratch + n + 1;
-  {
+  u64 cap = 0;
+  if (comm_window_bytes(cm) == 0) {
+    const bool filtered = P.has_pred || semi_words;
+    // a receiver gets ~ (all ranks' rows) / n ~ this rank's rows when balanced
+    u64 guess = std::max<u64>(filtered ? in->rows / 4 : in->rows * 5 / 4, 1ull << 16);
     TQ_CUDA(cudaMemcpyAsync(scratch + n, &guess, 8, cudaMemcpyHostToDevice, st));
     comm_allgather_u64(cm, scratch + n, scratch, 1, st);
     std::vector<u64> g(n);
     TQ_CUDA(cudaMemcpyAsync(g.data(), scratch, 8 * n, cudaMemcpyDeviceToHost, st));
     { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
     for (u64 x : g) guess = std::max(guess, x);
+    cap = guess;
+  } else {
+    // the largest capacity whose layout fits the current window
+    const u64 win = comm_window_bytes(cm);
+    u64 per_row8 = 0;  // bits per row
+    for (size_t k = 0; k < outs.size(); ++k) per_row8 += 8 * outs[k].width + (wv[k] ? 1 : 0);
+    const u64 slack = data0 + 2 * 256 * (outs.size() + 1);
+    cap = win > slack ? (win - slack) * 8 / std::max<u64>(1, per_row8) : 0;
+    while (cap > 0 && layout_end(cap) > win) cap -= std::max<u64>(1, cap / 1024);
   }
-  u64 cap = guess;
   const u64 plan_words = 4 + 4 * nslots + 6;
   u64* plan = (u64*)dalloc(c, plan_words * 8, st);
   static bool smem_set = false;
@@ -818,7 +843,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     smem_set = true;
   }
   for (int attempt = 0;; ++attempt) {
-    // layout of the data region (same on every rank)
+    // layout of the data region (same on every rank: cap is)
     std::vector<u64> voff(outs.size()), boff(outs.size(), 0);
     u64 end = data0;
     for (size_t k = 0; k < outs.size(); ++k) {
@@ -832,7 +857,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     TQ_HT("pex total attempt");
     PeerView v = [&] {
       TQ_HT("pex window");
-      return peer_window(cm, end, st);
+      return peer_window(cm, end, st, /*agreed=*/true);
     }();
     u64* counter = (u64*)v.local;
     u64* tails = (u64*)(v.local + 256);
@@ -905,6 +930,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
         TQ_CUDA(cudaMemcpyAsync(out->cols[k].validity, co.validity[k], (n_rows + 7) / 8, cudaMemcpyDeviceToDevice, st));
     }
     if (rows_sent) *rows_sent = sent_rows;
+    comm_last_cap(cm) = cap;
     break;
   }
   dfree(c, plan, plan_words * 8, st);
@@ -912,7 +938,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
 }
 
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
-                      tq_join_table** out, cudaStream_t st) {
+                      tq_join_table** out, cudaStream_t st, uint64_t bloom_keys = 0) {
   Plan L;
   plan_launch(c, in, P, L, 0, st);
   PipeParams& p = L.p;
@@ -942,8 +968,10 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   t->jt.kw = p.key_words;
   t->jt.stride = (u32)round_up(8 * (1 + p.key_words), 16);
   // blocked Bloom filter, ~8 bits per build row: rejects non-matching probes in L2
+  // (bloom_keys: size for that many keys instead, e.g. a capacity every rank
+  // agrees on, so the ranks' filters can be all-gathered as one partitioned filter)
   uint64_t words = 1024;
-  while (words * 32 < in->rows * 8) words <<= 1;
+  while (words * 32 < std::max<uint64_t>(in->rows, bloom_keys) * 8) words <<= 1;
   t->jt.bloom_mask = words - 1;
   uint64_t ebytes = cap * t->jt.stride;
   t->bytes = ebytes + words * 4 + 16;  // + the build's duplicate-key flag
@@ -1578,6 +1606,11 @@ tq_status tq_pipeline_partition(tq_ctx* c, const tq_batch* in, const tq_expr* pr
 
 tq_status tq_join_build(tq_ctx* c, const tq_batch* build, const uint32_t* keys, uint32_t nkeys, tq_join_table** out,
                         void* stream) {
+  return tq_join_build_sized(c, build, keys, nkeys, 0, out, stream);
+}
+
+tq_status tq_join_build_sized(tq_ctx* c, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
+                              uint64_t bloom_keys, tq_join_table** out, void* stream) {
   return guard([&] {
     check_device_batch(build);
     Prog P(schema_of(build));
@@ -1590,7 +1623,7 @@ tq_status tq_join_build(tq_ctx* c, const tq_batch* build, const uint32_t* keys, 
       ex[k] = tq_expr{&nodes[k], 1, 0};
     }
     compile_prog(P, build, nullptr, ex.data(), nkeys, false);
-    run_build(c, build, P, iota_u32(nkeys), out, pick(c, stream));
+    run_build(c, build, P, iota_u32(nkeys), out, pick(c, stream), bloom_keys);
   });
 }
 
@@ -1804,7 +1837,8 @@ void tq_agg_destroy(tq_agg_state* s) {
 struct tq_bloom {
   tq_ctx* ctx;
   uint32_t* words;
-  uint64_t nwords;  // power of two
+  uint64_t nwords;  // power of two (per part)
+  uint32_t parts = 1;  // > 1: part d = rank d's table filter, words [d * nwords, (d + 1) * nwords)
   uint32_t kw;
   std::vector<uint8_t> key_cls, key_scale;
 };
@@ -1867,7 +1901,7 @@ tq_status tq_bloom_build(tq_ctx* c, const tq_batch* in, const uint32_t* keys, ui
 
 void tq_bloom_destroy(tq_bloom* b) {
   if (!b) return;
-  dfree(b->ctx, b->words, b->nwords * 4, b->ctx->stream);
+  dfree(b->ctx, b->words, b->nwords * 4 * b->parts, b->ctx->stream);
   delete b;
 }
 
@@ -1903,12 +1937,51 @@ tq_status tq_pipeline_partition_semi(tq_ctx* c, const tq_batch* in, const tq_exp
         if (o.cls != semi->key_cls[k] || (o.cls == C_D && o.scale != semi->key_scale[k]))
           fail(TQ_INVALID_PLAN, "semi-join key types differ");
       }
+      if (semi->parts > 1 && semi->parts != nparts) fail(TQ_INVALID_PLAN, "partitioned semi filter: parts differ");
       A.semi_words = semi->words;
       A.semi_mask = semi->nwords - 1;
+      A.semi_part_words = semi->parts > 1 ? semi->nwords : 0;
     }
     run_materialize(c, in, P, A, out, part_offsets, pick(c, stream));
   });
 }
+
+tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* t, tq_bloom** out, void* stream) {
+  return guard([&] {
+    tq_ctx* c = comm_ctx(comm);
+    cudaStream_t st = pick(c, stream);
+    const int n = comm_size(comm);
+    if (!t->jt.bloom) fail(TQ_INVALID_PLAN, "join table has no Bloom filter");
+    const uint64_t per = t->jt.bloom_mask + 1;  // words; >= 1024, so a whole number of u64
+    tq_bloom* b = new tq_bloom();
+    b->ctx = c;
+    b->kw = t->jt.kw;
+    b->key_cls = t->key_cls;
+    b->key_scale = t->key_scale;
+    b->nwords = per;
+    b->parts = (uint32_t)n;
+    b->words = (uint32_t*)dalloc(c, per * 4 * n, st);
+    // every rank's filter has `per` words (sized from the agreed exchange
+    // capacity); a mismatch would misalign the gathered parts -> checked
+    u64* chk = (u64*)dalloc(c, 8 * (n + 1), st);
+    TQ_CUDA(cudaMemcpyAsync(chk + n, &per, 8, cudaMemcpyHostToDevice, st));
+    comm_allgather_u64(comm, chk + n, chk, 1, st);
+    comm_allgather_u64(comm, (const unsigned long long*)t->jt.bloom, (unsigned long long*)b->words, per / 2, st);
+    std::vector<u64> all(n);
+    TQ_CUDA(cudaMemcpyAsync(all.data(), chk, 8 * n, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaStreamSynchronize(st));
+    dfree(c, chk, 8 * (n + 1), st);
+    comm_add_sent(comm, per * 4 * (n - 1));
+    for (u64 x : all)
+      if (x != per) {
+        tq_bloom_destroy(b);
+        fail(TQ_INVALID_PLAN, "table Bloom filters differ in size across ranks");
+      }
+    *out = b;
+  });
+}
+
+uint64_t tq_comm_last_exchange_capacity(tq_comm* comm) { return comm_last_cap(comm); }
 
 tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, const tq_expr* pred,
                                          const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,
@@ -1920,7 +1993,7 @@ tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, cons
     compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
     std::vector<uint32_t> kr(keys, keys + nkeys);
     const uint32_t* sw = nullptr;
-    uint64_t sm = 0;
+    uint64_t sm = 0, spw = 0;
     if (semi) {
       if (semi->key_cls.size() != nkeys) fail(TQ_INVALID_PLAN, "semi-join key count differs");
       for (uint32_t k = 0; k < nkeys; ++k) {
@@ -1929,11 +2002,14 @@ tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, cons
         if (o.cls != semi->key_cls[k] || (o.cls == C_D && o.scale != semi->key_scale[k]))
           fail(TQ_INVALID_PLAN, "semi-join key types differ");
       }
+      if (semi->parts > 1 && semi->parts != (uint32_t)comm_size(comm))
+        fail(TQ_INVALID_PLAN, "partitioned semi filter: parts differ from the ranks");
       sw = semi->words;
       sm = semi->nwords - 1;
+      spw = semi->parts > 1 ? semi->nwords : 0;
     }
     uint64_t sent_rows = 0;
-    run_partition_exchange(c, comm, in, P, kr, sw, sm, out, &sent_rows, pick(c, stream));
+    run_partition_exchange(c, comm, in, P, kr, sw, sm, spw, out, &sent_rows, pick(c, stream));
     uint64_t row_bytes = 0;
     for (uint32_t k = 0; k < out->ncols; ++k) row_bytes += width_of(out->cols[k].kind);
     comm_add_sent(comm, sent_rows * row_bytes);

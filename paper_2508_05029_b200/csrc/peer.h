@@ -21,14 +21,17 @@ struct PeerView {
 
 // Collective: every rank calls with its wanted size; all get a window of at
 // least the max over ranks (re-allocated and re-mapped only when it grows).
-PeerView peer_window(tq_comm* cm, uint64_t bytes, cudaStream_t st);
+// agreed = every rank passes the same size: no size all-gather, no host sync.
+PeerView peer_window(tq_comm* cm, uint64_t bytes, cudaStream_t st, bool agreed = false);
+// Current window size (identical on every rank: windows only grow collectively).
+uint64_t comm_window_bytes(tq_comm* cm);
 // Collective stream-ordered barrier (a one-word NCCL all-gather).
 void peer_barrier(tq_comm* cm, cudaStream_t st);
 void comm_allgather_u64(tq_comm* cm, const unsigned long long* dev_in, unsigned long long* dev_out, uint64_t count, cudaStream_t st);
 tq_ctx* comm_ctx(tq_comm* cm);
 int comm_rank(tq_comm* cm);
 int comm_size(tq_comm* cm);
-uint64_t& comm_window_rows(tq_comm* cm);
+uint64_t& comm_last_cap(tq_comm* cm);  // rows capacity of the last fused exchange (same on every rank)
 void comm_add_sent(tq_comm* cm, uint64_t bytes);  // NVLink bytes accounting
 
 }  // namespace tq

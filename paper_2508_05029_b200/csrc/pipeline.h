@@ -158,6 +158,9 @@ struct PipeParams {
   // miss this Bloom filter are dropped before they are partitioned / shipped
   const uint32_t* semi_bloom;
   uint64_t semi_mask;
+  // partitioned semi filter: part d's Bloom words start at d * semi_part_words
+  // (each rank's build-side table Bloom, all-gathered); 0 = one global filter
+  uint64_t semi_part_words;
   // emit
   uint32_t nout;
   OutCol out[kMaxOut];

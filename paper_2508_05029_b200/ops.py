@@ -81,6 +81,7 @@ def lib():
         U32 = P(C.c_uint32)
         L.tq_hash_partition.argtypes = [V, B, U32, C.c_uint32, C.c_uint32, B, P(C.c_uint64), V]
         L.tq_join_build.argtypes = [V, B, U32, C.c_uint32, P(V), V]
+        L.tq_join_build_sized.argtypes = [V, B, U32, C.c_uint32, C.c_uint64, P(V), V]
         L.tq_join_probe.argtypes = [V, V, B, U32, C.c_uint32, B, V]
         L.tq_join_table_destroy.argtypes = [V, V]
         L.tq_aggregate.argtypes = [V, B, U32, C.c_uint32, P(TqAggC), C.c_uint32, B, V]
@@ -142,6 +143,9 @@ def lib():
                                                  P(C.c_uint64), V]
         L.tq_pipeline_partition_exchange.argtypes = [V, B, E, E, C.c_uint32, U32, C.c_uint32, V, B, V]
         L.tq_comm_bloom_union.argtypes = [V, V, V]
+        L.tq_comm_gather_table_blooms.argtypes = [V, V, P(V), V]
+        L.tq_comm_last_exchange_capacity.restype = C.c_uint64
+        L.tq_comm_last_exchange_capacity.argtypes = [V]
         L.tq_estimate_reservation.restype = C.c_uint64
         L.tq_estimate_reservation.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double]
         L.tq_jit_report.restype = C.c_uint64
@@ -369,9 +373,15 @@ class Context:
                                                C.byref(out), offs, stream), out)
         return r, list(offs)
 
-    def join_build(self, build: DeviceBatch, keys: Sequence[int], stream=None) -> JoinTable:
+    def join_build(self, build: DeviceBatch, keys: Sequence[int], stream=None, bloom_keys: int = 0) -> JoinTable:
+        """bloom_keys > 0: size the table's Bloom filter for that many keys
+        (tq_join_build_sized; equal sizes across ranks for gather_table_blooms)."""
         h = C.c_void_p()
-        self._check(lib().tq_join_build(self.handle, C.byref(build.c), _u32(keys), len(keys), C.byref(h), stream))
+        if bloom_keys:
+            self._check(lib().tq_join_build_sized(self.handle, C.byref(build.c), _u32(keys), len(keys), bloom_keys,
+                                                  C.byref(h), stream))
+        else:
+            self._check(lib().tq_join_build(self.handle, C.byref(build.c), _u32(keys), len(keys), C.byref(h), stream))
         return JoinTable(self, h, build)
 
     def join_probe(self, t: JoinTable, probe: DeviceBatch, keys: Sequence[int], stream=None) -> DeviceBatch:
@@ -540,6 +550,17 @@ class Comm:
 
     def bloom_union(self, bloom: "Bloom", stream=None):
         Context._check(lib().tq_comm_bloom_union(self.handle, bloom.handle, stream))
+
+    def gather_table_blooms(self, table: JoinTable, stream=None) -> "Bloom":
+        """Partitioned LIP filter: part d = rank d's join-table Bloom filter
+        (tq_comm_gather_table_blooms).  Collective."""
+        h = C.c_void_p()
+        Context._check(lib().tq_comm_gather_table_blooms(self.handle, table.handle, C.byref(h), stream))
+        return Bloom(self.ctx, h)
+
+    def last_exchange_capacity(self) -> int:
+        """Receive-window rows of the last partition_exchange (same on every rank)."""
+        return lib().tq_comm_last_exchange_capacity(self.handle)
 
     def bytes_sent(self) -> int:
         return lib().tq_comm_bytes_sent(self.handle)

@@ -161,8 +161,10 @@ def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True, 
     and exchanged all-to-all over NVLink; the build/probe/aggregate that
     follows is co-partitioned, so each rank's groups are final.
     lip=True adds Lookahead Information Passing: a Bloom filter
-    of the orders_f keys, OR-ed across ranks, drops lineitem rows that cannot
-    join before they are partitioned and shipped (same result).
+    of the orders_f keys drops lineitem rows that cannot join before they are
+    partitioned and shipped (same result).  Unfused: one filter of each rank's
+    local orders_f, OR-ed across ranks.  Fused: the all-gathered Bloom filters
+    of the ranks' (already shuffled) orders_f join tables, one part per rank.
     fused=True replaces each partition + all-to-all pair with the fused
     partition/scatter over NVLink peer memory (tq_pipeline_partition_exchange):
     rows are written once, straight into their destination rank's window."""
@@ -173,14 +175,22 @@ def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True, 
     of = ctx.pipeline_probe(ct, orders, Col(O_ORDERDATE) < 9204,
                             [Col(O_ORDERKEY), Col(O_ORDERDATE), Col(O_SHIPPRIORITY), Col(O_CUSTKEY)], [3], [])
     bloom = None
-    if lip:
-        bloom = ctx.bloom_build(of, [0], expected_keys=of.rows * n)
-        comm.bloom_union(bloom)
+    ot = None
     if fused:
+        # orders_f is shuffled first; each rank's orders_f table carries a Bloom
+        # filter of its partition (sized from the window capacity every rank
+        # agrees on), and the all-gathered filters are the LIP filter of the
+        # lineitem shuffle: a row is checked against its destination's part
         orx = comm.partition_exchange(of, None, None, [0])
+        ot = ctx.join_build(orx, [0], bloom_keys=comm.last_exchange_capacity())
+        if lip:
+            bloom = comm.gather_table_blooms(ot)
         lrx = comm.partition_exchange(lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], bloom)
         lp = lrx
     else:
+        if lip:
+            bloom = ctx.bloom_build(of, [0], expected_keys=of.rows * n)
+            comm.bloom_union(bloom)
         op, ooff = ctx.hash_partition(of, [0], n)
         orx, _ = comm.exchange(op, ooff)
         if lip:
@@ -189,7 +199,7 @@ def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True, 
         else:
             lp, loff = ctx.pipeline_partition(lineitem, Col(L_SHIPDATE) > 9204, [Col(L_ORDERKEY), REV], [0], n)
         lrx, _ = comm.exchange(lp, loff)
-    ot = ctx.join_build(orx, [0])
+        ot = ctx.join_build(orx, [0])
     j = ctx.pipeline_probe(ot, lrx, None, None, [0], [1, 2])
     out = ctx.aggregate_execute(j, [2, 0, 1], [(AGG_SUM, 3)])
     if stats is not None:

@@ -69,20 +69,25 @@ def main():
                                 [3], [])
         mark("orders filter+probe")
         bloom = None
-        if lip:
-            bloom = ctx.bloom_build(of, [0], expected_keys=of.rows * n)
-            mark("LIP bloom build")
-            comm.bloom_union(bloom)
-            mark("LIP bloom union")
         if a.fused:
             orx = comm.partition_exchange(of, None, None, [0])
             op = orx
             mark("orders fused partition+scatter")
+            ot = ctx.join_build(orx, [0], bloom_keys=comm.last_exchange_capacity())
+            mark("orders_f build")
+            if lip:
+                bloom = comm.gather_table_blooms(ot)
+                mark("LIP gather table blooms")
             lrx = comm.partition_exchange(t["lineitem"], Col(Q.L_SHIPDATE) > 9204, [Col(Q.L_ORDERKEY), Q.REV], [0],
                                           bloom)
             lp = lrx
             mark("lineitem fused filter+semi+partition+scatter")
         else:
+            if lip:
+                bloom = ctx.bloom_build(of, [0], expected_keys=of.rows * n)
+                mark("LIP bloom build")
+                comm.bloom_union(bloom)
+                mark("LIP bloom union")
             op, ooff = ctx.hash_partition(of, [0], n)
             mark("orders partition")
             orx, _ = comm.exchange(op, ooff)
@@ -96,8 +101,8 @@ def main():
             mark("lineitem filter+partition")
             lrx, _ = comm.exchange(lp, loff)
             mark("lineitem exchange")
-        ot = ctx.join_build(orx, [0])
-        mark("orders_f build")
+            ot = ctx.join_build(orx, [0])
+            mark("orders_f build")
         j = ctx.pipeline_probe(ot, lrx, None, None, [0], [1, 2])
         mark("lineitem probe")
         out = ctx.aggregate_execute(j, [2, 0, 1], [(Q.AGG_SUM, 3)])
