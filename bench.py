@@ -258,6 +258,13 @@ def run_suite(args, ctx, world, rank, stream):
             suite[f"q{q}_sf{sf:g}"] = {"ms": ms, "rows_per_s": rows / (ms * 1e-3)}
         for v in t.values():
             v.free()
+        # per-operator HBM roofline (each SPEC operator alone, SF10, kernel
+        # time vs algorithmic bytes; tools/op_roofline.py)
+        if os.environ.get("TQ_BENCH_OPS", "1") == "1":
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import op_roofline
+            peaks = measured_peaks()
+            suite["operators_sf10"] = op_roofline.measure(ctx, sf, stream, peaks["hbm_gbs"] if peaks else 6481.1)
         # config 5 (one worker's share: SF100 / 8 GPUs): Q5 / Q9 on the C++ worker
         # runtime with the tables in the pinned Host tier and a Device budget of a
         # quarter of the data, so scans go through load_to_device / preload and

@@ -306,6 +306,7 @@ __device__ __forceinline__ void store_out(const OutCol& o, u64 pos, const WCtx& 
 struct InterpP {
   static constexpr bool kInterp = true;
   static constexpr int kKwa = 0, kKw = 0, kNacc = 0;
+  static constexpr bool kKey1x8 = false;
   __device__ __forceinline__ static u32 nacc(const PipeParams& p) { return p.nacc; }
   __device__ __forceinline__ static u32 nplanes(const PipeParams& p) { return p.nplanes; }
   __device__ __forceinline__ static uint8_t acc_op(const PipeParams& p, u32 a) { return p.acc[a].op; }

@@ -295,6 +295,8 @@ struct Gen {
           "(u64)__mul64hi(x, y)); }\n";
     os << "struct Gen {\n  static constexpr bool kInterp = false;\n";
     os << "  static constexpr int kKwa = " << (kw + 1) << ", kKw = " << kw << ", kNacc = " << nacc << ";\n";
+    os << "  static constexpr bool kKey1x8 = " << ((p.nkeys == 1 && p.keys[0].bytes == 8 && p.keys[0].words == 1) ? "true" : "false")
+       << ";\n";
     os << "  __device__ __forceinline__ static u32 nacc(const PipeParams&) { return " << nacc << "; }\n";
     os << "  __device__ __forceinline__ static u32 nplanes(const PipeParams&) { return " << p.nplanes << "; }\n";
     os << "  __device__ __forceinline__ static uint8_t acc_op(const PipeParams&, u32 a) {\n    switch (a) {";

@@ -174,13 +174,14 @@ __device__ __forceinline__ long long table_find_insert(u32* state, u64* keys, u6
       if (cur == kStEmpty) {
         for (u32 i = 0; i < kwa; ++i) keys[s * kwa + i] = kw[i];
         init(s);
-        __threadfence();
-        atomicExch(state + s, kStReady);
+        // publish with release semantics (orders the key / accumulator
+        // stores before the state; no full fence + L1 invalidate per claim)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(state + s), "r"(kStReady) : "memory");
         if (counter) atomicAdd(counter, 1ull);
         return (long long)s;
       }
     }
-    while (cur == kStBusy) cur = *st;
+    while (cur == kStBusy) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(state + s) : "memory");
     const volatile u64* k = keys + s * kwa;
     bool eq = true;
 #pragma unroll
@@ -277,6 +278,18 @@ __device__ __forceinline__ u32 partition_of(const PipeParams& p, const u64* kw) 
     pos += ko.words;
   }
   return (u32)(h % p.ndest);
+}
+
+// partition_of specialised for generated programs whose key is one 8-byte
+// value (the common case): the FNV loop unrolls with constant shifts and kw
+// stays in registers (the generic form loops over runtime key widths).
+template <class P>
+__device__ __forceinline__ u32 partition_of_p(const PipeParams& p, const u64* kw) {
+  if constexpr (P::kKey1x8) {
+    if ((p.ndest & (p.ndest - 1)) == 0) return fnv32_bytes((u32)kFnvBasis, kw[0], 8) & (p.ndest - 1);
+    return (u32)(fnv_bytes(kFnvBasis, kw[0], 8) % p.ndest);
+  }
+  return partition_of(p, kw);
 }
 
 // The single build row matching kw (unique-key tables), or -1.
@@ -575,7 +588,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (pass) {
           u64 kw[kMaxKeyWords + 1];
           const bool has_null = P::keys(w, v, kw, raw[v]);
-          dest = partition_of(p, kw);
+          dest = partition_of_p<P>(p, kw);
           if (p.semi_bloom) {  // LIP: keys absent from the build side's Bloom filter cannot join
             const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)p.key_words);
             const u32 bb = bloom_bits(hb);
@@ -645,7 +658,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (pass && p.dest_kind != DEST_FILTER) {
           u64 kw[kMaxKeyWords + 1];
           bool has_null = P::keys(w, v, kw, raw[v]);
-          if (p.dest_kind == DEST_PARTITION) dest[v] = partition_of(p, kw);
+          if (p.dest_kind == DEST_PARTITION) dest[v] = partition_of_p<P>(p, kw);
           if (p.dest_kind == DEST_PARTITION && p.semi_bloom) {
             // Lookahead Information Passing: a key absent from the (global or
             // destination part's) build-side Bloom filter cannot join -> never shipped

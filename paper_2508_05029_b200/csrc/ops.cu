@@ -1208,20 +1208,28 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     if (sink_bytes(G) > avail) G = 0;
   }
   Plan L;
-  plan_launch(c, in, P, L, G ? sink_bytes(G) : 64, st);
   PipeParams& p = L.p;
-  set_keys(p, P.pb, kh);
+  auto setup = [&](u32 g) {
+    L = Plan{};
+    plan_launch(c, in, P, L, g ? sink_bytes(g) : 64, st);
+    set_keys(p, P.pb, kh);
+    p.nacc = nacc;
+    for (u32 i = 0; i < nacc; ++i) { p.acc[i] = acc[i]; p.acc_plane[i] = planes[i]; }
+    p.nplanes = std::max<u32>(1, nplanes);
+    p.local_groups = g;
+  };
+  setup(G);
   const u32 kwa = p.key_words + 1;
-  p.nacc = nacc;
-  for (u32 i = 0; i < nacc; ++i) { p.acc[i] = acc[i]; p.acc_plane[i] = planes[i]; }
-  p.nplanes = std::max<u32>(1, nplanes);
-  p.local_groups = G;
 
   // ---- global table; grows x4 and re-runs on overflow (on_oom-style retry)
   // initial table for min(rows, 1M) groups at load <= 0.5
   uint64_t cap = 1024;
   if (!kh.empty())
     while (cap < std::min<uint64_t>(in->rows, 1ull << 20) * 2) cap <<= 1;
+  {  // TQ_AGG_CAP: experiments only (initial global table slots)
+    static const uint64_t cap_env = [] { const char* e = getenv("TQ_AGG_CAP"); return e ? strtoull(e, nullptr, 10) : 0ull; }();
+    if (cap_env && !kh.empty()) { cap = 1024; while (cap < cap_env) cap <<= 1; }
+  }
   uint64_t ngroups = 0;
   AggTable t{};
   uint64_t tbytes = 0;
@@ -1252,7 +1260,15 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     if (!ovf) break;
     dfree(c, base, tbytes, st);
     if (attempt > 12) fail(TQ_RESERVATION_EXCEEDED, "aggregation table overflow");
-    cap *= 4;
+    // x16 while the input is much larger than the table (high-cardinality
+    // group-by: fewer discarded attempts), else x4
+    cap *= in->rows >= 8 * cap ? 16 : 4;
+    // more than ~0.5M groups: a per-CTA table of <= 64 groups only misses and
+    // its shared memory halves the resident CTAs -> global table only
+    if (G && cap >= (1ull << 22)) {
+      G = 0;
+      setup(0);
+    }
   }
   uint8_t* tbase = (uint8_t*)t.state;
   // ---- output batch

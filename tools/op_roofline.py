@@ -128,6 +128,12 @@ def main():
     except Exception:
         pass
     r = measure(ctx, a.sf, st, peak)
+    if os.environ.get("TQ_HOST_TIMING") == "1":
+        import ctypes as C
+        from paper_2508_05029_b200.ops import lib
+        buf = C.create_string_buffer(1 << 16)
+        lib().tq_host_timing_report(buf, len(buf))
+        print(buf.value.decode())
     for k, v in r.items():
         print(f"{k:22s} op {v['op_ms']:7.3f} ms  kernels {v['kernel_ms']:7.3f} ms  {v['kernel_gbs']} GB/s "
               f"({v['kernel_frac_of_hbm']})  rows {v['rows_in']} -> {v['rows_out']}")
