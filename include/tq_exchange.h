@@ -48,6 +48,13 @@ tq_status tq_comm_bloom_union(tq_comm* comm, tq_bloom* bloom, void* stream);
 tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, const tq_expr* pred,
                                          const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,
                                          const tq_bloom* semi, tq_batch* out, void* stream);
+/* Fused filter / project + broadcast over NVLink peer memory (replaces
+ * tq_pipeline_materialize + tq_comm_allgather for a broadcast join side,
+ * SPEC.md:580-588 exchange_decide -> Broadcast): every row that passes `pred`
+ * is written into every rank's receive window.  `out` = all ranks' rows, in
+ * unspecified order.  Collective. */
+tq_status tq_pipeline_broadcast(tq_comm* comm, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                uint32_t nexprs, tq_batch* out, void* stream);
 /* Partitioned LIP filter (PAPER.md:394 Lookahead Information Passing, after
  * the build side's shuffle): all-gather every rank's join-table Bloom filter
  * (equal sizes: tq_join_build_sized) into one filter whose part d is rank d's.

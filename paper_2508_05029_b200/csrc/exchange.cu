@@ -338,7 +338,10 @@ tq_status tq_comm_exchange(tq_comm* cm, const tq_batch* in, const uint64_t* part
 tq_status tq_comm_allgather(tq_comm* cm, const tq_batch* in, tq_batch* out, uint64_t* recv_offsets, void* stream) {
   return guard([&] {
     std::vector<uint64_t> off(cm->n, 0), cnt(cm->n, in->rows);
-    exchange_impl(cm, in, off, cnt, out, recv_offsets, pick(cm->ctx, stream));
+    cudaStream_t st = pick(cm->ctx, stream);
+    const int ph = prof_begin(cm->ctx, "nccl_allgather", st);
+    exchange_impl(cm, in, off, cnt, out, recv_offsets, st);
+    prof_end(cm->ctx, ph, st);
   });
 }
 

@@ -585,6 +585,34 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       for (int v = 0; v < kV; ++v) {
         bool pass = (pm[v] >> lane) & 1u;
         u32 dest = 0;
+        if (p.bcast) {
+          // broadcast (a join's build side to every rank): each passing row
+          // goes to every destination window
+          const u32 grp = __ballot_sync(kFull, pass);
+          if (grp) {
+            for (u32 d = 0; d < p.ndest; ++d) {
+              u64 a = 0, b = 0;
+              u32 k1 = 0;
+              if (lane == 0) {
+                chunk_reserve<true>(s_chunk + d, (u32)__popc(grp), p.peer_counter[d], a, k1, b);
+                s_cnt[warp * kMaxDest + d] += (u32)__popc(grp);
+              }
+              a = __shfl_sync(kFull, a, 0);
+              b = __shfl_sync(kFull, b, 0);
+              k1 = __shfl_sync(kFull, k1, 0);
+              if (pass) {
+                const u32 rank = __popc(grp & lanemask_lt());
+                const u64 pos = rank < k1 ? a + rank : b + (rank - k1);
+                if (pos < p.peer_cap) {
+                  w.out_delta = p.peer_delta[d];
+                  P::store(w, v, pos, -1, raw[v]);
+                  w.out_delta = 0;
+                }
+              }
+            }
+          }
+          continue;
+        }
         if (pass) {
           u64 kw[kMaxKeyWords + 1];
           const bool has_null = P::keys(w, v, kw, raw[v]);
@@ -604,7 +632,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           todo &= ~grp;
           u64 a = 0, b = 0;
           u32 k1 = 0;
-          if (lane == leader) chunk_reserve<true>(s_chunk + d, (u32)__popc(grp), p.peer_counter[d], a, k1, b);
+          if (lane == leader) {
+            chunk_reserve<true>(s_chunk + d, (u32)__popc(grp), p.peer_counter[d], a, k1, b);
+            s_cnt[warp * kMaxDest + d] += (u32)__popc(grp);  // rows per destination (NVLink accounting)
+          }
           a = __shfl_sync(kFull, a, leader);
           b = __shfl_sync(kFull, b, leader);
           k1 = __shfl_sync(kFull, k1, leader);
@@ -938,6 +969,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       unsigned long long* t = p.peer_tails[d] + 2ull * (p.tail_slot0 + blockIdx.x);
       t[0] = s_chunk[d].base[(word >> kChunkUsedBits) & 15];
       t[1] = used;
+      // rows this CTA stored into other ranks' windows
+      unsigned long long rows = 0;
+      for (u32 wi = 0; wi < (u32)kWarps; ++wi) rows += s_cnt[wi * kMaxDest + d];
+      if (rows && d != p.tail_slot0 / kMaxTailCtas && p.cursor) atomicAdd(p.cursor, rows);
     }
   }
   if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1) {

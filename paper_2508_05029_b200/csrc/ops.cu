@@ -110,9 +110,11 @@ static void scan_u32(tq_ctx* c, const u32* in, u64 n, u64* out, u64* total_dev, 
   u64 nb = (n + kScanBlock - 1) / kScanBlock;
   if (nb == 0) nb = 1;
   u64* partial = (u64*)dalloc(c, nb * 8, st);
+  const int ph = prof_begin(c, "scan", st);
   k_scan_partials<<<(u32)nb, 256, 0, st>>>(in, n, partial);
   k_scan_prefix<<<1, 256, 0, st>>>(partial, nb, total_dev);
   k_scan_apply<<<(u32)nb, 256, 0, st>>>(in, n, partial, out);
+  prof_end(c, ph, st);
   for (int i = 0; i < 3; ++i) counted_launch(c);
   TQ_CUDA(cudaGetLastError());
   dfree(c, partial, nb * 8, st);
@@ -637,9 +639,11 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     if (p.ntiles == 0) {
       TQ_CUDA(cudaMemsetAsync(plan, 0, 8, st));
     } else {
+      const int ph = prof_begin(c, "probe1_fixup", st);
       k_chunk_plan<<<1, 1024, (3 * L.grid + 2) * 8, st>>>(tails, L.grid, cursor, plan);
       k_chunk_move<<<c->sms * 2, 256, 0, st>>>(plan, L.grid, co);
       k_chunk_clear_tail<<<1, 32, 0, st>>>(plan, co);
+      prof_end(c, ph, st);
       for (int k = 0; k < 3; ++k) counted_launch(c);
       TQ_CUDA(cudaGetLastError());
     }
@@ -756,7 +760,7 @@ __global__ void k_tail_reset(u64* tails, u64 nslots) {
 static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, Prog& P,
                                    const std::vector<uint32_t>& key_roots, const uint32_t* semi_words,
                                    uint64_t semi_mask, uint64_t semi_part_words, tq_batch* out, uint64_t* rows_sent,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, bool bcast = false) {
   const int n = comm_size(cm), me = comm_rank(cm);
   if (n > kMaxPeers) fail(TQ_INVALID_PLAN, "too many ranks for the fused exchange");
   Plan L;
@@ -772,6 +776,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     kh.push_back(P.outs[k]);
   }
   set_keys(p, P.pb, kh);
+  p.bcast = bcast ? 1u : 0u;
   p.semi_bloom = semi_words;
   p.semi_mask = semi_mask;
   p.semi_part_words = semi_part_words;
@@ -817,7 +822,9 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
   if (comm_window_bytes(cm) == 0) {
     const bool filtered = P.has_pred || semi_words;
     // a receiver gets ~ (all ranks' rows) / n ~ this rank's rows when balanced
+    // (a broadcast: all ranks' rows)
     u64 guess = std::max<u64>(filtered ? in->rows / 4 : in->rows * 5 / 4, 1ull << 16);
+    if (bcast) guess *= (u64)n;
     TQ_CUDA(cudaMemcpyAsync(scratch + n, &guess, 8, cudaMemcpyHostToDevice, st));
     comm_allgather_u64(cm, scratch + n, scratch, 1, st);
     std::vector<u64> g(n);
@@ -869,7 +876,9 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
       if (wv[k]) TQ_CUDA(cudaMemsetAsync(v.local + boff[k], 0, (cap + 7) / 8, st));
     {
       TQ_HT("pex barrier1");
+      const int ph = prof_begin(c, "pex_barrier1", st);
       peer_barrier(cm, st);  // every window reset before anyone writes into it
+      prof_end(c, ph, st);
     }
     for (int d = 0; d < n; ++d) {
       p.peer_delta[d] = (long long)(v.peer[d] - v.local);
@@ -892,12 +901,16 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     launch(c, SINK_EMIT, L, P, st);
     {
       TQ_HT("pex barrier2");
+      const int ph = prof_begin(c, "pex_barrier2", st);
       peer_barrier(cm, st);  // every rank's scatter into this window has completed
+      prof_end(c, ph, st);
     }
+    const int ph_plan = prof_begin(c, "pex_plan_counts", st);
     k_chunk_plan<<<1, 1024, plan_smem, st>>>(tails, (u32)nslots, counter, plan);
     counted_launch(c);
     TQ_CUDA(cudaMemcpyAsync(scratch + n, counter, 8, cudaMemcpyDeviceToDevice, st));
     comm_allgather_u64(cm, scratch + n, scratch, 1, st);
+    prof_end(c, ph_plan, st);
     u64 n_rows = 0, moves = 0, rmax = 0, sent_rows = 0;
     {
       std::lock_guard<std::mutex> g(c->mu);
@@ -917,6 +930,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
       continue;
     }
     if (moves == ~0ull) fail(TQ_INTERNAL, "fused exchange chunk plan inconsistent");
+    const int ph_fix = prof_begin(c, "pex_fix_copyout", st);
     k_chunk_move<<<c->sms * 2, 256, 0, st>>>(plan, (u32)nslots, co);
     k_chunk_clear_tail<<<1, 32, 0, st>>>(plan, co);
     counted_launch(c);
@@ -929,6 +943,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
       if (wv[k] && n_rows)
         TQ_CUDA(cudaMemcpyAsync(out->cols[k].validity, co.validity[k], (n_rows + 7) / 8, cudaMemcpyDeviceToDevice, st));
     }
+    prof_end(c, ph_fix, st);
     if (rows_sent) *rows_sent = sent_rows;
     comm_last_cap(cm) = cap;
     break;
@@ -1338,7 +1353,9 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     f.counter = (unsigned long long*)(t.nused + 0);  // reuse as output cursor
     TQ_CUDA(cudaMemsetAsync(t.nused, 0, 8, st));
     u32 nb = (u32)std::min<uint64_t>(2048, (cap + 255) / 256);
+    const int ph = prof_begin(c, "agg_final", st);
     k_agg_final<<<nb, 256, 0, st>>>(f);
+    prof_end(c, ph, st);
     counted_launch(c);
     TQ_CUDA(cudaGetLastError());
   }
@@ -1982,7 +1999,9 @@ tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* t, tq_
     u64* chk = (u64*)dalloc(c, 8 * (n + 1), st);
     TQ_CUDA(cudaMemcpyAsync(chk + n, &per, 8, cudaMemcpyHostToDevice, st));
     comm_allgather_u64(comm, chk + n, chk, 1, st);
+    const int ph = prof_begin(c, "nccl_gather_blooms", st);
     comm_allgather_u64(comm, (const unsigned long long*)t->jt.bloom, (unsigned long long*)b->words, per / 2, st);
+    prof_end(c, ph, st);
     std::vector<u64> all(n);
     TQ_CUDA(cudaMemcpyAsync(all.data(), chk, 8 * n, cudaMemcpyDeviceToHost, st));
     TQ_CUDA(cudaStreamSynchronize(st));
@@ -1998,6 +2017,21 @@ tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* t, tq_
 }
 
 uint64_t tq_comm_last_exchange_capacity(tq_comm* comm) { return comm_last_cap(comm); }
+
+tq_status tq_pipeline_broadcast(tq_comm* comm, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                                uint32_t nexprs, tq_batch* out, void* stream) {
+  return guard([&] {
+    tq_ctx* c = comm_ctx(comm);
+    check_device_batch(in);
+    Prog P(schema_of(in));
+    compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
+    uint64_t sent_rows = 0;
+    run_partition_exchange(c, comm, in, P, {}, nullptr, 0, 0, out, &sent_rows, pick(c, stream), /*bcast=*/true);
+    uint64_t row_bytes = 0;
+    for (uint32_t k = 0; k < out->ncols; ++k) row_bytes += width_of(out->cols[k].kind);
+    comm_add_sent(comm, sent_rows * row_bytes);  // rows stored into other ranks' windows
+  });
+}
 
 tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, const tq_expr* pred,
                                          const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys, uint32_t nkeys,

@@ -152,6 +152,7 @@ struct PipeParams {
   unsigned long long* peer_counter[kMaxPeers];
   unsigned long long* peer_tails[kMaxPeers];
   uint64_t peer_cap;     // rows of every receive window
+  uint32_t bcast;        // DEST_PEER: every row to every rank (no keys)
   uint32_t tail_slot0;   // this rank's first tail slot (rank * kMaxTailCtas)
   JoinTable jt;
   // LIP semi-join filter on the key words (dest PARTITION): rows whose keys

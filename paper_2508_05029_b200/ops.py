@@ -144,6 +144,7 @@ def lib():
         L.tq_pipeline_partition_exchange.argtypes = [V, B, E, E, C.c_uint32, U32, C.c_uint32, V, B, V]
         L.tq_comm_bloom_union.argtypes = [V, V, V]
         L.tq_comm_gather_table_blooms.argtypes = [V, V, P(V), V]
+        L.tq_pipeline_broadcast.argtypes = [V, B, E, E, C.c_uint32, B, V]
         L.tq_comm_last_exchange_capacity.restype = C.c_uint64
         L.tq_comm_last_exchange_capacity.argtypes = [V]
         L.tq_estimate_reservation.restype = C.c_uint64
@@ -540,6 +541,15 @@ class Comm:
         Context._check(lib().tq_pipeline_partition_exchange(self.handle, C.byref(b.c), pp, arr, n, _u32(keys),
                                                             len(keys), semi.handle if semi else None,
                                                             C.byref(out), stream))
+        return DeviceBatch(self.ctx, out)
+
+    def broadcast(self, b: DeviceBatch, pred, exprs, stream=None) -> DeviceBatch:
+        """Fused filter/project + broadcast over NVLink peer memory
+        (tq_pipeline_broadcast): every rank's passing rows, unspecified order.  Collective."""
+        pp, _k1 = _pred(pred)
+        arr, n, _k2 = _exprs(exprs)
+        out = TqBatchC()
+        Context._check(lib().tq_pipeline_broadcast(self.handle, C.byref(b.c), pp, arr, n, C.byref(out), stream))
         return DeviceBatch(self.ctx, out)
 
     def allgather(self, b: DeviceBatch, stream=None) -> Tuple[DeviceBatch, List[int]]:

@@ -169,8 +169,11 @@ def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True, 
     partition/scatter over NVLink peer memory (tq_pipeline_partition_exchange):
     rows are written once, straight into their destination rank's window."""
     n = comm.n
-    cf = ctx.pipeline_materialize(customer, Col(C_MKTSEGMENT).eq(1), [Col(C_CUSTKEY)])
-    cb, _ = comm.allgather(cf)
+    if fused:  # filter + broadcast in one kernel over NVLink peer memory
+        cf = cb = comm.broadcast(customer, Col(C_MKTSEGMENT).eq(1), [Col(C_CUSTKEY)])
+    else:
+        cf = ctx.pipeline_materialize(customer, Col(C_MKTSEGMENT).eq(1), [Col(C_CUSTKEY)])
+        cb, _ = comm.allgather(cf)
     ct = ctx.join_build(cb, [0])
     of = ctx.pipeline_probe(ct, orders, Col(O_ORDERDATE) < 9204,
                             [Col(O_ORDERKEY), Col(O_ORDERDATE), Col(O_SHIPPRIORITY), Col(O_CUSTKEY)], [3], [])

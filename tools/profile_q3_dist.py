@@ -58,10 +58,14 @@ def main():
             e.record(st)
             marks.append((name, e))
         mark("start")
-        cf = ctx.pipeline_materialize(t["customer"], Col(Q.C_MKTSEGMENT).eq(1), [Col(Q.C_CUSTKEY)])
-        mark("customer filter")
-        cb, _ = comm.allgather(cf)
-        mark("customer allgather")
+        if a.fused:
+            cf = cb = comm.broadcast(t["customer"], Col(Q.C_MKTSEGMENT).eq(1), [Col(Q.C_CUSTKEY)])
+            mark("customer filter+broadcast")
+        else:
+            cf = ctx.pipeline_materialize(t["customer"], Col(Q.C_MKTSEGMENT).eq(1), [Col(Q.C_CUSTKEY)])
+            mark("customer filter")
+            cb, _ = comm.allgather(cf)
+            mark("customer allgather")
         ct = ctx.join_build(cb, [0])
         mark("customer build")
         of = ctx.pipeline_probe(ct, t["orders"], Col(Q.O_ORDERDATE) < 9204,
