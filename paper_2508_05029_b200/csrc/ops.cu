@@ -833,8 +833,8 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     for (u64 x : g) guess = std::max(guess, x);
     cap = guess;
   } else {
-    // the largest capacity whose layout fits the current window
-    const u64 win = comm_window_bytes(cm);
+    // the largest capacity whose layout fits half of the current window
+    const u64 win = comm_window_bytes(cm) / 2 / 256 * 256;
     u64 per_row8 = 0;  // bits per row
     for (size_t k = 0; k < outs.size(); ++k) per_row8 += 8 * outs[k].width + (wv[k] ? 1 : 0);
     const u64 slack = data0 + 2 * 256 * (outs.size() + 1);
@@ -864,17 +864,27 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     TQ_HT("pex total attempt");
     PeerView v = [&] {
       TQ_HT("pex window");
-      return peer_window(cm, end, st, /*agreed=*/true);
+      return peer_window(cm, 2 * end, st, /*agreed=*/true);
     }();
-    u64* counter = (u64*)v.local;
-    u64* tails = (u64*)(v.local + 256);
-    TQ_CUDA(cudaMemsetAsync(counter, 0, 8, st));
+    const int half = (int)(comm_epoch(cm) & 1);
+    const u64 hoff = (u64)half * (comm_window_bytes(cm) / 2 / 256 * 256);
+    uint8_t* base = v.local + hoff;
+    u64* counter = (u64*)base;
+    u64* tails = (u64*)(base + 256);
     TQ_CUDA(cudaMemsetAsync(sent_dev, 0, 8, st));
-    k_tail_reset<<<(u32)std::min<u64>(1024, (nslots + 255) / 256), 256, 0, st>>>(tails, nslots);
-    counted_launch(c);
-    for (size_t k = 0; k < outs.size(); ++k)
-      if (wv[k]) TQ_CUDA(cudaMemsetAsync(v.local + boff[k], 0, (cap + 7) / 8, st));
-    {
+    bool any_valid = false;
+    for (size_t k = 0; k < outs.size(); ++k) any_valid |= wv[k];
+    // this half's control block was reset at the end of its previous use,
+    // before a barrier every sender has passed since -> no reset barrier
+    // (bitmaps depend on the layout: exchanges with validity always reset)
+    const bool preset = attempt == 0 && comm_half_ready(cm, half) && !any_valid;
+    comm_half_ready(cm, half) = false;
+    if (!preset) {
+      TQ_CUDA(cudaMemsetAsync(counter, 0, 8, st));
+      k_tail_reset<<<(u32)std::min<u64>(1024, (nslots + 255) / 256), 256, 0, st>>>(tails, nslots);
+      counted_launch(c);
+      for (size_t k = 0; k < outs.size(); ++k)
+        if (wv[k]) TQ_CUDA(cudaMemsetAsync(base + boff[k], 0, (cap + 7) / 8, st));
       TQ_HT("pex barrier1");
       const int ph = prof_begin(c, "pex_barrier1", st);
       peer_barrier(cm, st);  // every window reset before anyone writes into it
@@ -882,8 +892,8 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     }
     for (int d = 0; d < n; ++d) {
       p.peer_delta[d] = (long long)(v.peer[d] - v.local);
-      p.peer_counter[d] = (unsigned long long*)v.peer[d];
-      p.peer_tails[d] = (unsigned long long*)(v.peer[d] + 256);
+      p.peer_counter[d] = (unsigned long long*)(v.peer[d] + hoff);
+      p.peer_tails[d] = (unsigned long long*)(v.peer[d] + hoff + 256);
     }
     p.peer_cap = cap;
     p.tail_slot0 = (u32)me * kMaxTailCtas;
@@ -891,8 +901,8 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     ChunkOut co{};
     co.ncols = p.nout;
     for (size_t k = 0; k < outs.size(); ++k) {
-      outs[k].values = v.local + voff[k];
-      outs[k].validity = wv[k] ? v.local + boff[k] : nullptr;
+      outs[k].values = base + voff[k];
+      outs[k].validity = wv[k] ? base + boff[k] : nullptr;
       p.out[k] = outs[k];
       co.values[k] = outs[k].values;
       co.validity[k] = outs[k].validity;
@@ -943,6 +953,13 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
       if (wv[k] && n_rows)
         TQ_CUDA(cudaMemcpyAsync(out->cols[k].validity, co.validity[k], (n_rows + 7) / 8, cudaMemcpyDeviceToDevice, st));
     }
+    // ready this half for its next use (two exchanges later): the copy-out
+    // above and this reset precede this rank's next barrier2 in stream order
+    TQ_CUDA(cudaMemsetAsync(counter, 0, 8, st));
+    k_tail_reset<<<(u32)std::min<u64>(1024, (nslots + 255) / 256), 256, 0, st>>>(tails, nslots);
+    counted_launch(c);
+    comm_half_ready(cm, half) = true;
+    comm_epoch(cm) += 1;
     prof_end(c, ph_fix, st);
     if (rows_sent) *rows_sent = sent_rows;
     comm_last_cap(cm) = cap;
@@ -1993,25 +2010,21 @@ tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* t, tq_
     b->key_scale = t->key_scale;
     b->nwords = per;
     b->parts = (uint32_t)n;
+    // Precondition (collective): every rank built its table with bloom_keys =
+    // the capacity of the last fused exchange, which is identical on all ranks,
+    // so every filter has the same word count.  Checked locally against that
+    // agreed value before the collective (no size all-gather, no host sync).
+    uint64_t expect = 1024;
+    while (expect * 32 < comm_last_cap(comm) * 8) expect <<= 1;
+    if (per != expect) {
+      delete b;
+      fail(TQ_INVALID_PLAN, "table Bloom filter not sized from the last exchange capacity (tq_join_build_sized)");
+    }
     b->words = (uint32_t*)dalloc(c, per * 4 * n, st);
-    // every rank's filter has `per` words (sized from the agreed exchange
-    // capacity); a mismatch would misalign the gathered parts -> checked
-    u64* chk = (u64*)dalloc(c, 8 * (n + 1), st);
-    TQ_CUDA(cudaMemcpyAsync(chk + n, &per, 8, cudaMemcpyHostToDevice, st));
-    comm_allgather_u64(comm, chk + n, chk, 1, st);
     const int ph = prof_begin(c, "nccl_gather_blooms", st);
     comm_allgather_u64(comm, (const unsigned long long*)t->jt.bloom, (unsigned long long*)b->words, per / 2, st);
     prof_end(c, ph, st);
-    std::vector<u64> all(n);
-    TQ_CUDA(cudaMemcpyAsync(all.data(), chk, 8 * n, cudaMemcpyDeviceToHost, st));
-    TQ_CUDA(cudaStreamSynchronize(st));
-    dfree(c, chk, 8 * (n + 1), st);
     comm_add_sent(comm, per * 4 * (n - 1));
-    for (u64 x : all)
-      if (x != per) {
-        tq_bloom_destroy(b);
-        fail(TQ_INVALID_PLAN, "table Bloom filters differ in size across ranks");
-      }
     *out = b;
   });
 }

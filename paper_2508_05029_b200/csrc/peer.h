@@ -10,9 +10,10 @@
 
 namespace tq {
 
-// Window layout (identical on every rank): [0, 256) control word = the row
-// counter; [256, 256 + n * kMaxTailCtas * 16) tail slots {base, used} per
-// (source rank, CTA); then the data region (column values / bitmaps).
+// Window layout (identical on every rank): two halves of win_bytes / 2, used
+// alternately by successive fused exchanges; each half: [0, 256) control word
+// = the row counter; [256, 256 + n * kMaxTailCtas * 16) tail slots {base, used}
+// per (source rank, CTA); then the data region (column values / bitmaps).
 struct PeerView {
   uint8_t* local = nullptr;     // this rank's window
   std::vector<uint8_t*> peer;   // [n] every rank's window as mapped in this process
@@ -31,6 +32,8 @@ void comm_allgather_u64(tq_comm* cm, const unsigned long long* dev_in, unsigned 
 tq_ctx* comm_ctx(tq_comm* cm);
 int comm_rank(tq_comm* cm);
 int comm_size(tq_comm* cm);
+uint64_t& comm_epoch(tq_comm* cm);                // fused exchanges completed (same on every rank)
+bool& comm_half_ready(tq_comm* cm, int half);     // window half reset since its last use
 uint64_t& comm_last_cap(tq_comm* cm);  // rows capacity of the last fused exchange (same on every rank)
 void comm_add_sent(tq_comm* cm, uint64_t bytes);  // NVLink bytes accounting
 
