@@ -295,10 +295,20 @@ __device__ __forceinline__ u32 partition_of_p(const PipeParams& p, const u64* kw
 // The single build row matching kw (unique-key tables), or -1.
 // First build row matching kw (-1: none).  With `walk` the rest of the
 // cluster is walked too, and a second match sets dup (non-unique build keys).
+__device__ __forceinline__ bool jt_exact_hit(const JoinTable& t, u64 key) {
+  if (key >= 32 * (t.bloom_mask + 1)) return false;
+  return (__ldg(t.exact_bits + (key >> 5)) >> (key & 31)) & 1u;
+}
+
+// exact: the build's membership bitmap is exact (jt.exact_flag == 0), so it
+// replaces the Bloom pre-check (no false positives).
 template <int KW>
-__device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u64* kw, bool walk, bool& dup) {
+__device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u64* kw, bool walk, bool& dup,
+                                                   bool exact = false) {
   const u64 h = key_hash(kw, KW > 0 ? KW : (int)t.kw);
-  if (t.bloom) {
+  if (exact) {
+    if (!jt_exact_hit(t, kw[0])) return -1;
+  } else if (t.bloom) {
     const u32 b = bloom_bits(h);
     if ((__ldg(t.bloom + bloom_word(h, t.bloom_mask)) & b) != b) return -1;
   }
@@ -321,9 +331,11 @@ __device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u6
 
 // Build rows matching kw, after the (L2-resident) Bloom filter check.
 template <int KW>
-__device__ __forceinline__ u32 jt_probe_count(const JoinTable& t, const u64* kw) {
+__device__ __forceinline__ u32 jt_probe_count(const JoinTable& t, const u64* kw, bool exact = false) {
   const u64 h = key_hash(kw, KW > 0 ? KW : (int)t.kw);
-  if (t.bloom) {
+  if (exact) {
+    if (!jt_exact_hit(t, kw[0])) return 0;
+  } else if (t.bloom) {
     const u32 b = bloom_bits(h);
     if ((__ldg(t.bloom + bloom_word(h, t.bloom_mask)) & b) != b) return 0;
   }
@@ -556,6 +568,14 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   // did not prove its keys unique
   bool walk_dups = true;
   if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 && p.jt.dup_dev) walk_dups = *p.jt.dup_dev != 0;
+  // probes: the build's exact membership bitmap replaces the Bloom check; a
+  // semi-join (no build columns) over proven-unique keys then skips the table
+  bool exact = false, semi_skip = false;
+  if ((SINK == SINK_EMIT || SINK == SINK_COUNT) && (p.dest_kind == DEST_PROBE1 || p.dest_kind == DEST_PROBE) &&
+      p.jt.exact_flag) {
+    exact = *p.jt.exact_flag == 0;
+    semi_skip = exact && p.probe_semi && p.dest_kind == DEST_PROBE1 && !walk_dups;
+  }
   for (u32 tile = first; tile < p.ntiles; tile += step) {
     uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
     mbar_wait(&full[s], ph);
@@ -659,7 +679,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         if (pass) {
           u64 kw[kMaxKeyWords + 1];
           bool dup = false;
-          if (!P::keys(w, v, kw, raw[v])) brow = jt_probe_first<P::kKw>(p.jt, kw, walk_dups, dup);
+          if (!P::keys(w, v, kw, raw[v])) {
+            if (semi_skip) brow = jt_exact_hit(p.jt, kw[0]) ? 0 : -1;  // no build column is read
+            else brow = jt_probe_first<P::kKw>(p.jt, kw, walk_dups, dup, exact);
+          }
           if (dup && *(volatile u32*)p.dup_flag == 0) *(volatile u32*)p.dup_flag = 1;
         }
         const u32 mm = __ballot_sync(kFull, brow >= 0);
@@ -699,7 +722,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
             if (has_null || (__ldg(sb + bloom_word(hb, p.semi_mask)) & bb) != bb) mult[v] = 0;
           }
           if (p.dest_kind != DEST_PARTITION)
-            mult[v] = has_null ? 0u : jt_probe_count<P::kKw>(p.jt, kw);  // null keys never match
+            mult[v] = has_null ? 0u : jt_probe_count<P::kKw>(p.jt, kw, exact);  // null keys never match
         }
       }
       u32* wc = s_cnt + warp * kMaxDest;  // this warp's per-destination counters
@@ -795,6 +818,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         u64 sl = hb & mask;
         long long row = (long long)(p.row_base + r0 + trow(w, v));
         if (t.bloom) atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
+        if (t.exact_bits) {
+          if (kw[0] < 32 * (t.bloom_mask + 1)) atomicOr(t.exact_bits + (kw[0] >> 5), 1u << (kw[0] & 31));
+          else if (*(volatile u32*)t.exact_flag == 0) *(volatile u32*)t.exact_flag = 1;
+        }
         if (!t.entries) continue;  // Bloom-only build (LIP filter)
         if ((P::kKw == 1 || (P::kKw == 0 && t.kw == 1)) && t.dup_dev) {
           // {row, key} claimed in one 128-bit CAS against the empty pattern

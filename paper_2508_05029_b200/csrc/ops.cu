@@ -561,6 +561,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
         fail(TQ_INVALID_PLAN, "join key types differ");
     }
     p.jt = t->jt;
+    p.probe_semi = A.build_cols.empty() ? 1u : 0u;
   }
   // output schema
   std::vector<tq_column> sch;
@@ -1006,7 +1007,10 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   while (words * 32 < std::max<uint64_t>(in->rows, bloom_keys) * 8) words <<= 1;
   t->jt.bloom_mask = words - 1;
   uint64_t ebytes = cap * t->jt.stride;
-  t->bytes = ebytes + words * 4 + 16;  // + the build's duplicate-key flag
+  // + the build's duplicate-key and exact-range flags; one-word keys also get
+  // an exact membership bitmap over [0, 32 * words) (same size as the Bloom)
+  const bool exact = t->jt.kw == 1;
+  t->bytes = ebytes + words * 4 + 16 + (exact ? words * 4 : 0);
   try {
     t->jt.entries = (uint8_t*)dalloc(c, t->bytes, st);
   } catch (...) {
@@ -1015,8 +1019,10 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   }
   t->jt.bloom = (uint32_t*)(t->jt.entries + ebytes);
   TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, ebytes, st));
-  TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, words * 4 + 16, st));
+  TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, words * 4 + 16 + (exact ? words * 4 : 0), st));
   t->jt.dup_dev = t->jt.kw == 1 && t->jt.stride == 16 ? (uint32_t*)(t->jt.bloom + words) : nullptr;
+  t->jt.exact_flag = exact ? (uint32_t*)(t->jt.bloom + words) + 1 : nullptr;
+  t->jt.exact_bits = exact ? (uint32_t*)(t->jt.bloom + words) + 4 : nullptr;
   {  // TQ_BLOOM=0: experiments only (probe without the Bloom pre-check)
     static const bool no_bloom = [] { const char* e = getenv("TQ_BLOOM"); return e && e[0] == '0'; }();
     if (no_bloom) t->jt.bloom = nullptr;

@@ -79,6 +79,11 @@ struct JoinTable {
   // (wider keys): single-pass probes then walk each cluster to check
   uint32_t* dup_dev;
   uint64_t bloom_mask;  // words - 1 (power of two)
+  // exact membership bitmap for one-word keys in [0, 32 * (bloom_mask + 1)):
+  // bit k set <=> key k was inserted.  exact_flag (device): 0 = every key was
+  // in range (the bitmap is exact), 1 = not; nullptr = not built
+  uint32_t* exact_bits;
+  uint32_t* exact_flag;
 };
 
 enum OutSrc : uint8_t { OUT_OPND = 0, OUT_BUILD = 1 };
@@ -175,6 +180,9 @@ struct PipeParams {
   // DEST_PROBE1: set when a probe key matches a second build row (the build
   // keys are not unique; the single-pass output is discarded)
   uint32_t* dup_flag;
+  // DEST_PROBE1 with no build columns (a semi-join): with an exact bitmap and
+  // proven-unique build keys the table itself is never read
+  uint32_t probe_semi;
 };
 
 }  // namespace tq

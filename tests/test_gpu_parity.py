@@ -136,6 +136,34 @@ def test_probe_unique_then_duplicate_keys(ctx, dups_probed):
     t.free()
 
 
+@pytest.mark.parametrize("out_of_range", [False, True])
+def test_probe_exact_bitmap_semi_join(ctx, out_of_range):
+    """Dense one-word build keys get an exact membership bitmap (no Bloom false
+    positives); a semi-join probe (no build columns) over proven-unique keys
+    then never reads the table.  A key outside [0, 32 x words) disables it."""
+    from paper_2508_05029_b200.expr import Col
+    rng = np.random.default_rng(11)
+    nb = 30000
+    bkeys = rng.permutation(np.arange(0, 4 * nb))[:nb].astype(np.int64)
+    if out_of_range:
+        bkeys[7] = -5
+        bkeys[9] = 1 << 40
+    build = HostBatch(nb, [HostBatch.col_i64(bkeys), HostBatch.col_i64(rng.integers(0, 100, nb))])
+    npr = 100000
+    pk = rng.integers(-100, 4 * nb + 100, npr).astype(np.int64)
+    pk[:3] = [-5, 1 << 40, 4 * nb]
+    probe = HostBatch(npr, [HostBatch.col_i64(pk), HostBatch.col_i64(rng.integers(0, 50, npr))])
+    t = ctx.join_build(ctx.upload(build), [0])
+    dp = ctx.upload(probe)
+    semi = ctx.pipeline_probe(t, dp, Col(1) < 40, [Col(0), Col(1)], [0], []).to_host()
+    keys = set(bkeys.tolist())
+    want = [(int(k), int(v)) for k, v in zip(pk, probe.cols[1].values.view(np.int64)) if v < 40 and int(k) in keys]
+    assert sorted(semi.to_rows()) == sorted(want)
+    full = ctx.join_probe(t, dp, [0]).to_host()  # with build columns: the table is read
+    assert_batches_equal(full, O.join_execute(build, probe, [0], [0]))
+    t.free()
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_aggregate_parity(ctx, seed):
     kinds = (INT64, DECIMAL, FLOAT64, BOOL, INT64)
