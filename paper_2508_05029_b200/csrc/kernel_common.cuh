@@ -808,6 +808,20 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       for (int v = 0; v < kV; ++v) {
         ok[v] = ((pm[v] >> lane) & 1u) && !P::keys(w, v, kws[v], raw[v]);  // null keys never match
       }
+      if (p.jt.exact_bits) {
+        // exact membership bits: lanes whose keys share a bitmap word (dense,
+        // often consecutive keys) merge their bits, one atomic per word
+        const u64 range = 32 * (p.jt.bloom_mask + 1);
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          const bool in = ok[v] && kws[v][0] < range;
+          const u64 word = in ? (kws[v][0] >> 5) : ~0ull;
+          const u32 peers = __match_any_sync(kFull, word);
+          const u32 bits = __reduce_or_sync(peers, in ? 1u << (kws[v][0] & 31) : 0u);
+          if (in && (peers & lanemask_lt()) == 0) atomicOr(p.jt.exact_bits + word, bits);
+          if (ok[v] && !in && *(volatile u32*)p.jt.exact_flag == 0) *(volatile u32*)p.jt.exact_flag = 1;
+        }
+      }
 #pragma unroll
       for (int v = 0; v < kV; ++v) {
         if (!ok[v]) continue;
@@ -818,10 +832,6 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         u64 sl = hb & mask;
         long long row = (long long)(p.row_base + r0 + trow(w, v));
         if (t.bloom) atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
-        if (t.exact_bits) {
-          if (kw[0] < 32 * (t.bloom_mask + 1)) atomicOr(t.exact_bits + (kw[0] >> 5), 1u << (kw[0] & 31));
-          else if (*(volatile u32*)t.exact_flag == 0) *(volatile u32*)t.exact_flag = 1;
-        }
         if (!t.entries) continue;  // Bloom-only build (LIP filter)
         if ((P::kKw == 1 || (P::kKw == 0 && t.kw == 1)) && t.dup_dev) {
           // {row, key} claimed in one 128-bit CAS against the empty pattern
