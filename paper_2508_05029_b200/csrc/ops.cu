@@ -324,7 +324,10 @@ static void launch(tq_ctx* c, int sink, Plan& L, const Prog& P, cudaStream_t st)
   TQ_HT("launch(pipeline)");
   if (L.p.ntiles == 0) return;
   static const char* names[] = {"pipe_count", "pipe_emit", "pipe_agg", "pipe_build"};
-  int h = prof_begin(c, names[sink], st);
+  const char* nm = names[sink];
+  if (sink == SINK_EMIT && L.p.dest_kind == DEST_PEER) nm = L.p.bcast ? "pipe_broadcast" : "pipe_scatter";
+  else if (sink == SINK_EMIT && L.p.dest_kind == DEST_PROBE1) nm = "pipe_probe1";
+  int h = prof_begin(c, nm, st);
   TQ_CUDA(launch_pipeline_prog(c, sink, L.p, L.smem, L.grid, st, P.pb.code(), P.pb.lits()));
   prof_end(c, h, st);
   counted_launch(c);

@@ -60,7 +60,7 @@ def main():
         ctx.sync()
         prof = ctx.profile_report()
         ctx.profile(False)
-        n, ms = prof["pipe_emit"]
+        n, ms = prof.get("pipe_probe1", prof.get("pipe_emit"))
         r = fn()
         res[name] = (round(ms / n * 1e3, 1), r.rows)
         r.free()
