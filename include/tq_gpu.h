@@ -96,6 +96,16 @@ tq_status tq_join_build(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys
  * which tq_comm_gather_table_blooms (tq_exchange.h) can all-gather. */
 tq_status tq_join_build_sized(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
                               uint64_t bloom_keys, tq_join_table** out, void* stream);
+/* Build side of a SEMI-join (the probe takes no build columns, e.g. the
+ * customer side of Q3): one-word keys go into an exact membership bitmap over
+ * [0, 32 x words); when every key was in range and no key repeated (checked
+ * from the atomicOr return values), no hash table is built at all and probes
+ * test one bit per row.  Otherwise this falls back to tq_join_build.  Probes
+ * of a semi-only table must pass no build columns (TQ_INVALID_PLAN). */
+tq_status tq_join_build_semi(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
+                             tq_join_table** out, void* stream);
+tq_status tq_pipeline_build_semi(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
+                                 uint32_t nkeys, tq_join_table** out, void* stream);
 /* join_execute probe side: inner equi-join, null keys never match; output =
  * build columns then probe columns. */
 tq_status tq_join_probe(tq_ctx* ctx, const tq_join_table* table, const tq_batch* probe, const uint32_t* keys,

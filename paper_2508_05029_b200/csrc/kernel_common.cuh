@@ -74,11 +74,21 @@ __device__ __forceinline__ bool jt_key_eq(const JoinTable& t, const long long* e
   return true;
 }
 
+// Home slot of a key: the mixed key hash.  (Keeping blocks of 16 consecutive
+// one-word keys in consecutive slots was measured: 2.4x slower builds — the
+// 128-bit CASes of a warp serialise on the same lines and colliding blocks
+// form long probe runs.)
+template <int KW>
+__device__ __forceinline__ u64 jt_home(const JoinTable& t, const u64* kw, u64 h) {
+  (void)kw;
+  return h & (t.cap - 1);
+}
+
 // Number of build rows whose keys equal kw.
 template <int KW>
 __device__ __forceinline__ u32 jt_count(const JoinTable& t, const u64* kw) {
   const u64 mask = t.cap - 1;
-  u64 s = key_hash(kw, KW > 0 ? KW : (int)t.kw) & mask;
+  u64 s = jt_home<KW>(t, kw, key_hash(kw, KW > 0 ? KW : (int)t.kw));
   u32 n = 0;
   for (;;) {
     const long long* e = jt_entry(t, s);
@@ -314,7 +324,7 @@ __device__ __forceinline__ long long jt_probe_first(const JoinTable& t, const u6
   }
   const u64 mask = t.cap - 1;
   long long found = -1;
-  for (u64 s = h & mask;; s = (s + 1) & mask) {
+  for (u64 s = jt_home<KW>(t, kw, h);; s = (s + 1) & mask) {
     const long long* e = jt_entry(t, s);
     const long long row = e[0];
     if (row < 0) return found;
@@ -340,7 +350,7 @@ __device__ __forceinline__ u32 jt_probe_count(const JoinTable& t, const u64* kw,
     if ((__ldg(t.bloom + bloom_word(h, t.bloom_mask)) & b) != b) return 0;
   }
   const u64 mask = t.cap - 1;
-  u64 s = h & mask;
+  u64 s = jt_home<KW>(t, kw, h);
   u32 n = 0;
   for (;;) {
     const long long* e = jt_entry(t, s);
@@ -576,6 +586,10 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     exact = *p.jt.exact_flag == 0;
     semi_skip = exact && p.probe_semi && p.dest_kind == DEST_PROBE1 && !walk_dups;
   }
+  // a semi-only build (no hash table) that turned out not exact / not unique:
+  // flag it (the host builds the table and re-runs this probe), touch nothing
+  const bool no_table = SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 && p.jt.entries == nullptr && !semi_skip;
+  if (no_table && threadIdx.x == 0) *(volatile u32*)p.dup_flag = 2;
   for (u32 tile = first; tile < p.ntiles; tile += step) {
     uint8_t* stage = smem + p.off_stage + s * p.stage_bytes;
     mbar_wait(&full[s], ph);
@@ -681,7 +695,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           bool dup = false;
           if (!P::keys(w, v, kw, raw[v])) {
             if (semi_skip) brow = jt_exact_hit(p.jt, kw[0]) ? 0 : -1;  // no build column is read
-            else brow = jt_probe_first<P::kKw>(p.jt, kw, walk_dups, dup, exact);
+            else if (!no_table) brow = jt_probe_first<P::kKw>(p.jt, kw, walk_dups, dup, exact);
           }
           if (dup && *(volatile u32*)p.dup_flag == 0) *(volatile u32*)p.dup_flag = 1;
         }
@@ -773,7 +787,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
               P::keys(w, v, kw, raw[v]);
               const JoinTable& t = p.jt;
               const u64 mask = t.cap - 1;
-              u64 sl = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw) & mask;
+              u64 sl = jt_home<P::kKw>(t, kw, key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw));
               for (;;) {
                 const long long* e = jt_entry(t, sl);
                 long long brow = e[0];
@@ -818,7 +832,13 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           const u64 word = in ? (kws[v][0] >> 5) : ~0ull;
           const u32 peers = __match_any_sync(kFull, word);
           const u32 bits = __reduce_or_sync(peers, in ? 1u << (kws[v][0] & 31) : 0u);
-          if (in && (peers & lanemask_lt()) == 0) atomicOr(p.jt.exact_bits + word, bits);
+          if (in && (peers & lanemask_lt()) == 0) {
+            const u32 old = atomicOr(p.jt.exact_bits + word, bits);
+            // a bit already set, or two lanes on one bit: a key inserted twice
+            if (((old & bits) != 0 || __popc(bits) < __popc(peers)) && p.jt.dup_dev &&
+                *(volatile u32*)p.jt.dup_dev == 0)
+              *(volatile u32*)p.jt.dup_dev = 1;
+          }
           if (ok[v] && !in && *(volatile u32*)p.jt.exact_flag == 0) *(volatile u32*)p.jt.exact_flag = 1;
         }
       }
@@ -829,7 +849,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         const JoinTable& t = p.jt;
         const u64 mask = t.cap - 1;
         const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw);
-        u64 sl = hb & mask;
+        u64 sl = jt_home<P::kKw>(t, kw, hb);
         long long row = (long long)(p.row_base + r0 + trow(w, v));
         if (t.bloom) atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
         if (!t.entries) continue;  // Bloom-only build (LIP filter)

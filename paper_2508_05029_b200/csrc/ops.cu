@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -16,6 +17,12 @@
 struct tq_join_table {
   tq_ctx* ctx;
   tq::JoinTable jt;
+  uint8_t* mem = nullptr;  // the allocation: [entries (none when semi-only) | Bloom | flags | exact bitmap]
+  // semi-only table (no entries): how to build the real table if a probe finds
+  // the bitmap was not exact / the keys not unique
+  std::shared_ptr<void> semi_prog;  // Prog
+  std::vector<uint32_t> semi_keys;
+  uint64_t semi_bloom_keys = 0;
   uint64_t bytes;
   cudaStream_t stream;
   tq_batch build;                      // borrowed descriptors (cols copied)
@@ -537,6 +544,26 @@ __global__ void k_chunk_clear_tail(const u64* plan, const __grid_constant__ Chun
   o.validity[c][n >> 3] &= (uint8_t)((1u << (n & 7)) - 1);
 }
 
+static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
+                      tq_join_table** out, cudaStream_t st, uint64_t bloom_keys, bool semi_only);
+
+// A semi-only table whose bitmap turned out not exact (or keys not unique):
+// build the real hash table from the same input and program, in place.
+static void semi_table_materialize(tq_ctx* c, tq_join_table* t, cudaStream_t st) {
+  tq_join_table* full = nullptr;
+  Prog& P = *(Prog*)t->semi_prog.get();
+  run_build(c, &t->build, P, t->semi_keys, &full, st, t->semi_bloom_keys, false);
+  dfree(c, t->mem, t->bytes, st);
+  std::free(t->build.cols);
+  t->jt = full->jt;
+  t->mem = full->mem;
+  t->bytes = full->bytes;
+  t->build = full->build;
+  t->semi_prog.reset();
+  full->build.cols = nullptr;
+  delete full;
+}
+
 static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArgs& A, tq_batch* out,
                             uint64_t* part_offsets, cudaStream_t st) {
   Plan L;
@@ -610,7 +637,11 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
   // only when it is small against the Device budget left
   uint64_t cap_bytes = in->rows * row_bytes;
   uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
-  const bool probe1 = A.mode == MAT_PROBE && A.table->jt.unique && cap_bytes <= (8ull << 30) && cap_bytes * 4 <= room;
+  const bool semi_table = A.mode == MAT_PROBE && A.table->jt.entries == nullptr;
+  if (semi_table && !A.build_cols.empty())
+    fail(TQ_INVALID_PLAN, "semi-join build table: the probe cannot take build columns");
+  const bool probe1 = A.mode == MAT_PROBE && A.table->jt.unique &&
+                      ((cap_bytes <= (8ull << 30) && cap_bytes * 4 <= room) || semi_table);
   if (probe1) {
     // single pass: capacity = probe rows (<= 1 match each), exact size read back
     p.dest_kind = DEST_PROBE1;
@@ -652,18 +683,27 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
       TQ_CUDA(cudaGetLastError());
     }
     uint64_t n = 0;
-    bool dup_keys = false;
+    bool dup_keys = false, need_table = false;
     {
       std::lock_guard<std::mutex> g(c->mu);
       TQ_CUDA(cudaMemcpyAsync(c->pinned, plan, 16, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaMemcpyAsync((uint8_t*)c->pinned + 16, dup, 4, cudaMemcpyDeviceToHost, st));
       { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
       n = ((uint64_t*)c->pinned)[0];
-      dup_keys = ((uint32_t*)c->pinned)[4] != 0;
-      if (!dup_keys && p.ntiles && ((uint64_t*)c->pinned)[1] == ~0ull)
+      const uint32_t flag = ((uint32_t*)c->pinned)[4];
+      dup_keys = flag == 1;
+      need_table = flag == 2;
+      if (!flag && p.ntiles && ((uint64_t*)c->pinned)[1] == ~0ull)
         fail(TQ_INTERNAL, "probe output chunk plan inconsistent");
     }
     dfree(c, sb, scratch, st);
+    if (need_table) {
+      // a semi-only build whose bitmap was not exact / keys not unique
+      tq_batch_free(c, out);
+      semi_table_materialize(c, const_cast<tq_join_table*>(A.table), st);
+      run_materialize(c, in, P, A, out, part_offsets, st);
+      return;
+    }
     if (dup_keys) {
       // a probe key matched two build rows: the build side is not unique on
       // this key -> drop this pass, remember it on the table, probe two-pass
@@ -974,7 +1014,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
 }
 
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
-                      tq_join_table** out, cudaStream_t st, uint64_t bloom_keys = 0) {
+                      tq_join_table** out, cudaStream_t st, uint64_t bloom_keys, bool semi_only) {
   Plan L;
   plan_launch(c, in, P, L, 0, st);
   PipeParams& p = L.p;
@@ -1009,21 +1049,24 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   uint64_t words = 1024;
   while (words * 32 < std::max<uint64_t>(in->rows, bloom_keys) * 8) words <<= 1;
   t->jt.bloom_mask = words - 1;
-  uint64_t ebytes = cap * t->jt.stride;
-  // + the build's duplicate-key and exact-range flags; one-word keys also get
-  // an exact membership bitmap over [0, 32 * words) (same size as the Bloom)
+  // one-word keys also get an exact membership bitmap over [0, 32 * words)
+  // (same size as the Bloom) and the build's duplicate-key / exact-range flags;
+  // a semi-only build (a semi-join's build side) has no hash table at all
   const bool exact = t->jt.kw == 1;
+  const bool semi = semi_only && exact;
+  uint64_t ebytes = semi ? 0 : cap * t->jt.stride;
   t->bytes = ebytes + words * 4 + 16 + (exact ? words * 4 : 0);
   try {
-    t->jt.entries = (uint8_t*)dalloc(c, t->bytes, st);
+    t->mem = (uint8_t*)dalloc(c, t->bytes, st);
   } catch (...) {
     delete t;
     throw;
   }
-  t->jt.bloom = (uint32_t*)(t->jt.entries + ebytes);
-  TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, ebytes, st));
+  t->jt.entries = semi ? nullptr : t->mem;
+  t->jt.bloom = (uint32_t*)(t->mem + ebytes);
+  if (!semi) TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, ebytes, st));
   TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, words * 4 + 16 + (exact ? words * 4 : 0), st));
-  t->jt.dup_dev = t->jt.kw == 1 && t->jt.stride == 16 ? (uint32_t*)(t->jt.bloom + words) : nullptr;
+  t->jt.dup_dev = t->jt.kw == 1 && (t->jt.stride == 16 || semi) ? (uint32_t*)(t->jt.bloom + words) : nullptr;
   t->jt.exact_flag = exact ? (uint32_t*)(t->jt.bloom + words) + 1 : nullptr;
   t->jt.exact_bits = exact ? (uint32_t*)(t->jt.bloom + words) + 4 : nullptr;
   {  // TQ_BLOOM=0: experiments only (probe without the Bloom pre-check)
@@ -1037,6 +1080,15 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   p.jt = t->jt;
   p.row_base = 0;
   launch(c, SINK_BUILD, L, P, st);
+  if (semi) {
+    // usable without a table only when the bitmap is exact and proved the
+    // keys unique (atomicOr return values) — known on the device only; a probe
+    // that finds otherwise flags it and the host then builds the real table
+    // (semi_table_materialize) and re-runs that probe.  No host sync here.
+    t->semi_prog = std::make_shared<Prog>(P);
+    t->semi_keys = key_roots;
+    t->semi_bloom_keys = bloom_keys;
+  }
   // No uniqueness pass and no host sync: a probe first assumes unique build
   // keys (the PK side of a PK-FK join) and runs in one pass.  One-word keys
   // are proven unique (or not) by the build itself (jt.dup_dev); otherwise the
@@ -1668,6 +1720,11 @@ tq_status tq_join_build(tq_ctx* c, const tq_batch* build, const uint32_t* keys, 
   return tq_join_build_sized(c, build, keys, nkeys, 0, out, stream);
 }
 
+tq_status tq_join_build_semi(tq_ctx* c, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
+                             tq_join_table** out, void* stream) {
+  return tq_pipeline_build_semi(c, build, nullptr, keys, nkeys, out, stream);
+}
+
 tq_status tq_join_build_sized(tq_ctx* c, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
                               uint64_t bloom_keys, tq_join_table** out, void* stream) {
   return guard([&] {
@@ -1682,12 +1739,12 @@ tq_status tq_join_build_sized(tq_ctx* c, const tq_batch* build, const uint32_t* 
       ex[k] = tq_expr{&nodes[k], 1, 0};
     }
     compile_prog(P, build, nullptr, ex.data(), nkeys, false);
-    run_build(c, build, P, iota_u32(nkeys), out, pick(c, stream), bloom_keys);
+    run_build(c, build, P, iota_u32(nkeys), out, pick(c, stream), bloom_keys, false);
   });
 }
 
-tq_status tq_pipeline_build(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const uint32_t* keys, uint32_t nkeys,
-                            tq_join_table** out, void* stream) {
+static tq_status pipeline_build_impl(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
+                                     uint32_t nkeys, tq_join_table** out, void* stream, bool semi) {
   return guard([&] {
     check_device_batch(in);
     Prog P(schema_of(in));
@@ -1700,8 +1757,18 @@ tq_status tq_pipeline_build(tq_ctx* c, const tq_batch* in, const tq_expr* pred, 
       ex[k] = tq_expr{&nodes[k], 1, 0};
     }
     compile_prog(P, in, pred, ex.data(), nkeys, false);
-    run_build(c, in, P, iota_u32(nkeys), out, pick(c, stream));
+    run_build(c, in, P, iota_u32(nkeys), out, pick(c, stream), 0, semi);
   });
+}
+
+tq_status tq_pipeline_build(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const uint32_t* keys, uint32_t nkeys,
+                            tq_join_table** out, void* stream) {
+  return pipeline_build_impl(c, in, pred, keys, nkeys, out, stream, false);
+}
+
+tq_status tq_pipeline_build_semi(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
+                                 uint32_t nkeys, tq_join_table** out, void* stream) {
+  return pipeline_build_impl(c, in, pred, keys, nkeys, out, stream, true);
 }
 
 tq_status tq_join_probe(tq_ctx* c, const tq_join_table* t, const tq_batch* probe, const uint32_t* keys,
@@ -1739,7 +1806,7 @@ tq_status tq_pipeline_probe(tq_ctx* c, const tq_join_table* t, const tq_batch* i
 void tq_join_table_destroy(tq_ctx* c, tq_join_table* t) {
   if (!t) return;
   (void)c;
-  dfree(t->ctx, t->jt.entries, t->bytes, t->ctx->stream);  // see tq_batch_free
+  dfree(t->ctx, t->mem, t->bytes, t->ctx->stream);  // see tq_batch_free
   std::free(t->build.cols);
   delete t;
 }

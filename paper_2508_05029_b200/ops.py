@@ -92,6 +92,8 @@ def lib():
                                             P(C.c_uint64), V]
         L.tq_pipeline_probe.argtypes = [V, V, B, E, E, C.c_uint32, U32, C.c_uint32, U32, C.c_uint32, B, V]
         L.tq_pipeline_build.argtypes = [V, B, E, U32, C.c_uint32, P(V), V]
+        L.tq_pipeline_build_semi.argtypes = [V, B, E, U32, C.c_uint32, P(V), V]
+        L.tq_join_build_semi.argtypes = [V, B, U32, C.c_uint32, P(V), V]
         L.tq_datagen.argtypes = [V, C.c_int, C.c_double, B, V]
         L.tq_datagen_shard.argtypes = [V, C.c_int, C.c_double, C.c_uint32, C.c_uint32, B, V]
         L.tq_ctx_stream.restype = V
@@ -374,11 +376,16 @@ class Context:
                                                C.byref(out), offs, stream), out)
         return r, list(offs)
 
-    def join_build(self, build: DeviceBatch, keys: Sequence[int], stream=None, bloom_keys: int = 0) -> JoinTable:
+    def join_build(self, build: DeviceBatch, keys: Sequence[int], stream=None, bloom_keys: int = 0,
+                   semi: bool = False) -> JoinTable:
         """bloom_keys > 0: size the table's Bloom filter for that many keys
-        (tq_join_build_sized; equal sizes across ranks for gather_table_blooms)."""
+        (tq_join_build_sized; equal sizes across ranks for gather_table_blooms).
+        semi=True: build side of a semi-join (tq_join_build_semi)."""
         h = C.c_void_p()
-        if bloom_keys:
+        if semi:
+            self._check(lib().tq_join_build_semi(self.handle, C.byref(build.c), _u32(keys), len(keys), C.byref(h),
+                                                 stream))
+        elif bloom_keys:
             self._check(lib().tq_join_build_sized(self.handle, C.byref(build.c), _u32(keys), len(keys), bloom_keys,
                                                   C.byref(h), stream))
         else:
@@ -468,11 +475,13 @@ class Context:
                                                         stream), out)
         return r, list(offs)
 
-    def pipeline_build(self, b: DeviceBatch, pred, keys: Sequence[int], stream=None) -> JoinTable:
+    def pipeline_build(self, b: DeviceBatch, pred, keys: Sequence[int], stream=None, semi: bool = False) -> JoinTable:
+        """semi=True: build side of a semi-join (tq_pipeline_build_semi) — probes
+        take no build columns; dense unique keys need no hash table."""
         pp, _k1 = _pred(pred)
         h = C.c_void_p()
-        self._check(lib().tq_pipeline_build(self.handle, C.byref(b.c), pp, _u32(keys), len(keys), C.byref(h),
-                                            stream))
+        fn = lib().tq_pipeline_build_semi if semi else lib().tq_pipeline_build
+        self._check(fn(self.handle, C.byref(b.c), pp, _u32(keys), len(keys), C.byref(h), stream))
         return JoinTable(self, h, b)
 
     def pipeline_probe(self, t: JoinTable, b: DeviceBatch, pred, exprs, keys: Sequence[int],

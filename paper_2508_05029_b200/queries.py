@@ -86,7 +86,8 @@ REV = Col(L_EXTPRICE) * (Dec(100) - Col(L_DISCOUNT))
 def q3(ctx, customer, orders, lineitem):
     """Q3-style: customer(BUILDING) >< orders(< 1995-03-15) >< lineitem(> 1995-03-15), group by
     (l_orderkey, o_orderdate, o_shippriority) sum(revenue)."""
-    ct = ctx.pipeline_build(customer, Col(C_MKTSEGMENT).eq(1), [C_CUSTKEY])
+    # customer contributes no columns: the build side of a semi-join
+    ct = ctx.pipeline_build(customer, Col(C_MKTSEGMENT).eq(1), [C_CUSTKEY], semi=True)
     of = ctx.pipeline_probe(ct, orders, Col(O_ORDERDATE) < 9204,
                             [Col(O_ORDERKEY), Col(O_ORDERDATE), Col(O_SHIPPRIORITY), Col(O_CUSTKEY)], [3], [])
     ot = ctx.join_build(of, [0])
@@ -174,7 +175,7 @@ def q3_distributed(ctx, comm, customer, orders, lineitem, stats=None, lip=True, 
     else:
         cf = ctx.pipeline_materialize(customer, Col(C_MKTSEGMENT).eq(1), [Col(C_CUSTKEY)])
         cb, _ = comm.allgather(cf)
-    ct = ctx.join_build(cb, [0])
+    ct = ctx.join_build(cb, [0], semi=True)  # customer contributes no columns: a semi-join build
     of = ctx.pipeline_probe(ct, orders, Col(O_ORDERDATE) < 9204,
                             [Col(O_ORDERKEY), Col(O_ORDERDATE), Col(O_SHIPPRIORITY), Col(O_CUSTKEY)], [3], [])
     bloom = None

@@ -164,6 +164,35 @@ def test_probe_exact_bitmap_semi_join(ctx, out_of_range):
     t.free()
 
 
+@pytest.mark.parametrize("case", ["unique", "duplicates", "out_of_range"])
+def test_semi_join_build(ctx, case):
+    """tq_join_build_semi: dense unique keys -> bitmap only (no hash table);
+    duplicate or out-of-range keys -> falls back to a real table.  Either way
+    the (inner-join) result equals the oracle's."""
+    from paper_2508_05029_b200.columnar import TqError
+    from paper_2508_05029_b200.expr import Col
+    rng = np.random.default_rng(3)
+    nb = 20000
+    bkeys = rng.permutation(np.arange(1, 3 * nb))[:nb].astype(np.int64)
+    if case == "duplicates":
+        bkeys[100:110] = bkeys[200:210]
+    if case == "out_of_range":
+        bkeys[5] = -3
+    build = HostBatch(nb, [HostBatch.col_i64(bkeys)])
+    npr = 80000
+    probe = HostBatch(npr, [HostBatch.col_i64(rng.integers(-10, 3 * nb + 10, npr)),
+                            HostBatch.col_dec(rng.integers(0, 999, npr))])
+    t = ctx.join_build(ctx.upload(build), [0], semi=True)
+    got = ctx.pipeline_probe(t, ctx.upload(probe), None, [Col(0), Col(1)], [0], []).to_host()
+    want = O.join_execute(build, probe, [0], [0])  # build key column first, then probe columns
+    want = HostBatch(want.rows, want.cols[1:])
+    assert_batches_equal(got, want)
+    if case == "unique":  # a semi-only table cannot hand out build columns
+        with pytest.raises(TqError):
+            ctx.pipeline_probe(t, ctx.upload(probe), None, [Col(0)], [0], [0])
+    t.free()
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_aggregate_parity(ctx, seed):
     kinds = (INT64, DECIMAL, FLOAT64, BOOL, INT64)

@@ -66,7 +66,7 @@ def main():
             mark("customer filter")
             cb, _ = comm.allgather(cf)
             mark("customer allgather")
-        ct = ctx.join_build(cb, [0])
+        ct = ctx.join_build(cb, [0], semi=True)
         mark("customer build")
         of = ctx.pipeline_probe(ct, t["orders"], Col(Q.O_ORDERDATE) < 9204,
                                 [Col(Q.O_ORDERKEY), Col(Q.O_ORDERDATE), Col(Q.O_SHIPPRIORITY), Col(Q.O_CUSTKEY)],
