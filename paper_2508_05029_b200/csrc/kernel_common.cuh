@@ -184,9 +184,10 @@ __device__ __forceinline__ long long table_find_insert(u32* state, u64* keys, u6
       if (cur == kStEmpty) {
         for (u32 i = 0; i < kwa; ++i) keys[s * kwa + i] = kw[i];
         init(s);
-        // publish with release semantics (orders the key / accumulator
-        // stores before the state; no full fence + L1 invalidate per claim)
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(state + s), "r"(kStReady) : "memory");
+        // publish: the key / accumulator stores are visible before the state
+        // (a full fence: readers compare keys with plain volatile loads)
+        __threadfence();
+        atomicExch(state + s, kStReady);
         if (counter) atomicAdd(counter, 1ull);
         return (long long)s;
       }
