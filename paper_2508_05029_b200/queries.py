@@ -101,9 +101,9 @@ def q3(ctx, customer, orders, lineitem):
 
 def q5(ctx, region, nation, customer, orders, lineitem, supplier):
     """Q5-style: ASIA nations, local supplier revenue per nation (1994)."""
-    rt = ctx.pipeline_build(region, Col(R_NAME).eq(2), [R_REGIONKEY])
+    rt = ctx.pipeline_build(region, Col(R_NAME).eq(2), [R_REGIONKEY], semi=True)  # semi-joins: no build columns
     nf = ctx.pipeline_probe(rt, nation, None, [Col(N_NATIONKEY), Col(N_REGIONKEY)], [1], [])
-    nt = ctx.join_build(nf, [0])
+    nt = ctx.join_build(nf, [0], semi=True)
     cf = ctx.pipeline_probe(nt, customer, None, [Col(C_CUSTKEY), Col(C_NATIONKEY)], [1], [])
     ct = ctx.join_build(cf, [0])
     of = ctx.pipeline_probe(ct, orders, (Col(O_ORDERDATE) >= 8766) & (Col(O_ORDERDATE) < 9131),
@@ -122,7 +122,7 @@ def q5(ctx, region, nation, customer, orders, lineitem, supplier):
 
 def q9(ctx, part, partsupp, lineitem, supplier, orders):
     """Q9-style: profit of 'green' parts per (nation, year)."""
-    pt = ctx.pipeline_build(part, Col(P_COLOR) < 54, [P_PARTKEY])
+    pt = ctx.pipeline_build(part, Col(P_COLOR) < 54, [P_PARTKEY], semi=True)  # semi-join: no part columns
     psf = ctx.pipeline_probe(pt, partsupp, None, None, [PS_PARTKEY], [])
     pst = ctx.join_build(psf, [PS_PARTKEY, PS_SUPPKEY])
     lj = ctx.pipeline_probe(pst, lineitem, None,
@@ -132,12 +132,16 @@ def q9(ctx, part, partsupp, lineitem, supplier, orders):
     st = ctx.join_build(supplier, [S_SUPPKEY])
     sj = ctx.pipeline_probe(st, lj, None, None, [3], [S_NATIONKEY])
     # sj: [s_nationkey, ps_supplycost, l_orderkey, l_partkey, l_suppkey, qty, ep, disc]
-    ot = ctx.join_build(orders, [O_ORDERKEY])
+    # the build side of the orders join is the SMALLER input: the
+    # ~5% of lineitem that survived, not all of orders
     amt = Col(6) * (Dec(100) - Col(7)) - Col(1) * Col(5)
-    oj = ctx.pipeline_probe(ot, sj, None, [Col(0), amt, Col(2)], [2], [O_YEAR])
-    # oj: [o_year, s_nationkey, amt, l_orderkey]
-    out = ctx.aggregate_execute(oj, [1, 0], [(AGG_SUM, 2)])
-    for t in (pt, pst, st, ot):
+    sjp = ctx.project_execute(sj, [Col(0), amt, Col(2)])
+    # sjp: [s_nationkey, amt, l_orderkey]
+    jt = ctx.join_build(sjp, [2])
+    oj = ctx.pipeline_probe(jt, orders, None, [Col(O_YEAR), Col(O_ORDERKEY)], [1], [0, 1])
+    # oj: [s_nationkey, amt, o_year, o_orderkey]
+    out = ctx.aggregate_execute(oj, [0, 2], [(AGG_SUM, 1)])
+    for t in (pt, pst, st, jt):
         t.free()
     return out
 
