@@ -508,6 +508,20 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int KWA = P::kKwa;  // > 0 when known at compile time
 
+  // single-pass probe of a table whose build saw a key twice (jt.dup_dev,
+  // exact for one-word keys): flag it at once — the host runs the two-pass
+  // probe — instead of scanning the input for the first duplicate match.
+  // (Uniform over the grid; every CTA leaves a "no hole" tail for the fix-up.)
+  if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 && p.jt.dup_dev && *(volatile u32*)p.jt.dup_dev) {
+    if (threadIdx.x == 0) {
+      p.chunk_tail[2 * blockIdx.x] = 0;
+      p.chunk_tail[2 * blockIdx.x + 1] = kChunk;
+      // (a semi-only build has no table to probe two-pass: ask for the table)
+      if (blockIdx.x == 0) *(volatile u32*)p.dup_flag = p.jt.entries ? 1u : 2u;
+    }
+    return;
+  }
+
   if (P::kInterp) {
     for (u32 i = threadIdx.x; i < p.ncode; i += kBlock) s_code[i] = p.code[i];
     for (u32 i = threadIdx.x; i < p.nlits; i += kBlock) s_lits[i] = p.lits[i];

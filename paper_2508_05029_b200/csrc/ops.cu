@@ -692,7 +692,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
       n = ((uint64_t*)c->pinned)[0];
       const uint32_t flag = ((uint32_t*)c->pinned)[4];
       dup_keys = flag == 1;
-      need_table = flag == 2;
+      need_table = flag == 2 || (flag == 1 && A.table->jt.entries == nullptr);
       if (!flag && p.ntiles && ((uint64_t*)c->pinned)[1] == ~0ull)
         fail(TQ_INTERNAL, "probe output chunk plan inconsistent");
     }

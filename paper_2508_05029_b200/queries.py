@@ -132,16 +132,12 @@ def q9(ctx, part, partsupp, lineitem, supplier, orders):
     st = ctx.join_build(supplier, [S_SUPPKEY])
     sj = ctx.pipeline_probe(st, lj, None, None, [3], [S_NATIONKEY])
     # sj: [s_nationkey, ps_supplycost, l_orderkey, l_partkey, l_suppkey, qty, ep, disc]
-    # the build side of the orders join is the SMALLER input: the
-    # ~5% of lineitem that survived, not all of orders
+    ot = ctx.join_build(orders, [O_ORDERKEY])
     amt = Col(6) * (Dec(100) - Col(7)) - Col(1) * Col(5)
-    sjp = ctx.project_execute(sj, [Col(0), amt, Col(2)])
-    # sjp: [s_nationkey, amt, l_orderkey]
-    jt = ctx.join_build(sjp, [2])
-    oj = ctx.pipeline_probe(jt, orders, None, [Col(O_YEAR), Col(O_ORDERKEY)], [1], [0, 1])
-    # oj: [s_nationkey, amt, o_year, o_orderkey]
-    out = ctx.aggregate_execute(oj, [0, 2], [(AGG_SUM, 1)])
-    for t in (pt, pst, st, jt):
+    oj = ctx.pipeline_probe(ot, sj, None, [Col(0), amt, Col(2)], [2], [O_YEAR])
+    # oj: [o_year, s_nationkey, amt, l_orderkey]
+    out = ctx.aggregate_execute(oj, [1, 0], [(AGG_SUM, 2)])
+    for t in (pt, pst, st, ot):
         t.free()
     return out
 
