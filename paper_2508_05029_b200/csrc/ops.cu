@@ -1120,19 +1120,34 @@ struct FinalParams {
   unsigned long long* counter;
 };
 
+// Output rows are reserved per BLOCK and iteration (one global atomic per 256
+// slots, not one per warp: at ~10% table load nearly every warp has a group,
+// and per-warp atomics on the one cursor serialised the kernel).
 __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  u64 stride = (u64)gridDim.x * blockDim.x;
-  const u64 cap = (f.t.cap + 31) / 32 * 32;  // whole warps stay converged for the ballot
-  for (u64 s = i; s < cap; s += stride) {
+  __shared__ u32 s_warp[8];
+  __shared__ unsigned long long s_base;
+  const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 cap = (f.t.cap + 255) / 256 * 256;  // whole blocks stay in the loop (block barriers)
+  for (u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += stride) {
     const bool occ = s < f.t.cap && f.t.state[s] == 2;
     const u32 m = __ballot_sync(0xffffffffu, occ);
-    if (!m) continue;
-    u64 base = 0;
-    if ((threadIdx.x & 31) == 0) base = atomicAdd(f.counter, (unsigned long long)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u32 tot = 0;
+      for (u32 w = 0; w < blockDim.x / 32; ++w) {
+        const u32 c = s_warp[w];
+        s_warp[w] = tot;
+        tot += c;
+      }
+      s_base = tot ? atomicAdd(f.counter, (unsigned long long)tot) : 0;
+    }
+    __syncthreads();
+    const u64 base = s_base + s_warp[warp];
+    __syncthreads();  // s_warp / s_base are rewritten next iteration
     if (!occ) continue;
-    u64 row = base + __popc(m & ((1u << (threadIdx.x & 31)) - 1));
+    u64 row = base + __popc(m & ((1u << lane) - 1));
     const u64* kw = f.t.keys + s * f.kwa;
     u64 nullw = kw[f.kwa - 1];
     for (u32 k = 0; k < f.nkeys; ++k) {
