@@ -837,7 +837,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       for (int v = 0; v < kV; ++v) {
         ok[v] = ((pm[v] >> lane) & 1u) && !P::keys(w, v, kws[v], raw[v]);  // null keys never match
       }
-      if (p.jt.exact_bits) {
+      if (p.jt.exact_bits && !p.build_skip_aux) {
         // exact membership bits: lanes whose keys share a bitmap word (dense,
         // often consecutive keys) merge their bits, one atomic per word
         const u64 range = 32 * (p.jt.bloom_mask + 1);
@@ -866,8 +866,12 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)t.kw);
         u64 sl = jt_home<P::kKw>(t, kw, hb);
         long long row = (long long)(p.row_base + r0 + trow(w, v));
-        if (t.bloom) atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
+        if (t.bloom && !p.build_skip_aux) atomicOr(t.bloom + bloom_word(hb, t.bloom_mask), bloom_bits(hb));
         if (!t.entries) continue;  // Bloom-only build (LIP filter)
+        // slot-range pass of a partitioned build: only keys whose home slot is
+        // in [slot_lo, slot_hi) are inserted by this launch (that range of the
+        // table stays L2-resident while it fills)
+        if (p.slot_hi && (sl < p.slot_lo || sl >= p.slot_hi)) continue;
         if ((P::kKw == 1 || (P::kKw == 0 && t.kw == 1)) && t.dup_dev) {
           // {row, key} claimed in one 128-bit CAS against the empty pattern
           // (all ones): an equal key already present is seen atomically

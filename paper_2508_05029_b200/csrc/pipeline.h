@@ -183,6 +183,11 @@ struct PipeParams {
   // DEST_PROBE1 with no build columns (a semi-join): with an exact bitmap and
   // proven-unique build keys the table itself is never read
   uint32_t probe_semi;
+  // BUILD, partitioned into slot ranges (tables much larger than L2): this
+  // launch inserts only home slots in [slot_lo, slot_hi) (slot_hi = 0: all);
+  // build_skip_aux: the Bloom / exact bits were set by an earlier range pass
+  uint64_t slot_lo, slot_hi;
+  uint32_t build_skip_aux;
 };
 
 }  // namespace tq
