@@ -27,7 +27,7 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
 
 METRIC = "query latency (ms) and input rows/sec per TPC-H-style query at 1/2/4/8 B200"
-SF_PER_GPU = 10.0
+SF_PER_GPU = float(os.environ.get("TQ_BENCH_SF", "10"))  # override: quick test runs only
 Q1_BYTES_PER_ROW = 88  # rf 8 + ls 8 + qty 16 + ep 16 + disc 16 + tax 16 + shipdate 8
 
 
@@ -215,13 +215,15 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def timed(ctx, fn, reps, world, stream):
-    """median device ms of fn() over reps (after one warm-up), max over ranks."""
+def timed(ctx, fn, reps, world, stream, keep=False):
+    """median device ms of fn() over reps (after one warm-up), max over ranks;
+    keep=True also returns the last output (host copy) for the parity check."""
     import torch
     fn().free()
     ctx.sync()
     ms = []
-    for _ in range(reps):
+    last = None
+    for i in range(reps):
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -230,41 +232,113 @@ def timed(ctx, fn, reps, world, stream):
         torch.cuda.synchronize()
         ctx.sync()
         ms.append(e0.elapsed_time(e1))
+        if keep and i == reps - 1:
+            last = out.to_host()
         out.free()
     if os.environ.get("TQ_BENCH_VERBOSE"):
         print(f"[timed rank{os.environ.get('RANK', '0')}] {[round(x, 3) for x in ms]}", file=sys.stderr, flush=True)
-    return max_over_ranks(world, statistics.median(ms))
+    m = max_over_ranks(world, statistics.median(ms))
+    return (m, last) if keep else m
 
 
-def run_suite(args, ctx, world, rank, stream):
+class OracleTables:
+    """The CPU oracle's copy of the synthetic tables (test infrastructure: the
+    parity checker of the timed results, never the thing measured)."""
+
+    def __init__(self, nthreads):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        self.O = O
+        self.nthreads = nthreads
+        self.cache = {}
+
+    def get(self, t, sf):
+        if (t, sf) not in self.cache:
+            self.cache[(t, sf)] = self.O.datagen(t, sf, self.nthreads)
+        return self.cache[(t, sf)]
+
+    def query(self, q, sf):
+        return self.O.query(q, {t: self.get(t, sf) for t in self.O.QUERY_TABLES[q]}, self.nthreads)
+
+    def drop(self):
+        self.cache.clear()
+
+
+def check(got, want) -> str:
+    """'exact' (integers / decimals / keys bit-exact after canonical sort,
+    Float64 within 1e-9 relative) or the mismatch."""
+    from paper_2508_05029_b200.columnar import assert_batches_equal
+    try:
+        assert_batches_equal(got, want)
+        return "exact"
+    except AssertionError as e:
+        return f"MISMATCH: {str(e)[:200]}"
+
+
+def q3_sharded_parity(got, sf, nthreads, shards=(0, 57), nshards=100) -> str:
+    """Config-4 result (Q3 at SF100) vs the oracle, exact on sampled orderkey
+    shards: the group-by key l_orderkey is co-partitioned with the orders
+    row-group subsets, so the result's groups whose orderkey lies in orders
+    shard s are exactly the oracle's Q3 over (all customers, orders shard s,
+    lineitem shard s = the lines of those orders)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import oracle as O
+    no = O.table_rows(O.T_ORDERS, sf)
+    cust = O.datagen(O.T_CUSTOMER, sf, nthreads)
+    keys = got.cols[0].i64()
+    groups = 0
+    for s in shards:
+        lo, hi = no * s // nshards, no * (s + 1) // nshards  # orderkeys lo+1 .. hi
+        tabs = {O.T_CUSTOMER: cust, O.T_ORDERS: O.datagen(O.T_ORDERS, sf, nthreads, s, nshards),
+                O.T_LINEITEM: O.datagen(O.T_LINEITEM, sf, nthreads, s, nshards)}
+        want = O.query(3, tabs, nthreads)
+        sel = O.take(got, np.nonzero((keys > lo) & (keys <= hi))[0].tolist())
+        r = check(sel, want)
+        if r != "exact":
+            return f"shard {s}: {r}"
+        groups += want.rows
+    return f"exact on orderkey shards {list(shards)} of {nshards} ({groups} groups)"
+
+
+def run_suite(args, ctx, world, rank, stream, oracle, parity):
     """The other BASELINE.json configs: Q6/Q3/Q5/Q9 at SF10 on one GPU, and the
     config-4 Q3 shuffle join (broadcast + NCCL all-to-all over NVLink) at
-    SF{shuffle_sf} total, strong scaling over the N GPUs."""
+    SF{shuffle_sf} total, strong scaling over the N GPUs.  Every timed result
+    is checked against the CPU oracle (`parity`, filled in place)."""
     import torch.distributed as dist
     from paper_2508_05029_b200 import queries
     from paper_2508_05029_b200.ops import Comm
     suite = {}
+    do_parity = os.environ.get("TQ_BENCH_PARITY", "1") == "1"
     if world == 1:
         sf = SF_PER_GPU
         names = ["customer", "orders", "lineitem", "supplier", "part", "partsupp", "nation", "region"]
         t = {n: ctx.datagen(queries.TABLE_IDS[n], sf) for n in names}
         li6 = t["lineitem"].select(queries.Q6_SCAN)
-        ms = timed(ctx, lambda: queries.q6_scan(ctx, li6), 5, world, stream)
-        suite[f"q6_sf{sf:g}"] = {"ms": ms, "rows_per_s": t["lineitem"].rows / (ms * 1e-3),
-                                 "hbm_gbs": t["lineitem"].rows * queries.Q6_SCAN_BYTES_PER_ROW / (ms * 1e-3) / 1e9}
+        ms, out = timed(ctx, lambda: queries.q6_scan(ctx, li6), 5, world, stream, keep=True)
+        key = f"q6_sf{sf:g}"
+        suite[key] = {"ms": ms, "rows_per_s": t["lineitem"].rows / (ms * 1e-3),
+                      "hbm_gbs": t["lineitem"].rows * queries.Q6_SCAN_BYTES_PER_ROW / (ms * 1e-3) / 1e9}
+        if do_parity:
+            parity[key] = suite[key]["parity"] = check(out, oracle.query(6, sf))
         for q in (3, 5, 9):
             rows = sum(t[n].rows for n in queries.QUERY_TABLES[q])
-            ms = timed(ctx, lambda: queries.run_join_query(ctx, q, t), 3, world, stream)
-            suite[f"q{q}_sf{sf:g}"] = {"ms": ms, "rows_per_s": rows / (ms * 1e-3)}
+            ms, out = timed(ctx, lambda: queries.run_join_query(ctx, q, t), 3, world, stream, keep=True)
+            key = f"q{q}_sf{sf:g}"
+            suite[key] = {"ms": ms, "rows_per_s": rows / (ms * 1e-3)}
+            if do_parity:
+                parity[key] = suite[key]["parity"] = check(out, oracle.query(q, sf))
         for v in t.values():
             v.free()
+        oracle.drop()
         # per-operator HBM roofline (each SPEC operator alone, SF10, kernel
         # time vs algorithmic bytes; tools/op_roofline.py)
         if os.environ.get("TQ_BENCH_OPS", "1") == "1":
             sys.path.insert(0, os.path.join(ROOT, "tools"))
             import op_roofline
             peaks = measured_peaks()
-            suite["operators_sf10"] = op_roofline.measure(ctx, sf, stream, peaks["hbm_gbs"] if peaks else 6481.1)
+            suite["operators_sf10"] = op_roofline.measure(ctx, sf, stream, peaks["hbm_gbs"] if peaks else 6538.6)
         # config 5 (one worker's share: SF100 / 8 GPUs): Q5 / Q9 on the C++ worker
         # runtime with the tables in the pinned Host tier and a Device budget of a
         # quarter of the data, so scans go through load_to_device / preload and
@@ -282,16 +356,19 @@ def run_suite(args, ctx, world, rank, stream):
             rows = sum(b.rows for b in host.values())
             runs = []
             for _ in range(2):
-                _, m = engine_run_query(ctx, q, host, compute_threads=4, preload=1, batch_rows=4 << 20,
-                                        device_budget=max(int(data_bytes / 2.5), 1 << 30))
+                res, m = engine_run_query(ctx, q, host, compute_threads=4, preload=1, batch_rows=4 << 20,
+                                          device_budget=max(int(data_bytes / 2.5), 1 << 30))
                 runs.append(m)
             m = runs[-1]
-            suite[f"q{q}_engine_hosttier_sf{sf5:g}"] = {
+            key = f"q{q}_engine_hosttier_sf{sf5:g}"
+            suite[key] = {
                 "ms": m["run_ms"], "rows_per_s": rows / (m["run_ms"] * 1e-3), "host_tier_bytes": data_bytes,
                 "device_budget": m["device_capacity"], "loads": m["loads"], "preloads": m["preloads"],
                 "spills": m["spills"], "spill_bytes": m["spill_bytes"], "h2d_bytes": m["load_bytes"],
                 "h2d_gbs": m["load_bytes"] / (m["run_ms"] * 1e-3) / 1e9, "oom_retries": m["oom_retries"],
                 "tasks": m["tasks"], "timing": "host wall clock of tq_engine_run_query's run phase"}
+            if do_parity:
+                parity[key] = suite[key]["parity"] = check(res, oracle.O.query(q, host, oracle.nthreads))
             del host
     # config 4: distributed shuffle join
     uid = [Comm.unique_id() if rank == 0 else None]
@@ -301,13 +378,15 @@ def run_suite(args, ctx, world, rank, stream):
     sf = args.shuffle_sf
     t = {n: ctx.datagen(queries.TABLE_IDS[n], sf, shard=rank, nshards=world) for n in ("customer", "orders", "lineitem")}
     rows = sum_over_ranks(world, float(sum(v.rows for v in t.values())))
+    results = {}
     for fused in (True, False):
         b0 = comm.bytes_sent()
         stats = {}
-        ms = timed(ctx, lambda: queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], stats,
-                                                       fused=fused), 3, world, stream)
+        ms, out = timed(ctx, lambda: queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], stats,
+                                                            fused=fused), 3, world, stream, keep=True)
         sent = (comm.bytes_sent() - b0) / 4.0  # 1 warm-up + 3 timed runs
         key = f"q3_shuffle_sf{sf:g}" if fused else f"q3_shuffle_nccl_sf{sf:g}"
+        results[key] = out
         suite[key] = {
             "ms": ms, "rows_per_s": rows / (ms * 1e-3), "scaling": "strong", "n_gpus": world,
             "nvlink_bytes_sent_per_gpu": sent, "nvlink_gbs_per_gpu": sent / (ms * 1e-3) / 1e9,
@@ -321,6 +400,27 @@ def run_suite(args, ctx, world, rank, stream):
     for v in t.values():
         v.free()
     comm.close()
+    if do_parity:
+        # the ranks' results concatenated (co-partitioned groups: disjoint)
+        import torch.distributed as dist
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        full = {}
+        for key, out in results.items():
+            parts = [out]
+            if world > 1:
+                parts = [None] * world
+                dist.all_gather_object(parts, out)
+            full[key] = O.concat(parts)
+        if rank == 0:
+            k_f, k_n = f"q3_shuffle_sf{sf:g}", f"q3_shuffle_nccl_sf{sf:g}"
+            r = q3_sharded_parity(full[k_f], sf, oracle.nthreads)
+            parity[k_f] = suite[k_f]["parity"] = r
+            # the unfused (NCCL) plan: the whole result equals the fused plan's
+            # (two GPU code paths), and the same oracle shards
+            same = check(full[k_n], full[k_f])
+            parity[k_n] = suite[k_n]["parity"] = (
+                q3_sharded_parity(full[k_n], sf, oracle.nthreads) + f"; full result vs fused plan: {same}")
     return suite
 
 
@@ -421,19 +521,24 @@ def run_tq(args, world, rank, local):
     for p in pinned:
         lib().tq_pinned_free(p)
 
-    # ---- correctness of what was timed vs the CPU oracle (rank 0, N=1)
-    parity = None
-    if rank == 0 and world == 1 and os.environ.get("TQ_BENCH_PARITY", "1") == "1":
-        try:
-            sys.path.insert(0, os.path.join(ROOT, "oracle"))
-            import oracle as O
-            from paper_2508_05029_b200.columnar import assert_batches_equal
-            hl = O.datagen(O.T_LINEITEM, sf_total, os.cpu_count() or 1)
-            assert_batches_equal(result, O.query(1, {O.T_LINEITEM: hl}, os.cpu_count() or 1))
-            parity = "bit-exact vs oracle (float avg within 1e-9)"
-            del hl
-        except AssertionError as e:
-            parity = f"MISMATCH: {e}"
+    # ---- correctness of what was timed vs the CPU oracle
+    nthreads = os.cpu_count() or 1
+    oracle = OracleTables(nthreads)
+    parity = {}
+    if os.environ.get("TQ_BENCH_PARITY", "1") == "1":
+        key = f"q1_sf{SF_PER_GPU:g}_per_gpu"
+        if world == 1:
+            parity[key] = check(result, oracle.query(1, sf_total))
+        elif rank == 0:
+            # each rank returns its shard's partial aggregates (merged after
+            # timing): rank 0's partial vs the oracle's operators on that shard
+            O = oracle.O
+            shard = O.datagen(O.T_LINEITEM, sf_total, nthreads, 0, world)
+            proj = O.project_execute(O.filter_execute(shard, queries.Q1_PRED), queries.Q1_EXPRS)
+            parity[key] = "rank-0 shard partial: " + check(result, O.aggregate_execute(proj, queries.Q1_KEYS,
+                                                                                        queries._Q1_PARTIAL_AGGS))
+            del shard, proj
+        oracle.drop()
 
     cpu = None
     if rank == 0 and world == 1:
@@ -443,7 +548,7 @@ def run_tq(args, world, rank, local):
                "sample": f"oracle Q1 on lineitem SF1 ({srows} rows), median of 3, {nthreads} threads"}
 
     del li, scan
-    suite = run_suite(args, ctx, world, rank, stream) if args.suite else None
+    suite = run_suite(args, ctx, world, rank, stream, oracle, parity) if args.suite else None
     if rank != 0:
         ctx.close()
         return
@@ -462,6 +567,7 @@ def run_tq(args, world, rank, local):
         "warmup": args.warmup,
         "ms_per_step": ms_max,
         "ms_per_step_by_rank": ms_ranks,
+        "parity": parity,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -487,7 +593,6 @@ def run_tq(args, world, rank, local):
         "gpu_launches": launches,
         "kernels_ms": {k: v[1] / max(1, v[0]) for k, v in prof.items()},
         "clocks": ck,
-        "parity": parity,
         "jit": ctx.jit_report(),
         "suite": suite,
     }

@@ -42,6 +42,15 @@ typedef struct tq_engine_opts {
   double low_watermark;         /* 0.70 */
   uint32_t protect_top_k;       /* 8 */
   uint32_t tables_on_host;      /* 1 = scan inputs start in the Host tier (config 5) */
+  uint32_t task_batches;        /* input batches per Filter/Project/Probe task (default 1); a task with
+                                   more than one is splittable by on_oom */
+  /* test-only fault injection: the first inject_oom_count tasks of the operator
+   * named inject_oom_op fail with ReservationExceeded before executing.
+   * mode 1: the estimate then doubles as usual; mode 2: the estimate is first
+   * raised to the Device capacity (the doubled one cannot fit: split / abort). */
+  uint32_t inject_oom_mode;
+  uint32_t inject_oom_count;
+  char inject_oom_op[32];
 } tq_engine_opts;
 
 /* Input tables: tables[t] (t = 0 orders, 1 lineitem, 2 customer, 3 supplier,
@@ -54,6 +63,13 @@ typedef struct tq_engine_opts {
  * a JSON object of executor metrics. */
 tq_status tq_engine_run_query(tq_ctx* ctx, tq_comm* comm, int query, const tq_batch* tables,
                               const tq_engine_opts* opts, tq_batch* result, char* metrics_json, uint64_t cap);
+
+/* on_oom: the estimate doubles (*new_estimate); a task
+ * whose doubled estimate fits the Device capacity (0 = unbounded) is retried,
+ * else a splittable task (> 1 input batch) is split into two halves, else the
+ * query aborts with OutOfMemoryUnsplittable. */
+enum { TQ_OOM_RETRY = 0, TQ_OOM_SPLIT = 1, TQ_OOM_ABORT = 2 };
+int tq_on_oom_decide(uint64_t estimate, uint64_t capacity, int splittable, uint64_t* new_estimate);
 
 /* max(ema_peak, ema_ratio*input) * safety, or multiplier *
  * input without history; never below input_bytes. */

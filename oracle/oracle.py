@@ -65,6 +65,7 @@ def lib():
         L.tqo_table_rows.restype = C.c_uint64
         L.tqo_table_rows.argtypes = [C.c_int, C.c_double]
         L.tqo_datagen.argtypes = [C.c_int, C.c_double, C.c_uint32, P(TqBatchC)]
+        L.tqo_datagen_shard.argtypes = [C.c_int, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32, P(TqBatchC)]
         L.tqo_query.argtypes = [C.c_int, P(TqBatchC), C.c_uint32, P(TqBatchC)]
         L.tqo_batch_free.argtypes = [P(TqBatchC)]
         _lib = L
@@ -203,8 +204,10 @@ def table_rows(t: int, sf: float) -> int:
     return lib().tqo_table_rows(t, sf)
 
 
-def datagen(t: int, sf: float, nthreads: int = 8) -> HostBatch:
+def datagen(t: int, sf: float, nthreads: int = 8, shard: int = 0, nshards: int = 1) -> HostBatch:
     L, out = lib(), TqBatchC()
+    if nshards > 1:
+        return _out(L, L.tqo_datagen_shard(t, sf, shard, nshards, nthreads, C.byref(out)), out)
     return _out(L, L.tqo_datagen(t, sf, nthreads, C.byref(out)), out)
 
 

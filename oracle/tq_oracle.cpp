@@ -1070,32 +1070,41 @@ uint64_t table_rows(int t, double sf) {
   fail(TQ_INVALID_PLAN, "unknown table");
 }
 
-OBatch datagen(int t, double sf, uint32_t nthreads) {
+// A worker's row-group subset (GPU tq_datagen_shard, datagen.cu): rows
+// [n * shard / nshards, n * (shard + 1) / nshards) of the full table, values
+// equal to the full table's rows; lineitem = the lines of those orders.
+OBatch datagen(int t, double sf, uint32_t nthreads, uint32_t shard = 0, uint32_t nshards = 1) {
   OBatch b;
+  if (nshards == 0 || shard >= nshards) fail(TQ_INVALID_PLAN, "bad shard");
   uint64_t nc = n_customer(sf), ns = n_supplier(sf), np = n_part(sf), no = n_orders(sf);
+  auto lo_of = [&](uint64_t n) { return n * shard / nshards; };
+  auto hi_of = [&](uint64_t n) { return n * (shard + 1) / nshards; };
   switch (t) {
     case TQ_T_ORDERS: {
-      b.rows = no;
-      b.cols = {mk_col(TQ_INT64, no), mk_col(TQ_INT64, no), mk_col(TQ_INT64, no), mk_col(TQ_INT64, no),
-                mk_col(TQ_INT64, no)};
+      const uint64_t lo = lo_of(no), n = hi_of(no) - lo;
+      b.rows = n;
+      b.cols = {mk_col(TQ_INT64, n), mk_col(TQ_INT64, n), mk_col(TQ_INT64, n), mk_col(TQ_INT64, n),
+                mk_col(TQ_INT64, n)};
       uint64_t s1 = col_seed("orders.o_custkey"), s2 = col_seed("orders.o_orderdate");
-      parallel_chunks(no, nthreads, kMorsel, [&](uint32_t, uint64_t r0, uint64_t r1) {
-        for (uint64_t i = r0; i < r1; ++i) {
+      parallel_chunks(n, nthreads, kMorsel, [&](uint32_t, uint64_t r0, uint64_t r1) {
+        for (uint64_t r = r0; r < r1; ++r) {
+          const uint64_t i = lo + r;
           int64_t od = 8035 + int64_t(U(s2, i, 2406));
-          put64(b.cols[0], i, int64_t(i + 1));
-          put64(b.cols[1], i, 1 + int64_t(U(s1, i, nc)));
-          put64(b.cols[2], i, od);
-          put64(b.cols[3], i, 0);
-          put64(b.cols[4], i, year_of(od));
+          put64(b.cols[0], r, int64_t(i + 1));
+          put64(b.cols[1], r, 1 + int64_t(U(s1, i, nc)));
+          put64(b.cols[2], r, od);
+          put64(b.cols[3], r, 0);
+          put64(b.cols[4], r, year_of(od));
         }
       });
       return b;
     }
     case TQ_T_LINEITEM: {
       uint64_t sl = col_seed("orders.o_nlines"), sod = col_seed("orders.o_orderdate");
+      const uint64_t olo = lo_of(no), ohi = hi_of(no);
       std::vector<uint64_t> off(no + 1, 0);
       for (uint64_t i = 0; i < no; ++i) off[i + 1] = off[i] + 1 + U(sl, i, 7);
-      uint64_t nl = off[no];
+      const uint64_t base = off[olo], nl = off[ohi] - base;
       b.rows = nl;
       for (int c = 0; c < 3; ++c) b.cols.push_back(mk_col(TQ_INT64, nl));
       for (int c = 0; c < 4; ++c) b.cols.push_back(mk_col(TQ_DECIMAL, nl, 11, 2));
@@ -1104,85 +1113,94 @@ OBatch datagen(int t, double sf, uint32_t nthreads) {
                sq = col_seed("lineitem.l_quantity"), sd = col_seed("lineitem.l_discount"),
                st = col_seed("lineitem.l_tax"), srd = col_seed("lineitem.l_receiptdate"),
                srf = col_seed("lineitem.l_returnflag"), ssd = col_seed("lineitem.l_shipdate");
-      parallel_chunks(no, nthreads, 1 << 14, [&](uint32_t, uint64_t o0, uint64_t o1) {
-        for (uint64_t o = o0; o < o1; ++o) {
+      parallel_chunks(ohi - olo, nthreads, 1 << 14, [&](uint32_t, uint64_t o0, uint64_t o1) {
+        for (uint64_t o = olo + o0; o < olo + o1; ++o) {
           int64_t od = 8035 + int64_t(U(sod, o, 2406));
           for (uint64_t r = off[o]; r < off[o + 1]; ++r) {
+            const uint64_t w = r - base;  // row within the shard
             int64_t pk = 1 + int64_t(U(sp, r, np));
             int64_t sk = ps_supp(pk, int64_t(U(ss, r, 4)), int64_t(ns));
             int64_t qty = 1 + int64_t(U(sq, r, 50));
             int64_t ship = od + 1 + int64_t(U(ssd, r, 121));
             int64_t receipt = ship + 1 + int64_t(U(srd, r, 30));
             int64_t rf = receipt <= 9298 ? (U(srf, r, 2) == 0 ? 'R' : 'A') : 'N';
-            put64(b.cols[0], r, int64_t(o + 1));
-            put64(b.cols[1], r, pk);
-            put64(b.cols[2], r, sk);
-            putdec(b.cols[3], r, (i128)qty * 100);
-            putdec(b.cols[4], r, (i128)qty * retail_cents(pk));
-            putdec(b.cols[5], r, (i128)U(sd, r, 11));
-            putdec(b.cols[6], r, (i128)U(st, r, 9));
-            put64(b.cols[7], r, rf);
-            put64(b.cols[8], r, ship > 9298 ? 'O' : 'F');
-            put64(b.cols[9], r, ship);
+            put64(b.cols[0], w, int64_t(o + 1));
+            put64(b.cols[1], w, pk);
+            put64(b.cols[2], w, sk);
+            putdec(b.cols[3], w, (i128)qty * 100);
+            putdec(b.cols[4], w, (i128)qty * retail_cents(pk));
+            putdec(b.cols[5], w, (i128)U(sd, r, 11));
+            putdec(b.cols[6], w, (i128)U(st, r, 9));
+            put64(b.cols[7], w, rf);
+            put64(b.cols[8], w, ship > 9298 ? 'O' : 'F');
+            put64(b.cols[9], w, ship);
           }
         }
       });
       return b;
     }
     case TQ_T_CUSTOMER: {
-      b.rows = nc;
-      b.cols = {mk_col(TQ_INT64, nc), mk_col(TQ_INT64, nc), mk_col(TQ_INT64, nc)};
+      const uint64_t lo = lo_of(nc), n = hi_of(nc) - lo;
+      b.rows = n;
+      b.cols = {mk_col(TQ_INT64, n), mk_col(TQ_INT64, n), mk_col(TQ_INT64, n)};
       uint64_t s1 = col_seed("customer.c_nationkey"), s2 = col_seed("customer.c_mktsegment");
-      for (uint64_t i = 0; i < nc; ++i) {
-        put64(b.cols[0], i, int64_t(i + 1));
-        put64(b.cols[1], i, int64_t(U(s1, i, 25)));
-        put64(b.cols[2], i, int64_t(U(s2, i, 5)));
+      for (uint64_t r = 0; r < n; ++r) {
+        const uint64_t i = lo + r;
+        put64(b.cols[0], r, int64_t(i + 1));
+        put64(b.cols[1], r, int64_t(U(s1, i, 25)));
+        put64(b.cols[2], r, int64_t(U(s2, i, 5)));
       }
       return b;
     }
     case TQ_T_SUPPLIER: {
-      b.rows = ns;
-      b.cols = {mk_col(TQ_INT64, ns), mk_col(TQ_INT64, ns)};
+      const uint64_t lo = lo_of(ns), n = hi_of(ns) - lo;
+      b.rows = n;
+      b.cols = {mk_col(TQ_INT64, n), mk_col(TQ_INT64, n)};
       uint64_t s1 = col_seed("supplier.s_nationkey");
-      for (uint64_t i = 0; i < ns; ++i) {
-        put64(b.cols[0], i, int64_t(i + 1));
-        put64(b.cols[1], i, int64_t(U(s1, i, 25)));
+      for (uint64_t r = 0; r < n; ++r) {
+        const uint64_t i = lo + r;
+        put64(b.cols[0], r, int64_t(i + 1));
+        put64(b.cols[1], r, int64_t(U(s1, i, 25)));
       }
       return b;
     }
     case TQ_T_PART: {
-      b.rows = np;
-      b.cols = {mk_col(TQ_INT64, np), mk_col(TQ_INT64, np)};
+      const uint64_t lo = lo_of(np), n = hi_of(np) - lo;
+      b.rows = n;
+      b.cols = {mk_col(TQ_INT64, n), mk_col(TQ_INT64, n)};
       uint64_t s1 = col_seed("part.p_color");
-      for (uint64_t i = 0; i < np; ++i) {
-        put64(b.cols[0], i, int64_t(i + 1));
-        put64(b.cols[1], i, int64_t(U(s1, i, 1000)));
+      for (uint64_t r = 0; r < n; ++r) {
+        const uint64_t i = lo + r;
+        put64(b.cols[0], r, int64_t(i + 1));
+        put64(b.cols[1], r, int64_t(U(s1, i, 1000)));
       }
       return b;
     }
     case TQ_T_PARTSUPP: {
-      uint64_t n = 4 * np;
+      const uint64_t lo = lo_of(4 * np), n = hi_of(4 * np) - lo;
       b.rows = n;
       b.cols = {mk_col(TQ_INT64, n), mk_col(TQ_INT64, n), mk_col(TQ_DECIMAL, n, 11, 2)};
       uint64_t s1 = col_seed("partsupp.ps_supplycost");
-      for (uint64_t i = 0; i < n; ++i) {
+      for (uint64_t r = 0; r < n; ++r) {
+        const uint64_t i = lo + r;
         int64_t p = int64_t(i / 4) + 1;
-        put64(b.cols[0], i, p);
-        put64(b.cols[1], i, ps_supp(p, int64_t(i % 4), int64_t(ns)));
-        putdec(b.cols[2], i, (i128)(100 + U(s1, i, 99901)));
+        put64(b.cols[0], r, p);
+        put64(b.cols[1], r, ps_supp(p, int64_t(i % 4), int64_t(ns)));
+        putdec(b.cols[2], r, (i128)(100 + U(s1, i, 99901)));
       }
       return b;
     }
-    case TQ_T_NATION: {
-      b.rows = 25;
-      b.cols = {mk_col(TQ_INT64, 25), mk_col(TQ_INT64, 25)};
-      for (uint64_t i = 0; i < 25; ++i) { put64(b.cols[0], i, int64_t(i)); put64(b.cols[1], i, kNationRegion[i]); }
-      return b;
-    }
+    case TQ_T_NATION:
     case TQ_T_REGION: {
-      b.rows = 5;
-      b.cols = {mk_col(TQ_INT64, 5), mk_col(TQ_INT64, 5)};
-      for (uint64_t i = 0; i < 5; ++i) { put64(b.cols[0], i, int64_t(i)); put64(b.cols[1], i, int64_t(i)); }
+      const uint64_t total = t == TQ_T_NATION ? 25 : 5;
+      const uint64_t lo = lo_of(total), n = hi_of(total) - lo;
+      b.rows = n;
+      b.cols = {mk_col(TQ_INT64, n), mk_col(TQ_INT64, n)};
+      for (uint64_t r = 0; r < n; ++r) {
+        const uint64_t i = lo + r;
+        put64(b.cols[0], r, int64_t(i));
+        put64(b.cols[1], r, t == TQ_T_NATION ? kNationRegion[i] : int64_t(i));
+      }
       return b;
     }
   }
@@ -1417,6 +1435,10 @@ uint64_t tqo_table_rows(int table, double sf) {
 }
 tq_status tqo_datagen(int table, double sf, uint32_t nthreads, tq_batch* out) {
   return guard([&] { export_batch(datagen(table, sf, nthreads), out); });
+}
+
+tq_status tqo_datagen_shard(int table, double sf, uint32_t shard, uint32_t nshards, uint32_t nthreads, tq_batch* out) {
+  return guard([&] { export_batch(datagen(table, sf, nthreads, shard, nshards), out); });
 }
 tq_status tqo_query(int q, const tq_batch* tables, uint32_t nthreads, tq_batch* out) {
   return guard([&] { export_batch(query(q, tables, nthreads), out); });

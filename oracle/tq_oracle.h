@@ -64,6 +64,8 @@ enum {
 };
 uint64_t tqo_table_rows(int table, double sf);
 tq_status tqo_datagen(int table, double sf, uint32_t nthreads, tq_batch* out);
+// A worker's row-group subset, equal to the GPU's tq_datagen_shard (datagen.cu).
+tq_status tqo_datagen_shard(int table, double sf, uint32_t shard, uint32_t nshards, uint32_t nthreads, tq_batch* out);
 
 /* whole queries.  tables[] is indexed by TQ_T_*; only the
  * tables the query reads must be set.  nthreads=1 → single-threaded oracle;

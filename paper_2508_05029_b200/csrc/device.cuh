@@ -215,6 +215,18 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, u32 bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// Acquire loads of a publication word (GPU scope, global / CTA scope, shared).
+__device__ __forceinline__ u32 ld_acquire_gpu(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u32 ld_acquire_cta_shared(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ u32 lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ u32 lanemask_lt() {
   u32 m;

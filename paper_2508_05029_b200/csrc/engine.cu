@@ -50,6 +50,7 @@ struct Handle {
   uint64_t bytes = 0;
   int pins = 0;
   bool view = false;  // borrows an input table's device memory: never freed or spilled
+  bool spilling = false;  // chosen as a spill victim (under rt->mu); the copy runs outside it
   tq_batch dev{};
   tq_chunked* host = nullptr;
   std::mutex mu;
@@ -158,10 +159,14 @@ class Runtime {
       h->host = nullptr;
     }
   }
-  // Device -> Host; caller ensures h is unpinned
+  // Device -> Host.  Runs WITHOUT rt->mu: the victim was
+  // chosen and marked (spilling, pinned) under it by pick_victims, so no task
+  // uses it meanwhile; a task that later wants it waits on h->mu and then
+  // finds it in the Host tier (load_to_device).  The D2H copies go on the
+  // memory executor's copy stream; only the spilling thread waits for them.
   bool spill(HP h) {
     std::lock_guard<std::mutex> g(h->mu);
-    if (h->tier != DEVICE || h->view || h->pins > 0 || !h->dev.cols) return false;
+    if (h->tier != DEVICE || h->view || !h->dev.cols) return false;
     tq_chunked* cb = nullptr;
     if (tq_spill(ctx, pool, &h->dev, &cb, copy_stream) != TQ_OK) return false;  // PoolExhausted: keep on Device
     cudaStreamSynchronize(copy_stream);
@@ -190,8 +195,14 @@ class Runtime {
   // spill unpinned Device handles, farthest from execution first, until `need`
   // more bytes fit under the capacity; protects the top-K queued tasks' inputs
   // (select_spill_victims).  Caller holds mu.
-  bool make_room(uint64_t need, uint64_t limit);
-  void watermark_tick();  // SPEC.md:304-312
+  // Choose spill victims so that `need` more bytes fit under `limit`; marks
+  // them (spilling + pinned) and returns them.  Caller holds mu.
+  std::vector<HP> pick_victims(uint64_t need, uint64_t limit);
+  // Spill the victims (caller does NOT hold mu), then unmark them.
+  void spill_victims(std::vector<HP>& v);
+  // High watermark: queue victims down to the low watermark
+  // for the memory executor thread.  Caller holds mu.
+  void watermark_tick();
   void submit(Task t) {
     t.seq = ++next_seq;
     queue.push_back(std::move(t));
@@ -229,13 +240,16 @@ class Runtime {
   int exchange_turn = 0;  // collectives run in DAG order on every worker
   // metrics
   std::atomic<uint64_t> m_tasks{0}, m_retries{0}, m_splits{0}, m_spills{0}, m_spill_bytes{0}, m_loads{0},
-      m_preloads{0}, m_load_bytes{0}, m_peak{0};
+      m_preloads{0}, m_load_bytes{0}, m_peak{0}, m_injected{0};
+  uint64_t spilling_bytes = 0;           // Device bytes of marked victims not yet freed (under mu)
+  std::deque<std::vector<HP>> spill_q;   // watermark spills for the memory executor (under mu)
   std::vector<HP> keep;  // handles alive until the query ends (build sides)
   std::vector<tq_batch> results;
 
  private:
   void worker(int idx);
   void preloader();
+  void memory_executor();
   void run_task(Task& t, cudaStream_t st);
   bool pick(Task& t);
 };
@@ -256,24 +270,43 @@ void Holder::close() {
   rt_->notify();
 }
 
-bool Runtime::make_room(uint64_t need, uint64_t limit) {
+std::vector<HP> Runtime::pick_victims(uint64_t need, uint64_t limit) {
+  std::vector<HP> out;
+  auto projected = [&] { return device_in_use() - std::min(device_in_use(), spilling_bytes); };
+  if (projected() + need <= limit) return out;
   std::set<Handle*> protect;
   std::vector<const Task*> top;
   for (const Task& t : queue) top.push_back(&t);
   std::sort(top.begin(), top.end(), [](const Task* a, const Task* b) { return a->seq < b->seq; });
   for (size_t i = 0; i < top.size() && i < opts.protect_top_k; ++i)
     for (const HP& h : top[i]->inputs) protect.insert(h.get());
-  // candidates: queued-in-holder handles, deepest plan position first, newest first
+  // candidates (select_spill_victims): unpinned Device
+  // handles not feeding the top-K queued tasks, newest (deepest) first
   std::vector<HP> cand;
   for (auto& w : registry)
     if (HP h = w.lock())
-      if (h->tier == DEVICE && !h->view && h->pins == 0 && !protect.count(h.get())) cand.push_back(h);
+      if (h->tier == DEVICE && !h->view && !h->spilling && h->pins == 0 && h->dev.cols && !protect.count(h.get()))
+        cand.push_back(h);
   std::sort(cand.begin(), cand.end(), [](const HP& a, const HP& b) { return a->id > b->id; });
   for (HP& h : cand) {
-    if (device_in_use() + need <= limit) return true;
-    spill(h);
+    if (projected() + need <= limit) break;
+    h->spilling = true;
+    h->pins++;
+    spilling_bytes += h->bytes;
+    out.push_back(h);
   }
-  return device_in_use() + need <= limit;
+  return out;
+}
+
+void Runtime::spill_victims(std::vector<HP>& v) {
+  for (HP& h : v) spill(h);
+  std::lock_guard<std::mutex> g(mu);
+  for (HP& h : v) {
+    h->spilling = false;
+    h->pins--;
+    spilling_bytes -= std::min(spilling_bytes, h->bytes);
+  }
+  cv.notify_all();
 }
 
 void Runtime::watermark_tick() {
@@ -281,8 +314,29 @@ void Runtime::watermark_tick() {
   uint64_t use = device_in_use();
   m_peak = std::max<uint64_t>(m_peak.load(), use);
   if (use >= (uint64_t)(opts.high_watermark * capacity)) {
-    uint64_t low = (uint64_t)(opts.low_watermark * capacity);
-    make_room(0, low);
+    std::vector<HP> v = pick_victims(0, (uint64_t)(opts.low_watermark * capacity));
+    if (!v.empty()) {
+      spill_q.push_back(std::move(v));
+      cv.notify_all();
+    }
+  }
+}
+
+// Memory executor (one thread): performs the watermark
+// spills queued by BatchHolder pushes, so the pushing compute thread and
+// everyone waiting on rt->mu keep running while the D2H copies proceed.
+void Runtime::memory_executor() {
+  cudaSetDevice(ctx->device);
+  for (;;) {
+    std::vector<HP> v;
+    {
+      std::unique_lock<std::mutex> g(mu);
+      cv.wait(g, [&] { return stop || !spill_q.empty(); });
+      if (spill_q.empty()) break;  // stop
+      v = std::move(spill_q.front());
+      spill_q.pop_front();
+    }
+    spill_victims(v);
   }
 }
 
@@ -321,8 +375,14 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
     std::unique_lock<std::mutex> g(mu);
     if (capacity) {
       while (device_in_use() + reserved + want > capacity) {
-        if (make_room(reserved + want, capacity)) break;
-        if (executing == 0) break;  // nobody can free memory: try it, on_oom on failure
+        std::vector<HP> v = pick_victims(reserved + want, capacity);
+        if (!v.empty()) {  // spill outside the lock, then re-check
+          g.unlock();
+          spill_victims(v);
+          g.lock();
+          continue;
+        }
+        if (executing == 0 && spilling_bytes == 0) break;  // nobody can free memory: try it, on_oom on failure
         cv.wait_for(g, std::chrono::milliseconds(2));
       }
     }
@@ -340,24 +400,37 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
   const uint64_t before = device_in_use();
   auto t0 = Clock::now();
   try {
+    // test-only fault injection (tq_engine_opts.inject_oom_*): the named
+    // operator's next tasks fail with ReservationExceeded before executing
+    if (opts.inject_oom_count && op->name == opts.inject_oom_op &&
+        m_injected.fetch_add(1) < opts.inject_oom_count) {
+      if (opts.inject_oom_mode == 2) t.estimate = std::max<uint64_t>(t.estimate, capacity);  // oversize
+      fail(TQ_RESERVATION_EXCEEDED, op->name + ": injected");
+    }
     for (HP& h : t.inputs) load(h, st, false);  // load_to_device
-    op->run(t, st);                             // execute + deposit
+    op->run(t, st);                             // execute + deposit (all-or-nothing per task)
     cudaStreamSynchronize(st);
   } catch (const Fail& f) {
     release();
     if (f.status == TQ_RESERVATION_EXCEEDED) {  // on_oom
+      uint64_t est = 0;
+      const int action = tq_on_oom_decide(t.estimate, capacity, op->splittable(t) ? 1 : 0, &est);
+      std::vector<HP> v;
+      {
+        std::lock_guard<std::mutex> g(mu);
+        // the Device may be full of other operators' data: spill what we can
+        if (capacity) v = pick_victims(capacity, capacity);
+      }
+      spill_victims(v);
       std::lock_guard<std::mutex> g(mu);
-      Task r = t;
-      r.estimate = t.estimate * 2;
-      // the Device may be full of other operators' data: spill what we can first
-      make_room(capacity, capacity);
-      if (r.estimate > capacity && t.attempt <= 3 && executing > 0) r.estimate = capacity;  // wait for others
-      if (capacity == 0 || r.estimate <= capacity) {
+      if (action == TQ_OOM_RETRY) {
+        Task r = t;
+        r.estimate = est;
         r.attempt++;
         m_retries++;
         op->running++;
         submit(std::move(r));
-      } else if (op->splittable(t)) {
+      } else if (action == TQ_OOM_SPLIT) {
         op->running += 2;
         m_splits++;
         Task a = t, b = t;
@@ -463,6 +536,7 @@ void Runtime::run() {
   std::vector<std::thread> threads;
   for (uint32_t i = 0; i < std::max<uint32_t>(1, opts.compute_threads); ++i) threads.emplace_back(&Runtime::worker, this, i);
   if (opts.preload) threads.emplace_back(&Runtime::preloader, this);
+  threads.emplace_back(&Runtime::memory_executor, this);
   // coordinator: poll operators for runnable tasks until every operator finished
   {
     std::unique_lock<std::mutex> g(mu);
@@ -579,36 +653,61 @@ class ScanOp : public Op {
   std::vector<HP> out_q, pending;
 };
 
-// Filter -> Project (one fused GPU pipeline per input batch)
+// Filter -> Project (one fused GPU pipeline per input batch).  A task takes up
+// to opts.task_batches batches; its outputs are deposited only after every
+// input succeeded (a failed task can be retried or split without duplicates).
+void run_all_or_nothing(Runtime* rt, Op* op, Task& t, cudaStream_t st,
+                        const std::function<void(const tq_batch&, tq_batch&)>& body) {
+  std::vector<tq_batch> outs;
+  try {
+    for (HP& h : t.inputs) {
+      tq_batch o{};
+      body(h->dev, o);
+      outs.push_back(o);
+    }
+    cudaStreamSynchronize(st);
+  } catch (...) {
+    cudaStreamSynchronize(st);
+    for (tq_batch& o : outs) tq_batch_free(rt->ctx, &o);
+    throw;
+  }
+  for (tq_batch& o : outs) {
+    op->stat.rows_out += o.rows;
+    op->out->push(rt->adopt(o, false));
+  }
+  for (HP& h : t.inputs)
+    if (!h->view) rt->free_handle(h);
+}
+
+void poll_batches(Runtime* rt, Op* op, Holder* in, std::vector<Task>& ts) {
+  const size_t k = std::max<uint32_t>(1, rt->opts.task_batches);
+  while (!in->empty()) {
+    Task t;
+    t.op = op;
+    while (!in->empty() && t.inputs.size() < k) t.inputs.push_back(in->pop());
+    ts.push_back(std::move(t));
+  }
+}
+
 class PipeOp : public Op {
  public:
   PipeOp(Runtime* rt, std::string n, int depth, Holder* in, EB* pred, std::vector<EB> exprs)
       : Op(rt, std::move(n), depth, 2.0), in(in), pred(pred ? *pred : EB()), has_pred(pred), exprs(std::move(exprs)) {}
   void poll(std::vector<Task>& ts) override {
-    while (!in->empty()) {
-      Task t;
-      t.op = this;
-      t.inputs.push_back(in->pop());
-      ts.push_back(std::move(t));
-    }
+    poll_batches(rt, this, in, ts);
     if (in->closed() && in->empty() && running == 0 && ts.empty()) {
       finished = true;
       closing = true;
     }
   }
   void run(Task& t, cudaStream_t st) override {
-    for (HP& h : t.inputs) {
-      std::vector<tq_expr> ex;
-      for (auto& e : exprs) ex.push_back(e.e());
-      tq_expr pe = pred.e();
-      tq_batch o{};
-      check(tq_pipeline_materialize(rt->ctx, &h->dev, has_pred ? &pe : nullptr, ex.empty() ? nullptr : ex.data(),
+    std::vector<tq_expr> ex;
+    for (auto& e : exprs) ex.push_back(e.e());
+    tq_expr pe = pred.e();
+    run_all_or_nothing(rt, this, t, st, [&](const tq_batch& b, tq_batch& o) {
+      check(tq_pipeline_materialize(rt->ctx, &b, has_pred ? &pe : nullptr, ex.empty() ? nullptr : ex.data(),
                                     (uint32_t)ex.size(), &o, st));
-      cudaStreamSynchronize(st);
-      stat.rows_out += o.rows;
-      out->push(rt->adopt(o, false));
-      if (!h->view) rt->free_handle(h);
-    }
+    });
   }
   Holder* in;
   EB pred;
@@ -683,30 +782,20 @@ class ProbeOp : public Op {
         exprs(std::move(exprs)), keys(std::move(keys)), build_cols(std::move(build_cols)) {}
   void poll(std::vector<Task>& ts) override {
     if (!b->ready) return;
-    while (!in->empty()) {
-      Task t;
-      t.op = this;
-      t.inputs.push_back(in->pop());
-      ts.push_back(std::move(t));
-    }
+    poll_batches(rt, this, in, ts);
     if (in->closed() && in->empty() && running == 0 && ts.empty()) finished = true;
   }
   void run(Task& t, cudaStream_t st) override {
-    for (HP& h : t.inputs) {
-      std::vector<tq_expr> ex;
-      for (auto& e : exprs) ex.push_back(e.e());
-      tq_expr pe = pred.e();
-      tq_batch o{};
-      static const uint32_t none = 0;  // NULL build_cols would mean "all build columns"
-      const uint32_t* bcols = build_cols.empty() ? &none : build_cols.data();
-      check(tq_pipeline_probe(rt->ctx, b->table, &h->dev, has_pred ? &pe : nullptr, ex.empty() ? nullptr : ex.data(),
+    std::vector<tq_expr> ex;
+    for (auto& e : exprs) ex.push_back(e.e());
+    tq_expr pe = pred.e();
+    static const uint32_t none = 0;  // NULL build_cols would mean "all build columns"
+    const uint32_t* bcols = build_cols.empty() ? &none : build_cols.data();
+    run_all_or_nothing(rt, this, t, st, [&](const tq_batch& in_b, tq_batch& o) {
+      check(tq_pipeline_probe(rt->ctx, b->table, &in_b, has_pred ? &pe : nullptr, ex.empty() ? nullptr : ex.data(),
                               (uint32_t)ex.size(), keys.data(), (uint32_t)keys.size(), bcols,
                               (uint32_t)build_cols.size(), &o, st));
-      cudaStreamSynchronize(st);
-      stat.rows_out += o.rows;
-      out->push(rt->adopt(o, false));
-      if (!h->view) rt->free_handle(h);
-    }
+    });
   }
   BuildOp* b;
   Holder* in;
@@ -1014,6 +1103,15 @@ uint64_t tq_estimate_reservation(uint64_t samples, double ema_peak, double ema_r
   return std::max<uint64_t>((uint64_t)est, input_bytes);
 }
 
+int tq_on_oom_decide(uint64_t estimate, uint64_t capacity, int splittable, uint64_t* new_estimate) {
+  // double the estimate; retry while it fits the Device
+  // capacity (0 = unbounded), else split a splittable task, else abort
+  const uint64_t e = std::max<uint64_t>(1, estimate) * 2;
+  if (new_estimate) *new_estimate = e;
+  if (capacity == 0 || e <= capacity) return TQ_OOM_RETRY;
+  return splittable ? TQ_OOM_SPLIT : TQ_OOM_ABORT;
+}
+
 tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batch* tables, const tq_engine_opts* o,
                               tq_batch* result, char* metrics_json, uint64_t cap) {
   return guard([&] {
@@ -1041,6 +1139,10 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
     rt.setup();
     int nranks = 1;
     if (comm) nranks = tq_comm_size(comm);
+    // a plan without a distributed form must not run as one worker of N: it
+    // would silently join / aggregate only this rank's shard
+    if (nranks > 1 && query != 3)
+      fail(TQ_INVALID_PLAN, "query " + std::to_string(query) + " has no distributed plan");
     Plan P{&rt, tables};
     Holder* res = build_plan(P, query);
     SinkOp* sink = rt.op<SinkOp>(res);

@@ -92,11 +92,8 @@ struct tq_comm {
   uint64_t win_bytes = 0;
   std::vector<uint8_t*> win_peer;  // [n]; win_peer[rank] == win
   uint64_t win_cap_rows = 0;       // capacity (rows) of the last fused exchange (identical on every rank)
-  // the window is used as two halves, alternating per fused exchange (epoch
-  // parity); a half whose control block was reset at the end of its previous
-  // use needs no "reset before anyone writes" barrier on its next use
+  // the window is used as two halves, alternating per fused exchange (epoch parity)
   uint64_t epoch = 0;
-  bool half_ready[2] = {false, false};
 };
 
 using namespace tq;
@@ -109,7 +106,6 @@ int comm_rank(tq_comm* cm) { return cm->rank; }
 int comm_size(tq_comm* cm) { return cm->n; }
 uint64_t& comm_last_cap(tq_comm* cm) { return cm->win_cap_rows; }
 uint64_t& comm_epoch(tq_comm* cm) { return cm->epoch; }
-bool& comm_half_ready(tq_comm* cm, int half) { return cm->half_ready[half & 1]; }
 void comm_add_sent(tq_comm* cm, uint64_t bytes) { cm->sent += bytes; }
 
 void comm_allgather_u64(tq_comm* cm, const unsigned long long* dev_in, unsigned long long* dev_out, uint64_t count, cudaStream_t st) {
@@ -156,7 +152,6 @@ PeerView peer_window(tq_comm* cm, uint64_t bytes, cudaStream_t st, bool agreed) 
     if (cm->win) cudaFree(cm->win);
     cm->win = nullptr;
     cm->win_peer.assign(n, nullptr);
-    cm->half_ready[0] = cm->half_ready[1] = false;  // a new window: both halves reset on first use
     const u64 alloc = round_up(std::max<u64>(bytes, 1ull << 20) * 5 / 4, 1ull << 21);
     TQ_CUDA(cudaMalloc(&cm->win, alloc));  // plain cudaMalloc: exportable with cudaIpcGetMemHandle
     cm->win_bytes = alloc;

@@ -253,7 +253,7 @@ __device__ __forceinline__ bool key_words(const WCtx& w, int v, u64* kw) {
 }
 
 // ------------------------------------------------------------------ emit helpers
-__device__ __forceinline__ void store_out(const OutCol& o, u64 pos, const WCtx& w, int v, long long brow) {
+__device__ __forceinline__ void store_out(const OutCol& o, u64 pos, const WCtx& w, int v, long long brow, bool vbit) {
   bool valid = true;
   uint8_t* dst = o.values + w.out_delta;
   if (o.src == OUT_BUILD) {
@@ -299,7 +299,7 @@ __device__ __forceinline__ void store_out(const OutCol& o, u64 pos, const WCtx& 
       }
     }
   }
-  if (o.validity && valid) bm_set_atomic(o.validity + w.out_delta, pos);
+  if (o.validity && vbit && valid) bm_set_atomic(o.validity + w.out_delta, pos);
 }
 
 
@@ -351,7 +351,7 @@ struct InterpP {
   }
   __device__ __forceinline__ static void store(const WCtx& w, int v, u64 pos, long long brow, const Raw&) {
     const PipeParams& p = *w.p;
-    for (u32 c = 0; c < p.nout; ++c) store_out(p.out[c], pos, w, v, brow);
+    for (u32 c = 0; c < p.nout; ++c) store_out(p.out[c], pos, w, v, brow, (w.vmask >> c) & 1u);
   }
 };
 

@@ -455,7 +455,8 @@ struct Gen {
               os << "    *(u64*)(" << oc << ".values + w.out_delta + pos * 8) = lo64(" << e << ");\n";
           }
         }
-        if (o.validity) os << "    set_valid(" << oc << ", pos, " << valid << ", w.out_delta);\n";
+        if (o.validity)
+          os << "    if ((w.vmask >> " << c << ") & 1u) set_valid(" << oc << ", pos, " << valid << ", w.out_delta);\n";
       }
     } else {
       os << "    (void)r; (void)p; (void)pos; (void)brow;\n";

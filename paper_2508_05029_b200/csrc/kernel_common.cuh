@@ -34,6 +34,7 @@ struct WCtx {
   u32 nrows;             // rows in the tile
   u32 lane;
   long long out_delta;   // added to output addresses (DEST_PEER: the destination rank's window)
+  u32 vmask;             // output c writes validity bits iff bit c (DEST_PEER: the ranks' agreed mask)
 };
 
 __device__ __forceinline__ u32 trow(const WCtx& w, int v) { return w.row0 + (u32)v * 32u + w.lane; }
@@ -134,8 +135,8 @@ __device__ __forceinline__ long long local_find_insert(u32* state, u64* keys, u3
   const u32 mask = cap - 1;
   u32 s = (h >> 16) & mask;  // top bits of the multiplicative hash
   for (u32 probe = 0; probe < cap; ++probe) {
-    volatile u32* st = state + s;
-    u32 cur = *st;
+    // acquire: a published tag orders the key loads below after it
+    u32 cur = ld_acquire_cta_shared(state + s);
     if (cur == kStEmpty) {
       cur = atomicCAS(state + s, kStEmpty, kStBusy);
       if (cur == kStEmpty) {
@@ -144,8 +145,9 @@ __device__ __forceinline__ long long local_find_insert(u32* state, u64* keys, u3
         atomicExch(state + s, tag);
         return (long long)s;
       }
+      if (cur != kStBusy) cur = ld_acquire_cta_shared(state + s);  // the CAS saw a published tag
     }
-    while (cur == kStBusy) cur = *st;
+    while (cur == kStBusy) cur = ld_acquire_cta_shared(state + s);
     if (cur == tag) {
       const volatile u64* k = keys + s * kwa;
       bool eq = true;
@@ -177,22 +179,25 @@ __device__ __forceinline__ long long table_find_insert(u32* state, u64* keys, u6
   const u64 mask = cap - 1;
   u64 s = h & mask;
   for (u64 probe = 0; probe < limit; ++probe) {
-    volatile u32* st = state + s;
-    u32 cur = *st;
+    // every state read that can observe Ready is an acquire, so the key
+    // loads below are ordered after the publication they observed (a plain
+    // load seeing Ready could otherwise compare stale key words and insert
+    // the group twice)
+    u32 cur = ld_acquire_gpu(state + s);
     if (cur == kStEmpty) {
       cur = atomicCAS(state + s, kStEmpty, kStBusy);
       if (cur == kStEmpty) {
         for (u32 i = 0; i < kwa; ++i) keys[s * kwa + i] = kw[i];
         init(s);
         // publish: the key / accumulator stores are visible before the state
-        // (a full fence: readers compare keys with plain volatile loads)
         __threadfence();
         atomicExch(state + s, kStReady);
         if (counter) atomicAdd(counter, 1ull);
         return (long long)s;
       }
+      if (cur != kStBusy) cur = ld_acquire_gpu(state + s);  // the (relaxed) CAS saw Ready
     }
-    while (cur == kStBusy) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(state + s) : "memory");
+    while (cur == kStBusy) cur = ld_acquire_gpu(state + s);
     const volatile u64* k = keys + s * kwa;
     bool eq = true;
 #pragma unroll
@@ -586,6 +591,14 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   w.row0 = warp * 32 * kV;
   w.lane = lane;
   w.out_delta = 0;
+  w.vmask = 0xffffffffu;
+  if (SINK == SINK_EMIT && p.dest_kind == DEST_PEER && p.peer_vmask) {
+    // a column has a bitmap on the receivers iff any rank's input can be null
+    // there (concat rule, transform.cpp:63-68): OR of the all-gathered masks
+    u64 m = 0;
+    for (u32 r = 0; r < p.ndest; ++r) m |= __ldg(p.peer_vmask + r);
+    w.vmask = (u32)m;
+  }
 
   const u32 first = blockIdx.x, step = gridDim.x;
   u32 s = 0, ph = 0;

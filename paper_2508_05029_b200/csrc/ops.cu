@@ -27,6 +27,11 @@ struct tq_join_table {
   cudaStream_t stream;
   tq_batch build;                      // borrowed descriptors (cols copied)
   std::vector<uint8_t> key_cls, key_scale;
+  // a semi-only table is materialised at most once, under this lock; the
+  // replaced allocation may still be read by another probe's kernel on another
+  // stream, so it is retired and freed with the table
+  std::mutex mu;
+  std::vector<std::pair<uint8_t*, uint64_t>> retired;
 };
 
 namespace tq {
@@ -550,10 +555,12 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
 // A semi-only table whose bitmap turned out not exact (or keys not unique):
 // build the real hash table from the same input and program, in place.
 static void semi_table_materialize(tq_ctx* c, tq_join_table* t, cudaStream_t st) {
+  std::lock_guard<std::mutex> g(t->mu);
+  if (t->jt.entries != nullptr) return;  // another probe materialised it first
   tq_join_table* full = nullptr;
   Prog& P = *(Prog*)t->semi_prog.get();
   run_build(c, &t->build, P, t->semi_keys, &full, st, t->semi_bloom_keys, false);
-  dfree(c, t->mem, t->bytes, st);
+  t->retired.emplace_back(t->mem, t->bytes);
   std::free(t->build.cols);
   t->jt = full->jt;
   t->mem = full->mem;
@@ -794,6 +801,8 @@ two_pass:
 // mappings of the peers' windows over NVLink — the partitioned staging batch
 // and the NCCL payload copy of partition + tq_comm_exchange disappear.
 // Receivers then close the holes of the chunked layout and copy their rows out.
+__global__ void k_set_u64(u64* p, u64 v) { *p = v; }
+
 __global__ void k_tail_reset(u64* tails, u64 nslots) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < nslots; i += (u64)gridDim.x * blockDim.x) {
     tails[2 * i] = 0;
@@ -847,21 +856,35 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
   // window capacity (rows).  The data-region layout is a function of the
   // capacity, and the capacity a function of the window size, which every
   // rank holds identically (windows only grow collectively) -> no per-call
-  // agreement and no host sync.  The first exchange on a communicator agrees
-  // on a first size (all-gather of every rank's guess); a receiver whose
-  // counter passed the capacity makes every rank grow the window and re-run.
+  // agreement on the size and no host sync before the kernel.  The first
+  // exchange on a communicator agrees on a first size (all-gather of every
+  // rank's guess); a receiver whose counter passed the capacity makes every
+  // rank grow the window and re-run.
+  // Validity: whether output k can be null is a LOCAL property (this rank's
+  // input bitmaps; a 0-row input has none), so the layout reserves a bitmap
+  // for every column and the ranks' masks are all-gathered before the kernel;
+  // bits are written for the OR of the masks and the output carries a bitmap
+  // iff any rank's part can hold a null (concat rule, transform.cpp:63-68).
+  u64 vmask_local = 0;
+  for (size_t k = 0; k < outs.size(); ++k)
+    if (wv[k]) vmask_local |= 1ull << k;
   const u64 nslots = (u64)n * kMaxTailCtas;
   const u64 data0 = round_up(256 + nslots * 16, 256);
   auto layout_end = [&](u64 cap) {
     u64 end = data0;
     for (size_t k = 0; k < outs.size(); ++k) {
       end = round_up(end + cap * outs[k].width, 256);
-      if (wv[k]) end = round_up(end + (cap + 7) / 8, 256);
+      end = round_up(end + (cap + 7) / 8, 256);
     }
     return end;
   };
-  u64* scratch = (u64*)dalloc(c, 8 * (2 * n + 8), st);  // [0..n) allgather out, [n] in, [n+1..] sent counter
+  // scratch: [0, n) all-gathered counts, [n] this rank's count, [n+1] rows sent,
+  // [n+2] this rank's validity mask, [n+3, 2n+3) the all-gathered masks
+  const u64 scratch_words = 3 * (u64)n + 8;
+  u64* scratch = (u64*)dalloc(c, 8 * scratch_words, st);
   u64* sent_dev = scratch + n + 1;
+  u64* vmask_in = scratch + n + 2;
+  u64* vmask_all = scratch + n + 3;
   u64 cap = 0;
   if (comm_window_bytes(cm) == 0) {
     const bool filtered = P.has_pred || semi_words;
@@ -880,7 +903,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     // the largest capacity whose layout fits half of the current window
     const u64 win = comm_window_bytes(cm) / 2 / 256 * 256;
     u64 per_row8 = 0;  // bits per row
-    for (size_t k = 0; k < outs.size(); ++k) per_row8 += 8 * outs[k].width + (wv[k] ? 1 : 0);
+    for (size_t k = 0; k < outs.size(); ++k) per_row8 += 8 * outs[k].width + 1;
     const u64 slack = data0 + 2 * 256 * (outs.size() + 1);
     cap = win > slack ? (win - slack) * 8 / std::max<u64>(1, per_row8) : 0;
     while (cap > 0 && layout_end(cap) > win) cap -= std::max<u64>(1, cap / 1024);
@@ -900,10 +923,8 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     for (size_t k = 0; k < outs.size(); ++k) {
       voff[k] = end;
       end = round_up(end + cap * outs[k].width, 256);
-      if (wv[k]) {
-        boff[k] = end;
-        end = round_up(end + (cap + 7) / 8, 256);
-      }
+      boff[k] = end;
+      end = round_up(end + (cap + 7) / 8, 256);
     }
     TQ_HT("pex total attempt");
     PeerView v = [&] {
@@ -916,22 +937,19 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     u64* counter = (u64*)base;
     u64* tails = (u64*)(base + 256);
     TQ_CUDA(cudaMemsetAsync(sent_dev, 0, 8, st));
-    bool any_valid = false;
-    for (size_t k = 0; k < outs.size(); ++k) any_valid |= wv[k];
-    // this half's control block was reset at the end of its previous use,
-    // before a barrier every sender has passed since -> no reset barrier
-    // (bitmaps depend on the layout: exchanges with validity always reset)
-    const bool preset = attempt == 0 && comm_half_ready(cm, half) && !any_valid;
-    comm_half_ready(cm, half) = false;
-    if (!preset) {
-      TQ_CUDA(cudaMemsetAsync(counter, 0, 8, st));
-      k_tail_reset<<<(u32)std::min<u64>(1024, (nslots + 255) / 256), 256, 0, st>>>(tails, nslots);
-      counted_launch(c);
-      for (size_t k = 0; k < outs.size(); ++k)
-        if (wv[k]) TQ_CUDA(cudaMemsetAsync(base + boff[k], 0, (cap + 7) / 8, st));
+    // reset this half of the window (row counter, tail slots, every column's
+    // bitmap); the validity-mask all-gather that follows is also the barrier
+    // that orders every rank's reset before any rank scatters into it
+    TQ_CUDA(cudaMemsetAsync(counter, 0, 8, st));
+    k_tail_reset<<<(u32)std::min<u64>(1024, (nslots + 255) / 256), 256, 0, st>>>(tails, nslots);
+    counted_launch(c);
+    for (size_t k = 0; k < outs.size(); ++k) TQ_CUDA(cudaMemsetAsync(base + boff[k], 0, (cap + 7) / 8, st));
+    k_set_u64<<<1, 1, 0, st>>>(vmask_in, vmask_local);
+    counted_launch(c);
+    {
       TQ_HT("pex barrier1");
       const int ph = prof_begin(c, "pex_barrier1", st);
-      peer_barrier(cm, st);  // every window reset before anyone writes into it
+      comm_allgather_u64(cm, vmask_in, vmask_all, 1, st);
       prof_end(c, ph, st);
     }
     for (int d = 0; d < n; ++d) {
@@ -941,15 +959,15 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     }
     p.peer_cap = cap;
     p.tail_slot0 = (u32)me * kMaxTailCtas;
+    p.peer_vmask = vmask_all;
     p.cursor = sent_dev;
     ChunkOut co{};
     co.ncols = p.nout;
     for (size_t k = 0; k < outs.size(); ++k) {
       outs[k].values = base + voff[k];
-      outs[k].validity = wv[k] ? base + boff[k] : nullptr;
+      outs[k].validity = base + boff[k];
       p.out[k] = outs[k];
       co.values[k] = outs[k].values;
-      co.validity[k] = outs[k].validity;
       co.width[k] = outs[k].width;
     }
     launch(c, SINK_EMIT, L, P, st);
@@ -965,18 +983,20 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     TQ_CUDA(cudaMemcpyAsync(scratch + n, counter, 8, cudaMemcpyDeviceToDevice, st));
     comm_allgather_u64(cm, scratch + n, scratch, 1, st);
     prof_end(c, ph_plan, st);
-    u64 n_rows = 0, moves = 0, rmax = 0, sent_rows = 0;
+    u64 n_rows = 0, moves = 0, rmax = 0, sent_rows = 0, vor = 0;
     {
       std::lock_guard<std::mutex> g(c->mu);
       u64* pin = (u64*)c->pinned;
       TQ_CUDA(cudaMemcpyAsync(pin, plan, 16, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaMemcpyAsync(pin + 2, scratch, 8 * n, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaMemcpyAsync(pin + 2 + n, sent_dev, 8, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync(pin + 3 + n, vmask_all, 8 * n, cudaMemcpyDeviceToHost, st));
       { TQ_HT("pex sync after plan"); TQ_CUDA(cudaStreamSynchronize(st)); }
       n_rows = pin[0];
       moves = pin[1];
       for (int d = 0; d < n; ++d) rmax = std::max(rmax, pin[2 + d]);
       sent_rows = pin[2 + n];
+      for (int d = 0; d < n; ++d) vor |= pin[3 + n + d];
     }
     if (rmax > cap) {  // some receiver overflowed: every rank sees the same rmax and re-runs
       if (attempt > 4) fail(TQ_INTERNAL, "fused exchange window did not converge");
@@ -984,25 +1004,24 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
       continue;
     }
     if (moves == ~0ull) fail(TQ_INTERNAL, "fused exchange chunk plan inconsistent");
+    std::vector<bool> wv_out(outs.size());
+    for (size_t k = 0; k < outs.size(); ++k) {
+      wv_out[k] = (vor >> k) & 1;
+      co.validity[k] = wv_out[k] ? outs[k].validity : nullptr;
+    }
     const int ph_fix = prof_begin(c, "pex_fix_copyout", st);
     k_chunk_move<<<c->sms * 2, 256, 0, st>>>(plan, (u32)nslots, co);
     k_chunk_clear_tail<<<1, 32, 0, st>>>(plan, co);
     counted_launch(c);
     counted_launch(c);
     TQ_CUDA(cudaGetLastError());
-    alloc_batch(c, n_rows, sch, wv, out, st);
+    alloc_batch(c, n_rows, sch, wv_out, out, st);
     for (size_t k = 0; k < outs.size(); ++k) {
       if (n_rows) TQ_CUDA(cudaMemcpyAsync(out->cols[k].values, co.values[k], n_rows * outs[k].width,
                                           cudaMemcpyDeviceToDevice, st));
-      if (wv[k] && n_rows)
+      if (wv_out[k] && n_rows)
         TQ_CUDA(cudaMemcpyAsync(out->cols[k].validity, co.validity[k], (n_rows + 7) / 8, cudaMemcpyDeviceToDevice, st));
     }
-    // ready this half for its next use (two exchanges later): the copy-out
-    // above and this reset precede this rank's next barrier2 in stream order
-    TQ_CUDA(cudaMemsetAsync(counter, 0, 8, st));
-    k_tail_reset<<<(u32)std::min<u64>(1024, (nslots + 255) / 256), 256, 0, st>>>(tails, nslots);
-    counted_launch(c);
-    comm_half_ready(cm, half) = true;
     comm_epoch(cm) += 1;
     prof_end(c, ph_fix, st);
     if (rows_sent) *rows_sent = sent_rows;
@@ -1010,7 +1029,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     break;
   }
   dfree(c, plan, plan_words * 8, st);
-  dfree(c, scratch, 8 * (2 * n + 8), st);
+  dfree(c, scratch, 8 * scratch_words, st);
 }
 
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
@@ -1837,6 +1856,7 @@ void tq_join_table_destroy(tq_ctx* c, tq_join_table* t) {
   if (!t) return;
   (void)c;
   dfree(t->ctx, t->mem, t->bytes, t->ctx->stream);  // see tq_batch_free
+  for (auto& r : t->retired) dfree(t->ctx, r.first, r.second, t->ctx->stream);
   std::free(t->build.cols);
   delete t;
 }

@@ -33,7 +33,6 @@ tq_ctx* comm_ctx(tq_comm* cm);
 int comm_rank(tq_comm* cm);
 int comm_size(tq_comm* cm);
 uint64_t& comm_epoch(tq_comm* cm);                // fused exchanges completed (same on every rank)
-bool& comm_half_ready(tq_comm* cm, int half);     // window half reset since its last use
 uint64_t& comm_last_cap(tq_comm* cm);  // rows capacity of the last fused exchange (same on every rank)
 void comm_add_sent(tq_comm* cm, uint64_t bytes);  // NVLink bytes accounting
 

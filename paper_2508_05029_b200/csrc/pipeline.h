@@ -159,6 +159,9 @@ struct PipeParams {
   uint64_t peer_cap;     // rows of every receive window
   uint32_t bcast;        // DEST_PEER: every row to every rank (no keys)
   uint32_t tail_slot0;   // this rank's first tail slot (rank * kMaxTailCtas)
+  // [ndest] every rank's local output-nullability mask (all-gathered before
+  // the kernel): validity bits are written for the OR of the masks
+  const unsigned long long* peer_vmask;
   JoinTable jt;
   // LIP semi-join filter on the key words (dest PARTITION): rows whose keys
   // miss this Bloom filter are dropped before they are partitioned / shipped

@@ -44,7 +44,8 @@ class TqEngineOptsC(C.Structure):
     _fields_ = [("compute_threads", C.c_uint32), ("preload", C.c_uint32), ("batch_rows", C.c_uint64),
                 ("device_budget", C.c_uint64), ("pool_buffer_size", C.c_uint64), ("pool_capacity", C.c_uint64),
                 ("high_watermark", C.c_double), ("low_watermark", C.c_double), ("protect_top_k", C.c_uint32),
-                ("tables_on_host", C.c_uint32)]
+                ("tables_on_host", C.c_uint32), ("task_batches", C.c_uint32), ("inject_oom_mode", C.c_uint32),
+                ("inject_oom_count", C.c_uint32), ("inject_oom_op", C.c_char * 32)]
 
 
 class TqOptsC(C.Structure):
@@ -149,6 +150,8 @@ def lib():
         L.tq_pipeline_broadcast.argtypes = [V, B, E, E, C.c_uint32, B, V]
         L.tq_comm_last_exchange_capacity.restype = C.c_uint64
         L.tq_comm_last_exchange_capacity.argtypes = [V]
+        L.tq_on_oom_decide.restype = C.c_int
+        L.tq_on_oom_decide.argtypes = [C.c_uint64, C.c_uint64, C.c_int, P(C.c_uint64)]
         L.tq_estimate_reservation.restype = C.c_uint64
         L.tq_estimate_reservation.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double]
         L.tq_jit_report.restype = C.c_uint64
@@ -665,6 +668,16 @@ def estimate_reservation(samples, ema_peak, ema_ratio, input_bytes, multiplier, 
     return lib().tq_estimate_reservation(samples, ema_peak, ema_ratio, input_bytes, multiplier, safety)
 
 
+OOM_ACTIONS = ("retry", "split", "abort")
+
+
+def on_oom_decide(estimate: int, capacity: int, splittable: bool) -> Tuple[str, int]:
+    """SPEC.md:390-398 on_oom rule -> (action, new estimate)."""
+    e = C.c_uint64()
+    a = lib().tq_on_oom_decide(estimate, capacity, 1 if splittable else 0, C.byref(e))
+    return OOM_ACTIONS[a], e.value
+
+
 def engine_run_query(ctx: Context, query: int, tables: dict, comm: "Comm" = None, **opts):
     """Run a benchmark query DAG on the C++ worker runtime (include/tq_engine.h).
     tables: {table_id: DeviceBatch or HostBatch}.  Returns (HostBatch, metrics)."""
@@ -680,7 +693,7 @@ def engine_run_query(ctx: Context, query: int, tables: dict, comm: "Comm" = None
             arr[t] = c
     o = TqEngineOptsC()
     for k, v in opts.items():
-        setattr(o, k, v)
+        setattr(o, k, v.encode() if isinstance(v, str) else v)
     out = TqBatchC()
     buf = C.create_string_buffer(1 << 16)
     Context._check(lib().tq_engine_run_query(ctx.handle, comm.handle if comm else None, query, arr, C.byref(o),

@@ -1,0 +1,71 @@
+"""torchrun helper (one process per GPU) for multi-rank operator checks that
+are not whole queries.  Run by tests/test_multigpu.py; exits non-zero on a
+mismatch.  Modes (TQ_MODE):
+  validity  the fused partition exchange / broadcast when ranks DISAGREE on
+            which columns can be null (rank 0 has nulls, rank 1 has no
+            bitmaps, rank 2 an empty input): every rank must lay out its
+            window identically and the output must carry the nulls."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")]
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def validity(ctx, comm, rank, world):
+    import oracle as O
+    from helpers import rand_batch
+    from paper_2508_05029_b200.columnar import DECIMAL, INT64
+    from paper_2508_05029_b200.expr import Col
+    rows = 0 if rank == 2 else 20000 + 3000 * rank
+    b = rand_batch(50 + rank, rows, (INT64, DECIMAL, INT64), null_frac=0.1 if rank == 0 else 0.0)
+    d = ctx.upload(b)
+    exprs = [Col(0), Col(1), Col(2) + 1]
+    px = comm.partition_exchange(d, None, exprs, [0]).to_host()
+    bc = comm.broadcast(d, Col(2) < 5, [Col(1), Col(0)]).to_host()
+    ins = [None] * world
+    outs = [None] * world
+    dist.all_gather_object(ins, b)
+    dist.all_gather_object(outs, (px, bc))
+    if rank != 0:
+        return True
+    from paper_2508_05029_b200.columnar import assert_batches_equal
+    allin = O.concat(ins)
+    assert_batches_equal(O.concat([o[0] for o in outs]), O.project_execute(allin, exprs))
+    want_bc = O.project_execute(O.filter_execute(allin, Col(2) < 5), [Col(1), Col(0)])
+    for o in outs:  # every rank receives every broadcast row
+        assert_batches_equal(o[1], want_bc)
+    return True
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dist.init_process_group("gloo")
+    torch.cuda.set_device(local)
+    from paper_2508_05029_b200.ops import Comm, Context
+    ctx = Context(local)
+    uid = [Comm.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = Comm(ctx, rank, world, uid[0])
+    mode = os.environ.get("TQ_MODE", "validity")
+    rc = 0
+    try:
+        {"validity": validity}[mode](ctx, comm, rank, world)
+        if rank == 0:
+            print(f"mgpu ops ok: mode={mode} world={world}")
+    except AssertionError as e:
+        print("MISMATCH", mode, e)
+        rc = 1
+    comm.close()
+    ctx.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(rc)
+
+
+if __name__ == "__main__":
+    main()

@@ -56,3 +56,29 @@ def test_engine_host_tables_under_budget(ctx, q):
     want = O.query(q, host, 8)
     assert_batches_equal(got, want)
     assert m["loads"] + m["preloads"] > 0, m
+
+
+@pytest.mark.parametrize("case", ["retry", "split", "unsplittable"])
+def test_engine_on_oom_paths(ctx, case):
+    """run_task's on_oom forced in a real query by injecting
+    ReservationExceeded into the lineitem filter/project tasks: the doubled
+    estimate is retried; a multi-batch task whose doubled estimate exceeds
+    the Device capacity is split in two; a single-batch one aborts the query
+    with OutOfMemoryUnsplittable.  Results stay identical to the oracle."""
+    from paper_2508_05029_b200.columnar import TqError
+    sf = 0.05
+    tabs = {t: ctx.datagen(t, sf) for t in O.QUERY_TABLES[3]}
+    want = O.query(3, {t: O.datagen(t, sf) for t in O.QUERY_TABLES[3]}, 8)
+    opts = dict(compute_threads=2, batch_rows=32 * 1024, device_budget=4 << 30, inject_oom_op="lineitem_f")
+    if case == "retry":
+        got, m = engine_run_query(ctx, 3, tabs, inject_oom_mode=1, inject_oom_count=2, **opts)
+        assert (m["oom_retries"], m["splits"]) == (2, 0), m
+        assert_batches_equal(got, want)
+    elif case == "split":
+        got, m = engine_run_query(ctx, 3, tabs, task_batches=4, inject_oom_mode=2, inject_oom_count=1, **opts)
+        assert m["splits"] == 1 and m["oom_retries"] == 0, m
+        assert_batches_equal(got, want)
+    else:
+        with pytest.raises(TqError) as e:
+            engine_run_query(ctx, 3, tabs, task_batches=1, inject_oom_mode=2, inject_oom_count=1, **opts)
+        assert e.value.errc == "OutOfMemoryUnsplittable"

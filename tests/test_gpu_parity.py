@@ -328,3 +328,33 @@ def test_partition_semi_bloom(ctx, seed):
     assert len(kept) < 0.2 * probe.rows            # most non-joining rows dropped
     j1 = O.join_execute(build, got, [0], [0])
     assert_batches_equal(j1, O.join_execute(build, probe, [0], [0]))
+
+
+@pytest.mark.parametrize("distinct", [40, 200000])
+def test_aggregate_publication_stress(ctx, distinct):
+    """Many lanes insert the same NEW keys at once (every key's first
+    occurrences are spread over the whole grid): a reader that observed a
+    published slot must compare the keys written before the publication, or
+    the same key lands in two slots (duplicate groups).  40 keys stress the
+    per-CTA shared-memory table, 200K the global table.  50 repetitions."""
+    rng = np.random.default_rng(1234 + distinct)
+    n = 2_000_000
+    k = rng.integers(0, distinct, n).astype(np.int64) * 7919 + 3
+    b = HostBatch(n, [HostBatch.col_i64(k), HostBatch.col_dec(rng.integers(-10**6, 10**6, n))])
+    aggs = [(AGG_SUM, 1), (AGG_COUNT_STAR, 0)]
+    want = O.aggregate_execute(b, [0], aggs)
+    d = ctx.upload(b)
+    for _ in range(50):
+        got = ctx.aggregate_execute(d, [0], aggs)
+        assert got.rows == want.rows  # no key was inserted twice
+        got.free()
+    assert_batches_equal(ctx.aggregate_execute(d, [0], aggs).to_host(), want)
+
+
+@pytest.mark.parametrize("t", [0, 1, 2, 5])
+def test_datagen_shard_bit_identical(ctx, t):
+    """GPU row-group subsets (tq_datagen_shard) == the oracle's shards."""
+    sf = 0.02
+    for s in (0, 3):
+        g = ctx.datagen(t, sf, shard=s, nshards=4).to_host()
+        assert_batches_equal(g, O.datagen(t, sf, 4, s, 4), ordered=True)

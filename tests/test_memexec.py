@@ -92,3 +92,19 @@ def test_estimate_reservation_examples():
     assert estimate_reservation(0, 0, 0, 10 * MiB, 2.0) == 20 * MiB
     assert estimate_reservation(5, 0, 3.0, 10 * MiB, 2.0, 1.25) == int(37.5 * MiB)
     assert estimate_reservation(5, 1, 0.1, 10 * MiB, 2.0) == 10 * MiB        # never below the input
+
+
+def test_on_oom_examples():
+    """SPEC.md:390-398, the three on_oom examples (the rule the engine's
+    run_task applies; tests/test_gpu_engine.py forces each path in a query)."""
+    from paper_2508_05029_b200.ops import on_oom_decide
+    assert on_oom_decide(10, 100, False) == ("retry", 20)      # estimate 10 -> 20 <= capacity: retry
+    assert on_oom_decide(60, 100, True) == ("split", 120)      # would exceed capacity, 4 batches: split
+    assert on_oom_decide(100, 100, False) == ("abort", 200)    # 2x capacity, 1 batch: OutOfMemoryUnsplittable
+    assert on_oom_decide(1 << 40, 0, False) == ("retry", 1 << 41)  # capacity 0 = unbounded
+    # retry monotonicity (SPEC.md invariants): the estimate strictly grows
+    e, seen = 3, []
+    for _ in range(5):
+        a, e = on_oom_decide(e, 1 << 30, False)
+        seen.append(e)
+    assert seen == sorted(set(seen))

@@ -28,3 +28,16 @@ def test_distributed_q3_nccl(world, mode):
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
     assert "mgpu q3 ok" in r.stdout
+
+
+@pytest.mark.parametrize("mode", ["validity"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_distributed_ops(world, mode):
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + world), os.path.join(ROOT, "tests", "mgpu_ops.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=dict(os.environ, TQ_MODE=mode))
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
+    assert "mgpu ops ok" in r.stdout

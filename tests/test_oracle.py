@@ -263,3 +263,16 @@ def test_q6_selectivity():
     out = O.query(6, {O.T_LINEITEM: li})
     ep = li.cols[4].dec_words()[:, 0]
     assert out.column_py(0)[0] == int((ep[m].astype(object) * disc[m].astype(object)).sum())
+
+
+@pytest.mark.parametrize("t", range(8))
+def test_datagen_shards_concat_to_full_table(t):
+    """A worker's row-group subset (tqo_datagen_shard) is a contiguous slice of
+    the full table: the shards concatenate back to it, value for value."""
+    sf = 0.02
+    full = O.datagen(t, sf, 4)
+    parts = [O.datagen(t, sf, 4, s, 5) for s in range(5)]
+    cat = O.concat(parts)
+    assert cat.rows == full.rows
+    for a, b in zip(cat.cols, full.cols):
+        assert (a.values == b.values).all()
