@@ -211,14 +211,15 @@ __device__ __forceinline__ long long table_find_insert(u32* state, u64* keys, u6
   return -1;
 }
 
-__device__ __forceinline__ void acc_identity(uint8_t op, u64& lo, u64& hi) {
-  switch (op) {
-    case ACC_MIN_I: lo = ~0ull; hi = 0x7fffffffffffffffull; break;
-    case ACC_MAX_I: lo = 0; hi = 0x8000000000000000ull; break;
-    case ACC_MIN_F: lo = 0x7ff0000000000000ull; hi = 0; break;
-    case ACC_MAX_F: lo = 0xfff0000000000000ull; hi = 0; break;
-    default: lo = 0; hi = 0;
-  }
+
+__device__ __forceinline__ i128 shfl_up_i128(i128 v, u32 o) {
+  const u64 lo = __shfl_up_sync(kFull, lo64(v), o);
+  const u64 hi = __shfl_up_sync(kFull, hi64(v), o);
+  return mk128(lo, hi);
+}
+// a float min / max run result differs from the identity (bit pattern)
+__device__ __forceinline__ bool valid_any_f(double v, u64 identity_bits) {
+  return (u64)__double_as_longlong(v) != identity_bits;
 }
 
 __device__ __forceinline__ void acc_apply_atomic(uint8_t op, u64* a, i128 xi, double xf, u64 cnt) {
@@ -312,7 +313,7 @@ __device__ __forceinline__ u32 partition_of_p(const PipeParams& p, const u64* kw
 // First build row matching kw (-1: none).  With `walk` the rest of the
 // cluster is walked too, and a second match sets dup (non-unique build keys).
 __device__ __forceinline__ bool jt_exact_hit(const JoinTable& t, u64 key) {
-  if (key >= 32 * (t.bloom_mask + 1)) return false;
+  if (key >= t.exact_range) return false;
   return (__ldg(t.exact_bits + (key >> 5)) >> (key & 31)) & 1u;
 }
 
@@ -517,7 +518,11 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   // exact for one-word keys): flag it at once — the host runs the two-pass
   // probe — instead of scanning the input for the first duplicate match.
   // (Uniform over the grid; every CTA leaves a "no hole" tail for the fix-up.)
-  if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 && p.jt.dup_dev && *(volatile u32*)p.jt.dup_dev) {
+  // (A table without hash entries — semi-only or direct — whose bitmap is not
+  // exact is flagged the same way: the host builds the hash table.)
+  if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 &&
+      ((p.jt.dup_dev && *(volatile u32*)p.jt.dup_dev) ||
+       (!p.jt.entries && p.jt.exact_flag && *(volatile u32*)p.jt.exact_flag))) {
     if (threadIdx.x == 0) {
       p.chunk_tail[2 * blockIdx.x] = 0;
       p.chunk_tail[2 * blockIdx.x + 1] = kChunk;
@@ -608,20 +613,27 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
   if (SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 && p.jt.dup_dev) walk_dups = *p.jt.dup_dev != 0;
   // probes: the build's exact membership bitmap replaces the Bloom check; a
   // semi-join (no build columns) over proven-unique keys then skips the table
-  bool exact = false, semi_skip = false;
+  bool exact = false, semi_skip = false, direct = false;
   if ((SINK == SINK_EMIT || SINK == SINK_COUNT) && (p.dest_kind == DEST_PROBE1 || p.dest_kind == DEST_PROBE) &&
       p.jt.exact_flag) {
     exact = *p.jt.exact_flag == 0;
     semi_skip = exact && p.probe_semi && p.dest_kind == DEST_PROBE1 && !walk_dups;
+    // direct-indexed table: exact bitmap + unique keys -> one 4-B slot read per hit
+    direct = !semi_skip && exact && p.dest_kind == DEST_PROBE1 && !walk_dups && p.jt.direct != nullptr;
   }
-  // a semi-only build (no hash table) that turned out not exact / not unique:
-  // flag it (the host builds the table and re-runs this probe), touch nothing
-  const bool no_table = SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 && p.jt.entries == nullptr && !semi_skip;
+  // a build without a hash table (semi-only or direct) that turned out not
+  // exact / not unique: flag it (the host builds the table and re-runs this
+  // probe), touch nothing
+  const bool no_table =
+      SINK == SINK_EMIT && p.dest_kind == DEST_PROBE1 && p.jt.entries == nullptr && !semi_skip && !direct;
   if (no_table && threadIdx.x == 0) *(volatile u32*)p.dup_flag = 2;
   // two-pass partition EMIT: this warp's scanned slice offsets (one per
   // destination) are fetched before waiting on the stage, so their latency
   // overlaps it (hash_partition 1.234 -> 1.169 ms SF10; a filter measured slower)
   const bool slice_emit = SINK == SINK_EMIT && p.tile_offsets && p.dest_kind == DEST_PARTITION;
+  // DEST_RANGE: this lane's running min / max of the first key word
+  long long r_min = 0x7fffffffffffffffll, r_max = (long long)0x8000000000000000ull;
+  bool r_null = false;
   for (u32 tile = first; tile < p.ntiles; tile += step) {
     unsigned long long pre_base = 0;
     if (slice_emit && lane < p.ndest)
@@ -719,6 +731,18 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           }
         }
       }
+    } else if (SINK == SINK_COUNT && p.dest_kind == DEST_RANGE) {
+#pragma unroll
+      for (int v = 0; v < kV; ++v) {
+        if (!((pm[v] >> lane) & 1u)) continue;
+        u64 kw[kMaxKeyWords + 1];
+        if (P::keys(w, v, kw, raw[v])) {
+          r_null = true;
+        } else {
+          r_min = min(r_min, (long long)kw[0]);
+          r_max = max(r_max, (long long)kw[0]);
+        }
+      }
     } else if ((SINK == SINK_COUNT || SINK == SINK_EMIT) && p.dest_kind == DEST_PROBE1) {
       // single pass: unique build keys -> at most one match per probe row
 #pragma unroll
@@ -730,6 +754,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           bool dup = false;
           if (!P::keys(w, v, kw, raw[v])) {
             if (semi_skip) brow = jt_exact_hit(p.jt, kw[0]) ? 0 : -1;  // no build column is read
+            else if (direct) brow = jt_exact_hit(p.jt, kw[0]) ? (long long)__ldg(p.jt.direct + kw[0]) : -1;
             else if (!no_table) brow = jt_probe_first<P::kKw>(p.jt, kw, walk_dups, dup, exact);
           }
           if (dup && *(volatile u32*)p.dup_flag == 0) *(volatile u32*)p.dup_flag = 1;
@@ -862,7 +887,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
       if (p.jt.exact_bits && !p.build_skip_aux) {
         // exact membership bits: lanes whose keys share a bitmap word (dense,
         // often consecutive keys) merge their bits, one atomic per word
-        const u64 range = 32 * (p.jt.bloom_mask + 1);
+        const u64 range = p.jt.exact_range;
 #pragma unroll
         for (int v = 0; v < kV; ++v) {
           const bool in = ok[v] && kws[v][0] < range;
@@ -877,6 +902,9 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
               *(volatile u32*)p.jt.dup_dev = 1;
           }
           if (ok[v] && !in && *(volatile u32*)p.jt.exact_flag == 0) *(volatile u32*)p.jt.exact_flag = 1;
+          // direct-indexed table: the row lands in its key's slot (dense keys:
+          // neighbouring lanes store to neighbouring slots)
+          if (in && p.jt.direct) p.jt.direct[kws[v][0]] = (u32)(p.row_base + r0 + trow(w, v));
         }
       }
 #pragma unroll
@@ -934,7 +962,77 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
         P::keys(w, v, xs[v].kw, raw[v]);
         P::accs(w, v, xs[v], raw[v]);
       }
-      if (any) {
+      if (p.agg.direct) {
+        // DIRECT: slot = key - key_min.  Lanes holding the same slot in a
+        // contiguous run (sorted / clustered keys) are reduced with a
+        // segmented warp scan first; the run's last lane applies it with one
+        // atomic per accumulator (one global atomic per run, not per row).
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          const bool pass = (pm[v] >> lane) & 1u;
+          RowVals& x = xs[v];
+          const u32 act = __ballot_sync(kFull, pass);
+          if (!act) continue;
+          u64 slot = ~0ull;
+          if (pass) slot = x.kw[kwa - 1] ? p.agg.direct_slots : x.kw[0] - (u64)p.agg.key_min;
+          const u64 prev = __shfl_up_sync(kFull, slot, 1);
+          const bool head = pass && (lane == 0 || prev != slot || !((act >> (lane - 1)) & 1u));
+          const u32 heads = __ballot_sync(kFull, head);
+          const u32 start = 31 - __clz(heads & (lanemask_lt() | (1u << lane)) | 1u);  // my run's first lane
+          const bool tail = pass && (lane == 31 || ((heads >> (lane + 1)) & 1u) || !((act >> (lane + 1)) & 1u));
+#pragma unroll
+          for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
+            if (a >= nacc) break;
+            const uint8_t op = P::acc_op(p, a);
+            const bool valid = pass && x.av[a];
+            u64* acc = p.agg.acc + (slot * nacc + a) * 2;
+            if (op == ACC_SUM_I || op == ACC_CNT) {
+              i128 sv = valid ? (op == ACC_CNT ? (i128)1 : x.ai[a]) : (i128)0;
+#pragma unroll
+              for (u32 o = 1; o < 32; o <<= 1) {
+                const i128 y = shfl_up_i128(sv, o);
+                if (lane >= start + o) sv = add128(sv, y);
+              }
+              if (tail) {
+                if (op == ACC_CNT) {
+                  const u64 old = atomicAdd((unsigned long long*)acc, (unsigned long long)lo64(sv));
+                  if (a == p.agg.cnt_acc && old == 0) atomicAdd(s_groups, 1ull);  // a new group
+                } else if (sv != 0) {
+                  atomic_add_i128(acc, sv);
+                }
+              }
+            } else if (op == ACC_SUM_F) {
+              double sv = valid ? x.af[a] : 0.0;
+#pragma unroll
+              for (u32 o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(kFull, sv, o);
+                if (lane >= start + o) sv += y;
+              }
+              if (tail) atomicAdd((double*)acc, sv);
+            } else if (op == ACC_MIN_I || op == ACC_MAX_I) {
+              u64 lo, hi;
+              acc_identity(op, lo, hi);
+              i128 sv = valid ? x.ai[a] : mk128(lo, hi);
+#pragma unroll
+              for (u32 o = 1; o < 32; o <<= 1) {
+                const i128 y = shfl_up_i128(sv, o);
+                if (lane >= start + o) sv = (op == ACC_MIN_I) ? (y < sv ? y : sv) : (y > sv ? y : sv);
+              }
+              if (tail && sv != mk128(lo, hi)) atomic_minmax_i128((u128*)acc, sv, op == ACC_MIN_I);
+            } else {
+              u64 lo, hi;
+              acc_identity(op, lo, hi);
+              double sv = valid ? x.af[a] : __longlong_as_double((long long)lo);
+#pragma unroll
+              for (u32 o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(kFull, sv, o);
+                if (lane >= start + o) sv = (op == ACC_MIN_F) ? fmin(sv, y) : fmax(sv, y);
+              }
+              if (tail && valid_any_f(sv, lo)) atomic_minmax_f64((double*)acc, sv, op == ACC_MIN_F);
+            }
+          }
+        }
+      } else if (any) {
 #pragma unroll
         for (int v = 0; v < kV; ++v) {
           bool pass = (pm[v] >> lane) & 1u;
@@ -1058,6 +1156,21 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
     if (++s == p.nstages) { s = 0; ph ^= 1u; }
   }
 
+  if (SINK == SINK_COUNT && p.dest_kind == DEST_RANGE) {
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) {
+      r_min = min(r_min, (long long)__shfl_xor_sync(kFull, (unsigned long long)r_min, m));
+      r_max = max(r_max, (long long)__shfl_xor_sync(kFull, (unsigned long long)r_max, m));
+    }
+    const bool any_null = __any_sync(kFull, r_null);
+    if (lane == 0) {  // one set of atomics per warp and launch
+      if (r_min <= r_max) {
+        atomicMin(p.key_range, r_min);
+        atomicMax(p.key_range + 1, r_max);
+      }
+      if (any_null) atomicOr((unsigned long long*)p.key_range + 2, 1ull);
+    }
+  }
   if (SINK == SINK_EMIT && p.dest_kind == DEST_PEER) {
     consumers_sync();
     if (threadIdx.x < p.ndest) {

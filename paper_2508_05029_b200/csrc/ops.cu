@@ -550,7 +550,8 @@ __global__ void k_chunk_clear_tail(const u64* plan, const __grid_constant__ Chun
 }
 
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
-                      tq_join_table** out, cudaStream_t st, uint64_t bloom_keys, bool semi_only);
+                      tq_join_table** out, cudaStream_t st, uint64_t bloom_keys, bool semi_only,
+                      bool allow_direct = true);
 
 // A semi-only table whose bitmap turned out not exact (or keys not unique):
 // build the real hash table from the same input and program, in place.
@@ -559,7 +560,7 @@ static void semi_table_materialize(tq_ctx* c, tq_join_table* t, cudaStream_t st)
   if (t->jt.entries != nullptr) return;  // another probe materialised it first
   tq_join_table* full = nullptr;
   Prog& P = *(Prog*)t->semi_prog.get();
-  run_build(c, &t->build, P, t->semi_keys, &full, st, t->semi_bloom_keys, false);
+  run_build(c, &t->build, P, t->semi_keys, &full, st, t->semi_bloom_keys, false, /*allow_direct=*/false);
   t->retired.emplace_back(t->mem, t->bytes);
   std::free(t->build.cols);
   t->jt = full->jt;
@@ -644,11 +645,13 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
   // only when it is small against the Device budget left
   uint64_t cap_bytes = in->rows * row_bytes;
   uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
-  const bool semi_table = A.mode == MAT_PROBE && A.table->jt.entries == nullptr;
-  if (semi_table && !A.build_cols.empty())
+  // a table without hash entries (semi-only, or direct-indexed) is probed
+  // single-pass; if it is not usable the probe asks for the hash table
+  const bool no_hash = A.mode == MAT_PROBE && A.table->jt.entries == nullptr;
+  if (no_hash && A.table->jt.direct == nullptr && !A.build_cols.empty())
     fail(TQ_INVALID_PLAN, "semi-join build table: the probe cannot take build columns");
-  const bool probe1 = A.mode == MAT_PROBE && A.table->jt.unique &&
-                      ((cap_bytes <= (8ull << 30) && cap_bytes * 4 <= room) || semi_table);
+  const bool probe1 = A.mode == MAT_PROBE && (A.table->jt.unique || no_hash) &&
+                      ((cap_bytes <= (8ull << 30) && cap_bytes * 4 <= room) || no_hash);
   if (probe1) {
     // single pass: capacity = probe rows (<= 1 match each), exact size read back
     p.dest_kind = DEST_PROBE1;
@@ -1033,7 +1036,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
 }
 
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
-                      tq_join_table** out, cudaStream_t st, uint64_t bloom_keys, bool semi_only) {
+                      tq_join_table** out, cudaStream_t st, uint64_t bloom_keys, bool semi_only, bool allow_direct) {
   Plan L;
   plan_launch(c, in, P, L, 0, st);
   PipeParams& p = L.p;
@@ -1068,26 +1071,53 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   uint64_t words = 1024;
   while (words * 32 < std::max<uint64_t>(in->rows, bloom_keys) * 8) words <<= 1;
   t->jt.bloom_mask = words - 1;
-  // one-word keys also get an exact membership bitmap over [0, 32 * words)
-  // (same size as the Bloom) and the build's duplicate-key / exact-range flags;
-  // a semi-only build (a semi-join's build side) has no hash table at all
+  // One-word keys also get an exact membership bitmap over [0, exact_range)
+  // and the build's duplicate-key / exact-range flags.  A semi-only build (a
+  // semi-join's build side) has no hash table at all.  Otherwise, when the
+  // address space fits, the build is DIRECT-indexed: a 4-B row slot per key
+  // value in [0, 32 x rows) (never initialised: the bitmap says which slots
+  // were written), no hash table, no CAS — a plain store per build row, and a
+  // probe reads one slot per hit.  Dense keys (TPC-H's) make both the stores
+  // and the probe's reads of neighbouring keys coalesce.  Keys outside the
+  // range or repeated send the first probe back to the host, which then
+  // builds the hash table (as for a semi-only table).
   const bool exact = t->jt.kw == 1;
   const bool semi = semi_only && exact;
-  uint64_t ebytes = semi ? 0 : cap * t->jt.stride;
-  t->bytes = ebytes + words * 4 + 16 + (exact ? words * 4 : 0);
+  uint64_t ewords = words;  // exact bitmap words (range 32 x ewords)
+  bool direct = false;
+  if (exact && !semi && allow_direct && in->rows < (1ull << 31)) {
+    static const bool no_direct = [] { const char* e = getenv("TQ_DIRECT"); return e && e[0] == '0'; }();
+    const uint64_t dw = std::max<uint64_t>(words, round_up(in->rows, 1024));  // range >= 32 x rows
+    const uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
+    if (!no_direct && dw * 32 * 4 <= room / 4) {
+      direct = true;
+      ewords = dw;
+    }
+  }
+  if (semi) ewords = std::max<uint64_t>(words, round_up(in->rows, 1024));  // bitmap only: 4 B per row
+  const bool hashed = !semi && !direct;
+  uint64_t ebytes = hashed ? cap * t->jt.stride : 0;
+  const uint64_t aux = words * 4 + 16 + (exact ? ewords * 4 : 0);  // Bloom, flags, exact bitmap
+  const uint64_t dbytes = direct ? ewords * 32 * 4 : 0;
+  t->bytes = ebytes + aux + dbytes;
   try {
     t->mem = (uint8_t*)dalloc(c, t->bytes, st);
   } catch (...) {
     delete t;
     throw;
   }
-  t->jt.entries = semi ? nullptr : t->mem;
+  t->jt.entries = hashed ? t->mem : nullptr;
   t->jt.bloom = (uint32_t*)(t->mem + ebytes);
-  if (!semi) TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, ebytes, st));
-  TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, words * 4 + 16 + (exact ? words * 4 : 0), st));
-  t->jt.dup_dev = t->jt.kw == 1 && (t->jt.stride == 16 || semi) ? (uint32_t*)(t->jt.bloom + words) : nullptr;
+  if (hashed) TQ_CUDA(cudaMemsetAsync(t->jt.entries, 0xff, ebytes, st));
+  TQ_CUDA(cudaMemsetAsync(t->jt.bloom, 0, aux, st));
+  t->jt.dup_dev = t->jt.kw == 1 && (t->jt.stride == 16 || !hashed) ? (uint32_t*)(t->jt.bloom + words) : nullptr;
   t->jt.exact_flag = exact ? (uint32_t*)(t->jt.bloom + words) + 1 : nullptr;
   t->jt.exact_bits = exact ? (uint32_t*)(t->jt.bloom + words) + 4 : nullptr;
+  t->jt.exact_range = exact ? ewords * 32 : 0;
+  t->jt.direct = direct ? (uint32_t*)(t->mem + ebytes + aux) : nullptr;
+  // a direct table's probes test the exact bitmap; its Bloom filter is only
+  // built when asked for (bloom_keys: the partitioned LIP filter)
+  if (direct && bloom_keys == 0) t->jt.bloom = nullptr;
   {  // TQ_BLOOM=0: experiments only (probe without the Bloom pre-check)
     static const bool no_bloom = [] { const char* e = getenv("TQ_BLOOM"); return e && e[0] == '0'; }();
     if (no_bloom) t->jt.bloom = nullptr;
@@ -1106,7 +1136,7 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   u32 passes = 1;
   {
     static const long env_passes = [] { const char* e = getenv("TQ_BUILD_PASSES"); return e ? atol(e) : -1L; }();
-    if (env_passes > 0 && !semi) passes = (u32)env_passes;
+    if (env_passes > 0 && hashed) passes = (u32)env_passes;
   }
   for (u32 k = 0; k < passes; ++k) {
     p.slot_lo = passes > 1 ? cap / passes * k : 0;
@@ -1114,8 +1144,8 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
     p.build_skip_aux = k > 0;
     launch(c, SINK_BUILD, L, P, st);
   }
-  if (semi) {
-    // usable without a table only when the bitmap is exact and proved the
+  if (!hashed) {
+    // usable without a hash table only when the bitmap is exact and proved the
     // keys unique (atomicOr return values) — known on the device only; a probe
     // that finds otherwise flags it and the host then builds the real table
     // (semi_table_materialize) and re-runs that probe.  No host sync here.
@@ -1152,6 +1182,9 @@ struct FinalParams {
   KeyOut keys[kMaxKeys];
   AggOut aggs[32];
   unsigned long long* counter;
+  u32 direct, cnt_acc;  // direct table: occupied iff acc[cnt_acc] != 0; key = key_min + slot
+  long long key_min;
+  u64 null_slot;
 };
 
 // Output rows are reserved per BLOCK and iteration (one global atomic per 256
@@ -1164,7 +1197,7 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const u64 cap = (f.t.cap + 255) / 256 * 256;  // whole blocks stay in the loop (block barriers)
   for (u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += stride) {
-    const bool occ = s < f.t.cap && f.t.state[s] == 2;
+    const bool occ = s < f.t.cap && (f.direct ? f.t.acc[(s * f.nacc + f.cnt_acc) * 2] != 0 : f.t.state[s] == 2);
     const u32 m = __ballot_sync(0xffffffffu, occ);
     if (lane == 0) s_warp[warp] = __popc(m);
     __syncthreads();
@@ -1182,7 +1215,8 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
     __syncthreads();  // s_warp / s_base are rewritten next iteration
     if (!occ) continue;
     u64 row = base + __popc(m & ((1u << lane) - 1));
-    const u64* kw = f.t.keys + s * f.kwa;
+    u64 dk[2] = {(u64)f.key_min + s, s == f.null_slot ? 1ull : 0ull};  // direct: key word, null word
+    const u64* kw = f.direct ? dk : f.t.keys + s * f.kwa;
     u64 nullw = kw[f.kwa - 1];
     for (u32 k = 0; k < f.nkeys; ++k) {
       const KeyOut& ko = f.keys[k];
@@ -1237,6 +1271,20 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
       }
       if (ao.validity && valid) bm_set_atomic(ao.validity, row);
     }
+  }
+}
+
+// direct aggregation table: every slot's accumulators start at their identity
+struct AccOps {
+  uint8_t op[kMaxAcc];
+};
+__global__ void k_acc_init(u64* acc, u64 slots, u32 nacc, AccOps ops) {
+  const u64 n = slots * nacc;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    u64 lo, hi;
+    acc_identity(ops.op[i % nacc], lo, hi);
+    acc[2 * i] = lo;
+    acc[2 * i + 1] = hi;
   }
 }
 
@@ -1363,6 +1411,55 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
   setup(G);
   const u32 kwa = p.key_words + 1;
 
+  // ---- DIRECT aggregation: one integer key whose values over the passing
+  // rows span a dense range (e.g. group by orderkey: 15M groups at SF10).
+  // A range pass (min / max of the key, only the key and predicate columns
+  // are read) sizes a table of one slot per key value; no hash, no claim
+  // protocol, no regrowth re-runs, and clustered keys update neighbouring
+  // slots.  Only for final aggregates with a Count(*) accumulator (it marks
+  // the occupied slots) and inputs large enough to pay for the range pass.
+  bool direct = false;
+  long long kmin = 0;
+  uint64_t R = 0;
+  u32 cnt_idx = 0;
+  {
+    static const bool no_direct = [] { const char* e = getenv("TQ_DIRECT"); return e && e[0] == '0'; }();
+    bool has_cnt = false;
+    for (u32 i = 0; i < nacc; ++i)
+      if (acc[i].op == ACC_CNT && acc[i].kind == K_NONE) { has_cnt = true; cnt_idx = i; break; }
+    if (!no_direct && ap && has_cnt && kh.size() == 1 && P.pb.root(kh[0]).cls == C_I && in->rows >= (4ull << 20)) {
+      Plan Lr;
+      plan_launch(c, in, P, Lr, 64, st);
+      set_keys(Lr.p, P.pb, kh);
+      Lr.p.dest_kind = DEST_RANGE;
+      std::vector<int> need = kh;
+      if (P.has_pred) need.push_back(P.pred_h);
+      Lr.p.load_mask = P.pb.column_deps(need);
+      long long* kr = (long long*)dalloc(c, 32, st);
+      const long long init[3] = {0x7fffffffffffffffll, (long long)0x8000000000000000ull, 0};
+      TQ_CUDA(cudaMemcpyAsync(kr, init, 24, cudaMemcpyHostToDevice, st));
+      Lr.p.key_range = kr;
+      launch(c, SINK_COUNT, Lr, P, st);
+      long long mn, mx;
+      {
+        std::lock_guard<std::mutex> g(c->mu);
+        TQ_CUDA(cudaMemcpyAsync(c->pinned, kr, 24, cudaMemcpyDeviceToHost, st));
+        { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+        mn = ((long long*)c->pinned)[0];
+        mx = ((long long*)c->pinned)[1];
+      }
+      dfree(c, kr, 32, st);
+      const uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
+      const uint64_t span = mx >= mn ? (uint64_t)mx - (uint64_t)mn + 1 : 0;  // 0: no non-null key
+      if ((mx < mn || (span != 0 && span <= 2 * in->rows)) && (span + 1) * nacc * 16 <= room / 2) {
+        direct = true;
+        kmin = mx >= mn ? mn : 0;
+        R = span;
+      }
+    }
+  }
+  if (direct) setup(0);
+
   // ---- global table; grows x4 and re-runs on overflow (on_oom-style retry)
   // initial table for min(rows, 1M) groups at load <= 0.5
   uint64_t cap = 1024;
@@ -1375,7 +1472,44 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
   uint64_t ngroups = 0;
   AggTable t{};
   uint64_t tbytes = 0;
-  for (int attempt = 0;; ++attempt) {
+  if (direct) {
+    // slots [0, R) = key values kmin .., slot R = the null key
+    cap = R + 1;
+    tbytes = cap * nacc * 16 + 64;
+    uint8_t* base = (uint8_t*)dalloc(c, tbytes, st);
+    t.state = (uint32_t*)base;  // (no state words: freed through this base)
+    t.keys = nullptr;
+    t.acc = (u64*)base;
+    t.cap = cap;
+    uint8_t* tail = base + cap * nacc * 16;
+    t.nused = (unsigned long long*)tail;
+    t.overflow = (uint32_t*)(tail + 8);
+    TQ_CUDA(cudaMemsetAsync(tail, 0, 16, st));
+    bool minmax = false;
+    AccOps ops{};
+    for (u32 i = 0; i < nacc; ++i) {
+      ops.op[i] = acc[i].op;
+      minmax |= acc[i].op == ACC_MIN_I || acc[i].op == ACC_MAX_I || acc[i].op == ACC_MIN_F || acc[i].op == ACC_MAX_F;
+    }
+    if (minmax) {
+      k_acc_init<<<(u32)std::min<uint64_t>((cap * nacc + 255) / 256, (uint64_t)c->sms * 8), 256, 0, st>>>(t.acc, cap,
+                                                                                                       nacc, ops);
+      counted_launch(c);
+    } else {
+      TQ_CUDA(cudaMemsetAsync(t.acc, 0, cap * nacc * 16, st));
+    }
+    t.direct = 1;
+    t.cnt_acc = cnt_idx;
+    t.key_min = kmin;
+    t.direct_slots = R;
+    p.agg = t;
+    launch(c, SINK_AGG, L, P, st);
+    std::lock_guard<std::mutex> g(c->mu);
+    TQ_CUDA(cudaMemcpyAsync(c->pinned, tail, 16, cudaMemcpyDeviceToHost, st));
+    { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+    ngroups = ((uint64_t*)c->pinned)[0];
+  }
+  for (int attempt = 0; !direct; ++attempt) {
     tbytes = cap * 4 + cap * kwa * 8 + cap * std::max<u32>(1, nacc) * 16 + 64;
     uint8_t* base = (uint8_t*)dalloc(c, tbytes, st);
     t.state = (uint32_t*)base;
@@ -1477,6 +1611,10 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       ao.values = (uint8_t*)out->cols[f.nkeys + a].values;
       ao.validity = out->cols[f.nkeys + a].validity;
     }
+    f.direct = direct ? 1u : 0u;
+    f.cnt_acc = cnt_idx;
+    f.key_min = kmin;
+    f.null_slot = R;
     f.counter = (unsigned long long*)(t.nused + 0);  // reuse as output cursor
     TQ_CUDA(cudaMemsetAsync(t.nused, 0, 8, st));
     u32 nb = (u32)std::min<uint64_t>(2048, (cap + 255) / 256);

@@ -40,7 +40,9 @@ enum SinkKind { SINK_COUNT = 0, SINK_EMIT = 1, SINK_AGG = 2, SINK_BUILD = 3 };
 // FILTER/PARTITION/PROBE: two passes (COUNT then EMIT), stable order.
 // PROBE1: single EMIT pass for unique build keys (<= 1 match per row);
 //         output rows are reserved with a warp-aggregated atomic cursor.
-enum DestKind { DEST_FILTER = 0, DEST_PARTITION = 1, DEST_PROBE = 2, DEST_PROBE1 = 3, DEST_PEER = 4 };
+// RANGE (with SINK_COUNT): min / max of the first key word over passing rows
+//         (+ whether a key is null) -> key_range[0..2]; sizes direct aggregation.
+enum DestKind { DEST_FILTER = 0, DEST_PARTITION = 1, DEST_PROBE = 2, DEST_PROBE1 = 3, DEST_PEER = 4, DEST_RANGE = 5 };
 constexpr int kMaxPeers = 16;       // DEST_PEER: ranks of one communicator
 constexpr int kMaxTailCtas = 512;   // DEST_PEER: per-source-rank tail slots in a receive window
 
@@ -79,11 +81,18 @@ struct JoinTable {
   // (wider keys): single-pass probes then walk each cluster to check
   uint32_t* dup_dev;
   uint64_t bloom_mask;  // words - 1 (power of two)
-  // exact membership bitmap for one-word keys in [0, 32 * (bloom_mask + 1)):
+  // exact membership bitmap for one-word keys in [0, exact_range):
   // bit k set <=> key k was inserted.  exact_flag (device): 0 = every key was
   // in range (the bitmap is exact), 1 = not; nullptr = not built
   uint32_t* exact_bits;
   uint32_t* exact_flag;
+  uint64_t exact_range;  // a multiple of 32
+  // direct-indexed table (one-word keys, no hash entries): direct[k] = the
+  // build row of key k, valid iff bit k of exact_bits is set (never
+  // initialised: the bitmap says which slots were written).  Usable when the
+  // bitmap is exact and the keys proved unique (dup_dev); otherwise a probe
+  // asks the host for the hash table.  nullptr = not built
+  uint32_t* direct;
 };
 
 enum OutSrc : uint8_t { OUT_OPND = 0, OUT_BUILD = 1 };
@@ -109,6 +118,19 @@ struct AccSpec {
   uint8_t _pad[3];
 };
 
+#ifdef __CUDACC__
+// Identity of an accumulator (16 B: lo, hi words).
+__host__ __device__ __forceinline__ void acc_identity(uint8_t op, unsigned long long& lo, unsigned long long& hi) {
+  switch (op) {
+    case ACC_MIN_I: lo = ~0ull; hi = 0x7fffffffffffffffull; break;
+    case ACC_MAX_I: lo = 0; hi = 0x8000000000000000ull; break;
+    case ACC_MIN_F: lo = 0x7ff0000000000000ull; hi = 0; break;
+    case ACC_MAX_F: lo = 0xfff0000000000000ull; hi = 0; break;
+    default: lo = 0; hi = 0;
+  }
+}
+#endif
+
 // Global aggregation hash table.
 struct AggTable {
   uint32_t* state;   // 0 empty, 1 writing, 2 ready
@@ -117,6 +139,14 @@ struct AggTable {
   uint64_t cap;      // power of two
   unsigned long long* nused;
   uint32_t* overflow;
+  // DIRECT aggregation (one integer key with a dense value range [key_min,
+  // key_min + direct_slots)): the accumulators of key k live in slot
+  // k - key_min (slot direct_slots = the null key); no state / key words; a
+  // group exists iff its Count(*) accumulator (index cnt_acc) is non-zero
+  uint32_t direct;
+  uint32_t cnt_acc;
+  long long key_min;
+  uint64_t direct_slots;
 };
 
 struct PipeParams {
@@ -191,6 +221,8 @@ struct PipeParams {
   // build_skip_aux: the Bloom / exact bits were set by an earlier range pass
   uint64_t slot_lo, slot_hi;
   uint32_t build_skip_aux;
+  // DEST_RANGE output: {min, max, any null} of the first key word
+  long long* key_range;
 };
 
 }  // namespace tq

@@ -358,3 +358,29 @@ def test_datagen_shard_bit_identical(ctx, t):
     for s in (0, 3):
         g = ctx.datagen(t, sf, shard=s, nshards=4).to_host()
         assert_batches_equal(g, O.datagen(t, sf, 4, s, 4), ordered=True)
+
+
+@pytest.mark.parametrize("case", ["clustered", "shuffled", "nulls", "sparse"])
+def test_aggregate_direct_dense_key(ctx, case):
+    """One integer group key over >= 4M rows: a range pass sizes a DIRECT
+    table (slot = key - min) when the keys are dense — clustered keys (like
+    lineitem by orderkey) are reduced per warp run before one atomic per run;
+    a null key gets its own slot; a sparse key range falls back to the hash
+    table.  Every path equals the oracle."""
+    rng = np.random.default_rng({"clustered": 1, "shuffled": 2, "nulls": 3, "sparse": 4}[case])
+    n = 4_500_000
+    if case == "sparse":
+        k = rng.integers(0, 1 << 40, n // 8).repeat(8)[:n]
+    else:
+        k = np.sort(rng.integers(-1000, n // 4, n))
+        if case == "shuffled":
+            k = rng.permutation(k)
+    valid = rng.random(n) >= 0.01 if case == "nulls" else None
+    v = rng.integers(-10**9, 10**9, n)
+    f = rng.integers(-400, 400, n) * 0.25  # exact in binary: float sums do not depend on the order
+    b = HostBatch(n, [HostBatch.col_i64(k.astype(np.int64), valid), HostBatch.col_dec(v.astype(np.int64)),
+                      HostBatch.col_f64(f, rng.random(n) >= 0.05)])
+    aggs = [(AGG_SUM, 1), (AGG_COUNT_STAR, 0), (AGG_MIN, 1), (AGG_MAX, 2), (AGG_AVG, 1), (AGG_SUM, 2),
+            (AGG_COUNT, 2), (AGG_MIN, 2)]
+    got = ctx.aggregate_execute(ctx.upload(b), [0], aggs).to_host()
+    assert_batches_equal(got, O.aggregate_execute(b, [0], aggs))
