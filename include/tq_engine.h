@@ -51,14 +51,23 @@ typedef struct tq_engine_opts {
   uint32_t inject_oom_mode;
   uint32_t inject_oom_count;
   char inject_oom_op[32];
+  /* distributed plans (comm with > 1 rank): */
+  uint32_t force_exchange;       /* 0 = exchange_decide; 1 = force Broadcast; 2 = force HashPartition */
+  uint32_t exchange_impl;        /* 0 = fused partition / broadcast over NVLink peer memory; 1 = NCCL */
+  uint64_t broadcast_threshold;  /* per worker, 0 = TQ_BROADCAST_THRESHOLD (16 MiB) */
 } tq_engine_opts;
 
 /* Input tables: tables[t] (t = 0 orders, 1 lineitem, 2 customer, 3 supplier,
  * 4 part, 5 partsupp, 6 nation, 7 region) are DEVICE batches; unused entries
  * may be zero.  With tables_on_host the engine first moves each scan batch to
  * the pinned Host pool so every scan task goes through load_to_device.
- * comm may be NULL (single worker); with a communicator the query runs as one
- * worker of a distributed plan (exchanges over NCCL).  The result is a HOST
+ * comm may be NULL (single worker); with a communicator of N > 1 ranks the
+ * query runs as one worker of its distributed plan: an AdaptiveExchange pair
+ * per join (estimates after 5% of the scan, all-gathered,
+ * tq_exchange_decide -> Broadcast the small side or HashPartition both, over
+ * the fused NVLink exchange), aggregates co-partitioned or pre-aggregated and
+ * exchanged on the group keys; every worker returns its share of the result
+ * (the union over workers is the query result; disjoint groups).  The result is a HOST
  * batch (free with tq_host_batch_free); metrics_json (may be NULL) receives
  * a JSON object of executor metrics. */
 tq_status tq_engine_run_query(tq_ctx* ctx, tq_comm* comm, int query, const tq_batch* tables,

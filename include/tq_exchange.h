@@ -68,6 +68,25 @@ uint64_t tq_comm_last_exchange_capacity(tq_comm* comm);
 uint64_t tq_comm_bytes_sent(tq_comm* comm);
 int tq_comm_size(tq_comm* comm);
 int tq_comm_rank(tq_comm* comm);
+/* All-gather `count` u64 per rank through the communicator (host buffers:
+ * in[count] -> out[nranks * count], rank order).  Collective; blocks. */
+tq_status tq_comm_allgather_host_u64(tq_comm* comm, const uint64_t* in, uint64_t* out, uint64_t count, void* stream);
+
+/* ---- AdaptiveExchange control: pure functions, the same
+ * code on every worker (the engine's exchange pairs and the Python mirror,
+ * paper_2508_05029_b200/exchange.py). */
+#define TQ_SAMPLE_FRACTION 0.05
+#define TQ_BROADCAST_THRESHOLD (16ull << 20)    /* 16 MiB per worker */
+/* exchange_phase1: once scan progress >= sample_fraction (or the scan is
+ * complete: progress >= 1) returns 1 with *estimate = bytes_so_far /
+ * progress (0 for an empty finished input); 0 = not yet. */
+int tq_exchange_phase1(uint64_t bytes_so_far, double progress, double sample_fraction, uint64_t* estimate);
+enum { TQ_XCHG_HASH_PARTITION = 0, TQ_XCHG_BROADCAST = 1 };
+/* exchange_decide: est0 / est1 = every worker's estimate of side 0 / 1 (n
+ * each).  Broadcast of the smaller side (*broadcast_side, ties -> side 0)
+ * if min(totals) <= threshold * n, else HashPartition both.  Deterministic. */
+int tq_exchange_decide(const uint64_t* est0, const uint64_t* est1, int n, uint64_t threshold, int* broadcast_side,
+                       uint64_t* total0, uint64_t* total1);
 
 #ifdef __cplusplus
 }

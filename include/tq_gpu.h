@@ -106,6 +106,18 @@ tq_status tq_join_build_semi(tq_ctx* ctx, const tq_batch* build, const uint32_t*
                              tq_join_table** out, void* stream);
 tq_status tq_pipeline_build_semi(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
                                  uint32_t nkeys, tq_join_table** out, void* stream);
+/* tq_pipeline_build / _semi with the table's Bloom filter sized for
+ * bloom_keys (>= rows; 0 = rows): a capacity every worker agrees on, so the
+ * workers' filters can be all-gathered as one partitioned LIP filter. */
+tq_status tq_pipeline_build_ex(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
+                               uint32_t nkeys, uint64_t bloom_keys, int semi, tq_join_table** out, void* stream);
+/* Size estimate of pred / exprs over `in` without materialising it: one
+ * COUNT pass over the predicate columns -> *out_rows, and the output row
+ * width of exprs -> *out_row_bytes (exprs NULL: every input column).  Feeds
+ * exchange_phase1 for an exchange side whose filter / projection is fused
+ * into the exchange kernel. */
+tq_status tq_pipeline_estimate(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                               uint32_t nexprs, uint64_t* out_rows, uint64_t* out_row_bytes, void* stream);
 /* join_execute probe side: inner equi-join, null keys never match; output =
  * build columns then probe columns. */
 tq_status tq_join_probe(tq_ctx* ctx, const tq_join_table* table, const tq_batch* probe, const uint32_t* keys,
@@ -123,6 +135,13 @@ typedef struct tq_agg_state tq_agg_state;
 tq_status tq_agg_create(tq_ctx* ctx, const tq_expr* pred, const tq_expr* exprs, uint32_t nexprs, const uint32_t* keys,
                         uint32_t nkeys, const tq_agg* aggs, uint32_t naggs, tq_agg_state** out);
 tq_status tq_agg_update(tq_agg_state* state, const tq_batch* in, void* stream);
+/* Two-phase use across workers (local pre-aggregation, exchange
+ * of the partials on the group keys, merge): take_partial merges the
+ * accumulated partials into ONE partial batch (keys, then one raw accumulator
+ * per column) and clears them; add_partial appends a partial batch (e.g.
+ * received from other workers, possibly 0 rows) to be merged by finalize. */
+tq_status tq_agg_take_partial(tq_agg_state* state, tq_batch* out, void* stream);
+tq_status tq_agg_add_partial(tq_agg_state* state, const tq_batch* partial, void* stream);
 tq_status tq_agg_finalize(tq_agg_state* state, tq_batch* out, void* stream);
 void tq_agg_destroy(tq_agg_state* state);
 

@@ -110,6 +110,14 @@ struct Task {
   int kind = 0;  // op-defined
 };
 
+struct XPair {
+  int decide_turn = 0;
+  bool est_ready[2] = {false, false};
+  uint64_t est[2] = {0, 0};
+  bool decide_submitted = false, decided = false;
+  int strategy = TQ_XCHG_HASH_PARTITION, bcast_side = -1;
+  uint64_t totals[2] = {0, 0};
+};
 class Op {
  public:
   Op(Runtime* rt, std::string name, int depth, double mult) : rt(rt), name(std::move(name)), depth(depth), mult(mult) {}
@@ -243,6 +251,13 @@ class Runtime {
       m_preloads{0}, m_load_bytes{0}, m_peak{0}, m_injected{0};
   uint64_t spilling_bytes = 0;           // Device bytes of marked victims not yet freed (under mu)
   std::deque<std::vector<HP>> spill_q;   // watermark spills for the memory executor (under mu)
+  struct Decision {
+    std::string name;
+    int strategy, side;
+    uint64_t total0, total1;
+  };
+  std::vector<Decision> decisions;  // exchange_decide outcomes (metrics)
+  std::vector<std::unique_ptr<XPair>> pairs;
   std::vector<HP> keep;  // handles alive until the query ends (build sides)
   std::vector<tq_batch> results;
 
@@ -633,6 +648,7 @@ class ScanOp : public Op {
       if (table.rows == 0) break;
     }
     for (HP& h : hs) out_q.push_back(h);
+    nbatches = hs.size();
     finished = true;
     // pushes happen outside the coordinator lock
     pending = std::move(hs);
@@ -651,6 +667,7 @@ class ScanOp : public Op {
   tq_batch table;
   std::deque<std::vector<tq_column>> views;
   std::vector<HP> out_q, pending;
+  uint64_t nbatches = 0;  // batches this scan publishes (phase-1 progress of the exchanges it drives)
 };
 
 // Filter -> Project (one fused GPU pipeline per input batch).  A task takes up
@@ -717,10 +734,19 @@ class PipeOp : public Op {
 };
 
 // Join build side: waits for EndOfStream, concatenates, builds the table
+class XSideOp;
+uint64_t side_capacity(const XSideOp* x);
+
 class BuildOp : public Op {
  public:
-  BuildOp(Runtime* rt, std::string n, int depth, Holder* in, EB* pred, std::vector<uint32_t> keys)
-      : Op(rt, std::move(n), depth, 3.0), in(in), pred(pred ? *pred : EB()), has_pred(pred), keys(std::move(keys)) {}
+  // semi: a semi-join build (no build columns are taken); bloom_from: the
+  // exchange side that produced this build's input — its agreed window
+  // capacity sizes the table's Bloom filter so the workers' filters can be
+  // all-gathered as one partitioned LIP filter (tq_comm_gather_table_blooms)
+  BuildOp(Runtime* rt, std::string n, int depth, Holder* in, EB* pred, std::vector<uint32_t> keys, bool semi = false,
+          XSideOp* bloom_from = nullptr)
+      : Op(rt, std::move(n), depth, 3.0), in(in), pred(pred ? *pred : EB()), has_pred(pred), keys(std::move(keys)),
+        semi(semi), bloom_from(bloom_from) {}
   void poll(std::vector<Task>& ts) override {
     while (!in->empty()) got.push_back(in->pop());
     if (in->closed() && !submitted) {
@@ -751,7 +777,9 @@ class BuildOp : public Op {
     }
     tq_expr pe = pred.e();
     tq_join_table* jt = nullptr;
-    check(tq_pipeline_build(rt->ctx, &b->dev, has_pred ? &pe : nullptr, keys.data(), (uint32_t)keys.size(), &jt, st));
+    const uint64_t bloom_keys = bloom_from ? side_capacity(bloom_from) : 0;
+    check(tq_pipeline_build_ex(rt->ctx, &b->dev, has_pred ? &pe : nullptr, keys.data(), (uint32_t)keys.size(),
+                               bloom_keys, semi ? 1 : 0, &jt, st));
     cudaStreamSynchronize(st);
     std::lock_guard<std::mutex> g(rt->mu);
     b->pins++;  // the probe gathers build columns by row id until the query ends
@@ -767,6 +795,8 @@ class BuildOp : public Op {
   EB pred;
   bool has_pred;
   std::vector<uint32_t> keys;
+  bool semi;
+  XSideOp* bloom_from;
   std::vector<HP> got;
   bool submitted = false, ready = false;
   HP build;
@@ -805,13 +835,21 @@ class ProbeOp : public Op {
   std::vector<uint32_t> keys, build_cols;
 };
 
+bool pair_hash_partitioned(const XPair* x);
+
 // Hash aggregate: one GPU update per batch into partial accumulators
 // (serialised per operator), then finalize after EndOfStream.
+// Distributed (dist): the aggregate's input must be partitioned on the group
+// keys.  When it is — the join feeding it was hash-partitioned
+// on a group key (copart decided HashPartition) — each worker's finalize is
+// final; otherwise the worker's partial (keys + raw accumulators) is
+// hash-partitioned on the group keys over the fused exchange and the
+// received partials are merged (local pre-aggregation).
 class AggOp : public Op {
  public:
   AggOp(Runtime* rt, std::string n, int depth, Holder* in, EB* pred, std::vector<EB> exprs, std::vector<uint32_t> keys,
-        std::vector<tq_agg> aggs)
-      : Op(rt, std::move(n), depth, 2.0), in(in) {
+        std::vector<tq_agg> aggs, bool dist = false, const XPair* copart = nullptr, int turn = -1)
+      : Op(rt, std::move(n), depth, 2.0), in(in), nkeys((uint32_t)keys.size()), dist(dist), copart(copart), turn(turn) {
     std::vector<tq_expr> ex;
     for (auto& e : exprs) ex.push_back(e.e());
     EB p = pred ? *pred : EB();
@@ -829,7 +867,8 @@ class AggOp : public Op {
       ts.push_back(std::move(t));
       return;
     }
-    if (in->closed() && !final_submitted) {
+    // (distributed: the final step is a collective, taken in DAG order)
+    if (in->closed() && !final_submitted && (!dist || rt->exchange_turn == turn)) {
       final_submitted = true;
       Task t;
       t.op = this;
@@ -849,6 +888,20 @@ class AggOp : public Op {
       }
       return;
     }
+    if (dist && !(copart && pair_hash_partitioned(copart))) {
+      tq_batch part{}, recv{};
+      check(tq_agg_take_partial(state, &part, st));
+      std::vector<uint32_t> kk(nkeys);
+      for (uint32_t k = 0; k < nkeys; ++k) kk[k] = k;
+      tq_status r = tq_pipeline_partition_exchange(rt->comm, &part, nullptr, nullptr, 0, kk.data(), nkeys, nullptr,
+                                                   &recv, st);
+      tq_batch_free(rt->ctx, &part);
+      check(r);
+      r = tq_agg_add_partial(state, &recv, st);
+      cudaStreamSynchronize(st);
+      tq_batch_free(rt->ctx, &recv);
+      check(r);
+    }
     tq_batch o{};
     check(tq_agg_finalize(state, &o, st));
     cudaStreamSynchronize(st);
@@ -856,76 +909,271 @@ class AggOp : public Op {
     out->push(rt->adopt(o, false));
     std::lock_guard<std::mutex> g(rt->mu);
     done = true;
+    if (dist) rt->exchange_turn++;
   }
   Holder* in;
+  uint32_t nkeys;
+  bool dist;
+  const XPair* copart;
+  int turn;
   tq_agg_state* state = nullptr;
   bool final_submitted = false, done = false;
 };
 
-// Exchange: HashPartition on key columns or Broadcast, one
-// NCCL collective per exchange after EndOfStream, in DAG order on all workers.
-class ExchangeOp : public Op {
+// ------------------------------------------------------------------ AdaptiveExchange
+// One exchange PAIR per distributed join: side 0 and side 1 feed the join's
+// two inputs.  Phase 1: each side, once its driving scan passed
+// TQ_SAMPLE_FRACTION (or ended), estimates its total bytes
+// (tq_exchange_phase1); the DecideOp all-gathers both sides' estimates of every
+// worker and applies tq_exchange_decide — the same pure function on every
+// worker, so every worker takes the same decision.  Phase 2 (after the side's
+// EndOfStream): Broadcast the smaller side (the other stays local) or
+// HashPartition both on the join keys (fnv1a64 mod N).  Every collective (a
+// decide, a side's data movement, a distributed aggregate's exchange) runs in
+// DAG order on every worker (rt->exchange_turn), as NCCL requires.
+bool pair_hash_partitioned(const XPair* x) { return x->decided && x->strategy == TQ_XCHG_HASH_PARTITION; }
+
+class DecideOp : public Op {
  public:
-  ExchangeOp(Runtime* rt, std::string n, int depth, Holder* in, int turn, bool broadcast, std::vector<uint32_t> keys)
-      : Op(rt, std::move(n), depth, 1.5), in(in), turn(turn), broadcast(broadcast), keys(std::move(keys)) {}
+  DecideOp(Runtime* rt, std::string n, XPair* x) : Op(rt, std::move(n), 50, 1.0), x(x) {}
   void poll(std::vector<Task>& ts) override {
-    while (!in->empty()) got.push_back(in->pop());
-    if (in->closed() && !submitted && rt->exchange_turn == turn) {
-      submitted = true;
+    if (!x->decide_submitted && x->est_ready[0] && x->est_ready[1] && rt->exchange_turn == x->decide_turn) {
+      x->decide_submitted = true;
       Task t;
       t.op = this;
-      t.inputs = got;
       ts.push_back(std::move(t));
     }
-    if (done) finished = true;
+    if (x->decided) finished = true;
   }
   bool splittable(const Task&) const override { return false; }
-  void run(Task& t, cudaStream_t st) override {
-    tq_batch cat{};
-    bool owned = false;
-    if (t.inputs.size() == 1) {
-      cat = t.inputs[0]->dev;
-    } else {
-      std::vector<tq_batch> bs;
-      for (HP& h : t.inputs) bs.push_back(h->dev);
-      check(tq_concat(rt->ctx, bs.data(), (uint32_t)bs.size(), &cat, st));
-      owned = true;
+  void run(Task&, cudaStream_t st) override {
+    const int n = tq_comm_size(rt->comm);
+    uint64_t mine[2], est0[kMaxRanks], est1[kMaxRanks], all[2 * kMaxRanks];
+    {
+      std::lock_guard<std::mutex> g(rt->mu);
+      mine[0] = x->est[0];
+      mine[1] = x->est[1];
     }
+    check(tq_comm_allgather_host_u64(rt->comm, mine, all, 2, st));
+    for (int r = 0; r < n; ++r) {
+      est0[r] = all[2 * r];
+      est1[r] = all[2 * r + 1];
+    }
+    int side = -1;
+    uint64_t t0 = 0, t1 = 0;
+    int strategy = tq_exchange_decide(est0, est1, n, rt->opts.broadcast_threshold ? rt->opts.broadcast_threshold
+                                                                                  : TQ_BROADCAST_THRESHOLD,
+                                      &side, &t0, &t1);
+    // forced strategies (strategy-equivalence tests)
+    if (rt->opts.force_exchange == 1) {
+      strategy = TQ_XCHG_BROADCAST;
+      side = t0 <= t1 ? 0 : 1;
+    } else if (rt->opts.force_exchange == 2) {
+      strategy = TQ_XCHG_HASH_PARTITION;
+      side = -1;
+    }
+    std::lock_guard<std::mutex> g(rt->mu);
+    x->strategy = strategy;
+    x->bcast_side = side;
+    x->totals[0] = t0;
+    x->totals[1] = t1;
+    x->decided = true;
+    rt->exchange_turn++;
+    rt->decisions.push_back({name, strategy, side, t0, t1});
+  }
+  XPair* x;
+  static constexpr int kMaxRanks = 64;
+};
+
+// Merge the input batches of one exchange side: consecutive row-group views
+// of one table are one larger view (zero copy); anything else is
+// concatenated.  Returns true when `out` is a new owned batch.
+bool merge_inputs(Runtime* rt, std::vector<HP>& in, tq_batch& out, std::vector<tq_column>& cols, cudaStream_t st) {
+  if (in.size() == 1) {
+    out = in[0]->dev;
+    return false;
+  }
+  bool contiguous = !in.empty();
+  for (size_t i = 0; contiguous && i < in.size(); ++i) {
+    const tq_batch& b = in[i]->dev;
+    contiguous = in[i]->view && b.ncols == in[0]->dev.ncols;
+    if (!contiguous || i == 0) continue;
+    const tq_batch& a = in[i - 1]->dev;
+    for (uint32_t c = 0; c < b.ncols && contiguous; ++c) {
+      const size_t w = width_of(b.cols[c].kind);
+      contiguous = b.cols[c].kind != TQ_UTF8 && (const uint8_t*)b.cols[c].values == (const uint8_t*)a.cols[c].values + a.rows * w &&
+                   (a.rows % 8 == 0) && ((b.cols[c].validity == nullptr) == (a.cols[c].validity == nullptr)) &&
+                   (!b.cols[c].validity || b.cols[c].validity == a.cols[c].validity + a.rows / 8);
+    }
+  }
+  if (contiguous) {
+    out = in[0]->dev;
+    cols.assign(out.cols, out.cols + out.ncols);
+    uint64_t rows = 0;
+    for (HP& h : in) rows += h->dev.rows;
+    for (auto& c : cols) c.values_bytes = rows * width_of(c.kind);
+    out.rows = rows;
+    out.cols = cols.data();
+    out.owner = nullptr;
+    return false;
+  }
+  std::vector<tq_batch> bs;
+  for (HP& h : in) bs.push_back(h->dev);
+  check(tq_concat(rt->ctx, bs.data(), (uint32_t)bs.size(), &out, st));
+  return true;
+}
+
+class XSideOp : public Op {
+ public:
+  // pred / exprs: filter + projection fused into the exchange kernel (none:
+  // the input columns as they are); keys: hash-partition keys (indices into
+  // the side's output columns); lip: HashPartition drops rows whose keys
+  // miss the other side's (already exchanged) join table — the partitioned
+  // LIP filter; src: the scan whose progress drives phase 1
+  XSideOp(Runtime* rt, std::string n, int depth, XPair* x, int side, int turn, Holder* in, class ScanOp* src,
+          EB* pred, std::vector<EB> exprs, std::vector<uint32_t> keys, BuildOp* lip)
+      : Op(rt, std::move(n), depth, 1.5), x(x), side(side), turn(turn), in(in), src(src), pred(pred ? *pred : EB()),
+        has_pred(pred), exprs(std::move(exprs)), keys(std::move(keys)), lip(lip) {}
+  bool fused() const { return has_pred || !exprs.empty(); }
+  void poll(std::vector<Task>& ts) override;
+  bool splittable(const Task&) const override { return false; }
+  void run(Task& t, cudaStream_t st) override;
+  XPair* x;
+  int side, turn;
+  Holder* in;
+  class ScanOp* src;
+  EB pred;
+  bool has_pred;
+  std::vector<EB> exprs;
+  std::vector<uint32_t> keys;
+  BuildOp* lip;
+  std::vector<HP> got;
+  uint64_t bytes = 0;
+  double est_progress = 0;
+  bool est_submitted = false, submitted = false, done = false;
+  uint64_t out_capacity = 0;  // agreed row capacity of this side's fused HashPartition (0: none)
+};
+uint64_t side_capacity(const XSideOp* x) { return x->out_capacity; }
+
+void XSideOp::poll(std::vector<Task>& ts) {
+  while (!in->empty()) {
+    HP h = in->pop();
+    bytes += h->bytes;
+    got.push_back(h);
+  }
+  // ---- phase 1: a local estimate once the driving scan
+  // passed the sample fraction, or this side's input ended
+  if (!x->est_ready[side] && !est_submitted) {
+    const uint64_t total = src ? src->nbatches : 0;
+    const double progress = in->closed() ? 1.0 : total ? (double)got.size() / (double)total : 0.0;
+    if (progress >= 1.0 || progress >= TQ_SAMPLE_FRACTION) {
+      if (fused() && !got.empty()) {
+        // the rows this side will ship are pred / exprs of its input: measured
+        // on the batches so far (a COUNT pass over the predicate columns)
+        est_submitted = true;
+        est_progress = progress;
+        Task t;
+        t.op = this;
+        t.kind = 1;
+        t.inputs = got;
+        ts.push_back(std::move(t));
+      } else {
+        uint64_t e = 0;
+        tq_exchange_phase1(bytes, progress, TQ_SAMPLE_FRACTION, &e);
+        x->est[side] = e;
+        x->est_ready[side] = true;
+      }
+    }
+  }
+  // ---- phase 2: the data movement, after EndOfStream, in DAG order
+  const bool lip_wait = lip && x->decided && x->strategy == TQ_XCHG_HASH_PARTITION && !lip->ready &&
+                        rt->opts.exchange_impl == 0;
+  if (x->decided && x->est_ready[side] && in->closed() && !submitted && rt->exchange_turn == turn && !lip_wait) {
+    submitted = true;
+    Task t;
+    t.op = this;
+    t.inputs = got;
+    ts.push_back(std::move(t));
+  }
+  if (done) finished = true;
+}
+
+void XSideOp::run(Task& t, cudaStream_t st) {
+  std::vector<tq_expr> ex;
+  for (auto& e : exprs) ex.push_back(e.e());
+  tq_expr pe = pred.e();
+  const tq_expr* pp = has_pred ? &pe : nullptr;
+  const tq_expr* ep = ex.empty() ? nullptr : ex.data();
+  if (t.kind == 1) {  // phase-1 estimate of a fused side
+    uint64_t out_bytes = 0;
+    for (HP& h : t.inputs) {
+      uint64_t rows = 0, rb = 0;
+      check(tq_pipeline_estimate(rt->ctx, &h->dev, pp, ep, (uint32_t)ex.size(), &rows, &rb, st));
+      out_bytes += rows * rb;
+    }
+    uint64_t e = 0;
+    tq_exchange_phase1(out_bytes, est_progress, TQ_SAMPLE_FRACTION, &e);
+    std::lock_guard<std::mutex> g(rt->mu);
+    x->est[side] = e;
+    x->est_ready[side] = true;
+    return;
+  }
+  const bool bcast = x->strategy == TQ_XCHG_BROADCAST;
+  const bool local = bcast && side != x->bcast_side;
+  std::vector<tq_column> vcols;
+  tq_batch merged{};
+  bool owned = false;
+  if (local && !fused()) {
+    // the side that stays local passes its batches through untouched
+    for (HP& h : t.inputs) out->push(h);
+  } else {
+    owned = merge_inputs(rt, t.inputs, merged, vcols, st);
     tq_batch o{};
-    if (!rt->comm) {
-      if (owned) o = cat;
-      else check(tq_slice(rt->ctx, &cat, 0, cat.rows, &o, st));
-      owned = false;
-    } else if (broadcast) {
-      check(tq_comm_allgather(rt->comm, &cat, &o, nullptr, st));
+    tq_status r = TQ_OK;
+    const bool fused_impl = rt->opts.exchange_impl == 0;
+    if (local) {
+      r = tq_pipeline_materialize(rt->ctx, &merged, pp, ep, (uint32_t)ex.size(), &o, st);
+    } else if (bcast) {
+      if (fused_impl) {
+        r = tq_pipeline_broadcast(rt->comm, &merged, pp, ep, (uint32_t)ex.size(), &o, st);
+      } else {
+        tq_batch m{};
+        r = tq_pipeline_materialize(rt->ctx, &merged, pp, ep, (uint32_t)ex.size(), &m, st);
+        if (r == TQ_OK) r = tq_comm_allgather(rt->comm, &m, &o, nullptr, st);
+        cudaStreamSynchronize(st);
+        tq_batch_free(rt->ctx, &m);
+      }
+    } else if (fused_impl) {
+      tq_bloom* bloom = nullptr;
+      if (lip) r = tq_comm_gather_table_blooms(rt->comm, lip->table, &bloom, st);
+      if (r == TQ_OK)
+        r = tq_pipeline_partition_exchange(rt->comm, &merged, pp, ep, (uint32_t)ex.size(), keys.data(),
+                                           (uint32_t)keys.size(), bloom, &o, st);
+      out_capacity = tq_comm_last_exchange_capacity(rt->comm);
+      cudaStreamSynchronize(st);
+      if (bloom) tq_bloom_destroy(bloom);
     } else {
-      int n = 0;
-      std::vector<uint64_t> offs(257);
+      const int n = tq_comm_size(rt->comm);
+      std::vector<uint64_t> offs(n + 1);
       tq_batch part{};
-      // nparts = world size (the communicator's n, recovered from the allgather header size)
-      n = nranks;
-      check(tq_hash_partition(rt->ctx, &cat, keys.data(), (uint32_t)keys.size(), (uint32_t)n, &part, offs.data(), st));
-      check(tq_comm_exchange(rt->comm, &part, offs.data(), &o, nullptr, st));
+      r = tq_pipeline_partition(rt->ctx, &merged, pp, ep, (uint32_t)ex.size(), keys.data(), (uint32_t)keys.size(),
+                                (uint32_t)n, &part, offs.data(), st);
+      if (r == TQ_OK) r = tq_comm_exchange(rt->comm, &part, offs.data(), &o, nullptr, st);
       cudaStreamSynchronize(st);
       tq_batch_free(rt->ctx, &part);
     }
     cudaStreamSynchronize(st);
-    if (owned) tq_batch_free(rt->ctx, &cat);
+    if (owned) tq_batch_free(rt->ctx, &merged);
+    check(r);
+    stat.rows_out += o.rows;
+    out->push(rt->adopt(o, false));
     for (HP& h : t.inputs)
       if (!h->view) rt->free_handle(h);
-    out->push(rt->adopt(o, false));
-    std::lock_guard<std::mutex> g(rt->mu);
-    done = true;
-    rt->exchange_turn++;
   }
-  Holder* in;
-  int turn;
-  bool broadcast;
-  std::vector<uint32_t> keys;
-  std::vector<HP> got;
-  bool submitted = false, done = false;
-  int nranks = 1;
-};
+  std::lock_guard<std::mutex> g(rt->mu);
+  done = true;
+  rt->exchange_turn++;
+}
 
 // Sink: collects the query result
 class SinkOp : public Op {
@@ -949,13 +1197,14 @@ struct Plan {
   Runtime* rt;
   const tq_batch* tables;
   std::vector<ScanOp*> scans;
-  std::vector<Op*> wiring;  // ops whose `out` must be connected
+  std::map<Holder*, ScanOp*> scan_of;
   int turns = 0;
   Holder* scan(int t) {
     if (!tables[t].cols) fail(TQ_INVALID_PLAN, "query needs table " + std::to_string(t));
     ScanOp* s = rt->op<ScanOp>("scan" + std::to_string(t), &tables[t]);
     s->out = rt->holder();
     scans.push_back(s);
+    scan_of[s->out] = s;
     return s->out;
   }
   template <class T>
@@ -963,12 +1212,24 @@ struct Plan {
     o->out = rt->holder();
     return o->out;
   }
-  Holder* exchange(Holder* in, int depth, bool broadcast, std::vector<uint32_t> keys) {
-    if (!rt->comm) return in;
-    auto* x = rt->op<ExchangeOp>("exchange" + std::to_string(turns), depth, in, turns, broadcast, std::move(keys));
-    turns++;
-    return wire(x);
+  // ---- distributed plans: one exchange pair per join (its decide is a
+  // collective turn), one turn per side's data movement, in DAG order
+  XPair* pair(const std::string& name) {
+    rt->pairs.emplace_back(new XPair());
+    XPair* x = rt->pairs.back().get();
+    x->decide_turn = turns++;
+    rt->op<DecideOp>("decide_" + name, x);
+    return x;
   }
+  Holder* side(XPair* x, int sd, const std::string& name, int depth, Holder* in, Holder* driving_scan, EB* pred,
+               std::vector<EB> exprs, std::vector<uint32_t> keys, BuildOp* lip = nullptr, XSideOp** op = nullptr) {
+    auto it = scan_of.find(driving_scan);
+    auto* o = rt->op<XSideOp>("xchg_" + name, depth, x, sd, turns++, in, it == scan_of.end() ? nullptr : it->second,
+                              pred, std::move(exprs), std::move(keys), lip);
+    if (op) *op = o;
+    return wire(o);
+  }
+  int agg_turn() { return turns++; }
 };
 
 EB rev() {  // ep * (1.00 - disc)
@@ -1007,7 +1268,6 @@ Holder* build_plan(Plan& P, int q) {
     EB fc;
     fc.cmp(TQ_EQ).col(2).i64(1);
     Holder* cf = P.wire(rt->op<PipeOp>("customer_f", 1, cu, &fc, std::vector<EB>{Col(0)}));
-    cf = P.exchange(cf, 2, true, {});
     auto* cb = rt->op<BuildOp>("customer_build", 3, cf, nullptr, std::vector<uint32_t>{0});
     Holder* od = P.scan(T_ORDERS);
     EB fo;
@@ -1015,13 +1275,11 @@ Holder* build_plan(Plan& P, int q) {
     Holder* of = P.wire(rt->op<ProbeOp>("orders_probe", 4, cb, od, &fo,
                                         std::vector<EB>{Col(O_ORDERKEY), Col(O_ORDERDATE), Col(O_SHIPPRIORITY), Col(O_CUSTKEY)},
                                         std::vector<uint32_t>{3}, std::vector<uint32_t>{}));
-    of = P.exchange(of, 5, false, {0});
     auto* ob = rt->op<BuildOp>("orders_build", 6, of, nullptr, std::vector<uint32_t>{0});
     Holder* li = P.scan(T_LINEITEM);
     EB fl;
     fl.cmp(TQ_GT).col(L_SHIPDATE).i64(9204);
     Holder* lf = P.wire(rt->op<PipeOp>("lineitem_f", 1, li, &fl, std::vector<EB>{Col(L_ORDERKEY), rev()}));
-    lf = P.exchange(lf, 5, false, {0});
     Holder* j = P.wire(rt->op<ProbeOp>("lineitem_probe", 7, ob, lf, nullptr, std::vector<EB>{}, std::vector<uint32_t>{0},
                                        std::vector<uint32_t>{1, 2}));
     // j: [o_orderdate, o_shippriority, l_orderkey, rev]
@@ -1088,6 +1346,167 @@ Holder* build_plan(Plan& P, int q) {
   fail(TQ_INVALID_PLAN, "unknown query " + std::to_string(q));
 }
 
+// Distributed plans (one worker per GPU, each over its own
+// row-group subset): an exchange pair before every join (broadcast the small
+// side or hash-partition both, decided at run time from the workers'
+// estimates), aggregates either co-partitioned with the last join or
+// pre-aggregated and exchanged on the group keys.  Results: the union over
+// workers of their result batches (disjoint groups).
+Holder* build_dist_plan(Plan& P, int q) {
+  Runtime* rt = P.rt;
+  const std::vector<uint32_t> none;
+  if (q == 1 || q == 6) {
+    Holder* li = P.scan(T_LINEITEM);
+    EB f;
+    std::vector<EB> ex;
+    std::vector<uint32_t> keys;
+    std::vector<tq_agg> ag;
+    if (q == 6) {
+      f.land().land().cmp(TQ_GE).col(L_SHIPDATE).i64(8766).cmp(TQ_LT).col(L_SHIPDATE).i64(9131)
+          .land().land().cmp(TQ_GE).col(L_DISCOUNT).dec(5).cmp(TQ_LE).col(L_DISCOUNT).dec(7)
+          .cmp(TQ_LT).col(L_QUANTITY).dec(2400);
+      EB r;
+      r.ar(TQ_MUL).col(L_EXTPRICE).col(L_DISCOUNT);
+      ex = {r};
+      ag = {{TQ_AGG_SUM, 0}};
+    } else {
+      f.cmp(TQ_LE).col(L_SHIPDATE).i64(10471);
+      EB dp, ch;
+      dp.ar(TQ_MUL).col(L_EXTPRICE).ar(TQ_SUB).dec(100).col(L_DISCOUNT);
+      ch.ar(TQ_MUL).ar(TQ_MUL).col(L_EXTPRICE).ar(TQ_SUB).dec(100).col(L_DISCOUNT).ar(TQ_ADD).dec(100).col(L_TAX);
+      ex = {Col(L_RETURNFLAG), Col(L_LINESTATUS), Col(L_QUANTITY), Col(L_EXTPRICE), Col(L_DISCOUNT), dp, ch};
+      keys = {0, 1};
+      ag = {{TQ_AGG_SUM, 2}, {TQ_AGG_SUM, 3}, {TQ_AGG_SUM, 5}, {TQ_AGG_SUM, 6},
+            {TQ_AGG_AVG, 2}, {TQ_AGG_AVG, 3}, {TQ_AGG_AVG, 4}, {TQ_AGG_COUNT_STAR, 0}};
+    }
+    return P.wire(rt->op<AggOp>(q == 6 ? "q6_agg" : "q1_agg", 1, li, &f, ex, keys, ag, true, nullptr, P.agg_turn()));
+  }
+  if (q == 3) {
+    Holder* cu = P.scan(T_CUSTOMER);
+    Holder* od = P.scan(T_ORDERS);
+    Holder* li = P.scan(T_LINEITEM);
+    // join 1: customer_f (BUILDING) x orders on custkey — customer_f is broadcast at SF100 (24 MB)
+    XPair* x1 = P.pair("customer_orders");
+    EB fc;
+    fc.cmp(TQ_EQ).col(2).i64(1);
+    Holder* cfx = P.side(x1, 0, "customer_f", 2, cu, cu, &fc, {Col(0)}, {0});
+    Holder* odx = P.side(x1, 1, "orders", 2, od, od, nullptr, {}, {O_CUSTKEY});
+    auto* cb = rt->op<BuildOp>("customer_build", 3, cfx, nullptr, std::vector<uint32_t>{0}, /*semi=*/true);
+    EB fo;
+    fo.cmp(TQ_LT).col(O_ORDERDATE).i64(9204);
+    Holder* of = P.wire(rt->op<ProbeOp>("orders_probe", 4, cb, odx, &fo,
+                                        std::vector<EB>{Col(O_ORDERKEY), Col(O_ORDERDATE), Col(O_SHIPPRIORITY), Col(O_CUSTKEY)},
+                                        std::vector<uint32_t>{3}, none));
+    // join 2: orders_f x lineitem_f on orderkey — both hash-partitioned at SF100;
+    // lineitem_f's shuffle drops rows missing the orders_f tables (partitioned LIP)
+    XPair* x2 = P.pair("orders_lineitem");
+    XSideOp* ofs = nullptr;
+    Holder* ofx = P.side(x2, 0, "orders_f", 5, of, od, nullptr, {}, {0}, nullptr, &ofs);
+    auto* ob = rt->op<BuildOp>("orders_build", 6, ofx, nullptr, std::vector<uint32_t>{0}, false, ofs);
+    EB fl;
+    fl.cmp(TQ_GT).col(L_SHIPDATE).i64(9204);
+    Holder* lfx = P.side(x2, 1, "lineitem_f", 5, li, li, &fl, {Col(L_ORDERKEY), rev()}, {0}, ob);
+    Holder* j = P.wire(rt->op<ProbeOp>("lineitem_probe", 7, ob, lfx, nullptr, std::vector<EB>{}, std::vector<uint32_t>{0},
+                                       std::vector<uint32_t>{1, 2}));
+    // j: [o_orderdate, o_shippriority, l_orderkey, rev]; grouped by l_orderkey: co-partitioned with join 2
+    return P.wire(rt->op<AggOp>("q3_agg", 8, j, nullptr, std::vector<EB>{}, std::vector<uint32_t>{2, 0, 1},
+                                std::vector<tq_agg>{{TQ_AGG_SUM, 3}}, true, x2, P.agg_turn()));
+  }
+  if (q == 5) {
+    Holder* re = P.scan(T_REGION);
+    Holder* na = P.scan(T_NATION);
+    Holder* cu = P.scan(T_CUSTOMER);
+    Holder* od = P.scan(T_ORDERS);
+    Holder* li = P.scan(T_LINEITEM);
+    Holder* su = P.scan(T_SUPPLIER);
+    XPair* x1 = P.pair("region_nation");
+    EB fr;
+    fr.cmp(TQ_EQ).col(1).i64(2);
+    Holder* rx = P.side(x1, 0, "region_f", 1, re, re, &fr, {Col(0)}, {0});
+    Holder* nx = P.side(x1, 1, "nation", 1, na, na, nullptr, {}, {1});
+    auto* rb = rt->op<BuildOp>("region_build", 2, rx, nullptr, std::vector<uint32_t>{0}, true);
+    Holder* nf = P.wire(rt->op<ProbeOp>("nation_probe", 3, rb, nx, nullptr, std::vector<EB>{Col(0), Col(1)},
+                                        std::vector<uint32_t>{1}, none));
+    XPair* x2 = P.pair("nation_customer");
+    Holder* nfx = P.side(x2, 0, "nation_f", 4, nf, na, nullptr, {}, {0});
+    Holder* cux = P.side(x2, 1, "customer", 4, cu, cu, nullptr, {}, {1});
+    auto* nb = rt->op<BuildOp>("nation_build", 5, nfx, nullptr, std::vector<uint32_t>{0}, true);
+    Holder* cf = P.wire(rt->op<ProbeOp>("customer_probe", 6, nb, cux, nullptr, std::vector<EB>{Col(0), Col(1)},
+                                        std::vector<uint32_t>{1}, none));
+    XPair* x3 = P.pair("customer_orders");
+    Holder* cfx = P.side(x3, 0, "customer_f", 7, cf, cu, nullptr, {}, {0});
+    EB fo;
+    fo.land().cmp(TQ_GE).col(O_ORDERDATE).i64(8766).cmp(TQ_LT).col(O_ORDERDATE).i64(9131);
+    Holder* odx = P.side(x3, 1, "orders_f", 7, od, od, &fo, {Col(O_ORDERKEY), Col(O_CUSTKEY)}, {1});
+    auto* cb = rt->op<BuildOp>("customer_build", 8, cfx, nullptr, std::vector<uint32_t>{0});
+    Holder* of = P.wire(rt->op<ProbeOp>("orders_probe", 9, cb, odx, nullptr, std::vector<EB>{},
+                                        std::vector<uint32_t>{1}, std::vector<uint32_t>{1}));
+    // of: [c_nationkey, o_orderkey, o_custkey]
+    XPair* x4 = P.pair("orders_lineitem");
+    Holder* ofx = P.side(x4, 0, "orders_j", 10, of, od, nullptr, {}, {1});
+    Holder* lix = P.side(x4, 1, "lineitem", 10, li, li, nullptr, {Col(L_ORDERKEY), Col(L_SUPPKEY), rev()}, {0});
+    auto* ob = rt->op<BuildOp>("orders_build", 11, ofx, nullptr, std::vector<uint32_t>{1});
+    Holder* lj = P.wire(rt->op<ProbeOp>("lineitem_probe", 12, ob, lix, nullptr, std::vector<EB>{},
+                                        std::vector<uint32_t>{0}, std::vector<uint32_t>{0}));
+    // lj: [c_nationkey, l_orderkey, l_suppkey, rev]
+    XPair* x5 = P.pair("supplier_lineitem");
+    Holder* sux = P.side(x5, 0, "supplier", 13, su, su, nullptr, {}, {0, 1});
+    Holder* ljx = P.side(x5, 1, "lineitem_j", 13, lj, li, nullptr, {}, {2, 0});
+    auto* sb = rt->op<BuildOp>("supplier_build", 14, sux, nullptr, std::vector<uint32_t>{0, 1});
+    Holder* sj = P.wire(rt->op<ProbeOp>("supplier_probe", 15, sb, ljx, nullptr, std::vector<EB>{},
+                                        std::vector<uint32_t>{2, 0}, std::vector<uint32_t>{1}));
+    // sj: [s_nationkey, c_nationkey, l_orderkey, l_suppkey, rev]
+    return P.wire(rt->op<AggOp>("q5_agg", 16, sj, nullptr, std::vector<EB>{}, std::vector<uint32_t>{0},
+                                std::vector<tq_agg>{{TQ_AGG_SUM, 4}}, true, nullptr, P.agg_turn()));
+  }
+  if (q == 9) {
+    Holder* pa = P.scan(T_PART);
+    Holder* ps = P.scan(T_PARTSUPP);
+    Holder* li = P.scan(T_LINEITEM);
+    Holder* su = P.scan(T_SUPPLIER);
+    Holder* od = P.scan(T_ORDERS);
+    XPair* x1 = P.pair("part_partsupp");
+    EB fp;
+    fp.cmp(TQ_LT).col(1).i64(54);
+    Holder* pax = P.side(x1, 0, "part_f", 1, pa, pa, &fp, {Col(0)}, {0});
+    Holder* psx = P.side(x1, 1, "partsupp", 1, ps, ps, nullptr, {}, {0});
+    auto* pb = rt->op<BuildOp>("part_build", 2, pax, nullptr, std::vector<uint32_t>{0}, true);
+    Holder* psf = P.wire(rt->op<ProbeOp>("partsupp_probe", 3, pb, psx, nullptr, std::vector<EB>{},
+                                         std::vector<uint32_t>{0}, none));
+    // psf: [ps_partkey, ps_suppkey, ps_supplycost]
+    XPair* x2 = P.pair("partsupp_lineitem");
+    Holder* psfx = P.side(x2, 0, "partsupp_f", 4, psf, ps, nullptr, {}, {0, 1});
+    Holder* lix = P.side(x2, 1, "lineitem", 4, li, li, nullptr,
+                         {Col(L_ORDERKEY), Col(L_PARTKEY), Col(L_SUPPKEY), Col(L_QUANTITY), Col(L_EXTPRICE),
+                          Col(L_DISCOUNT)},
+                         {1, 2});
+    auto* pst = rt->op<BuildOp>("partsupp_build", 5, psfx, nullptr, std::vector<uint32_t>{0, 1});
+    Holder* lj = P.wire(rt->op<ProbeOp>("lineitem_probe", 6, pst, lix, nullptr, std::vector<EB>{},
+                                        std::vector<uint32_t>{1, 2}, std::vector<uint32_t>{2}));
+    // lj: [ps_supplycost, l_orderkey, l_partkey, l_suppkey, qty, ep, disc]
+    XPair* x3 = P.pair("supplier_lineitem");
+    Holder* sux = P.side(x3, 0, "supplier", 7, su, su, nullptr, {}, {0});
+    Holder* ljx = P.side(x3, 1, "lineitem_j", 7, lj, li, nullptr, {}, {3});
+    auto* sb = rt->op<BuildOp>("supplier_build", 8, sux, nullptr, std::vector<uint32_t>{0});
+    Holder* sj = P.wire(rt->op<ProbeOp>("supplier_probe", 9, sb, ljx, nullptr, std::vector<EB>{},
+                                        std::vector<uint32_t>{3}, std::vector<uint32_t>{1}));
+    // sj: [s_nationkey, ps_supplycost, l_orderkey, l_partkey, l_suppkey, qty, ep, disc]
+    XPair* x4 = P.pair("orders_lineitem");
+    Holder* odx = P.side(x4, 0, "orders", 10, od, od, nullptr, {Col(O_ORDERKEY), Col(O_YEAR)}, {0});
+    EB amt;
+    amt.ar(TQ_SUB).ar(TQ_MUL).col(6).ar(TQ_SUB).dec(100).col(7).ar(TQ_MUL).col(1).col(5);
+    Holder* sjx = P.side(x4, 1, "lineitem_s", 10, sj, li, nullptr, {Col(0), Col(2), amt}, {1});
+    // sjx: [s_nationkey, l_orderkey, amt]
+    auto* ob = rt->op<BuildOp>("orders_build", 11, odx, nullptr, std::vector<uint32_t>{0});
+    Holder* oj = P.wire(rt->op<ProbeOp>("orders_probe", 12, ob, sjx, nullptr, std::vector<EB>{},
+                                        std::vector<uint32_t>{1}, std::vector<uint32_t>{1}));
+    // oj: [o_year, s_nationkey, l_orderkey, amt]
+    return P.wire(rt->op<AggOp>("q9_agg", 13, oj, nullptr, std::vector<EB>{}, std::vector<uint32_t>{1, 0},
+                                std::vector<tq_agg>{{TQ_AGG_SUM, 3}}, true, nullptr, P.agg_turn()));
+  }
+  fail(TQ_INVALID_PLAN, "query " + std::to_string(q) + " has no distributed plan");
+}
+
 }  // namespace exec
 }  // namespace tq
 
@@ -1139,15 +1558,11 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
     rt.setup();
     int nranks = 1;
     if (comm) nranks = tq_comm_size(comm);
-    // a plan without a distributed form must not run as one worker of N: it
-    // would silently join / aggregate only this rank's shard
-    if (nranks > 1 && query != 3)
-      fail(TQ_INVALID_PLAN, "query " + std::to_string(query) + " has no distributed plan");
+    // N > 1 workers: the distributed plan (a query without one fails with
+    // InvalidPlan rather than joining / aggregating only this worker's shard)
     Plan P{&rt, tables};
-    Holder* res = build_plan(P, query);
+    Holder* res = nranks > 1 ? build_dist_plan(P, query) : build_plan(P, query);
     SinkOp* sink = rt.op<SinkOp>(res);
-    for (auto& op : rt.ops)
-      if (auto* x = dynamic_cast<ExchangeOp*>(op.get())) x->nranks = nranks;
     // publish the scans: device tables as zero-copy row-group views; HOST
     // tables are encoded into the pinned pool (Host tier) and every scan task
     // goes through load_to_device
@@ -1180,6 +1595,7 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
             rt.registry.push_back(h);
           }
           s->out->push(h);
+          s->nbatches++;
           if (s->table.rows == 0) break;
         }
         s->finished = true;
@@ -1221,7 +1637,15 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
       js << "{\"wall_ms\": " << wall << ", \"setup_ms\": " << setup_ms << ", \"run_ms\": " << run_ms << ", \"tasks\": " << rt.m_tasks << ", \"oom_retries\": " << rt.m_retries
          << ", \"splits\": " << rt.m_splits << ", \"spills\": " << rt.m_spills << ", \"spill_bytes\": " << rt.m_spill_bytes
          << ", \"loads\": " << rt.m_loads << ", \"preloads\": " << rt.m_preloads << ", \"load_bytes\": " << rt.m_load_bytes
-         << ", \"peak_device_bytes\": " << rt.m_peak << ", \"device_capacity\": " << rt.capacity << ", \"ops\": {";
+         << ", \"peak_device_bytes\": " << rt.m_peak << ", \"device_capacity\": " << rt.capacity
+         << ", \"exchange_decisions\": [";
+      for (size_t i = 0; i < rt.decisions.size(); ++i) {
+        const auto& d = rt.decisions[i];
+        js << (i ? ", " : "") << "{\"pair\": \"" << d.name << "\", \"strategy\": \""
+           << (d.strategy == TQ_XCHG_BROADCAST ? "Broadcast" : "HashPartition") << "\", \"broadcast_side\": " << d.side
+           << ", \"total0\": " << d.total0 << ", \"total1\": " << d.total1 << "}";
+      }
+      js << "], \"ops\": {";
       bool first = true;
       for (auto& op : rt.ops) {
         if (!op->stat.tasks) continue;

@@ -368,3 +368,49 @@ int tq_comm_size(tq_comm* cm) { return cm->n; }
 int tq_comm_rank(tq_comm* cm) { return cm->rank; }
 
 }  // extern "C"
+
+// ---- AdaptiveExchange control
+extern "C" {
+
+tq_status tq_comm_allgather_host_u64(tq_comm* cm, const uint64_t* in, uint64_t* out, uint64_t count, void* stream) {
+  return guard([&] {
+    tq_ctx* c = cm->ctx;
+    cudaStream_t st = pick(c, stream);
+    const uint64_t n = (uint64_t)cm->n;
+    u64* g = (u64*)dalloc(c, 8 * count * (n + 1), st);
+    TQ_CUDA(cudaMemcpyAsync(g, in, 8 * count, cudaMemcpyHostToDevice, st));
+    comm_allgather_u64(cm, g, g + count, count, st);
+    TQ_CUDA(cudaMemcpyAsync(out, g + count, 8 * count * n, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaStreamSynchronize(st));
+    dfree(c, g, 8 * count * (n + 1), st);
+  });
+}
+
+int tq_exchange_phase1(uint64_t bytes_so_far, double progress, double sample_fraction, uint64_t* estimate) {
+  if (progress >= 1.0) {  // scan complete: the bytes are exact (0 for an empty input)
+    if (estimate) *estimate = bytes_so_far;
+    return 1;
+  }
+  if (progress <= 0.0 || progress < sample_fraction) return 0;
+  if (estimate) *estimate = (uint64_t)((double)bytes_so_far / progress);  // 10 MiB at 25% -> 40 MiB
+  return 1;
+}
+
+int tq_exchange_decide(const uint64_t* est0, const uint64_t* est1, int n, uint64_t threshold, int* broadcast_side,
+                       uint64_t* total0, uint64_t* total1) {
+  uint64_t t0 = 0, t1 = 0;
+  for (int i = 0; i < n; ++i) {
+    t0 += est0[i];
+    t1 += est1[i];
+  }
+  if (total0) *total0 = t0;
+  if (total1) *total1 = t1;
+  if (std::min(t0, t1) <= threshold * (uint64_t)n) {
+    if (broadcast_side) *broadcast_side = t0 <= t1 ? 0 : 1;
+    return TQ_XCHG_BROADCAST;
+  }
+  if (broadcast_side) *broadcast_side = -1;
+  return TQ_XCHG_HASH_PARTITION;
+}
+
+}  // extern "C"

@@ -995,10 +995,20 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
               }
               if (tail) {
                 if (op == ACC_CNT) {
-                  const u64 old = atomicAdd((unsigned long long*)acc, (unsigned long long)lo64(sv));
-                  if (a == p.agg.cnt_acc && old == 0) atomicAdd(s_groups, 1ull);  // a new group
+                  atomicAdd((unsigned long long*)acc, (unsigned long long)lo64(sv));  // RED: no return
                 } else if (sv != 0) {
-                  atomic_add_i128(acc, sv);
+                  // limb form {sum of low 32-bit limbs, sum of signed high parts}:
+                  // two fire-and-forget REDs (an int128 add with carry needs the
+                  // old value back: one dependent ATOM round trip per run).
+                  // Exact while every run's sum fits int64 (else the host
+                  // re-runs this aggregate on the hash table)
+                  if (fits64(sv)) {
+                    const long long v = (long long)lo64(sv);
+                    atomicAdd((unsigned long long*)acc, (unsigned long long)(v & 0xffffffffll));
+                    atomicAdd((unsigned long long*)acc + 1, (unsigned long long)(v >> 32));
+                  } else if (*(volatile u32*)p.agg.overflow == 0) {
+                    atomicExch(p.agg.overflow, 1u);
+                  }
                 }
               }
             } else if (op == ACC_SUM_F) {

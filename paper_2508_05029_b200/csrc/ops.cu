@@ -1235,6 +1235,14 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
     for (u32 a = 0; a < f.naggs; ++a) {
       const AggOut& ao = f.aggs[a];
       const u64* m = acc + 2 * ao.acc;
+      u64 limb[2];
+      if (f.direct && (ao.kind == AO_SUM_I64 || ao.kind == AO_SUM_DEC || ao.kind == AO_AVG_I)) {
+        // direct table: integer sums are kept as {low-limb sum, high-part sum}
+        const i128 v = add128((i128)(long long)m[1] * ((i128)1 << 32), (i128)m[0]);
+        limb[0] = lo64(v);
+        limb[1] = hi64(v);
+        m = limb;
+      }
       u64 cnt = ao.cnt != 0xff ? acc[2 * ao.cnt] : 1;
       bool valid = cnt != 0;
       switch (ao.kind) {
@@ -1372,7 +1380,8 @@ static AggSpec plan_aggs(const tq_batch* in, Prog& P, const tq_agg* aggs, uint32
 // columns then one column per raw accumulator (int128 accumulators as
 // Decimal(38,0), counts Int64, float accumulators Float64) for a later merge.
 static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<int>& kh,
-                     const std::vector<AccSpec>& acc, const std::vector<AggPlan>* ap, tq_batch* out, cudaStream_t st) {
+                     const std::vector<AccSpec>& acc, const std::vector<AggPlan>* ap, tq_batch* out, cudaStream_t st,
+                     const std::vector<uint8_t>* raw_ops = nullptr) {
   const u32 nacc = (u32)acc.size();
   // local (per-CTA) group table: per-lane private accumulator planes (8 B;
   // MIN/MAX of int128 take two) sized to the shared memory left after two stages
@@ -1504,10 +1513,22 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     t.direct_slots = R;
     p.agg = t;
     launch(c, SINK_AGG, L, P, st);
-    std::lock_guard<std::mutex> g(c->mu);
-    TQ_CUDA(cudaMemcpyAsync(c->pinned, tail, 16, cudaMemcpyDeviceToHost, st));
-    { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
-    ngroups = ((uint64_t*)c->pinned)[0];
+    uint32_t ovf = 0;
+    {
+      std::lock_guard<std::mutex> g(c->mu);
+      TQ_CUDA(cudaMemcpyAsync(c->pinned, tail, 16, cudaMemcpyDeviceToHost, st));
+      { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+      ovf = ((uint32_t*)c->pinned)[2];
+    }
+    if (ovf) {  // a run's integer sum beyond int64: re-run exactly on the hash table
+      dfree(c, base, tbytes, st);
+      direct = false;
+      t = AggTable{};
+      setup(G);
+    } else {
+      // groups are counted by the finalize (its output cursor): capacity R + 1
+      ngroups = cap;
+    }
   }
   for (int attempt = 0; !direct; ++attempt) {
     tbytes = cap * 4 + cap * kwa * 8 + cap * std::max<u32>(1, nacc) * 16 + 64;
@@ -1563,7 +1584,9 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       AggPlan a{};
       a.acc = (uint8_t)i;
       a.cnt = 0xff;
-      switch (acc[i].op) {
+      // (raw_ops: the ORIGINAL accumulator ops when merging partials, whose
+      // counts are summed as ints but stay Int64 partial columns)
+      switch (raw_ops ? (*raw_ops)[i] : acc[i].op) {
         case ACC_SUM_I: case ACC_MIN_I: case ACC_MAX_I: a.kind = AO_SUM_DEC; a.col.kind = TQ_DECIMAL; a.col.precision = 38; break;
         case ACC_CNT: a.kind = AO_SUM_I64; a.col.kind = TQ_INT64; break;
         default: a.kind = AO_SUM_F; a.col.kind = TQ_FLOAT64;
@@ -1623,6 +1646,20 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     prof_end(c, ph, st);
     counted_launch(c);
     TQ_CUDA(cudaGetLastError());
+    if (direct) {  // the output was sized for every slot: trim to the groups written
+      uint64_t n = 0;
+      {
+        std::lock_guard<std::mutex> g(c->mu);
+        TQ_CUDA(cudaMemcpyAsync(c->pinned, t.nused, 8, cudaMemcpyDeviceToHost, st));
+        { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+        n = ((uint64_t*)c->pinned)[0];
+      }
+      out->rows = n;
+      for (uint32_t i = 0; i < out->ncols; ++i) {
+        out->cols[i].values_bytes = n * width_of(out->cols[i].kind);
+        if (n == 0) out->cols[i].validity = nullptr;
+      }
+    }
   }
   dfree(c, tbase, tbytes, st);
 }
@@ -1931,7 +1968,8 @@ tq_status tq_join_build_sized(tq_ctx* c, const tq_batch* build, const uint32_t* 
 }
 
 static tq_status pipeline_build_impl(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
-                                     uint32_t nkeys, tq_join_table** out, void* stream, bool semi) {
+                                     uint32_t nkeys, tq_join_table** out, void* stream, bool semi,
+                                     uint64_t bloom_keys = 0) {
   return guard([&] {
     check_device_batch(in);
     Prog P(schema_of(in));
@@ -1944,7 +1982,53 @@ static tq_status pipeline_build_impl(tq_ctx* c, const tq_batch* in, const tq_exp
       ex[k] = tq_expr{&nodes[k], 1, 0};
     }
     compile_prog(P, in, pred, ex.data(), nkeys, false);
-    run_build(c, in, P, iota_u32(nkeys), out, pick(c, stream), 0, semi);
+    run_build(c, in, P, iota_u32(nkeys), out, pick(c, stream), bloom_keys, semi);
+  });
+}
+
+tq_status tq_pipeline_build_ex(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
+                               uint32_t nkeys, uint64_t bloom_keys, int semi, tq_join_table** out, void* stream) {
+  return pipeline_build_impl(c, in, pred, keys, nkeys, out, stream, semi != 0, bloom_keys);
+}
+
+tq_status tq_pipeline_estimate(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,
+                               uint32_t nexprs, uint64_t* out_rows, uint64_t* out_row_bytes, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    cudaStream_t st = pick(c, stream);
+    Prog P(schema_of(in));
+    compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
+    uint64_t w = 0;
+    for (int h : P.outs) {
+      uint8_t prec, scale;
+      w += width_of(out_kind_of(P.pb.root(h), in, P.pb, &prec, &scale));
+    }
+    if (out_row_bytes) *out_row_bytes = w;
+    uint64_t rows = in->rows;
+    if (P.has_pred && in->rows > 0) {
+      // the COUNT pass of a filter over the predicate columns only
+      Plan L;
+      plan_launch(c, in, P, L, kWarps * kMaxDest * 4 + kWarps * kMaxDest * 8, st);
+      PipeParams& p = L.p;
+      p.dest_kind = DEST_FILTER;
+      p.ndest = 1;
+      const u64 ncnt = (u64)p.ntiles * kWarps;
+      u32* counts = (u32*)dalloc(c, ncnt * 4, st);
+      u64* offsets = (u64*)dalloc(c, (ncnt + 1) * 8, st);
+      p.tile_counts = counts;
+      p.load_mask = P.pb.column_deps({P.pred_h});
+      launch(c, SINK_COUNT, L, P, st);
+      scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
+      {
+        std::lock_guard<std::mutex> g(c->mu);
+        TQ_CUDA(cudaMemcpyAsync(c->pinned, offsets + ncnt, 8, cudaMemcpyDeviceToHost, st));
+        { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+        rows = ((uint64_t*)c->pinned)[0];
+      }
+      dfree(c, counts, ncnt * 4, st);
+      dfree(c, offsets, (ncnt + 1) * 8, st);
+    }
+    if (out_rows) *out_rows = rows;
   });
 }
 
@@ -2095,6 +2179,62 @@ tq_status tq_agg_update(tq_agg_state* s, const tq_batch* in, void* stream) {
     tq_batch part{};
     agg_core(c, in, P, key_handles(P, s->keys.data(), (uint32_t)s->keys.size()), S.acc, nullptr, &part, st);
     s->partials.push_back(part);
+  });
+}
+
+tq_status tq_agg_take_partial(tq_agg_state* s, tq_batch* out, void* stream) {
+  return guard([&] {
+    tq_ctx* c = s->ctx;
+    cudaStream_t st = pick(c, stream);
+    if (!s->planned) fail(TQ_INVALID_PLAN, "aggregate state has seen no batch (no schema)");
+    const uint32_t nk = (uint32_t)s->keys.size();
+    if (s->partials.empty()) fail(TQ_INTERNAL, "no partial to take (every update appends one)");
+    tq_batch merged{};
+    const tq_batch* src = &s->partials[0];
+    if (s->partials.size() > 1) {
+      tq_status r = tq_concat(c, s->partials.data(), (uint32_t)s->partials.size(), &merged, st);
+      if (r != TQ_OK) fail(r, g_err);
+      src = &merged;
+    }
+    // merge the partials into one partial (sum of sums, min of mins, ...)
+    Prog P(schema_of(src));
+    compile_prog(P, src, nullptr, nullptr, 0, true);
+    std::vector<int> kh;
+    for (uint32_t k = 0; k < nk; ++k) kh.push_back(P.outs[k]);
+    std::vector<AccSpec> macc;
+    for (size_t i = 0; i < s->acc_ops.size(); ++i) {
+      const Operand& o = P.pb.root(P.outs[nk + i]);
+      AccSpec a{};
+      a.op = s->acc_ops[i] == ACC_CNT ? (uint8_t)ACC_SUM_I : s->acc_ops[i];
+      a.kind = o.kind;
+      a.idx = o.idx;
+      macc.push_back(a);
+    }
+    try {
+      agg_core(c, src, P, kh, macc, nullptr, out, st, &s->acc_ops);
+    } catch (...) {
+      if (src == &merged) tq_batch_free(c, &merged);
+      throw;
+    }
+    if (src == &merged) tq_batch_free(c, &merged);
+    // a merged count partial is an int128 sum: keep the partial schema (Int64 counts)
+    for (size_t i = 0; i < s->acc_ops.size(); ++i)
+      if (s->acc_ops[i] == ACC_CNT && out->cols[nk + i].kind != TQ_INT64) fail(TQ_INTERNAL, "partial count schema");
+    for (auto& b : s->partials) tq_batch_free(c, &b);
+    s->partials.clear();
+  });
+}
+
+tq_status tq_agg_add_partial(tq_agg_state* s, const tq_batch* partial, void* stream) {
+  return guard([&] {
+    check_device_batch(partial);
+    tq_ctx* c = s->ctx;
+    if (!s->planned) fail(TQ_INVALID_PLAN, "aggregate state has seen no batch (no schema)");
+    if (partial->ncols != s->keys.size() + s->acc_ops.size()) fail(TQ_SCHEMA_MISMATCH, "partial aggregate schema");
+    tq_batch copy{};
+    tq_status r = tq_slice(c, partial, 0, partial->rows, &copy, stream);
+    if (r != TQ_OK) fail(r, g_err);
+    s->partials.push_back(copy);
   });
 }
 

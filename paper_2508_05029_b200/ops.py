@@ -45,7 +45,8 @@ class TqEngineOptsC(C.Structure):
                 ("device_budget", C.c_uint64), ("pool_buffer_size", C.c_uint64), ("pool_capacity", C.c_uint64),
                 ("high_watermark", C.c_double), ("low_watermark", C.c_double), ("protect_top_k", C.c_uint32),
                 ("tables_on_host", C.c_uint32), ("task_batches", C.c_uint32), ("inject_oom_mode", C.c_uint32),
-                ("inject_oom_count", C.c_uint32), ("inject_oom_op", C.c_char * 32)]
+                ("inject_oom_count", C.c_uint32), ("inject_oom_op", C.c_char * 32), ("force_exchange", C.c_uint32),
+                ("exchange_impl", C.c_uint32), ("broadcast_threshold", C.c_uint64)]
 
 
 class TqOptsC(C.Structure):

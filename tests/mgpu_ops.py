@@ -4,7 +4,12 @@ mismatch.  Modes (TQ_MODE):
   validity  the fused partition exchange / broadcast when ranks DISAGREE on
             which columns can be null (rank 0 has nulls, rank 1 has no
             bitmaps, rank 2 an empty input): every rank must lay out its
-            window identically and the output must carry the nulls."""
+            window identically and the output must carry the nulls.
+  engine    the C++ worker runtime's distributed plans (tq_engine_run_query
+            with a communicator) for Q1 / Q3 / Q5 / Q6 / Q9: exchange_decide
+            (adaptive), forced Broadcast and forced HashPartition (SPEC.md:613
+            strategy equivalence), fused NVLink and NCCL exchanges; the union
+            of the workers' results must equal the oracle every time."""
 import os
 import sys
 
@@ -41,6 +46,37 @@ def validity(ctx, comm, rank, world):
     return True
 
 
+def engine(ctx, comm, rank, world):
+    import oracle as O
+    from paper_2508_05029_b200.columnar import assert_batches_equal
+    from paper_2508_05029_b200.ops import engine_run_query
+    sf = float(os.environ.get("TQ_SF", "0.1"))
+    queries = [int(q) for q in os.environ.get("TQ_QUERIES", "1,3,5,6,9").split(",")]
+    cases = [("adaptive", 0, 0), ("broadcast", 1, 0), ("hash", 2, 0), ("hash_nccl", 2, 1)]
+    ok = True
+    for q in queries:
+        tabs = {t: ctx.datagen(t, sf, shard=rank, nshards=world) for t in O.QUERY_TABLES[q]}
+        want = O.query(q, {t: O.datagen(t, sf) for t in O.QUERY_TABLES[q]}, 8) if rank == 0 else None
+        for name, force, impl in cases:
+            out, m = engine_run_query(ctx, q, tabs, comm=comm, compute_threads=4, batch_rows=64 * 1024,
+                                      force_exchange=force, exchange_impl=impl)
+            parts = [None] * world
+            dist.all_gather_object(parts, out)
+            if rank == 0:
+                try:
+                    assert_batches_equal(O.concat(parts), want)
+                    print(f"  q{q} {name}: ok rows={want.rows} decisions="
+                          f"{[(d['pair'], d['strategy']) for d in m['exchange_decisions']]}")
+                except AssertionError as e:
+                    print(f"  q{q} {name}: MISMATCH {e}")
+                    ok = False
+        for v in tabs.values():
+            v.free()
+    flag = [ok]
+    dist.broadcast_object_list(flag, src=0)
+    assert flag[0]
+
+
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -54,7 +90,8 @@ def main():
     mode = os.environ.get("TQ_MODE", "validity")
     rc = 0
     try:
-        {"validity": validity}[mode](ctx, comm, rank, world)
+        {"validity": validity, "engine": engine}[mode](ctx, comm, rank, world)
+        dist.barrier()
         if rank == 0:
             print(f"mgpu ops ok: mode={mode} world={world}")
     except AssertionError as e:

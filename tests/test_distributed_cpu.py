@@ -22,6 +22,7 @@ def test_exchange_phase1_examples():
     assert exchange_phase1(10 << 20, 0.25) == 40 << 20
     assert exchange_phase1(0, 1.0) == 0
     assert exchange_phase1(123, 0.01) is None                 # below sample fraction
+    assert exchange_phase1(5 << 20, 1.0) == 5 << 20           # scan complete: exact bytes
 
 
 def test_exchange_decide_examples():
@@ -31,6 +32,9 @@ def test_exchange_decide_examples():
     assert d.strategy == HASH_PARTITION
     # identical on every worker for identical inputs
     assert exchange_decide([5, 6], [7, 8], 2) == exchange_decide([5, 6], [7, 8], 2)
+    # the smaller side is broadcast, whichever it is; ties -> side 0
+    assert exchange_decide([1 << 30], [1 << 20], 1).broadcast_side == 1
+    assert exchange_decide([7], [7], 1).broadcast_side == 0
     # config 4 at SF100: customer_f 24 MB broadcast for N >= 2, orders/lineitem partitioned
     assert exchange_decide([24_000_000], [10 ** 10], 2).strategy == BROADCAST
     assert exchange_decide([24_000_000], [10 ** 10], 1).strategy == HASH_PARTITION

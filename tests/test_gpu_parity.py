@@ -360,14 +360,14 @@ def test_datagen_shard_bit_identical(ctx, t):
         assert_batches_equal(g, O.datagen(t, sf, 4, s, 4), ordered=True)
 
 
-@pytest.mark.parametrize("case", ["clustered", "shuffled", "nulls", "sparse"])
+@pytest.mark.parametrize("case", ["clustered", "shuffled", "nulls", "sparse", "huge"])
 def test_aggregate_direct_dense_key(ctx, case):
     """One integer group key over >= 4M rows: a range pass sizes a DIRECT
     table (slot = key - min) when the keys are dense — clustered keys (like
     lineitem by orderkey) are reduced per warp run before one atomic per run;
     a null key gets its own slot; a sparse key range falls back to the hash
     table.  Every path equals the oracle."""
-    rng = np.random.default_rng({"clustered": 1, "shuffled": 2, "nulls": 3, "sparse": 4}[case])
+    rng = np.random.default_rng({"clustered": 1, "shuffled": 2, "nulls": 3, "sparse": 4, "huge": 5}[case])
     n = 4_500_000
     if case == "sparse":
         k = rng.integers(0, 1 << 40, n // 8).repeat(8)[:n]
@@ -376,7 +376,9 @@ def test_aggregate_direct_dense_key(ctx, case):
         if case == "shuffled":
             k = rng.permutation(k)
     valid = rng.random(n) >= 0.01 if case == "nulls" else None
-    v = rng.integers(-10**9, 10**9, n)
+    # "huge": runs whose integer sums pass int64 (the direct table's limb
+    # form cannot hold them: the aggregate re-runs exactly on the hash table)
+    v = rng.integers(1 << 61, 1 << 62, n) if case == "huge" else rng.integers(-10**9, 10**9, n)
     f = rng.integers(-400, 400, n) * 0.25  # exact in binary: float sums do not depend on the order
     b = HostBatch(n, [HostBatch.col_i64(k.astype(np.int64), valid), HostBatch.col_dec(v.astype(np.int64)),
                       HostBatch.col_f64(f, rng.random(n) >= 0.05)])
