@@ -13,7 +13,7 @@ if [ ! -d "$REF/src" ]; then
   exit 0
 fi
 mkdir -p "$OUT"
-g++ -std=c++20 -O2 -fPIC -shared -Wall -Wextra \
+g++ -std=c++20 -O2 -fPIC -shared -Wall -Wextra -pthread \
   -I"$REF/include" \
   "$REF/src/common.cpp" \
   "$REF/src/columnar/types.cpp" \

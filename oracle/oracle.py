@@ -13,6 +13,8 @@ import os
 import sys
 from typing import List, Optional, Sequence
 
+import numpy as np
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 if ROOT not in sys.path:
@@ -96,6 +98,13 @@ def ref():
         L.tqr_chunked_layout.argtypes = [P(TqBatchC), C.c_uint64, C.c_uint64, P(C.c_uint64), P(C.c_uint64),
                                          P(C.c_uint32), C.c_uint32, P(C.c_uint32), P(C.c_int)]
         L.tqr_batch_free.argtypes = [P(TqBatchC)]
+        L.tqr_resident_make.restype = C.c_void_p
+        L.tqr_resident_make.argtypes = [P(TqBatchC)]
+        L.tqr_resident_free.argtypes = [C.c_void_p]
+        L.tqr_q1_fused.restype = C.c_double
+        L.tqr_q1_fused.argtypes = [C.c_void_p, C.c_uint32, P(C.c_uint64), C.c_uint32]
+        L.tqr_read_bw.restype = C.c_double
+        L.tqr_read_bw.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32]
         _ref = L
     return _ref
 
@@ -242,3 +251,59 @@ def ref_slice(b: HostBatch, start, n) -> HostBatch:
     L, out = ref(), TqBatchC()
     bc = b.to_c()
     return _out(L, L.tqr_slice(C.byref(bc), start, n, C.byref(out)), out, "tqr")
+
+
+class RefResident:
+    """A lineitem batch held as the REFERENCE's own ColumnBatch (converted once,
+    kept resident like the GPU's HBM tables) for the CPU baseline."""
+
+    def __init__(self, lineitem: HostBatch):
+        L = ref()
+        self._keep = lineitem.to_c()
+        self.h = L.tqr_resident_make(C.byref(self._keep))
+        if not self.h:
+            raise RuntimeError("tqr_resident_make failed")
+
+    def q1_fused(self, nthreads: int):
+        """Q1 as one fused pass over Column::i64_at / dec_at (types.cpp:66-90),
+        nthreads row ranges.  -> (HostBatch like query(1), seconds)."""
+        L = ref()
+        out = (C.c_uint64 * (1 + 16 * 64))()
+        sec = L.tqr_q1_fused(self.h, nthreads, out, 64)
+        n = int(out[0])
+
+        def i128(lo, hi):
+            v = (int(hi) << 64) | int(lo)
+            return v - (1 << 128) if v >> 127 else v
+        rows = []
+        for g in range(n):
+            o = out[1 + 16 * g: 1 + 16 * (g + 1)]
+            q, e, dp, ch, d = (i128(o[2 + 2 * k], o[3 + 2 * k]) for k in range(5))
+            cnt = int(o[12])
+            avg = lambda v, sc: float(v) / (10.0 ** sc) / cnt
+            rows.append((int(np.int64(np.uint64(o[0]))), int(np.int64(np.uint64(o[1]))), q, e, dp, ch,
+                         avg(q, 2), avg(e, 2), avg(d, 2), cnt))
+        b = HostBatch(n)
+        cols = list(zip(*rows)) if rows else [[]] * 10
+        b.cols = [HostBatch.col_i64(list(cols[0])), HostBatch.col_i64(list(cols[1])),
+                  HostBatch.col_dec(list(cols[2]), 38, 2), HostBatch.col_dec(list(cols[3]), 38, 2),
+                  HostBatch.col_dec(list(cols[4]), 38, 4), HostBatch.col_dec(list(cols[5]), 38, 6),
+                  HostBatch.col_f64(list(cols[6])), HostBatch.col_f64(list(cols[7])), HostBatch.col_f64(list(cols[8])),
+                  HostBatch.col_i64(list(cols[9]))]
+        return b, sec
+
+    def close(self):
+        if self.h:
+            ref().tqr_resident_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def host_read_bw(bytes_: int = 1 << 30, nthreads: int = 1, reps: int = 3) -> float:
+    """Host memory read bandwidth (GB/s) with nthreads."""
+    return ref().tqr_read_bw(bytes_, nthreads, reps)

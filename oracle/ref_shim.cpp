@@ -7,9 +7,11 @@
 // (oracle/tq_oracle.cpp) and the GPU take/concat/slice against the
 // reference's transform.cpp:21-154, common.hpp:128-158, types.cpp:146-170
 // and chunked.cpp:19-124.
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tierq/columnar/chunked.hpp"
@@ -180,6 +182,115 @@ int tqr_chunked_layout(const tq_batch* in, uint64_t buffer_size, uint64_t capaci
     *roundtrip_ok = decode_chunked(*cb, pool) == b ? 1 : 0;
     release_chunked(*cb, pool);
   });
+}
+
+
+// ---- CPU baseline over the REFERENCE's own batch and accessors -------------
+// A lineitem batch converted once into the reference's ColumnBatch and kept
+// resident (the GPU's tables are resident in HBM too); the timed work is a
+// fused single pass of Q1 over Column::i64_at / dec_at
+// (types.cpp:66-90), one thread per row range, per-thread group accumulators
+// merged at the end.  Group keys are the l_returnflag / l_linestatus codes.
+void* tqr_resident_make(const tq_batch* in) {
+  try {
+    return new ColumnBatch(to_ref(in));
+  } catch (...) {
+    return nullptr;
+  }
+}
+void tqr_resident_free(void* b) { delete static_cast<ColumnBatch*>(b); }
+
+// out: ngroups, then per group {rf, ls, sum_qty(lo,hi), sum_ep, sum_dp, sum_ch, sum_disc, count} as u64 words
+// (16 words per group); returns the seconds of the fused pass.
+double tqr_q1_fused(void* batch, uint32_t nthreads, uint64_t* out, uint32_t cap_groups) {
+  const ColumnBatch& b = *static_cast<ColumnBatch*>(batch);
+  enum { OK, PK, SK, QTY, EP, DISC, TAX, RF, LS, SD };
+  struct Acc {
+    int64_t rf, ls;
+    int128_t qty, ep, dp, ch, disc;
+    uint64_t n;
+  };
+  const uint64_t rows = b.rows();
+  nthreads = std::max<uint32_t>(1, nthreads);
+  std::vector<std::vector<Acc>> part(nthreads);
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> ts;
+  for (uint32_t t = 0; t < nthreads; ++t)
+    ts.emplace_back([&, t] {
+      const uint64_t r0 = rows * t / nthreads, r1 = rows * (t + 1) / nthreads;
+      const Column &sd = b.column(SD), &rf = b.column(RF), &ls = b.column(LS), &qty = b.column(QTY),
+                   &ep = b.column(EP), &disc = b.column(DISC), &tax = b.column(TAX);
+      std::vector<Acc>& g = part[t];
+      for (uint64_t r = r0; r < r1; ++r) {
+        if (!(sd.i64_at(r) <= 10471)) continue;
+        const int64_t k0 = rf.i64_at(r), k1 = ls.i64_at(r);
+        Acc* a = nullptr;
+        for (Acc& x : g)
+          if (x.rf == k0 && x.ls == k1) { a = &x; break; }
+        if (!a) { g.push_back(Acc{k0, k1, 0, 0, 0, 0, 0, 0}); a = &g.back(); }
+        const int128_t q = qty.dec_at(r), e = ep.dec_at(r), d = disc.dec_at(r), x = tax.dec_at(r);
+        const int128_t dp = e * (int128_t(100) - d);
+        a->qty += q;
+        a->ep += e;
+        a->dp += dp;
+        a->ch += dp * (int128_t(100) + x);
+        a->disc += d;
+        a->n += 1;
+      }
+    });
+  for (auto& t : ts) t.join();
+  std::vector<Acc> all;
+  for (auto& g : part)
+    for (const Acc& x : g) {
+      Acc* a = nullptr;
+      for (Acc& y : all)
+        if (y.rf == x.rf && y.ls == x.ls) { a = &y; break; }
+      if (!a) { all.push_back(x); continue; }
+      a->qty += x.qty; a->ep += x.ep; a->dp += x.dp; a->ch += x.ch; a->disc += x.disc; a->n += x.n;
+    }
+  const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  out[0] = all.size();
+  for (size_t i = 0; i < all.size() && i < cap_groups; ++i) {
+    uint64_t* o = out + 1 + 16 * i;
+    const Acc& a = all[i];
+    o[0] = (uint64_t)a.rf;
+    o[1] = (uint64_t)a.ls;
+    const int128_t v[5] = {a.qty, a.ep, a.dp, a.ch, a.disc};
+    for (int k = 0; k < 5; ++k) {
+      o[2 + 2 * k] = (uint64_t)v[k];
+      o[3 + 2 * k] = (uint64_t)((unsigned __int128)v[k] >> 64);
+    }
+    o[12] = a.n;
+  }
+  return sec;
+}
+
+// Host memory read bandwidth (GB/s): nthreads sum disjoint slices of a
+// `bytes` buffer, best of `reps` passes.
+double tqr_read_bw(uint64_t bytes, uint32_t nthreads, uint32_t reps) {
+  nthreads = std::max<uint32_t>(1, nthreads);
+  const uint64_t n = bytes / 8;
+  std::vector<uint64_t> buf(n);
+  for (uint64_t i = 0; i < n; ++i) buf[i] = i * 0x9e3779b97f4a7c15ull;
+  double best = 0;
+  std::vector<uint64_t> sink(nthreads * 8);
+  for (uint32_t k = 0; k < reps; ++k) {
+    auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> ts;
+    for (uint32_t t = 0; t < nthreads; ++t)
+      ts.emplace_back([&, t] {
+        const uint64_t a = n * t / nthreads, e = n * (t + 1) / nthreads;
+        uint64_t s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+        uint64_t i = a;
+        for (; i + 4 <= e; i += 4) { s0 += buf[i]; s1 += buf[i + 1]; s2 += buf[i + 2]; s3 += buf[i + 3]; }
+        for (; i < e; ++i) s0 += buf[i];
+        sink[t * 8] = s0 + s1 + s2 + s3;
+      });
+    for (auto& t : ts) t.join();
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    best = std::max(best, (double)(n * 8) / sec / 1e9);
+  }
+  return best;
 }
 
 }  // extern "C"

@@ -985,7 +985,7 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
             if (a >= nacc) break;
             const uint8_t op = P::acc_op(p, a);
             const bool valid = pass && x.av[a];
-            u64* acc = p.agg.acc + (slot * nacc + a) * 2;
+            u64* acc = direct_acc(p.agg, a, pass ? slot : 0);
             if (op == ACC_SUM_I || op == ACC_CNT) {
               i128 sv = valid ? (op == ACC_CNT ? (i128)1 : x.ai[a]) : (i128)0;
 #pragma unroll

@@ -1197,7 +1197,7 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const u64 cap = (f.t.cap + 255) / 256 * 256;  // whole blocks stay in the loop (block barriers)
   for (u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += stride) {
-    const bool occ = s < f.t.cap && (f.direct ? f.t.acc[(s * f.nacc + f.cnt_acc) * 2] != 0 : f.t.state[s] == 2);
+    const bool occ = s < f.t.cap && (f.direct ? *direct_acc(f.t, f.cnt_acc, s) != 0 : f.t.state[s] == 2);
     const u32 m = __ballot_sync(0xffffffffu, occ);
     if (lane == 0) s_warp[warp] = __popc(m);
     __syncthreads();
@@ -1234,7 +1234,7 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
     const u64* acc = f.t.acc + s * f.nacc * 2;
     for (u32 a = 0; a < f.naggs; ++a) {
       const AggOut& ao = f.aggs[a];
-      const u64* m = acc + 2 * ao.acc;
+      const u64* m = f.direct ? direct_acc(f.t, ao.acc, s) : acc + 2 * ao.acc;
       u64 limb[2];
       if (f.direct && (ao.kind == AO_SUM_I64 || ao.kind == AO_SUM_DEC || ao.kind == AO_AVG_I)) {
         // direct table: integer sums are kept as {low-limb sum, high-part sum}
@@ -1243,7 +1243,7 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
         limb[1] = hi64(v);
         m = limb;
       }
-      u64 cnt = ao.cnt != 0xff ? acc[2 * ao.cnt] : 1;
+      u64 cnt = ao.cnt == 0xff ? 1 : f.direct ? *direct_acc(f.t, ao.cnt, s) : acc[2 * ao.cnt];
       bool valid = cnt != 0;
       switch (ao.kind) {
         case AO_SUM_I64:
@@ -1286,13 +1286,15 @@ __global__ void k_agg_final(const __grid_constant__ FinalParams f) {
 struct AccOps {
   uint8_t op[kMaxAcc];
 };
-__global__ void k_acc_init(u64* acc, u64 slots, u32 nacc, AccOps ops) {
+__global__ void k_acc_init(AggTable t, u64 slots, u32 nacc, AccOps ops) {
   const u64 n = slots * nacc;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const u32 a = (u32)(i / slots);
     u64 lo, hi;
-    acc_identity(ops.op[i % nacc], lo, hi);
-    acc[2 * i] = lo;
-    acc[2 * i + 1] = hi;
+    acc_identity(ops.op[a], lo, hi);
+    u64* m = direct_acc(t, a, i % slots);
+    m[0] = lo;
+    if (t.dwidth[a] > 1) m[1] = hi;
   }
 }
 
@@ -1460,7 +1462,8 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       dfree(c, kr, 32, st);
       const uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
       const uint64_t span = mx >= mn ? (uint64_t)mx - (uint64_t)mn + 1 : 0;  // 0: no non-null key
-      if ((mx < mn || (span != 0 && span <= 2 * in->rows)) && (span + 1) * nacc * 16 <= room / 2) {
+      if ((mx < mn || (span != 0 && span <= 2 * in->rows)) && (span + 1) * nacc * 16 <= room / 2 &&
+          span < (1ull << 40)) {
         direct = true;
         kmin = mx >= mn ? mn : 0;
         R = span;
@@ -1483,14 +1486,20 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
   uint64_t tbytes = 0;
   if (direct) {
     // slots [0, R) = key values kmin .., slot R = the null key
+    const uint64_t cap0 = cap;  // (the hash table's first size, if this falls back)
     cap = R + 1;
-    tbytes = cap * nacc * 16 + 64;
+    uint64_t words = 0;  // per slot, over all accumulators (counts take one word)
+    for (u32 i = 0; i < nacc; ++i) {
+      t.dwidth[i] = acc[i].op == ACC_CNT ? 1 : 2;
+      words += t.dwidth[i];
+    }
+    tbytes = cap * words * 8 + 64;
     uint8_t* base = (uint8_t*)dalloc(c, tbytes, st);
     t.state = (uint32_t*)base;  // (no state words: freed through this base)
     t.keys = nullptr;
     t.acc = (u64*)base;
     t.cap = cap;
-    uint8_t* tail = base + cap * nacc * 16;
+    uint8_t* tail = base + cap * words * 8;
     t.nused = (unsigned long long*)tail;
     t.overflow = (uint32_t*)(tail + 8);
     TQ_CUDA(cudaMemsetAsync(tail, 0, 16, st));
@@ -1500,17 +1509,17 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       ops.op[i] = acc[i].op;
       minmax |= acc[i].op == ACC_MIN_I || acc[i].op == ACC_MAX_I || acc[i].op == ACC_MIN_F || acc[i].op == ACC_MAX_F;
     }
-    if (minmax) {
-      k_acc_init<<<(u32)std::min<uint64_t>((cap * nacc + 255) / 256, (uint64_t)c->sms * 8), 256, 0, st>>>(t.acc, cap,
-                                                                                                       nacc, ops);
-      counted_launch(c);
-    } else {
-      TQ_CUDA(cudaMemsetAsync(t.acc, 0, cap * nacc * 16, st));
-    }
     t.direct = 1;
     t.cnt_acc = cnt_idx;
     t.key_min = kmin;
     t.direct_slots = R;
+    if (minmax) {
+      k_acc_init<<<(u32)std::min<uint64_t>((cap * nacc + 255) / 256, (uint64_t)c->sms * 8), 256, 0, st>>>(t, cap,
+                                                                                                       nacc, ops);
+      counted_launch(c);
+    } else {
+      TQ_CUDA(cudaMemsetAsync(t.acc, 0, cap * words * 8, st));
+    }
     p.agg = t;
     launch(c, SINK_AGG, L, P, st);
     uint32_t ovf = 0;
@@ -1524,6 +1533,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       dfree(c, base, tbytes, st);
       direct = false;
       t = AggTable{};
+      cap = cap0;
       setup(G);
     } else {
       // groups are counted by the finalize (its output cursor): capacity R + 1
@@ -2175,7 +2185,10 @@ tq_status tq_agg_update(tq_agg_state* s, const tq_batch* in, void* stream) {
     } else if (S.acc.size() != s->acc_ops.size()) {
       fail(TQ_SCHEMA_MISMATCH, "aggregate input schema changed between batches");
     }
-    if (in->rows == 0) return;
+    // an empty batch adds nothing, except that the state's first partial
+    // (0 rows) carries the partial schema (finalize / take_partial of a
+    // worker whose input was empty)
+    if (in->rows == 0 && !s->partials.empty()) return;
     tq_batch part{};
     agg_core(c, in, P, key_handles(P, s->keys.data(), (uint32_t)s->keys.size()), S.acc, nullptr, &part, st);
     s->partials.push_back(part);

@@ -147,7 +147,19 @@ struct AggTable {
   uint32_t cnt_acc;
   long long key_min;
   uint64_t direct_slots;
+  // direct layout: one array per accumulator (structure of arrays), slot
+  // width dwidth[a] words (1 = a count, 2 = a 16-B sum / min / max), each
+  // array direct_slots + 1 slots long
+  uint8_t dwidth[kMaxAcc];
 };
+
+#ifdef __CUDACC__
+__host__ __device__ __forceinline__ unsigned long long* direct_acc(const AggTable& t, uint32_t a, uint64_t slot) {
+  uint64_t off = 0;
+  for (uint32_t b = 0; b < a; ++b) off += t.dwidth[b];
+  return t.acc + off * (t.direct_slots + 1) + slot * t.dwidth[a];
+}
+#endif
 
 struct PipeParams {
   uint64_t rows;

@@ -56,6 +56,7 @@ def measure(ctx, sf: float, stream, peak_gbs: float, reps: int = 5) -> dict:
             ctx.profile(False)
             op.append(e0.elapsed_time(e1))
             kern.append(sum(v[1] for v in prof.values()))
+            by_kernel = {k: round(v[1], 4) for k, v in prof.items()}
             out_rows = out.rows if hasattr(out, "rows") else 0
             out.free()
         op_ms, k_ms = statistics.median(op), statistics.median(kern)
@@ -64,7 +65,7 @@ def measure(ctx, sf: float, stream, peak_gbs: float, reps: int = 5) -> dict:
                      "op_ms": round(op_ms, 4), "kernel_ms": round(k_ms, 4),
                      "kernel_gbs": round(b / (k_ms * 1e-3) / 1e9, 1) if k_ms else None,
                      "kernel_frac_of_hbm": round(b / (k_ms * 1e-3) / 1e9 / peak_gbs, 3) if k_ms else None,
-                     "op_gbs": round(b / (op_ms * 1e-3) / 1e9, 1), "note": note}
+                     "op_gbs": round(b / (op_ms * 1e-3) / 1e9, 1), "kernels_ms": by_kernel, "note": note}
 
     run("filter_execute", lambda: ctx.filter_execute(L, Col(3) > 9204),
         lambda m: n * 48 + m * 48, "4 lineitem cols, shipdate > 1995-03-15 (54%); COUNT pass + stable EMIT pass", n)
