@@ -980,35 +980,70 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
           const u32 heads = __ballot_sync(kFull, head);
           const u32 start = 31 - __clz(heads & (lanemask_lt() | (1u << lane)) | 1u);  // my run's first lane
           const bool tail = pass && (lane == 31 || ((heads >> (lane + 1)) & 1u) || !((act >> (lane + 1)) & 1u));
+          // sorted key column: a run whose key differs from the warp's first and
+          // last row's key holds every row of that key (the rows before / after
+          // this warp's 32 consecutive rows cannot have it) -> plain stores
+          bool excl = false;
+          if (p.agg.sorted) {
+            const u64 rslot = trow(w, v) < w.nrows ? x.kw[0] - (u64)p.agg.key_min : ~1ull;
+            const u64 first = __shfl_sync(kFull, rslot, 0), last = __shfl_sync(kFull, rslot, 31);
+            excl = slot != first && slot != last;
+          }
 #pragma unroll
           for (u32 a = 0; a < (P::kNacc > 0 ? (u32)P::kNacc : (u32)kMaxAcc); ++a) {
             if (a >= nacc) break;
             const uint8_t op = P::acc_op(p, a);
             const bool valid = pass && x.av[a];
             u64* acc = direct_acc(p.agg, a, pass ? slot : 0);
-            if (op == ACC_SUM_I || op == ACC_CNT) {
-              i128 sv = valid ? (op == ACC_CNT ? (i128)1 : x.ai[a]) : (i128)0;
+            if (op == ACC_CNT) {
+              u32 sv = valid ? 1u : 0u;  // a run is <= 32 rows
 #pragma unroll
               for (u32 o = 1; o < 32; o <<= 1) {
-                const i128 y = shfl_up_i128(sv, o);
-                if (lane >= start + o) sv = add128(sv, y);
+                const u32 y = __shfl_up_sync(kFull, sv, o);
+                if (lane >= start + o) sv += y;
               }
               if (tail) {
-                if (op == ACC_CNT) {
-                  atomicAdd((unsigned long long*)acc, (unsigned long long)lo64(sv));  // RED: no return
-                } else if (sv != 0) {
-                  // limb form {sum of low 32-bit limbs, sum of signed high parts}:
-                  // two fire-and-forget REDs (an int128 add with carry needs the
-                  // old value back: one dependent ATOM round trip per run).
-                  // Exact while every run's sum fits int64 (else the host
-                  // re-runs this aggregate on the hash table)
-                  if (fits64(sv)) {
-                    const long long v = (long long)lo64(sv);
+                if (excl) acc[0] = sv;
+                else atomicAdd((unsigned long long*)acc, (unsigned long long)sv);  // RED: no return
+              }
+            } else if (op == ACC_SUM_I) {
+              // 64-bit scan when every lane's value is within +-2^58 (32 of
+              // them cannot overflow), else the int128 scan
+              const i128 xv = valid ? x.ai[a] : (i128)0;
+              const bool narrow = __all_sync(kFull, (((u128)xv + ((u128)1 << 58)) >> 59) == 0);
+              i128 sv;
+              if (narrow) {
+                long long v64 = (long long)lo64(xv);
+#pragma unroll
+                for (u32 o = 1; o < 32; o <<= 1) {
+                  const long long y = (long long)__shfl_up_sync(kFull, (unsigned long long)v64, o);
+                  if (lane >= start + o) v64 += y;
+                }
+                sv = (i128)v64;
+              } else {
+                sv = xv;
+#pragma unroll
+                for (u32 o = 1; o < 32; o <<= 1) {
+                  const i128 y = shfl_up_i128(sv, o);
+                  if (lane >= start + o) sv = add128(sv, y);
+                }
+              }
+              if (tail && sv != 0) {
+                // limb form {sum of low 32-bit limbs, sum of signed high parts}:
+                // two fire-and-forget REDs (an int128 add with carry needs the
+                // old value back: one dependent ATOM round trip per run).
+                // Exact while every run's sum fits int64 (else the host
+                // re-runs this aggregate on the hash table)
+                if (fits64(sv)) {
+                  const long long v = (long long)lo64(sv);
+                  if (excl) {
+                    *(ulonglong2*)acc = make_ulonglong2((unsigned long long)(v & 0xffffffffll), (unsigned long long)(v >> 32));
+                  } else {
                     atomicAdd((unsigned long long*)acc, (unsigned long long)(v & 0xffffffffll));
                     atomicAdd((unsigned long long*)acc + 1, (unsigned long long)(v >> 32));
-                  } else if (*(volatile u32*)p.agg.overflow == 0) {
-                    atomicExch(p.agg.overflow, 1u);
                   }
+                } else if (*(volatile u32*)p.agg.overflow == 0) {
+                  atomicExch(p.agg.overflow, 1u);
                 }
               }
             } else if (op == ACC_SUM_F) {

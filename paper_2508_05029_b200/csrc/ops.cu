@@ -1187,98 +1187,217 @@ struct FinalParams {
   u64 null_slot;
 };
 
-// Output rows are reserved per BLOCK and iteration (one global atomic per 256
-// slots, not one per warp: at ~10% table load nearly every warp has a group,
-// and per-warp atomics on the one cursor serialised the kernel).
-__global__ void k_agg_final(const __grid_constant__ FinalParams f) {
-  __shared__ u32 s_warp[8];
+__device__ __forceinline__ bool agg_slot_used(const FinalParams& f, u64 s) {
+  return s < f.t.cap && (f.direct ? *direct_acc(f.t, f.cnt_acc, s) != 0 : f.t.state[s] == 2);
+}
+__device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 row);
+
+// Compaction of the occupied slots into output rows, in slot order.  A block
+// takes chunks of kFinItems x 256 contiguous slots; item i of thread t is slot
+// chunk + i * 256 + t (coalesced reads), its row = the chunk's base + the
+// occupied slots before it in the chunk (coalesced writes: a warp's item
+// lands on consecutive rows), and the chunk's rows are reserved with ONE
+// global atomic (a reservation per 256 slots put ~60K atomics on the one
+// cursor for 15M groups).
+constexpr u32 kFinItems = 4;
+__global__ void __launch_bounds__(256) k_agg_final(const __grid_constant__ FinalParams f) {
+  __shared__ u32 s_off[kFinItems][8];   // per (item, warp): rows before it in the chunk
+  __shared__ u32 s_ball[kFinItems][8];  // per (item, warp): occupied lanes
   __shared__ unsigned long long s_base;
   const u32 lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u64 chunk = (u64)kFinItems * 256;
+  const u64 nchunks = (f.t.cap + chunk - 1) / chunk;
+  for (u64 c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const u64 s0 = c * chunk + threadIdx.x;
+#pragma unroll
+    for (u32 i = 0; i < kFinItems; ++i) {
+      const u32 b = __ballot_sync(kFull, agg_slot_used(f, s0 + (u64)i * 256));
+      if (lane == 0) {
+        s_off[i][warp] = __popc(b);
+        s_ball[i][warp] = b;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the kFinItems x 8 (item, warp) counts, item-major
+      constexpr u32 kPer = kFinItems * 8 / 32;
+      u32 v[kPer], sum = 0;
+#pragma unroll
+      for (u32 k = 0; k < kPer; ++k) {
+        v[k] = (&s_off[0][0])[lane * kPer + k];
+        sum += v[k];
+      }
+      u32 incl = sum;
+#pragma unroll
+      for (u32 o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+      }
+      u32 run = incl - sum;
+#pragma unroll
+      for (u32 k = 0; k < kPer; ++k) {
+        (&s_off[0][0])[lane * kPer + k] = run;
+        run += v[k];
+      }
+      const u32 tot = __shfl_sync(kFull, incl, 31);
+      if (lane == 0) s_base = tot ? atomicAdd(f.counter, (unsigned long long)tot) : 0;
+    }
+    __syncthreads();
+    const u64 base = s_base;
+    // (4 items unrolled: independent accumulator loads in flight; 16 unrolled
+    // copies of the emit body stalled on instruction fetch)
+#pragma unroll
+    for (u32 i = 0; i < kFinItems; ++i) {
+      const u32 b = s_ball[i][warp];
+      if ((b >> lane) & 1u) agg_emit_group(f, s0 + (u64)i * 256, base + s_off[i][warp] + __popc(b & lanemask_lt()));
+    }
+    __syncthreads();  // s_off / s_base are rewritten next chunk
+  }
+}
+
+__device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 row) {
+  u64 dk[2] = {(u64)f.key_min + s, s == f.null_slot ? 1ull : 0ull};  // direct: key word, null word
+  const u64* kw = f.direct ? dk : f.t.keys + s * f.kwa;
+  u64 nullw = kw[f.kwa - 1];
+  for (u32 k = 0; k < f.nkeys; ++k) {
+    const KeyOut& ko = f.keys[k];
+    bool isnull = (nullw >> ko.bit) & 1;
+    if (ko.kind == TQ_DECIMAL) {
+      ((u64*)ko.values)[2 * row] = kw[ko.word];
+      ((u64*)ko.values)[2 * row + 1] = kw[ko.word + 1];
+    } else if (ko.kind == TQ_BOOL) {
+      ko.values[row] = (uint8_t)kw[ko.word];
+    } else {
+      ((u64*)ko.values)[row] = kw[ko.word];
+    }
+    if (ko.validity && !isnull) bm_set_atomic(ko.validity, row);
+  }
+  const u64* acc = f.t.acc + s * f.nacc * 2;
+  for (u32 a = 0; a < f.naggs; ++a) {
+    const AggOut& ao = f.aggs[a];
+    const u64* m = f.direct ? direct_acc(f.t, ao.acc, s) : acc + 2 * ao.acc;
+    u64 limb[2];
+    if (f.direct && (ao.kind == AO_SUM_I64 || ao.kind == AO_SUM_DEC || ao.kind == AO_AVG_I)) {
+      // direct table: integer sums are kept as {low-limb sum, high-part sum}
+      const i128 v = add128((i128)(long long)m[1] * ((i128)1 << 32), (i128)m[0]);
+      limb[0] = lo64(v);
+      limb[1] = hi64(v);
+      m = limb;
+    }
+    u64 cnt = ao.cnt == 0xff ? 1 : f.direct ? *direct_acc(f.t, ao.cnt, s) : acc[2 * ao.cnt];
+    bool valid = cnt != 0;
+    switch (ao.kind) {
+      case AO_SUM_I64:
+      case AO_MM_I64:
+        ((u64*)ao.values)[row] = m[0];
+        break;
+      case AO_SUM_DEC:
+      case AO_MM_DEC:
+        ((u64*)ao.values)[2 * row] = m[0];
+        ((u64*)ao.values)[2 * row + 1] = m[1];
+        break;
+      case AO_MM_BOOL:
+        ao.values[row] = m[0] != 0;
+        break;
+      case AO_SUM_F:
+      case AO_MM_F:
+        ((u64*)ao.values)[row] = m[0];
+        break;
+      case AO_CNT:
+        ((u64*)ao.values)[row] = m[0];
+        valid = true;
+        break;
+      case AO_AVG_I: {
+        double d = valid ? i128_to_f64(mk128(m[0], m[1])) / pow(10.0, (double)ao.scale) / (double)cnt : 0.0;
+        ((double*)ao.values)[row] = d;
+        break;
+      }
+      case AO_AVG_F: {
+        double d = valid ? __longlong_as_double((long long)m[0]) / (double)cnt : 0.0;
+        ((double*)ao.values)[row] = d;
+        break;
+      }
+    }
+    if (ao.validity && valid) bm_set_atomic(ao.validity, row);
+  }
+}
+
+// min / max of a plain Int64 key column (+ whether any row is null), for the
+// direct aggregation's range pass when there is no predicate: 16-B loads,
+// one set of atomics per block.
+// out[3] != 0: the column is NOT non-decreasing (or has a null).
+__global__ void __launch_bounds__(256) k_key_range(const long long* v, const uint8_t* valid, u64 rows, long long* out) {
+  __shared__ long long s_mn[8], s_mx[8];
+  __shared__ int s_null, s_unsorted;
+  if (threadIdx.x == 0) s_null = s_unsorted = 0;
+  __syncthreads();
+  long long mn = 0x7fffffffffffffffll, mx = (long long)0x8000000000000000ull;
+  bool nul = false, unsorted = false;
+  const u64 pairs = rows / 2;
+  const longlong2* v2 = (const longlong2*)v;
   const u64 stride = (u64)gridDim.x * blockDim.x;
-  const u64 cap = (f.t.cap + 255) / 256 * 256;  // whole blocks stay in the loop (block barriers)
-  for (u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x; s < cap; s += stride) {
-    const bool occ = s < f.t.cap && (f.direct ? *direct_acc(f.t, f.cnt_acc, s) != 0 : f.t.state[s] == 2);
-    const u32 m = __ballot_sync(0xffffffffu, occ);
-    if (lane == 0) s_warp[warp] = __popc(m);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      u32 tot = 0;
-      for (u32 w = 0; w < blockDim.x / 32; ++w) {
-        const u32 c = s_warp[w];
-        s_warp[w] = tot;
-        tot += c;
+  u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!valid) {  // no bitmap: four independent 16-B loads in flight per thread
+    const u64 lane = threadIdx.x & 31;
+    // (warp-uniform trip count: the shuffles below need every lane)
+    for (; i0 - lane + 31 + 3 * stride < pairs; i0 += 4 * stride) {
+      longlong2 x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[k] = __ldg(v2 + i0 + k * stride);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mn = min(mn, min(x[k].x, x[k].y));
+        mx = max(mx, max(x[k].x, x[k].y));
+        // sortedness: within the pair, and against the next pair's first value
+        // (the next lane's; lane 31 loads it)
+        long long nx = (long long)__shfl_down_sync(kFull, (unsigned long long)x[k].x, 1);
+        const u64 pi = i0 + k * stride;
+        if ((threadIdx.x & 31) == 31) nx = 2 * pi + 2 < rows ? __ldg(v + 2 * pi + 2) : x[k].y;
+        unsorted |= x[k].x > x[k].y || x[k].y > nx;
       }
-      s_base = tot ? atomicAdd(f.counter, (unsigned long long)tot) : 0;
     }
-    __syncthreads();
-    const u64 base = s_base + s_warp[warp];
-    __syncthreads();  // s_warp / s_base are rewritten next iteration
-    if (!occ) continue;
-    u64 row = base + __popc(m & ((1u << lane) - 1));
-    u64 dk[2] = {(u64)f.key_min + s, s == f.null_slot ? 1ull : 0ull};  // direct: key word, null word
-    const u64* kw = f.direct ? dk : f.t.keys + s * f.kwa;
-    u64 nullw = kw[f.kwa - 1];
-    for (u32 k = 0; k < f.nkeys; ++k) {
-      const KeyOut& ko = f.keys[k];
-      bool isnull = (nullw >> ko.bit) & 1;
-      if (ko.kind == TQ_DECIMAL) {
-        ((u64*)ko.values)[2 * row] = kw[ko.word];
-        ((u64*)ko.values)[2 * row + 1] = kw[ko.word + 1];
-      } else if (ko.kind == TQ_BOOL) {
-        ko.values[row] = (uint8_t)kw[ko.word];
-      } else {
-        ((u64*)ko.values)[row] = kw[ko.word];
+  }
+  for (u64 i = i0; i < pairs + (rows & 1); i += stride) {
+    long long a, b;
+    bool va = true, vb = true;
+    if (i < pairs) {
+      const longlong2 x = __ldg(v2 + i);
+      a = x.x;
+      b = x.y;
+      if (valid) {
+        va = bm_get(valid, 2 * i);
+        vb = bm_get(valid, 2 * i + 1);
       }
-      if (ko.validity && !isnull) bm_set_atomic(ko.validity, row);
+    } else {  // odd tail row
+      a = b = v[rows - 1];
+      if (valid) va = vb = bm_get(valid, rows - 1);
     }
-    const u64* acc = f.t.acc + s * f.nacc * 2;
-    for (u32 a = 0; a < f.naggs; ++a) {
-      const AggOut& ao = f.aggs[a];
-      const u64* m = f.direct ? direct_acc(f.t, ao.acc, s) : acc + 2 * ao.acc;
-      u64 limb[2];
-      if (f.direct && (ao.kind == AO_SUM_I64 || ao.kind == AO_SUM_DEC || ao.kind == AO_AVG_I)) {
-        // direct table: integer sums are kept as {low-limb sum, high-part sum}
-        const i128 v = add128((i128)(long long)m[1] * ((i128)1 << 32), (i128)m[0]);
-        limb[0] = lo64(v);
-        limb[1] = hi64(v);
-        m = limb;
-      }
-      u64 cnt = ao.cnt == 0xff ? 1 : f.direct ? *direct_acc(f.t, ao.cnt, s) : acc[2 * ao.cnt];
-      bool valid = cnt != 0;
-      switch (ao.kind) {
-        case AO_SUM_I64:
-        case AO_MM_I64:
-          ((u64*)ao.values)[row] = m[0];
-          break;
-        case AO_SUM_DEC:
-        case AO_MM_DEC:
-          ((u64*)ao.values)[2 * row] = m[0];
-          ((u64*)ao.values)[2 * row + 1] = m[1];
-          break;
-        case AO_MM_BOOL:
-          ao.values[row] = m[0] != 0;
-          break;
-        case AO_SUM_F:
-        case AO_MM_F:
-          ((u64*)ao.values)[row] = m[0];
-          break;
-        case AO_CNT:
-          ((u64*)ao.values)[row] = m[0];
-          valid = true;
-          break;
-        case AO_AVG_I: {
-          double d = valid ? i128_to_f64(mk128(m[0], m[1])) / pow(10.0, (double)ao.scale) / (double)cnt : 0.0;
-          ((double*)ao.values)[row] = d;
-          break;
-        }
-        case AO_AVG_F: {
-          double d = valid ? __longlong_as_double((long long)m[0]) / (double)cnt : 0.0;
-          ((double*)ao.values)[row] = d;
-          break;
-        }
-      }
-      if (ao.validity && valid) bm_set_atomic(ao.validity, row);
+    if (va) { mn = min(mn, a); mx = max(mx, a); } else nul = true;
+    if (vb) { mn = min(mn, b); mx = max(mx, b); } else nul = true;
+    unsorted |= a > b || (2 * i + 2 < rows && b > __ldg(v + 2 * i + 2));
+  }
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    mn = min(mn, (long long)__shfl_xor_sync(kFull, (unsigned long long)mn, m));
+    mx = max(mx, (long long)__shfl_xor_sync(kFull, (unsigned long long)mx, m));
+  }
+  if (__any_sync(kFull, nul) && (threadIdx.x & 31) == 0) s_null = 1;
+  if (__any_sync(kFull, unsorted) && (threadIdx.x & 31) == 0) s_unsorted = 1;
+  if ((threadIdx.x & 31) == 0) {
+    s_mn[threadIdx.x >> 5] = mn;
+    s_mx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      mn = min(mn, s_mn[w]);
+      mx = max(mx, s_mx[w]);
     }
+    if (mn <= mx) {
+      atomicMin(out, mn);
+      atomicMax(out + 1, mx);
+    }
+    if (s_null) atomicOr((unsigned long long*)out + 2, 1ull);
+    if (s_unsorted || s_null) atomicOr((unsigned long long*)out + 3, 1ull);
   }
 }
 
@@ -1429,7 +1548,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
   // protocol, no regrowth re-runs, and clustered keys update neighbouring
   // slots.  Only for final aggregates with a Count(*) accumulator (it marks
   // the occupied slots) and inputs large enough to pay for the range pass.
-  bool direct = false;
+  bool direct = false, key_sorted = false;
   long long kmin = 0;
   uint64_t R = 0;
   u32 cnt_idx = 0;
@@ -1447,17 +1566,32 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       if (P.has_pred) need.push_back(P.pred_h);
       Lr.p.load_mask = P.pb.column_deps(need);
       long long* kr = (long long*)dalloc(c, 32, st);
-      const long long init[3] = {0x7fffffffffffffffll, (long long)0x8000000000000000ull, 0};
-      TQ_CUDA(cudaMemcpyAsync(kr, init, 24, cudaMemcpyHostToDevice, st));
+      // {min, max, any null, not sorted}; the pipeline range pass (a predicate
+      // or a computed key) does not check sortedness
+      const long long init[4] = {0x7fffffffffffffffll, (long long)0x8000000000000000ull, 0, 1};
+      TQ_CUDA(cudaMemcpyAsync(kr, init, 32, cudaMemcpyHostToDevice, st));
       Lr.p.key_range = kr;
-      launch(c, SINK_COUNT, Lr, P, st);
+      const Operand& ko = P.pb.root(kh[0]);
+      if (!P.has_pred && ko.kind == K_COL_I64) {  // a plain key column: one streaming reduction
+        const tq_column& col = in->cols[P.pb.staged()[ko.idx]];
+        TQ_CUDA(cudaMemsetAsync(kr + 3, 0, 8, st));
+        const int ph = prof_begin(c, "key_range", st);
+        k_key_range<<<c->sms * 4, 256, 0, st>>>((const long long*)col.values, in->rows ? col.validity : nullptr,
+                                                 in->rows, kr);
+        prof_end(c, ph, st);
+        counted_launch(c);
+        TQ_CUDA(cudaGetLastError());
+      } else {
+        launch(c, SINK_COUNT, Lr, P, st);
+      }
       long long mn, mx;
       {
         std::lock_guard<std::mutex> g(c->mu);
-        TQ_CUDA(cudaMemcpyAsync(c->pinned, kr, 24, cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaMemcpyAsync(c->pinned, kr, 32, cudaMemcpyDeviceToHost, st));
         { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
         mn = ((long long*)c->pinned)[0];
         mx = ((long long*)c->pinned)[1];
+        key_sorted = ((long long*)c->pinned)[3] == 0;
       }
       dfree(c, kr, 32, st);
       const uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
@@ -1493,13 +1627,14 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       t.dwidth[i] = acc[i].op == ACC_CNT ? 1 : 2;
       words += t.dwidth[i];
     }
-    tbytes = cap * words * 8 + 64;
+    t.dstride = (cap + 1) & ~1ull;
+    tbytes = t.dstride * words * 8 + 64;
     uint8_t* base = (uint8_t*)dalloc(c, tbytes, st);
     t.state = (uint32_t*)base;  // (no state words: freed through this base)
     t.keys = nullptr;
     t.acc = (u64*)base;
     t.cap = cap;
-    uint8_t* tail = base + cap * words * 8;
+    uint8_t* tail = base + t.dstride * words * 8;
     t.nused = (unsigned long long*)tail;
     t.overflow = (uint32_t*)(tail + 8);
     TQ_CUDA(cudaMemsetAsync(tail, 0, 16, st));
@@ -1510,6 +1645,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       minmax |= acc[i].op == ACC_MIN_I || acc[i].op == ACC_MAX_I || acc[i].op == ACC_MIN_F || acc[i].op == ACC_MAX_F;
     }
     t.direct = 1;
+    t.sorted = key_sorted ? 1u : 0u;
     t.cnt_acc = cnt_idx;
     t.key_min = kmin;
     t.direct_slots = R;
@@ -1518,7 +1654,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
                                                                                                        nacc, ops);
       counted_launch(c);
     } else {
-      TQ_CUDA(cudaMemsetAsync(t.acc, 0, cap * words * 8, st));
+      TQ_CUDA(cudaMemsetAsync(t.acc, 0, t.dstride * words * 8, st));
     }
     p.agg = t;
     launch(c, SINK_AGG, L, P, st);
@@ -1650,7 +1786,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     f.null_slot = R;
     f.counter = (unsigned long long*)(t.nused + 0);  // reuse as output cursor
     TQ_CUDA(cudaMemsetAsync(t.nused, 0, 8, st));
-    u32 nb = (u32)std::min<uint64_t>(2048, (cap + 255) / 256);
+    u32 nb = (u32)std::min<uint64_t>((uint64_t)c->sms * 16, (cap + kFinItems * 256 - 1) / (kFinItems * 256));
     const int ph = prof_begin(c, "agg_final", st);
     k_agg_final<<<nb, 256, 0, st>>>(f);
     prof_end(c, ph, st);

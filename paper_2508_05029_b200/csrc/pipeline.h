@@ -149,15 +149,21 @@ struct AggTable {
   uint64_t direct_slots;
   // direct layout: one array per accumulator (structure of arrays), slot
   // width dwidth[a] words (1 = a count, 2 = a 16-B sum / min / max), each
-  // array direct_slots + 1 slots long
+  // array dstride >= direct_slots + 1 slots long (even: 16-B arrays stay
+  // 16-B aligned for the int128 min / max CAS)
   uint8_t dwidth[kMaxAcc];
+  uint64_t dstride;
+  // the key column is non-decreasing (the range pass checked it): a run of
+  // one key strictly inside a warp's 32 consecutive rows holds EVERY row of
+  // that key, so its slot is written with plain stores instead of atomics
+  uint32_t sorted;
 };
 
 #ifdef __CUDACC__
 __host__ __device__ __forceinline__ unsigned long long* direct_acc(const AggTable& t, uint32_t a, uint64_t slot) {
   uint64_t off = 0;
   for (uint32_t b = 0; b < a; ++b) off += t.dwidth[b];
-  return t.acc + off * (t.direct_slots + 1) + slot * t.dwidth[a];
+  return t.acc + off * t.dstride + slot * t.dwidth[a];
 }
 #endif
 
