@@ -73,6 +73,14 @@ tq_status tq_concat(tq_ctx* ctx, const tq_batch* ins, uint32_t n, tq_batch* out,
 /* slice: transform.cpp:21-47. */
 tq_status tq_slice(tq_ctx* ctx, const tq_batch* in, uint64_t start, uint64_t len, tq_batch* out,
                    void* stream);
+/* rebatch (reference transform.cpp:122-154): the concatenation of `ins`
+ * re-cut so every output but the last holds >= target_bytes by the
+ * reference's per-row estimate (sum of fixed widths + 1 per column, + the Utf8
+ * payload), i.e. lands in [target / 2, 2 * target]; one batch when the total
+ * (batch_size_bytes) is <= 2 * target.  *outs is malloc'ed (free with free()),
+ * each batch with tq_batch_free. */
+tq_status tq_rebatch(tq_ctx* ctx, const tq_batch* ins, uint32_t n, uint64_t target_bytes, tq_batch** outs,
+                     uint32_t* nout, void* stream);
 
 /* ---- operators ---------------------------------------- */
 /* filter_execute: rows where pred is true; schema unchanged. */

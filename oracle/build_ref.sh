@@ -25,3 +25,20 @@ g++ -std=c++20 -O2 -fPIC -shared -Wall -Wextra -pthread \
   -o "$OUT/libtierq_ref.so.tmp"
 mv "$OUT/libtierq_ref.so.tmp" "$OUT/libtierq_ref.so"
 echo "build_ref: built $OUT/libtierq_ref.so"
+
+# The C++ binding of INTEGRATION.md §2-3, compiled against the reference's
+# headers + columnar sources and libtq_gpu.so's C-ABI (test infrastructure;
+# needs a GPU to run: tests/test_boundary.py, -m gpu).
+LIB="$HERE/../paper_2508_05029_b200"
+if [ -f "$LIB/libtq_gpu.so" ]; then
+  g++ -std=c++20 -O2 -Wall -Wextra -pthread \
+    -I"$REF/include" -I"$HERE/../include" \
+    "$HERE/boundary_test.cpp" \
+    "$REF/src/common.cpp" \
+    "$REF/src/columnar/types.cpp" \
+    "$REF/src/columnar/transform.cpp" \
+    -L"$LIB" -ltq_gpu -Wl,-rpath,'$ORIGIN/../../paper_2508_05029_b200' \
+    -o "$OUT/boundary_test.tmp"
+  mv "$OUT/boundary_test.tmp" "$OUT/boundary_test"
+  echo "build_ref: built $OUT/boundary_test"
+fi

@@ -247,6 +247,23 @@ def ref_concat(bs) -> HostBatch:
     return _out(L, L.tqr_concat(arr, len(cs), C.byref(out)), out, "tqr")
 
 
+def ref_batch_size_bytes(b: HostBatch) -> int:
+    """The REFERENCE's batch_size_bytes (types.cpp:166-170)."""
+    bc = b.to_c()
+    return int(ref().tqr_batch_size_bytes(C.byref(bc)))
+
+
+def ref_rebatch_rows(b: HostBatch, target: int) -> List[int]:
+    """Row counts of the REFERENCE's rebatch (transform.cpp:122-154) of one batch."""
+    L = ref()
+    bc = b.to_c()
+    cap = max(16, b.rows + 1)
+    rows = (C.c_uint64 * cap)()
+    n = C.c_uint32()
+    _check(L.tqr_rebatch_rows(C.byref(bc), target, rows, cap, C.byref(n)), L, "tqr")
+    return [int(rows[i]) for i in range(n.value)]
+
+
 def ref_slice(b: HostBatch, start, n) -> HostBatch:
     L, out = ref(), TqBatchC()
     bc = b.to_c()

@@ -2006,6 +2006,125 @@ tq_status tq_concat(tq_ctx* c, const tq_batch* ins, uint32_t n, tq_batch* out, v
   });
 }
 
+// rebatch cut points (transform.cpp:133-150): one thread walks the prefix
+// sums of the per-row cost, each cut a binary search for the first row where
+// the bytes since the last cut reach the target.
+__global__ void k_rebatch_cuts(const u64* pref, u64 rows, u64 target, u64* cuts, u32 cap, u32* ncuts) {
+  u64 start = 0;
+  u32 n = 0;
+  while (start < rows && n < cap) {
+    // first r >= start with pref[r + 1] - pref[start] >= target
+    u64 lo = start, hi = rows;  // answer in [start, rows)
+    while (lo < hi) {
+      const u64 mid = (lo + hi) / 2;
+      if (pref[mid + 1] - pref[start] >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    if (lo + 1 >= rows) break;  // the rest is the last batch
+    cuts[n++] = lo + 1;
+    start = lo + 1;
+  }
+  *ncuts = n;
+}
+
+__global__ void k_row_cost(const int32_t* const* offs, u32 nutf8, u64 rows, u32 fixed, u32* cost) {
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (u64)gridDim.x * blockDim.x) {
+    u32 c = fixed;
+    for (u32 k = 0; k < nutf8; ++k) c += (u32)(offs[k][r + 1] - offs[k][r]);
+    cost[r] = c;
+  }
+}
+
+tq_status tq_rebatch(tq_ctx* c, const tq_batch* ins, uint32_t n, uint64_t target, tq_batch** outs, uint32_t* nout,
+                     void* stream) {
+  return guard([&] {
+    if (target == 0) fail(TQ_INTERNAL, "rebatch target must be positive");
+    *outs = nullptr;
+    *nout = 0;
+    if (n == 0) return;
+    cudaStream_t st = pick(c, stream);
+    tq_batch all{};
+    bool owned = false;
+    if (n == 1) {
+      check_device_batch(&ins[0]);
+      all = ins[0];
+    } else {
+      tq_status r = tq_concat(c, ins, n, &all, st);
+      if (r != TQ_OK) fail(r, g_err);
+      owned = true;
+    }
+    // batch_size_bytes (types.cpp:166-170) and the fixed per-row estimate
+    uint64_t total = 0, fixed = 0;
+    std::vector<const int32_t*> utf8;
+    for (uint32_t k = 0; k < all.ncols; ++k) {
+      const tq_column& col = all.cols[k];
+      total += col.values_bytes;
+      if (col.validity && all.rows) total += (all.rows + 7) / 8;
+      if (col.kind == TQ_UTF8) {
+        total += (all.rows + 1) * 4;
+        utf8.push_back(col.offsets);
+      }
+      fixed += width_of(col.kind) + 1;
+    }
+    std::vector<uint64_t> cuts;
+    if (all.rows > 0 && total > target * 2) {
+      if (utf8.empty()) {
+        // every row costs `fixed`: cut every ceil(target / fixed) rows
+        const uint64_t k = (target + fixed - 1) / fixed;
+        for (uint64_t r = k; r < all.rows; r += k) cuts.push_back(r);
+      } else {
+        const uint64_t rows = all.rows;
+        u32* cost = (u32*)dalloc(c, rows * 4, st);
+        u64* pref = (u64*)dalloc(c, (rows + 1) * 8, st);
+        const int32_t** d_offs = (const int32_t**)dalloc(c, utf8.size() * 8, st);
+        TQ_CUDA(cudaMemcpyAsync(d_offs, utf8.data(), utf8.size() * 8, cudaMemcpyHostToDevice, st));
+        k_row_cost<<<grid_for(c, rows), 256, 0, st>>>(d_offs, (u32)utf8.size(), rows, (u32)fixed, cost);
+        counted_launch(c);
+        // exclusive scan into pref[0..rows), total at pref[rows]: pref[r+1] - pref[s] = bytes of rows s..r
+        scan_u32(c, cost, rows, pref, pref + rows, st);
+        const uint32_t cap = (uint32_t)std::min<uint64_t>(rows, total / std::max<uint64_t>(1, target / 2) + 4);
+        u64* d_cuts = (u64*)dalloc(c, cap * 8ull + 8, st);
+        u32* d_n = (u32*)(d_cuts + cap);
+        k_rebatch_cuts<<<1, 1, 0, st>>>(pref, rows, target, d_cuts, cap, d_n);
+        counted_launch(c);
+        uint32_t nc = 0;
+        TQ_CUDA(cudaMemcpyAsync(&nc, d_n, 4, cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaStreamSynchronize(st));
+        cuts.resize(nc);
+        if (nc) TQ_CUDA(cudaMemcpy(cuts.data(), d_cuts, nc * 8ull, cudaMemcpyDeviceToHost));
+        dfree(c, d_cuts, cap * 8ull + 8, st);
+        dfree(c, d_offs, utf8.size() * 8, st);
+        dfree(c, pref, (rows + 1) * 8, st);
+        dfree(c, cost, rows * 4, st);
+      }
+    }
+    std::vector<tq_batch> parts;
+    if (cuts.empty()) {
+      if (owned) {
+        parts.push_back(all);
+        owned = false;
+      } else {
+        tq_batch cp{};
+        take_impl(c, &all, nullptr, all.rows, 0, &cp, st);  // the reference returns a copy
+        parts.push_back(cp);
+      }
+    } else {
+      uint64_t start = 0;
+      cuts.push_back(all.rows);
+      for (uint64_t e : cuts) {
+        tq_batch part{};
+        take_impl(c, &all, nullptr, e - start, start, &part, st);
+        parts.push_back(part);
+        start = e;
+      }
+    }
+    if (owned) tq_batch_free(c, &all);
+    *outs = (tq_batch*)std::malloc(sizeof(tq_batch) * parts.size());
+    std::memcpy(*outs, parts.data(), sizeof(tq_batch) * parts.size());
+    *nout = (uint32_t)parts.size();
+  });
+}
+
 }  // extern "C"
 
 // ================================================================== operator entry points

@@ -78,6 +78,7 @@ def lib():
         L.tq_take.argtypes = [V, B, V, C.c_uint64, B, V]
         L.tq_concat.argtypes = [V, B, C.c_uint32, B, V]
         L.tq_slice.argtypes = [V, B, C.c_uint64, C.c_uint64, B, V]
+        L.tq_rebatch.argtypes = [V, B, C.c_uint32, C.c_uint64, P(P(TqBatchC)), P(C.c_uint32), V]
         L.tq_filter.argtypes = [V, B, TqExprC, B, V]
         L.tq_project.argtypes = [V, B, P(TqExprC), C.c_uint32, B, V]
         U32 = P(C.c_uint32)
@@ -360,6 +361,23 @@ class Context:
     def slice(self, b: DeviceBatch, start: int, n: int, stream=None) -> DeviceBatch:
         out = TqBatchC()
         return self._wrap(lib().tq_slice(self.handle, C.byref(b.c), start, n, C.byref(out), stream), out)
+
+    def rebatch(self, bs: Sequence[DeviceBatch], target_bytes: int, stream=None) -> List[DeviceBatch]:
+        """reference rebatch (transform.cpp:122-154) on the GPU."""
+        arr = (TqBatchC * max(1, len(bs)))(*[b.c for b in bs])
+        outs = C.POINTER(TqBatchC)()
+        n = C.c_uint32()
+        self._check(lib().tq_rebatch(self.handle, arr, len(bs), target_bytes, C.byref(outs), C.byref(n), stream))
+        res = []
+        for i in range(n.value):
+            c = TqBatchC()
+            C.memmove(C.byref(c), C.byref(outs[i]), C.sizeof(TqBatchC))
+            res.append(DeviceBatch(self, c))
+        if n.value:
+            libc = C.CDLL(None)
+            libc.free.argtypes = [C.c_void_p]
+            libc.free(C.cast(outs, C.c_void_p))
+        return res
 
     # ---- operators (SPEC.md:560-611) --------------------------------------
     def filter_execute(self, b: DeviceBatch, pred: Expr, stream=None) -> DeviceBatch:

@@ -4,11 +4,12 @@ exports every symbol include/*.h declares, and refuses to run without one
 import ctypes as C
 import os
 import re
+import subprocess
 
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADERS = [os.path.join(ROOT, "include", h) for h in ("tq_gpu.h", "tq_exchange.h", "tq_memexec.h")]
+HEADERS = [os.path.join(ROOT, "include", h) for h in ("tq_gpu.h", "tq_exchange.h", "tq_memexec.h", "tq_engine.h")]
 
 
 def declared_functions():
@@ -65,3 +66,25 @@ def test_product_does_not_reference_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "liboracle" not in src and "tqo_" not in src and "import oracle" not in src, f
+
+
+BOUNDARY_TEST = os.path.join(ROOT, "oracle", "_ref", "boundary_test")
+
+
+def test_cpp_boundary_binding_builds():
+    """INTEGRATION.md §2-3's C++ binding compiles against the reference's own
+    headers and links libtq_gpu.so (oracle/build_ref.sh)."""
+    if not os.path.exists(BOUNDARY_TEST):
+        pytest.skip("reference sources absent: oracle/_ref/boundary_test not built")
+    out = subprocess.run(["ldd", BOUNDARY_TEST], capture_output=True, text=True).stdout
+    assert "libtq_gpu.so" in out and "not found" not in out
+
+
+@pytest.mark.gpu
+def test_cpp_boundary_binding_runs():
+    """reference ColumnBatch -> tq_batch -> tq_filter / tq_aggregate on the GPU
+    -> ColumnBatch, equal to the reference's own take() / SPEC examples by the
+    reference's operator==; statuses come back as tierq::Error{Errc}."""
+    r = subprocess.run([BOUNDARY_TEST], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0 and "boundary_test ok" in r.stdout

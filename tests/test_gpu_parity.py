@@ -386,3 +386,25 @@ def test_aggregate_direct_dense_key(ctx, case):
             (AGG_COUNT, 2), (AGG_MIN, 2)]
     got = ctx.aggregate_execute(ctx.upload(b), [0], aggs).to_host()
     assert_batches_equal(got, O.aggregate_execute(b, [0], aggs))
+
+
+@pytest.mark.parametrize("case", ["fixed", "utf8", "small", "many_inputs"])
+def test_rebatch_matches_reference(ctx, case):
+    """tq_rebatch == the reference's rebatch (transform.cpp:122-154): the same
+    cut points (row counts from the reference library itself) and the same rows."""
+    seed = {"fixed": 1, "utf8": 2, "small": 3, "many_inputs": 4}[case]
+    rows = {"fixed": 50000, "utf8": 30000, "small": 100, "many_inputs": 20000}[case]
+    b = rand_batch(seed, rows, (INT64, DECIMAL, BOOL), null_frac=0.1, utf8=case == "utf8")
+    target = {"fixed": 64 << 10, "utf8": 40 << 10, "small": 1 << 20, "many_inputs": 50 << 10}[case]
+    d = ctx.upload(b)
+    ins = [ctx.slice(d, s, min(3000, b.rows - s)) for s in range(0, b.rows, 3000)] if case == "many_inputs" else [d]
+    parts = ctx.rebatch(ins, target)
+    want_rows = O.ref_rebatch_rows(b, target)
+    assert [p.rows for p in parts] == want_rows
+    at = 0
+    for p in parts:
+        assert_batches_equal(p.to_host(), O.slice_(b, at, p.rows), ordered=True)
+        at += p.rows
+    if len(want_rows) > 1:  # every output but the last in [target / 2, 2 * target] bytes
+        sizes = [O.ref_batch_size_bytes(O.slice_(b, int(s), n)) for s, n in zip(np.cumsum([0] + want_rows[:-1]), want_rows)]
+        assert all(target // 2 <= x <= 2 * target for x in sizes[:-1])
