@@ -36,6 +36,7 @@ const char* tq_last_error(void);                 /* thread-local message of the 
 const char* tq_errc_name(tq_status status);      /* common.cpp:19-41 errc_name */
 tq_status tq_sync(tq_ctx* ctx, void* stream);
 uint64_t tq_device_bytes_in_use(tq_ctx* ctx);    /* ledger: allocated Device-tier bytes */
+uint64_t tq_device_bytes_reserved(tq_ctx* ctx);  /* device memory the context's pool holds (>= in use) */
 uint32_t tq_kernel_launches(tq_ctx* ctx);        /* kernels this context has launched */
 void* tq_ctx_stream(tq_ctx* ctx);                /* the context's own cudaStream_t */
 /* CUDA-event timing of every pipeline kernel launch (on its launching stream);

@@ -300,9 +300,9 @@ def assert_batches_equal(got: HostBatch, want: HostBatch, rtol: float = 1e-9, or
         vg, vw = got.validity_of(c)[og], want.validity_of(c)[ow]
         assert np.array_equal(vg, vw), f"col {c}: validity differs at rows {np.nonzero(vg != vw)[0][:10]}"
         if g.kind == UTF8:
-            assert got.column_py(c) is not None
-            pg = [got.column_py(c)[i] for i in og]
-            pw = [want.column_py(c)[i] for i in ow]
+            cg, cw = got.column_py(c), want.column_py(c)
+            pg = [cg[i] for i in og]
+            pw = [cw[i] for i in ow]
             assert pg == pw, f"col {c}: utf8 values differ"
             continue
         if g.kind == FLOAT64:

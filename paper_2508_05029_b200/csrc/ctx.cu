@@ -76,6 +76,49 @@ void cuda_check(cudaError_t e, const char* what) {
   }
 }
 
+namespace {
+// Pinned read-back slots are recycled process-wide: a thread takes one on
+// first use and hands it back when it exits (the engine starts executor
+// threads per query; a cudaHostAlloc / cudaFreeHost pair per thread would
+// pin memory and synchronise the device every time).
+std::mutex g_pinned_mu;
+std::vector<void*>* g_pinned_free = new std::vector<void*>;  // never destroyed
+struct PinnedScratch {
+  void* p = nullptr;
+  ~PinnedScratch() {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(g_pinned_mu);
+    g_pinned_free->push_back(p);
+  }
+};
+thread_local PinnedScratch t_pinned;
+}  // namespace
+
+void* pinned_scratch(tq_ctx* c) {
+  (void)c;
+  if (!t_pinned.p) {
+    {
+      std::lock_guard<std::mutex> g(g_pinned_mu);
+      if (!g_pinned_free->empty()) {
+        t_pinned.p = g_pinned_free->back();
+        g_pinned_free->pop_back();
+      }
+    }
+    if (!t_pinned.p) TQ_CUDA(cudaHostAlloc(&t_pinned.p, 4096, cudaHostAllocPortable));
+  }
+  return t_pinned.p;
+}
+
+cudaStream_t exec_stream(tq_ctx* c, int idx) {
+  std::lock_guard<std::mutex> g(c->mu);
+  while ((int)c->exec_streams.size() <= idx) {
+    cudaStream_t s;
+    TQ_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    c->exec_streams.push_back(s);
+  }
+  return c->exec_streams[idx];
+}
+
 void counted_launch(tq_ctx* c) { c->launches.fetch_add(1, std::memory_order_relaxed); }
 
 int prof_begin(tq_ctx* c, const char* name, cudaStream_t st) {
@@ -216,6 +259,10 @@ void tq_ctx_destroy(tq_ctx* c) {
   for (auto& kv : c->prog_cache) cudaFree(kv.second);
   if (c->host_pool && c->host_pool_free) c->host_pool_free(c->host_pool);
   cudaFreeHost(c->pinned);
+  for (cudaStream_t s : c->exec_streams) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -225,6 +272,12 @@ tq_status tq_sync(tq_ctx* c, void* stream) {
 }
 
 uint64_t tq_device_bytes_in_use(tq_ctx* c) { return c->in_use.load(); }
+
+uint64_t tq_device_bytes_reserved(tq_ctx* c) {
+  unsigned long long v = 0;
+  cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemCurrent, &v);
+  return (uint64_t)v;
+}
 
 void tq_profile_enable(tq_ctx* c, int on) {
   std::lock_guard<std::mutex> g(c->mu);

@@ -21,6 +21,7 @@ struct tq_ctx {
   std::atomic<uint64_t> in_use{0};     // ledger: allocated bytes
   std::atomic<uint32_t> launches{0};   // kernels launched by this context
   void* pinned = nullptr;              // small pinned readback area (4 KiB)
+  std::vector<cudaStream_t> exec_streams;  // engine executor streams (exec_stream)
   std::mutex mu;                       // guards pinned + program cache
   std::map<std::string, void*> prog_cache;  // program bytes -> device copy
   // optional per-kernel CUDA-event timing (tq_profile_*): events recorded on
@@ -69,6 +70,16 @@ void alloc_batch(tq_ctx* c, uint64_t rows, const std::vector<tq_column>& schema,
                  tq_batch* out, cudaStream_t st, const std::vector<uint64_t>* utf8_bytes = nullptr);
 void counted_launch(tq_ctx* c);
 // begin/end an event-timed region for kernel `name` (no-op unless profiling)
+// This thread's small pinned read-back area (4 KiB, portable, device-visible):
+// data-dependent counts are copied here and read after a stream sync, with
+// no context-wide lock held across the sync (concurrent operators on other
+// threads' streams — and a peer rank's collectives — never wait on it).
+void* pinned_scratch(tq_ctx* c);
+// The context's executor stream `idx` (created on first use, kept for the
+// context's lifetime: the engine's Compute / Memory / Pre-loading threads of
+// every query reuse them, so stream-ordered pool memory freed by one query is
+// reused by the next without new mappings).
+cudaStream_t exec_stream(tq_ctx* c, int idx);
 int prof_begin(tq_ctx* c, const char* name, cudaStream_t st);
 void prof_end(tq_ctx* c, int h, cudaStream_t st);
 

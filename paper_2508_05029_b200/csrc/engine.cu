@@ -74,6 +74,8 @@ void check(tq_status s) {
 struct OpStat {
   uint64_t tasks = 0;
   double ms = 0;
+  double gpu_ms = 0;       // stream time between events around the operator calls (Filter/Project/Probe)
+  double first_call_ms = 0;  // host time of the first operator call's return (launch + host syncs inside)
   std::atomic<uint64_t> rows_out{0};
 };
 
@@ -486,8 +488,8 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
 
 void Runtime::worker(int idx) {
   cudaSetDevice(ctx->device);
-  cudaStream_t st;
-  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);  // one stream per Compute thread
+  // one stream per Compute thread, kept by the context across queries
+  cudaStream_t st = exec_stream(ctx, 2 + idx);
   for (;;) {
     Task t;
     {
@@ -511,8 +513,6 @@ void Runtime::worker(int idx) {
     }
   }
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
-  (void)idx;
 }
 
 // Pre-loading executor: promote Host-resident inputs of the first queued
@@ -591,14 +591,13 @@ Runtime::~Runtime() {
       h->dev.cols = nullptr;
     }
   // the pool belongs to the context (reused by the next query)
-  if (copy_stream) cudaStreamDestroy(copy_stream);
-  if (preload_stream) cudaStreamDestroy(preload_stream);
+  // (copy / preload streams belong to the context)
 }
 
 void Runtime::setup() {
   cudaSetDevice(ctx->device);
-  cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking);
-  cudaStreamCreateWithFlags(&preload_stream, cudaStreamNonBlocking);
+  copy_stream = exec_stream(ctx, 0);
+  preload_stream = exec_stream(ctx, 1);
   if (opts.pool_capacity) {
     const uint64_t bs = opts.pool_buffer_size ? opts.pool_buffer_size : (1 << 20);
     if (ctx->host_pool && ctx->host_pool_buffer_size == bs && ctx->host_pool_buffers >= opts.pool_capacity &&
@@ -676,15 +675,30 @@ class ScanOp : public Op {
 void run_all_or_nothing(Runtime* rt, Op* op, Task& t, cudaStream_t st,
                         const std::function<void(const tq_batch&, tq_batch&)>& body) {
   std::vector<tq_batch> outs;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
   try {
+    cudaEventRecord(e0, st);
+    auto h0 = Clock::now();
     for (HP& h : t.inputs) {
       tq_batch o{};
       body(h->dev, o);
       outs.push_back(o);
     }
+    const double call_ms = std::chrono::duration<double, std::milli>(Clock::now() - h0).count();
+    cudaEventRecord(e1, st);
     cudaStreamSynchronize(st);
+    float g = 0;
+    cudaEventElapsedTime(&g, e0, e1);
+    op->stat.gpu_ms += g;
+    op->stat.first_call_ms += call_ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   } catch (...) {
     cudaStreamSynchronize(st);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     for (tq_batch& o : outs) tq_batch_free(rt->ctx, &o);
     throw;
   }
@@ -849,7 +863,8 @@ class AggOp : public Op {
  public:
   AggOp(Runtime* rt, std::string n, int depth, Holder* in, EB* pred, std::vector<EB> exprs, std::vector<uint32_t> keys,
         std::vector<tq_agg> aggs, bool dist = false, const XPair* copart = nullptr, int turn = -1)
-      : Op(rt, std::move(n), depth, 2.0), in(in), nkeys((uint32_t)keys.size()), dist(dist), copart(copart), turn(turn) {
+      : Op(rt, std::move(n), depth, 2.0), in(in), nkeys((uint32_t)keys.size()), dist(dist), copart(copart), turn(turn),
+        pred(pred ? *pred : EB()), has_pred(pred), exprs(exprs), keys(keys), aggs(aggs) {
     std::vector<tq_expr> ex;
     for (auto& e : exprs) ex.push_back(e.e());
     EB p = pred ? *pred : EB();
@@ -860,10 +875,19 @@ class AggOp : public Op {
   ~AggOp() override { tq_agg_destroy(state); }
   void poll(std::vector<Task>& ts) override {
     if (running) return;
+    // the first batch is held back: a single-batch input is aggregated and
+    // finalised in one call (no partial state + merge pass)
+    if (!in->empty() && !first && !updated) {
+      first = in->pop();
+      return;
+    }
     if (!in->empty()) {
       Task t;
       t.op = this;
+      if (first) t.inputs.push_back(first);
+      first = nullptr;
       t.inputs.push_back(in->pop());
+      updated = true;
       ts.push_back(std::move(t));
       return;
     }
@@ -873,6 +897,8 @@ class AggOp : public Op {
       Task t;
       t.op = this;
       t.kind = 1;
+      if (first) t.inputs.push_back(first);
+      first = nullptr;
       ts.push_back(std::move(t));
       return;
     }
@@ -888,7 +914,30 @@ class AggOp : public Op {
       }
       return;
     }
-    if (dist && !(copart && pair_hash_partitioned(copart))) {
+    const bool local = !dist || (copart && pair_hash_partitioned(copart));
+    if (local && !updated && t.inputs.size() == 1) {  // the whole input in one batch: one call
+      std::vector<tq_expr> ex;
+      for (auto& e : exprs) ex.push_back(e.e());
+      tq_expr pe = pred.e();
+      tq_batch o{};
+      check(tq_pipeline_aggregate(rt->ctx, &t.inputs[0]->dev, has_pred ? &pe : nullptr, ex.empty() ? nullptr : ex.data(),
+                                  (uint32_t)ex.size(), keys.data(), (uint32_t)keys.size(), aggs.data(),
+                                  (uint32_t)aggs.size(), &o, st));
+      cudaStreamSynchronize(st);
+      if (!t.inputs[0]->view) rt->free_handle(t.inputs[0]);
+      stat.rows_out += o.rows;
+      out->push(rt->adopt(o, false));
+      std::lock_guard<std::mutex> g(rt->mu);
+      done = true;
+      if (dist) rt->exchange_turn++;
+      return;
+    }
+    for (HP& h : t.inputs) {  // a held-back first batch
+      check(tq_agg_update(state, &h->dev, st));
+      cudaStreamSynchronize(st);
+      if (!h->view) rt->free_handle(h);
+    }
+    if (!local) {
       tq_batch part{}, recv{};
       check(tq_agg_take_partial(state, &part, st));
       std::vector<uint32_t> kk(nkeys);
@@ -916,7 +965,14 @@ class AggOp : public Op {
   bool dist;
   const XPair* copart;
   int turn;
+  EB pred;
+  bool has_pred;
+  std::vector<EB> exprs;
+  std::vector<uint32_t> keys;
+  std::vector<tq_agg> aggs;
   tq_agg_state* state = nullptr;
+  HP first;              // held-back first input batch
+  bool updated = false;  // some batch went through tq_agg_update
   bool final_submitted = false, done = false;
 };
 
@@ -1105,14 +1161,36 @@ void XSideOp::run(Task& t, cudaStream_t st) {
   const tq_expr* pp = has_pred ? &pe : nullptr;
   const tq_expr* ep = ex.empty() ? nullptr : ex.data();
   if (t.kind == 1) {  // phase-1 estimate of a fused side
-    uint64_t out_bytes = 0;
+    // measure pred / exprs on a sample of the arrived rows: the first
+    // TQ_SAMPLE_FRACTION of the side's (estimated) total rows, taken as a
+    // zero-copy row prefix of the arrived batches
+    uint64_t arrived = 0;
+    for (HP& h : t.inputs) arrived += h->dev.rows;
+    const double total_rows = est_progress > 0 ? (double)arrived / est_progress : (double)arrived;
+    uint64_t want = std::max<uint64_t>(1 << 16, (uint64_t)(total_rows * TQ_SAMPLE_FRACTION));
+    uint64_t sampled = 0, out_bytes = 0;
     for (HP& h : t.inputs) {
+      if (sampled >= want) break;
+      tq_batch v = h->dev;
+      std::vector<tq_column> cols(v.cols, v.cols + v.ncols);
+      uint64_t take = std::min<uint64_t>(v.rows, want - sampled);
+      bool prefix_ok = true;
+      for (auto& c : cols) prefix_ok &= c.kind != TQ_UTF8;
+      if (prefix_ok && take < v.rows) {
+        take = take / 512 * 512 ? take / 512 * 512 : take;  // tile-aligned prefix view
+        for (auto& c : cols) c.values_bytes = take * width_of(c.kind);
+        v.rows = take;
+        v.cols = cols.data();
+      }
       uint64_t rows = 0, rb = 0;
-      check(tq_pipeline_estimate(rt->ctx, &h->dev, pp, ep, (uint32_t)ex.size(), &rows, &rb, st));
+      check(tq_pipeline_estimate(rt->ctx, &v, pp, ep, (uint32_t)ex.size(), &rows, &rb, st));
       out_bytes += rows * rb;
+      sampled += v.rows;
     }
+    // bytes of the arrived input, extrapolated from the sample, then phase 1
+    const uint64_t arrived_bytes = sampled ? (uint64_t)((double)out_bytes * (double)arrived / (double)sampled) : 0;
     uint64_t e = 0;
-    tq_exchange_phase1(out_bytes, est_progress, TQ_SAMPLE_FRACTION, &e);
+    tq_exchange_phase1(arrived_bytes, est_progress, TQ_SAMPLE_FRACTION, &e);
     std::lock_guard<std::mutex> g(rt->mu);
     x->est[side] = e;
     x->est_ready[side] = true;
@@ -1650,6 +1728,7 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
       for (auto& op : rt.ops) {
         if (!op->stat.tasks) continue;
         js << (first ? "" : ", ") << "\"" << op->name << "\": {\"tasks\": " << op->stat.tasks << ", \"ms\": " << op->stat.ms
+           << ", \"gpu_ms\": " << op->stat.gpu_ms << ", \"call_ms\": " << op->stat.first_call_ms
            << ", \"rows_out\": " << op->stat.rows_out.load() << "}";
         first = false;
       }

@@ -302,6 +302,7 @@ __device__ __forceinline__ u32 partition_of(const PipeParams& p, const u64* kw) 
 // stays in registers (the generic form loops over runtime key widths).
 template <class P>
 __device__ __forceinline__ u32 partition_of_p(const PipeParams& p, const u64* kw) {
+  if (p.key_prehashed) return (u32)(kw[0] % p.ndest);
   if constexpr (P::kKey1x8) {
     if ((p.ndest & (p.ndest - 1)) == 0) return fnv32_bytes((u32)kFnvBasis, kw[0], 8) & (p.ndest - 1);
     return (u32)(fnv_bytes(kFnvBasis, kw[0], 8) % p.ndest);

@@ -375,6 +375,7 @@ struct MatArgs {
   uint32_t nparts = 1;
   const tq_join_table* table = nullptr;
   std::vector<uint32_t> build_cols;
+  bool prehashed = false;  // the one key is the row's partition hash (Utf8 keys)
 };
 
 // ---- closing the holes of DEST_PROBE1's chunked output (kernel_common.cuh,
@@ -587,6 +588,7 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     kh.push_back(P.outs[k]);
   }
   set_keys(p, P.pb, kh);
+  p.key_prehashed = A.prehashed ? 1u : 0u;
   p.semi_bloom = A.semi_words;
   p.semi_mask = A.semi_mask;
   p.semi_part_words = A.semi_part_words;
@@ -695,15 +697,14 @@ static void run_materialize(tq_ctx* c, const tq_batch* in, Prog& P, const MatArg
     uint64_t n = 0;
     bool dup_keys = false, need_table = false;
     {
-      std::lock_guard<std::mutex> g(c->mu);
-      TQ_CUDA(cudaMemcpyAsync(c->pinned, plan, 16, cudaMemcpyDeviceToHost, st));
-      TQ_CUDA(cudaMemcpyAsync((uint8_t*)c->pinned + 16, dup, 4, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync(pinned_scratch(c), plan, 16, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync((uint8_t*)pinned_scratch(c) + 16, dup, 4, cudaMemcpyDeviceToHost, st));
       { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
-      n = ((uint64_t*)c->pinned)[0];
-      const uint32_t flag = ((uint32_t*)c->pinned)[4];
+      n = ((uint64_t*)pinned_scratch(c))[0];
+      const uint32_t flag = ((uint32_t*)pinned_scratch(c))[4];
       dup_keys = flag == 1;
       need_table = flag == 2 || (flag == 1 && A.table->jt.entries == nullptr);
-      if (!flag && p.ntiles && ((uint64_t*)c->pinned)[1] == ~0ull)
+      if (!flag && p.ntiles && ((uint64_t*)pinned_scratch(c))[1] == ~0ull)
         fail(TQ_INTERNAL, "probe output chunk plan inconsistent");
     }
     dfree(c, sb, scratch, st);
@@ -757,8 +758,7 @@ two_pass:
     }
     scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
     {
-      std::lock_guard<std::mutex> g(c->mu);
-      u64* pin = (u64*)c->pinned;
+      u64* pin = (u64*)pinned_scratch(c);
       k_dest_starts<<<1, 128, 0, st>>>(offsets, (u32)nslices, p.ndest, offsets + ncnt, pin);
       counted_launch(c);
       TQ_CUDA(cudaGetLastError());
@@ -988,8 +988,7 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     prof_end(c, ph_plan, st);
     u64 n_rows = 0, moves = 0, rmax = 0, sent_rows = 0, vor = 0;
     {
-      std::lock_guard<std::mutex> g(c->mu);
-      u64* pin = (u64*)c->pinned;
+      u64* pin = (u64*)pinned_scratch(c);
       TQ_CUDA(cudaMemcpyAsync(pin, plan, 16, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaMemcpyAsync(pin + 2, scratch, 8 * n, cudaMemcpyDeviceToHost, st));
       TQ_CUDA(cudaMemcpyAsync(pin + 2 + n, sent_dev, 8, cudaMemcpyDeviceToHost, st));
@@ -1586,12 +1585,11 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
       }
       long long mn, mx;
       {
-        std::lock_guard<std::mutex> g(c->mu);
-        TQ_CUDA(cudaMemcpyAsync(c->pinned, kr, 32, cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaMemcpyAsync(pinned_scratch(c), kr, 32, cudaMemcpyDeviceToHost, st));
         { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
-        mn = ((long long*)c->pinned)[0];
-        mx = ((long long*)c->pinned)[1];
-        key_sorted = ((long long*)c->pinned)[3] == 0;
+        mn = ((long long*)pinned_scratch(c))[0];
+        mx = ((long long*)pinned_scratch(c))[1];
+        key_sorted = ((long long*)pinned_scratch(c))[3] == 0;
       }
       dfree(c, kr, 32, st);
       const uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
@@ -1660,10 +1658,9 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     launch(c, SINK_AGG, L, P, st);
     uint32_t ovf = 0;
     {
-      std::lock_guard<std::mutex> g(c->mu);
-      TQ_CUDA(cudaMemcpyAsync(c->pinned, tail, 16, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync(pinned_scratch(c), tail, 16, cudaMemcpyDeviceToHost, st));
       { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
-      ovf = ((uint32_t*)c->pinned)[2];
+      ovf = ((uint32_t*)pinned_scratch(c))[2];
     }
     if (ovf) {  // a run's integer sum beyond int64: re-run exactly on the hash table
       dfree(c, base, tbytes, st);
@@ -1694,11 +1691,10 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     launch(c, SINK_AGG, L, P, st);
     uint32_t ovf = 0;
     {
-      std::lock_guard<std::mutex> g(c->mu);
-      TQ_CUDA(cudaMemcpyAsync(c->pinned, tail, 16, cudaMemcpyDeviceToHost, st));
+      TQ_CUDA(cudaMemcpyAsync(pinned_scratch(c), tail, 16, cudaMemcpyDeviceToHost, st));
       { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
-      ngroups = ((uint64_t*)c->pinned)[0];
-      ovf = ((uint32_t*)c->pinned)[2];
+      ngroups = ((uint64_t*)pinned_scratch(c))[0];
+      ovf = ((uint32_t*)pinned_scratch(c))[2];
     }
     if (!ovf) break;
     dfree(c, base, tbytes, st);
@@ -1795,10 +1791,9 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
     if (direct) {  // the output was sized for every slot: trim to the groups written
       uint64_t n = 0;
       {
-        std::lock_guard<std::mutex> g(c->mu);
-        TQ_CUDA(cudaMemcpyAsync(c->pinned, t.nused, 8, cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaMemcpyAsync(pinned_scratch(c), t.nused, 8, cudaMemcpyDeviceToHost, st));
         { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
-        n = ((uint64_t*)c->pinned)[0];
+        n = ((uint64_t*)pinned_scratch(c))[0];
       }
       out->rows = n;
       for (uint32_t i = 0; i < out->ncols; ++i) {
@@ -2127,6 +2122,185 @@ tq_status tq_rebatch(tq_ctx* c, const tq_batch* ins, uint32_t n, uint64_t target
 
 }  // extern "C"
 
+// ================================================================== Utf8 columns on the pipeline path
+// The pipeline kernels move fixed-width values.  A Utf8 column rides through
+// filter / project / partition as the ROW ID of its row (an appended iota
+// column the program copies instead), and the strings are gathered by those
+// ids afterwards with the reference's take (transform.cpp:90-120: bitmap iff
+// the input had one).  Utf8 partition keys: a pre-pass computes the row's
+// partition hash — fnv1a64 chained over the key columns' bytes, the string's
+// bytes for Utf8 (a null string adds none, a null fixed-width key its width in
+// zero bytes) — and the kernel partitions on it as is (key_prehashed).
+// Utf8 in predicates, arithmetic, join / group keys: InvalidPlan.
+namespace tq {
+
+__global__ void k_iota(u64* v, u64 n) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) v[i] = i;
+}
+
+struct HashKeyCol {
+  const uint8_t* values;
+  const int32_t* offsets;  // Utf8
+  const uint8_t* validity;
+  uint32_t width;          // fixed width (0 = Utf8)
+};
+struct HashKeys {
+  HashKeyCol k[kMaxKeys];
+  u32 n;
+};
+__global__ void k_partition_hash(const __grid_constant__ HashKeys K, u64 rows, u64* out) {
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (u64)gridDim.x * blockDim.x) {
+    u64 h = kFnvBasis;
+    for (u32 k = 0; k < K.n; ++k) {
+      const HashKeyCol& c = K.k[k];
+      const bool valid = !c.validity || bm_get(c.validity, r);
+      if (c.width == 0) {
+        if (!valid) continue;
+        for (int32_t i = c.offsets[r]; i < c.offsets[r + 1]; ++i) h = (h ^ c.values[i]) * kFnvPrime;
+      } else {
+        for (u32 i = 0; i < c.width; ++i) h = (h ^ (valid ? c.values[r * c.width + i] : 0)) * kFnvPrime;
+      }
+    }
+    out[r] = h;
+  }
+}
+
+struct Utf8Lower {
+  bool active = false;
+  tq_batch aug{};                // the input + iota (row id) column [+ partition hash column]
+  std::vector<tq_column> cols;
+  uint32_t rowid = 0, hash = 0;  // column indices in aug
+  void* iota = nullptr;
+  void* hmem = nullptr;
+  uint64_t bytes = 0;
+  tq_ctx* c = nullptr;
+  cudaStream_t st = nullptr;
+  ~Utf8Lower() {
+    if (iota) dfree(c, iota, bytes, st);
+    if (hmem) dfree(c, hmem, bytes, st);
+  }
+};
+
+bool has_utf8(const tq_batch* in) {
+  for (uint32_t i = 0; i < in->ncols; ++i)
+    if (in->cols[i].kind == TQ_UTF8) return true;
+  return false;
+}
+
+// aug = in + an Int64 row-id column (+ the partition hash of `hash_keys`)
+void utf8_lower(tq_ctx* c, const tq_batch* in, Utf8Lower& U, cudaStream_t st, const uint32_t* hash_keys = nullptr,
+                uint32_t nhash = 0) {
+  U.active = true;
+  U.c = c;
+  U.st = st;
+  U.bytes = std::max<uint64_t>(8, in->rows * 8);
+  U.cols.assign(in->cols, in->cols + in->ncols);
+  U.iota = dalloc(c, U.bytes, st);
+  k_iota<<<grid_for(c, in->rows), 256, 0, st>>>((u64*)U.iota, in->rows);
+  counted_launch(c);
+  tq_column id{};
+  id.kind = TQ_INT64;
+  id.values = U.iota;
+  id.values_bytes = in->rows * 8;
+  U.rowid = (uint32_t)U.cols.size();
+  U.cols.push_back(id);
+  if (nhash) {
+    if (nhash > (uint32_t)kMaxKeys) fail(TQ_INVALID_PLAN, "too many keys");
+    HashKeys K{};
+    K.n = nhash;
+    for (uint32_t k = 0; k < nhash; ++k) {
+      if (hash_keys[k] >= in->ncols) fail(TQ_INVALID_PLAN, "key column out of range");
+      const tq_column& col = in->cols[hash_keys[k]];
+      if (col.kind == TQ_FLOAT64) fail(TQ_INVALID_PLAN, "unsupported partition key type");
+      K.k[k] = HashKeyCol{(const uint8_t*)col.values, col.offsets, in->rows ? col.validity : nullptr,
+                          col.kind == TQ_UTF8 ? 0u : (uint32_t)width_of(col.kind)};
+    }
+    U.hmem = dalloc(c, U.bytes, st);
+    k_partition_hash<<<grid_for(c, in->rows), 256, 0, st>>>(K, in->rows, (u64*)U.hmem);
+    counted_launch(c);
+    tq_column hc{};
+    hc.kind = TQ_INT64;
+    hc.values = U.hmem;
+    hc.values_bytes = in->rows * 8;
+    U.hash = (uint32_t)U.cols.size();
+    U.cols.push_back(hc);
+  }
+  TQ_CUDA(cudaGetLastError());
+  U.aug = *in;
+  U.aug.ncols = (uint32_t)U.cols.size();
+  U.aug.cols = U.cols.data();
+  U.aug.owner = nullptr;
+}
+
+// The expressions the kernel evaluates: a pure Utf8 column reference becomes
+// the row-id column (src[j] = that Utf8 input column), anything else is kept.
+struct LoweredExprs {
+  std::vector<std::vector<tq_expr_node>> nodes;
+  std::vector<tq_expr> ex;
+  std::vector<int> src;  // per output: the Utf8 input column to gather, or -1
+};
+void lower_exprs(const tq_batch* in, const Utf8Lower& U, const tq_expr* exprs, uint32_t n, LoweredExprs& L) {
+  const uint32_t cnt = exprs ? n : in->ncols;
+  L.nodes.resize(cnt);
+  for (uint32_t j = 0; j < cnt; ++j) {
+    tq_expr_node col{};
+    col.tag = TQ_EX_COL;
+    if (!exprs) {
+      col.column = in->cols[j].kind == TQ_UTF8 ? U.rowid : j;
+      L.nodes[j] = {col};
+      L.src.push_back(in->cols[j].kind == TQ_UTF8 ? (int)j : -1);
+    } else {
+      const tq_expr& e = exprs[j];
+      const bool utf8_col = e.len == 1 && e.nodes[0].tag == TQ_EX_COL && e.nodes[0].column < in->ncols &&
+                            in->cols[e.nodes[0].column].kind == TQ_UTF8;
+      if (utf8_col) {
+        col.column = U.rowid;
+        L.nodes[j] = {col};
+        L.src.push_back((int)e.nodes[0].column);
+      } else {
+        L.nodes[j].assign(e.nodes, e.nodes + e.len);
+        L.src.push_back(-1);
+      }
+    }
+  }
+  for (auto& v : L.nodes) L.ex.push_back(tq_expr{v.data(), (uint32_t)v.size(), 0});
+}
+
+// Replace every row-id output column j (src[j] >= 0) by the strings of input
+// column src[j] gathered at those ids; drop the outputs >= keep.
+void utf8_raise(tq_ctx* c, const tq_batch* in, const std::vector<int>& src, uint32_t keep, tq_batch* out,
+                cudaStream_t st) {
+  Owner* own = (Owner*)out->owner;
+  auto release = [&](void* p) {
+    for (size_t b = 0; b < own->bufs.size(); ++b)
+      if (own->bufs[b].first == p) {
+        dfree(c, p, own->bufs[b].second, st);
+        own->bufs.erase(own->bufs.begin() + b);
+        return;
+      }
+  };
+  for (uint32_t j = 0; j < out->ncols && j < src.size(); ++j) {
+    if (src[j] < 0) continue;
+    tq_batch one{in->rows, 1, TQ_MEM_DEVICE, &in->cols[src[j]], nullptr};
+    tq_batch g{};
+    take_impl(c, &one, (const u64*)out->cols[j].values, out->rows, 0, &g, st);
+    release(out->cols[j].values);
+    if (out->cols[j].validity) release(out->cols[j].validity);
+    out->cols[j] = g.cols[0];
+    Owner* go = (Owner*)g.owner;
+    for (auto& b : go->bufs) own->bufs.push_back(b);
+    delete go;
+    std::free(g.cols);
+  }
+  for (uint32_t j = keep; j < out->ncols; ++j) {
+    release(out->cols[j].values);
+    if (out->cols[j].validity) release(out->cols[j].validity);
+  }
+  out->ncols = std::min(out->ncols, keep);
+}
+
+}  // namespace tq
+
 // ================================================================== operator entry points
 namespace {
 using namespace tq;
@@ -2144,9 +2318,74 @@ void compile_all(Prog& P, const tq_batch* in, const tq_expr* pred) { compile_pro
 
 extern "C" {
 
+// Filter / project / partition over a batch that holds Utf8 columns (see
+// "Utf8 columns on the pipeline path").  part_keys: hash-partition keys given
+// as INPUT column indices (hash_partition) or output indices (nullptr: none).
+void materialize_utf8(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs, uint32_t nexprs,
+                      const uint32_t* keys, uint32_t nkeys, bool keys_are_inputs, uint32_t nparts, tq_batch* out,
+                      uint64_t* part_offsets, cudaStream_t st) {
+  // partition keys that are (or project) a Utf8 column are hashed by the pre-pass
+  bool utf8_key = false;
+  std::vector<uint32_t> in_keys;
+  for (uint32_t k = 0; k < nkeys; ++k) {
+    uint32_t col = keys[k];
+    if (!keys_are_inputs) {
+      if (!exprs) {
+        col = keys[k];
+      } else {
+        if (keys[k] >= nexprs) fail(TQ_INVALID_PLAN, "key column out of range");
+        const tq_expr& e = exprs[keys[k]];
+        if (!(e.len == 1 && e.nodes[0].tag == TQ_EX_COL)) {
+          // a computed key: fixed width by construction, no pre-pass unless another key needs it
+          in_keys.push_back(~0u);
+          continue;
+        }
+        col = e.nodes[0].column;
+      }
+    }
+    if (col >= in->ncols) fail(TQ_INVALID_PLAN, "key column out of range");
+    utf8_key |= in->cols[col].kind == TQ_UTF8;
+    in_keys.push_back(col);
+  }
+  if (utf8_key)
+    for (uint32_t k : in_keys)
+      if (k == ~0u) fail(TQ_INVALID_PLAN, "a computed key next to a Utf8 key is not supported");
+  Utf8Lower U;
+  utf8_lower(c, in, U, st, utf8_key ? in_keys.data() : nullptr, utf8_key ? (uint32_t)in_keys.size() : 0);
+  LoweredExprs L;
+  lower_exprs(in, U, exprs, nexprs, L);
+  const uint32_t nout = (uint32_t)L.ex.size();
+  std::vector<uint32_t> kr;
+  if (nkeys && utf8_key) {  // partition on the precomputed hash: an extra output, dropped after
+    tq_expr_node h{};
+    h.tag = TQ_EX_COL;
+    h.column = U.hash;
+    L.nodes.push_back({h});
+    L.ex.push_back(tq_expr{L.nodes.back().data(), 1, 0});
+    kr.push_back(nout);
+  } else {
+    for (uint32_t k = 0; k < nkeys; ++k) kr.push_back(keys[k]);
+  }
+  // (the kernel sees the batch with the row-id / hash columns; its program
+  // never references a Utf8 column — a predicate or expression that does fails)
+  for (size_t j = 0; j < L.nodes.size(); ++j) L.ex[j].nodes = L.nodes[j].data();
+  Prog P(schema_of(&U.aug));
+  compile_prog(P, &U.aug, pred, L.ex.data(), (uint32_t)L.ex.size(), false);
+  MatArgs A;
+  if (nkeys) {
+    A.mode = MAT_PARTITION;
+    A.key_roots = kr;
+    A.nparts = nparts;
+  }
+  A.prehashed = nkeys && utf8_key;
+  run_materialize(c, &U.aug, P, A, out, part_offsets, st);
+  utf8_raise(c, in, L.src, nout, out, st);
+}
+
 tq_status tq_filter(tq_ctx* c, const tq_batch* in, tq_expr pred, tq_batch* out, void* stream) {
   return guard([&] {
     check_device_batch(in);
+    if (has_utf8(in)) return materialize_utf8(c, in, &pred, nullptr, 0, nullptr, 0, false, 1, out, nullptr, pick(c, stream));
     Prog P(schema_of(in));
     compile_all(P, in, &pred);
     MatArgs A;
@@ -2157,6 +2396,7 @@ tq_status tq_filter(tq_ctx* c, const tq_batch* in, tq_expr pred, tq_batch* out, 
 tq_status tq_project(tq_ctx* c, const tq_batch* in, const tq_expr* exprs, uint32_t n, tq_batch* out, void* stream) {
   return guard([&] {
     check_device_batch(in);
+    if (has_utf8(in)) return materialize_utf8(c, in, nullptr, exprs, n, nullptr, 0, false, 1, out, nullptr, pick(c, stream));
     Prog P(schema_of(in));
     compile_prog(P, in, nullptr, exprs, n, false);
     MatArgs A;
@@ -2168,6 +2408,8 @@ tq_status tq_pipeline_materialize(tq_ctx* c, const tq_batch* in, const tq_expr* 
                                   uint32_t nexprs, tq_batch* out, void* stream) {
   return guard([&] {
     check_device_batch(in);
+    if (has_utf8(in))
+      return materialize_utf8(c, in, pred, exprs, nexprs, nullptr, 0, false, 1, out, nullptr, pick(c, stream));
     Prog P(schema_of(in));
     compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
     MatArgs A;
@@ -2179,6 +2421,9 @@ tq_status tq_hash_partition(tq_ctx* c, const tq_batch* in, const uint32_t* keys,
                             tq_batch* out, uint64_t* part_offsets, void* stream) {
   return guard([&] {
     check_device_batch(in);
+    if (has_utf8(in))
+      return materialize_utf8(c, in, nullptr, nullptr, 0, keys, nkeys, true, nparts, out, part_offsets,
+                              pick(c, stream));
     Prog P(schema_of(in));
     compile_all(P, in, nullptr);
     MatArgs A;
@@ -2194,6 +2439,9 @@ tq_status tq_pipeline_partition(tq_ctx* c, const tq_batch* in, const tq_expr* pr
                                 tq_batch* out, uint64_t* part_offsets, void* stream) {
   return guard([&] {
     check_device_batch(in);
+    if (has_utf8(in))
+      return materialize_utf8(c, in, pred, exprs, nexprs, keys, nkeys, false, nparts, out, part_offsets,
+                              pick(c, stream));
     Prog P(schema_of(in));
     compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
     MatArgs A;
@@ -2285,10 +2533,9 @@ tq_status tq_pipeline_estimate(tq_ctx* c, const tq_batch* in, const tq_expr* pre
       launch(c, SINK_COUNT, L, P, st);
       scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
       {
-        std::lock_guard<std::mutex> g(c->mu);
-        TQ_CUDA(cudaMemcpyAsync(c->pinned, offsets + ncnt, 8, cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaMemcpyAsync(pinned_scratch(c), offsets + ncnt, 8, cudaMemcpyDeviceToHost, st));
         { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
-        rows = ((uint64_t*)c->pinned)[0];
+        rows = ((uint64_t*)pinned_scratch(c))[0];
       }
       dfree(c, counts, ncnt * 4, st);
       dfree(c, offsets, (ncnt + 1) * 8, st);

@@ -241,6 +241,9 @@ struct PipeParams {
   uint32_t build_skip_aux;
   // DEST_RANGE output: {min, max, any null} of the first key word
   long long* key_range;
+  // the one key is the row's partition hash already (fnv1a64 chained over
+  // key columns that include Utf8, computed by a pre-pass): part = key mod n
+  uint32_t key_prehashed;
 };
 
 }  // namespace tq

@@ -408,3 +408,27 @@ def test_rebatch_matches_reference(ctx, case):
     if len(want_rows) > 1:  # every output but the last in [target / 2, 2 * target] bytes
         sizes = [O.ref_batch_size_bytes(O.slice_(b, int(s), n)) for s, n in zip(np.cumsum([0] + want_rows[:-1]), want_rows)]
         assert all(target // 2 <= x <= 2 * target for x in sizes[:-1])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_utf8_payload_and_partition_keys(ctx, seed):
+    """Utf8 columns through filter / project / partition (carried as row ids
+    through the kernel, gathered after with the reference take semantics) and
+    Utf8 partition keys (fnv1a64 over the string bytes, chained with the other
+    keys; a null string adds no bytes) — equal to the oracle."""
+    kinds = (INT64, DECIMAL, BOOL)
+    rows = [0, 1, 700, 5000, 40000, 3][seed]
+    b = rand_batch(seed, rows, kinds, null_frac=0.1 if seed % 2 else 0.0, utf8=True)
+    u = len(kinds)  # the Utf8 column
+    d = ctx.upload(b)
+    pred = rand_pred(random.Random(seed), kinds, 2)
+    assert_batches_equal(ctx.filter_execute(d, pred).to_host(), O.filter_execute(b, pred), ordered=True)
+    exprs = [Col(u), Col(0) + 1, Col(u), Col(1)]
+    assert_batches_equal(ctx.project_execute(d, exprs).to_host(), O.project_execute(b, exprs), ordered=True)
+    for keys, n in (([u], 4), ([0, u], 3), ([1], 8)):
+        part, offs = ctx.hash_partition(d, keys, n)
+        got = part.to_host()
+        want = O.hash_partition(b, keys, n)
+        assert offs[-1] == b.rows
+        for p in range(n):
+            assert_batches_equal(O.slice_(got, offs[p], offs[p + 1] - offs[p]), want[p], ordered=True)
