@@ -511,7 +511,10 @@ def run_tq(args, world, rank, local):
     from paper_2508_05029_b200.ops import Context, DeviceBatch, lib
 
     torch.cuda.set_device(local)
-    ctx = Context(local)
+    # map most of the GPU's memory into the context's pool once: the suite's
+    # SF100 tables and the queries' temporaries then never map memory mid-query
+    free, _ = torch.cuda.mem_get_info(local)
+    ctx = Context(local, pool_reserve_bytes=int(free * 0.7))
     sf_total = SF_PER_GPU * world
     li = ctx.datagen(1, sf_total, shard=rank, nshards=world)
     scan = li.select(queries.Q1_SCAN)

@@ -27,6 +27,9 @@ typedef struct tq_opts {
   uint32_t ctas_per_sm;          /* persistent grid = ctas_per_sm x SMs (0 = auto) */
   uint64_t device_budget_bytes;  /* Device-tier capacity for the ledger (0 = unlimited);
                                     SPEC.md:259-276 reserve/alloc_within */
+  uint64_t pool_reserve_bytes;   /* map this much device memory into the context's pool up front
+                                    (kept mapped: later allocations reuse it instead of mapping new
+                                    physical memory, ~25 ms per GB, mid-query); 0 = grow on demand */
 } tq_opts;
 
 /* ---- context / errors (reference common.hpp:57-74 Error, Errc) --------- */

@@ -157,7 +157,15 @@ void* dalloc(tq_ctx* c, uint64_t bytes, cudaStream_t st) {
                                       std::to_string(c->budget) + " bytes");
   }
   void* p = nullptr;
+  const long long t0 = host_timing_on() ? now_ns() : 0;
   cudaError_t e = cudaMallocFromPoolAsync(&p, b, c->pool, st);
+  if (t0 && now_ns() - t0 > 1000000) {
+    unsigned long long res = 0, used = 0;
+    cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrReservedMemCurrent, &res);
+    cudaMemPoolGetAttribute(c->pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    fprintf(stderr, "[tq] slow dalloc %.3f ms: %llu bytes on stream %p (pool reserved %.2f GB, used %.2f GB)\n",
+            (now_ns() - t0) / 1e6, (unsigned long long)b, (void*)st, res / 1e9, used / 1e9);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     c->in_use.fetch_sub(b);
@@ -244,10 +252,32 @@ tq_status tq_ctx_create(const tq_opts* opts, tq_ctx** out) {
     c->ctas_per_sm = opts ? opts->ctas_per_sm : 0;
     c->budget = opts ? opts->device_budget_bytes : 0;
     TQ_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    TQ_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, dev));
+    // a pool of our own (not the device's default pool, which other libraries
+    // in the process — NCCL, PyTorch — may trim or reconfigure): memory it has
+    // mapped stays mapped (release threshold = never), so steady-state
+    // allocations are reuse, never a new physical mapping (~25 ms per GB)
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    TQ_CUDA(cudaMemPoolCreate(&c->pool, &props));
     uint64_t thresh = ~0ull;
     TQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    int on = 1;
+    TQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowOpportunistic, &on));
+    TQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &on));
+    TQ_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseFollowEventDependencies, &on));
     TQ_CUDA(cudaHostAlloc(&c->pinned, 4096, cudaHostAllocPortable));
+    if (opts && opts->pool_reserve_bytes) {
+      void* p = nullptr;
+      if (cudaMallocFromPoolAsync(&p, opts->pool_reserve_bytes, c->pool, c->stream) == cudaSuccess) {
+        cudaFreeAsync(p, c->stream);
+        TQ_CUDA(cudaStreamSynchronize(c->stream));
+      } else {
+        cudaGetLastError();
+      }
+    }
     *out = c;
   });
 }
@@ -264,6 +294,7 @@ void tq_ctx_destroy(tq_ctx* c) {
     cudaStreamDestroy(s);
   }
   cudaStreamDestroy(c->stream);
+  cudaMemPoolDestroy(c->pool);  // (outstanding allocations keep it alive until freed)
   delete c;
 }
 

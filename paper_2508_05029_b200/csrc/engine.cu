@@ -248,6 +248,7 @@ class Runtime {
   bool stop = false;
   std::exception_ptr error;
   int exchange_turn = 0;  // collectives run in DAG order on every worker
+  bool poll_changed = false;  // the coordinator's current pass changed some operator's state
   // metrics
   std::atomic<uint64_t> m_tasks{0}, m_retries{0}, m_splits{0}, m_spills{0}, m_spill_bytes{0}, m_loads{0},
       m_preloads{0}, m_load_bytes{0}, m_peak{0}, m_injected{0};
@@ -259,6 +260,13 @@ class Runtime {
     uint64_t total0, total1;
   };
   std::vector<Decision> decisions;  // exchange_decide outcomes (metrics)
+  struct Span {
+    std::string op;
+    int kind;
+    double t0, t1;  // ms since the run phase started
+  };
+  std::vector<Span> timeline;  // every task's [start, end) (metrics)
+  Clock::time_point run_start = Clock::now();
   std::vector<std::unique_ptr<XPair>> pairs;
   std::vector<HP> keep;  // handles alive until the query ends (build sides)
   std::vector<tq_batch> results;
@@ -468,6 +476,8 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
   const uint64_t peak = std::max<uint64_t>(device_in_use(), before) - std::min<uint64_t>(device_in_use(), before);
   {
     std::lock_guard<std::mutex> g(mu);
+    const double s0 = std::chrono::duration<double, std::milli>(t0 - run_start).count();
+    timeline.push_back({op->name, t.kind, s0, s0 + ms});
     // stats from successful tasks only (EMA alpha 0.3)
     const double a = 0.3;
     double ratio = in_bytes ? (double)peak / (double)in_bytes : 0;
@@ -490,6 +500,10 @@ void Runtime::worker(int idx) {
   cudaSetDevice(ctx->device);
   // one stream per Compute thread, kept by the context across queries
   cudaStream_t st = exec_stream(ctx, 2 + idx);
+  {  // TQ_ENGINE_ONE_STREAM=1 (experiments): every task on the context stream
+    static const bool one = [] { const char* e = getenv("TQ_ENGINE_ONE_STREAM"); return e && e[0] == '1'; }();
+    if (one) st = ctx->stream;
+  }
   for (;;) {
     Task t;
     {
@@ -548,6 +562,7 @@ void Runtime::preloader() {
 }
 
 void Runtime::run() {
+  run_start = Clock::now();
   std::vector<std::thread> threads;
   for (uint32_t i = 0; i < std::max<uint32_t>(1, opts.compute_threads); ++i) threads.emplace_back(&Runtime::worker, this, i);
   if (opts.preload) threads.emplace_back(&Runtime::preloader, this);
@@ -558,10 +573,12 @@ void Runtime::run() {
     for (;;) {
       if (error) break;
       bool all = true;
+      poll_changed = false;
       for (auto& o : ops) {
         if (o->finished) continue;
         std::vector<Task> ts;
         o->poll(ts);
+        poll_changed |= !ts.empty();
         for (Task& t : ts) {
           o->running++;
           submit(std::move(t));
@@ -570,9 +587,14 @@ void Runtime::run() {
           o->out->close_locked();  // EndOfStream after the last output
           cv.notify_all();
         }
+        poll_changed |= o->finished;
         all = all && o->finished;
       }
       if (all) break;
+      // a poll can make an op polled earlier in this pass runnable (an exchange
+      // side's estimate readies its decide, an EndOfStream its consumer): go
+      // again at once instead of waiting for the next wake-up
+      if (poll_changed) continue;
       cv.wait_for(g, std::chrono::milliseconds(1));
     }
     stop = true;
@@ -1138,6 +1160,7 @@ void XSideOp::poll(std::vector<Task>& ts) {
         tq_exchange_phase1(bytes, progress, TQ_SAMPLE_FRACTION, &e);
         x->est[side] = e;
         x->est_ready[side] = true;
+        rt->poll_changed = true;
       }
     }
   }
@@ -1722,6 +1745,11 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
         js << (i ? ", " : "") << "{\"pair\": \"" << d.name << "\", \"strategy\": \""
            << (d.strategy == TQ_XCHG_BROADCAST ? "Broadcast" : "HashPartition") << "\", \"broadcast_side\": " << d.side
            << ", \"total0\": " << d.total0 << ", \"total1\": " << d.total1 << "}";
+      }
+      js << "], \"timeline\": [";
+      for (size_t i = 0; i < rt.timeline.size(); ++i) {
+        const auto& sp = rt.timeline[i];
+        js << (i ? ", " : "") << "[\"" << sp.op << "\", " << sp.kind << ", " << sp.t0 << ", " << sp.t1 << "]";
       }
       js << "], \"ops\": {";
       bool first = true;

@@ -50,7 +50,8 @@ class TqEngineOptsC(C.Structure):
 
 
 class TqOptsC(C.Structure):
-    _fields_ = [("device", C.c_int), ("ctas_per_sm", C.c_uint32), ("device_budget_bytes", C.c_uint64)]
+    _fields_ = [("device", C.c_int), ("ctas_per_sm", C.c_uint32), ("device_budget_bytes", C.c_uint64),
+                ("pool_reserve_bytes", C.c_uint64)]
 
 
 def lib():
@@ -261,10 +262,10 @@ class JoinTable:
 class Context:
     """One tq context per GPU (tq_ctx_create)."""
 
-    def __init__(self, device: int = 0, device_budget_bytes: int = 0, ctas_per_sm: int = 0):
+    def __init__(self, device: int = 0, device_budget_bytes: int = 0, ctas_per_sm: int = 0, pool_reserve_bytes: int = 0):
         L = lib()
         h = C.c_void_p()
-        opts = TqOptsC(device, ctas_per_sm, device_budget_bytes)
+        opts = TqOptsC(device, ctas_per_sm, device_budget_bytes, pool_reserve_bytes)
         self._check(L.tq_ctx_create(C.byref(opts), C.byref(h)))
         self.handle = h
         _LIVE.add(self)

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--sf", type=float, default=100)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--threads", type=int, default=4)
+    ap.add_argument("--kprof", type=int, default=0, help="per-kernel CUDA-event profile of the last rep")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -31,7 +32,7 @@ def main():
     torch.cuda.set_device(local)
     from paper_2508_05029_b200 import queries
     from paper_2508_05029_b200.ops import Comm, Context, engine_run_query
-    ctx = Context(local)
+    ctx = Context(local, pool_reserve_bytes=int(float(os.environ.get("TQ_POOL_RESERVE_GB", "0")) * 1e9))
     uid = [Comm.unique_id() if rank == 0 else None]
     if world > 1:
         dist.broadcast_object_list(uid, src=0)
@@ -41,6 +42,17 @@ def main():
     for i in range(a.reps + 1):
         if world > 1:
             dist.barrier()
+        if a.kprof and i == a.reps:
+            ctx.profile(True)
+        if i == a.reps and os.environ.get("TQ_HOST_TIMING") == "1":  # host phases of the last rep only
+            import ctypes as C
+            from paper_2508_05029_b200.ops import lib
+            lib().tq_host_timing_report(C.create_string_buffer(1 << 16), 1 << 16)
+        import ctypes as _C
+        from paper_2508_05029_b200.ops import lib as _lib
+        _lib().tq_device_bytes_reserved.restype = _C.c_uint64
+        _lib().tq_device_bytes_reserved.argtypes = [_C.c_void_p]
+        res0 = _lib().tq_device_bytes_reserved(ctx.handle)
         t0 = time.perf_counter()
         _, m = engine_run_query(ctx, a.q, t, comm=comm if world > 1 else None, compute_threads=a.threads,
                                 batch_rows=1 << 40)
@@ -49,14 +61,19 @@ def main():
             from paper_2508_05029_b200.ops import lib
             lib().tq_device_bytes_reserved.restype = __import__("ctypes").c_uint64
             lib().tq_device_bytes_reserved.argtypes = [__import__("ctypes").c_void_p]
-            print("pool reserved GB", lib().tq_device_bytes_reserved(ctx.handle) / 1e9, flush=True)
+            print("pool reserved GB before / after", res0 / 1e9, lib().tq_device_bytes_reserved(ctx.handle) / 1e9,
+                  "in use GB", ctx.bytes_in_use() / 1e9, flush=True)
             ops = sorted(m["ops"].items(), key=lambda kv: -kv[1]["ms"])
             print(json.dumps({"rep": i, "wall_ms": round(wall, 3), "run_ms": round(m["run_ms"], 3),
                               "setup_ms": round(m["setup_ms"], 3), "tasks": m["tasks"],
                               "ops": {k: (v["tasks"], round(v["ms"], 3), round(v["gpu_ms"], 3), round(v["call_ms"], 3))
                                       for k, v in ops}}), flush=True)
+            print("timeline", json.dumps([(n, k, round(a, 3), round(b, 3)) for n, k, a, b in m["timeline"]]),
+                  flush=True)
     if rank == 0:
         print("jit", ctx.jit_report(), flush=True)
+        if a.kprof:
+            print("kernels", json.dumps({k: (v[0], round(v[1], 3)) for k, v in ctx.profile_report().items()}), flush=True)
     if rank == 0 and os.environ.get("TQ_HOST_TIMING") == "1":
         import ctypes as C
         from paper_2508_05029_b200.ops import lib
