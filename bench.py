@@ -451,6 +451,29 @@ def run_suite(args, ctx, world, rank, stream, oracle, parity):
                          "then NCCL grouped send/recv"),
             "recv_rows_rank0": {k: v for k, v in stats.items()},
         }
+    if world > 1:
+        # LIP off: the lineitem shuffle ships every filtered row; the scatter
+        # kernels' NVLink throughput = bytes stored into other ranks' windows /
+        # the scatter kernels' time (CUDA events around each launch)
+        queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], fused=True, lip=False).free()
+        ctx.sync()
+        barrier(world)
+        b0 = comm.bytes_sent()
+        ctx.profile(True)
+        queries.q3_distributed(ctx, comm, t["customer"], t["orders"], t["lineitem"], fused=True, lip=False).free()
+        ctx.sync()
+        prof = ctx.profile_report()
+        ctx.profile(False)
+        sent = comm.bytes_sent() - b0
+        n_sc, sc_ms = prof.get("pipe_scatter", (0, 0.0))
+        n_bc, bc_ms = prof.get("pipe_broadcast", (0, 0.0))
+        gbs = sent / ((sc_ms + bc_ms) * 1e-3) / 1e9 if sc_ms else None
+        gbs = max_over_ranks(world, gbs or 0.0)
+        suite[f"q3_shuffle_nolip_sf{sf:g}_scatter"] = {
+            "nvlink_bytes_sent_per_gpu": sent, "scatter_kernels_ms": sc_ms + bc_ms, "launches": n_sc + n_bc,
+            "nvlink_gbs_per_gpu": gbs, "nvlink_frac_of_770": gbs / 770.0 if gbs else None,
+            "what": "fused partition + scatter / broadcast kernels of config 4 without LIP: remote bytes stored "
+                    "over NVLink per GPU / those kernels' CUDA-event time (max over ranks)"}
     # the same query through the C++ worker runtime (tq_engine_run_query): its
     # distributed Q3 plan decides the exchanges itself (exchange_decide) and
     # runs them over the same fused NVLink kernels; one batch per table shard

@@ -61,7 +61,7 @@ def test_engine_host_tables_under_budget(ctx, q):
 @pytest.mark.parametrize("case", ["retry", "split", "unsplittable"])
 def test_engine_on_oom_paths(ctx, case):
     """run_task's on_oom forced in a real query by injecting
-    ReservationExceeded into the lineitem filter/project tasks: the doubled
+    ReservationExceeded into the lineitem probe tasks (filter + project + probe): the doubled
     estimate is retried; a multi-batch task whose doubled estimate exceeds
     the Device capacity is split in two; a single-batch one aborts the query
     with OutOfMemoryUnsplittable.  Results stay identical to the oracle."""
@@ -69,7 +69,7 @@ def test_engine_on_oom_paths(ctx, case):
     sf = 0.05
     tabs = {t: ctx.datagen(t, sf) for t in O.QUERY_TABLES[3]}
     want = O.query(3, {t: O.datagen(t, sf) for t in O.QUERY_TABLES[3]}, 8)
-    opts = dict(compute_threads=2, batch_rows=32 * 1024, device_budget=4 << 30, inject_oom_op="lineitem_f")
+    opts = dict(compute_threads=2, batch_rows=32 * 1024, device_budget=4 << 30, inject_oom_op="lineitem_probe")
     if case == "retry":
         got, m = engine_run_query(ctx, 3, tabs, inject_oom_mode=1, inject_oom_count=2, **opts)
         assert (m["oom_retries"], m["splits"]) == (2, 0), m
