@@ -148,6 +148,8 @@ class Runtime {
   Runtime(tq_ctx* c, tq_comm* comm, const tq_engine_opts& o) : ctx(c), comm(comm), opts(o) {}
   ~Runtime();
   void setup();
+  void start_threads();
+  void stop_threads();
   void run();
 
   HP adopt(const tq_batch& b, bool view) {
@@ -242,13 +244,16 @@ class Runtime {
   std::vector<std::unique_ptr<Holder>> holders;
   std::vector<Task> queue;
   std::vector<std::weak_ptr<Handle>> registry;
+  std::vector<std::thread> threads;  // executor threads (start_threads .. stop_threads)
   uint64_t next_id = 0, next_seq = 0, reserved = 0;
   int running_tasks = 0;
   int executing = 0;  // tasks past their reservation (the ones that can free memory)
   bool stop = false;
   std::exception_ptr error;
   int exchange_turn = 0;  // collectives run in DAG order on every worker
-  bool poll_changed = false;  // the coordinator's current pass changed some operator's state
+  bool poll_changed = false;  // the current coordination pass changed some operator's state
+  bool all_done = false;      // every operator finished (a pass saw it)
+  bool poll_all();            // one coordination pass; caller holds mu
   // metrics
   std::atomic<uint64_t> m_tasks{0}, m_retries{0}, m_splits{0}, m_spills{0}, m_spill_bytes{0}, m_loads{0},
       m_preloads{0}, m_load_bytes{0}, m_peak{0}, m_injected{0};
@@ -523,6 +528,10 @@ void Runtime::worker(int idx) {
       std::lock_guard<std::mutex> g(mu);
       running_tasks--;
       t.op->running--;
+      // the finishing worker polls the DAG itself: the follow-up task is
+      // queued (and often picked by this same thread) without a wake-up of
+      // the coordinator in between
+      if (!error && !all_done) poll_all();
       cv.notify_all();
     }
   }
@@ -561,50 +570,79 @@ void Runtime::preloader() {
   }
 }
 
-void Runtime::run() {
-  run_start = Clock::now();
-  std::vector<std::thread> threads;
+// One coordination pass (caller holds mu): poll every unfinished operator for
+// runnable tasks, close the outputs of finished ones (EndOfStream), and go
+// again while a pass changed something — a poll can make an op polled earlier
+// in the pass runnable (an exchange side's estimate readies its decide, an
+// EndOfStream its consumer).  Returns true when every operator finished.
+bool Runtime::poll_all() {
+  for (;;) {
+    bool all = true;
+    poll_changed = false;
+    for (auto& o : ops) {
+      if (o->finished) continue;
+      std::vector<Task> ts;
+      o->poll(ts);
+      poll_changed |= !ts.empty();
+      for (Task& t : ts) {
+        o->running++;
+        submit(std::move(t));
+      }
+      if (o->finished && o->out && !o->out->closed()) {
+        o->out->close_locked();  // EndOfStream after the last output
+        cv.notify_all();
+      }
+      poll_changed |= o->finished;
+      all = all && o->finished;
+    }
+    if (all) {
+      all_done = true;
+      cv.notify_all();
+      return true;
+    }
+    if (!poll_changed) return false;
+  }
+}
+
+// Executor threads are started before the run phase (they wait for tasks):
+// starting them is setup, not query work.
+void Runtime::start_threads() {
   for (uint32_t i = 0; i < std::max<uint32_t>(1, opts.compute_threads); ++i) threads.emplace_back(&Runtime::worker, this, i);
   if (opts.preload) threads.emplace_back(&Runtime::preloader, this);
   threads.emplace_back(&Runtime::memory_executor, this);
+}
+
+void Runtime::stop_threads() {
+  {
+    std::lock_guard<std::mutex> g(mu);
+    stop = true;
+    cv.notify_all();
+  }
+  for (auto& t : threads)
+    if (t.joinable()) t.join();
+  threads.clear();
+}
+
+void Runtime::run() {
+  run_start = Clock::now();
+  if (threads.empty()) start_threads();
   // coordinator: poll operators for runnable tasks until every operator finished
   {
     std::unique_lock<std::mutex> g(mu);
     for (;;) {
       if (error) break;
-      bool all = true;
-      poll_changed = false;
-      for (auto& o : ops) {
-        if (o->finished) continue;
-        std::vector<Task> ts;
-        o->poll(ts);
-        poll_changed |= !ts.empty();
-        for (Task& t : ts) {
-          o->running++;
-          submit(std::move(t));
-        }
-        if (o->finished && o->out && !o->out->closed()) {
-          o->out->close_locked();  // EndOfStream after the last output
-          cv.notify_all();
-        }
-        poll_changed |= o->finished;
-        all = all && o->finished;
-      }
-      if (all) break;
-      // a poll can make an op polled earlier in this pass runnable (an exchange
-      // side's estimate readies its decide, an EndOfStream its consumer): go
-      // again at once instead of waiting for the next wake-up
-      if (poll_changed) continue;
+      if (poll_all()) break;
       cv.wait_for(g, std::chrono::milliseconds(1));
     }
     stop = true;
     cv.notify_all();
   }
-  for (auto& t : threads) t.join();
+  stop_threads();
   if (error) std::rethrow_exception(error);
 }
 
 Runtime::~Runtime() {
+  stop_threads();
   for (auto& w : registry)
     if (HP h = w.lock()) {
       if (h->tier == DEVICE && !h->view && h->dev.cols) tq_batch_free(ctx, &h->dev);
@@ -1712,6 +1750,7 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
       s->out->close();
     }
     if (rt.capacity) c->budget = rt.capacity;
+    rt.start_threads();
     const auto t_run = Clock::now();
     const double setup_ms = std::chrono::duration<double, std::milli>(t_run - t0).count();
     try {

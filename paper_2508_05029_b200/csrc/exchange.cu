@@ -378,10 +378,16 @@ tq_status tq_comm_allgather_host_u64(tq_comm* cm, const uint64_t* in, uint64_t* 
     cudaStream_t st = pick(c, stream);
     const uint64_t n = (uint64_t)cm->n;
     u64* g = (u64*)dalloc(c, 8 * count * (n + 1), st);
-    TQ_CUDA(cudaMemcpyAsync(g, in, 8 * count, cudaMemcpyHostToDevice, st));
+    // staged through this thread's pinned slot: asynchronous copies, one sync
+    u64* pin = (u64*)pinned_scratch(c);
+    const bool fits = 8 * count * (n + 1) <= 4096;
+    if (fits) std::memcpy(pin, in, 8 * count);
+    TQ_CUDA(cudaMemcpyAsync(g, fits ? (const void*)pin : (const void*)in, 8 * count, cudaMemcpyHostToDevice, st));
     comm_allgather_u64(cm, g, g + count, count, st);
-    TQ_CUDA(cudaMemcpyAsync(out, g + count, 8 * count * n, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaMemcpyAsync(fits ? (void*)(pin + count) : (void*)out, g + count, 8 * count * n, cudaMemcpyDeviceToHost,
+                            st));
     TQ_CUDA(cudaStreamSynchronize(st));
+    if (fits) std::memcpy(out, pin + count, 8 * count * n);
     dfree(c, g, 8 * count * (n + 1), st);
   });
 }
