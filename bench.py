@@ -318,6 +318,30 @@ class OracleTables:
         self.cache.clear()
 
 
+def local_device() -> int:
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def pinned_h2d_gbs(device: int, stream, nbytes: int = 1 << 30, reps: int = 5) -> float:
+    """Pinned host -> device copy bandwidth on this box, measured in the same run
+    (the denominator of the config-5 Host-tier runs' H2D GB/s): best of `reps`
+    1-GiB cudaMemcpyAsync copies, CUDA events on the bench stream."""
+    import torch
+    src = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
+    best = 0.0
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dst.copy_(src, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del src, dst
+    return best
+
+
 def check(got, want) -> str:
     """'exact' (integers / decimals / keys bit-exact after canonical sort,
     Float64 within 1e-9 relative) or the mismatch."""
@@ -399,6 +423,7 @@ def run_suite(args, ctx, world, rank, stream, oracle, parity):
         # holders spill (PCIe-bound by design)
         from paper_2508_05029_b200.ops import engine_run_query
         sf5 = args.spill_sf
+        h2d_peak = pinned_h2d_gbs(local_device(), stream)
         for q in (5, 9):
             names = queries.QUERY_TABLES[q]
             host = {}
@@ -419,7 +444,9 @@ def run_suite(args, ctx, world, rank, stream, oracle, parity):
                 "ms": m["run_ms"], "rows_per_s": rows / (m["run_ms"] * 1e-3), "host_tier_bytes": data_bytes,
                 "device_budget": m["device_capacity"], "loads": m["loads"], "preloads": m["preloads"],
                 "spills": m["spills"], "spill_bytes": m["spill_bytes"], "h2d_bytes": m["load_bytes"],
-                "h2d_gbs": m["load_bytes"] / (m["run_ms"] * 1e-3) / 1e9, "oom_retries": m["oom_retries"],
+                "h2d_gbs": m["load_bytes"] / (m["run_ms"] * 1e-3) / 1e9, "pinned_h2d_probe_gbs": h2d_peak,
+                "h2d_frac_of_probe": m["load_bytes"] / (m["run_ms"] * 1e-3) / 1e9 / h2d_peak if h2d_peak else None,
+                "oom_retries": m["oom_retries"],
                 "tasks": m["tasks"], "timing": "host wall clock of tq_engine_run_query's run phase"}
             if do_parity:
                 parity[key] = suite[key]["parity"] = check(res, oracle.O.query(q, host, oracle.nthreads))
