@@ -310,6 +310,7 @@ struct InterpP {
   __device__ __forceinline__ static u32 nacc(const PipeParams& p) { return p.nacc; }
   __device__ __forceinline__ static u32 nplanes(const PipeParams& p) { return p.nplanes; }
   __device__ __forceinline__ static uint8_t acc_op(const PipeParams& p, u32 a) { return p.acc[a].op; }
+  __device__ __forceinline__ static uint8_t acc_kind(const PipeParams& p, u32 a) { return p.acc[a].kind; }
   __device__ __forceinline__ static u32 acc_plane(const PipeParams& p, u32 a) { return p.acc_plane[a]; }
 
   struct Raw {};  // the interpreter reads the stage directly (held until the tile ends)

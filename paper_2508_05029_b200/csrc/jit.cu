@@ -302,6 +302,9 @@ struct Gen {
     os << "  __device__ __forceinline__ static uint8_t acc_op(const PipeParams&, u32 a) {\n    switch (a) {";
     for (int a = 0; a < nacc; ++a) os << " case " << a << ": return " << (int)p.acc[a].op << ";";
     os << " default: return 0; }\n  }\n";
+    os << "  __device__ __forceinline__ static uint8_t acc_kind(const PipeParams&, u32 a) {\n    switch (a) {";
+    for (int a = 0; a < nacc; ++a) os << " case " << a << ": return " << (int)p.acc[a].kind << ";";
+    os << " default: return 0; }\n  }\n";
     os << "  __device__ __forceinline__ static u32 acc_plane(const PipeParams&, u32 a) {\n    switch (a) {";
     for (int a = 0; a < nacc; ++a) os << " case " << a << ": return " << (int)p.acc_plane[a] << ";";
     os << " default: return 0; }\n  }\n";

@@ -995,13 +995,18 @@ __device__ __forceinline__ void pipe_body(const PipeParams& p) {
             if (a >= nacc) break;
             const uint8_t op = P::acc_op(p, a);
             const bool valid = pass && x.av[a];
-            u64* acc = direct_acc(p.agg, a, pass ? slot : 0);
+            u64* acc = tail ? direct_acc(p.agg, a, slot) : nullptr;
             if (op == ACC_CNT) {
-              u32 sv = valid ? 1u : 0u;  // a run is <= 32 rows
+              u32 sv;
+              if (P::acc_kind(p, a) == K_NONE) {
+                sv = lane - start + 1;  // Count(*): every row of the run counts
+              } else {
+                sv = valid ? 1u : 0u;  // a run is <= 32 rows
 #pragma unroll
-              for (u32 o = 1; o < 32; o <<= 1) {
-                const u32 y = __shfl_up_sync(kFull, sv, o);
-                if (lane >= start + o) sv += y;
+                for (u32 o = 1; o < 32; o <<= 1) {
+                  const u32 y = __shfl_up_sync(kFull, sv, o);
+                  if (lane >= start + o) sv += y;
+                }
               }
               if (tail) {
                 if (excl) acc[0] = sv;

@@ -33,7 +33,8 @@ def main():
     if world > 1:
         dist.init_process_group("gloo")
     torch.cuda.set_device(local)
-    ctx = Context(local)
+    free, _ = torch.cuda.mem_get_info(local)
+    ctx = Context(local, pool_reserve_bytes=int(free * 0.7))
     uid = [Comm.unique_id() if rank == 0 else None]
     if world > 1:
         dist.broadcast_object_list(uid, src=0)
