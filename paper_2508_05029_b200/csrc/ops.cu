@@ -2,6 +2,7 @@
 // the pipeline kernels, plus the small helper kernels: tile-count scan,
 // aggregation-table init/finalize, take / concat / slice.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -559,6 +560,14 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
 static void semi_table_materialize(tq_ctx* c, tq_join_table* t, cudaStream_t st) {
   std::lock_guard<std::mutex> g(t->mu);
   if (t->jt.entries != nullptr) return;  // another probe materialised it first
+  if (host_timing_on()) {
+    uint32_t f[2] = {0, 0};
+    if (t->jt.dup_dev) cudaMemcpy(&f[0], t->jt.dup_dev, 4, cudaMemcpyDeviceToHost);
+    if (t->jt.exact_flag) cudaMemcpy(&f[1], t->jt.exact_flag, 4, cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[tq] materialise %s table: %llu rows, dup %u, not-exact %u, range %llu\n",
+            t->jt.direct ? "direct" : "semi", (unsigned long long)t->build.rows, f[0], f[1],
+            (unsigned long long)t->jt.exact_range);
+  }
   tq_join_table* full = nullptr;
   Prog& P = *(Prog*)t->semi_prog.get();
   run_build(c, &t->build, P, t->semi_keys, &full, st, t->semi_bloom_keys, false, /*allow_direct=*/false);
@@ -1034,6 +1043,86 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
   dfree(c, scratch, 8 * scratch_words, st);
 }
 
+// min / max of a plain Int64 key column (+ whether any row is null), for the
+// direct aggregation's range pass when there is no predicate: 16-B loads,
+// one set of atomics per block.
+// out[3] != 0: the column is NOT non-decreasing (or has a null).
+__global__ void __launch_bounds__(256) k_key_range(const long long* v, const uint8_t* valid, u64 rows, long long* out) {
+  __shared__ long long s_mn[8], s_mx[8];
+  __shared__ int s_null, s_unsorted;
+  if (threadIdx.x == 0) s_null = s_unsorted = 0;
+  __syncthreads();
+  long long mn = 0x7fffffffffffffffll, mx = (long long)0x8000000000000000ull;
+  bool nul = false, unsorted = false;
+  const u64 pairs = rows / 2;
+  const longlong2* v2 = (const longlong2*)v;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (!valid) {  // no bitmap: four independent 16-B loads in flight per thread
+    const u64 lane = threadIdx.x & 31;
+    // (warp-uniform trip count: the shuffles below need every lane)
+    for (; i0 - lane + 31 + 3 * stride < pairs; i0 += 4 * stride) {
+      longlong2 x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[k] = __ldg(v2 + i0 + k * stride);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mn = min(mn, min(x[k].x, x[k].y));
+        mx = max(mx, max(x[k].x, x[k].y));
+        // sortedness: within the pair, and against the next pair's first value
+        // (the next lane's; lane 31 loads it)
+        long long nx = (long long)__shfl_down_sync(kFull, (unsigned long long)x[k].x, 1);
+        const u64 pi = i0 + k * stride;
+        if ((threadIdx.x & 31) == 31) nx = 2 * pi + 2 < rows ? __ldg(v + 2 * pi + 2) : x[k].y;
+        unsorted |= x[k].x > x[k].y || x[k].y > nx;
+      }
+    }
+  }
+  for (u64 i = i0; i < pairs + (rows & 1); i += stride) {
+    long long a, b;
+    bool va = true, vb = true;
+    if (i < pairs) {
+      const longlong2 x = __ldg(v2 + i);
+      a = x.x;
+      b = x.y;
+      if (valid) {
+        va = bm_get(valid, 2 * i);
+        vb = bm_get(valid, 2 * i + 1);
+      }
+    } else {  // odd tail row
+      a = b = v[rows - 1];
+      if (valid) va = vb = bm_get(valid, rows - 1);
+    }
+    if (va) { mn = min(mn, a); mx = max(mx, a); } else nul = true;
+    if (vb) { mn = min(mn, b); mx = max(mx, b); } else nul = true;
+    unsorted |= a > b || (2 * i + 2 < rows && b > __ldg(v + 2 * i + 2));
+  }
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) {
+    mn = min(mn, (long long)__shfl_xor_sync(kFull, (unsigned long long)mn, m));
+    mx = max(mx, (long long)__shfl_xor_sync(kFull, (unsigned long long)mx, m));
+  }
+  if (__any_sync(kFull, nul) && (threadIdx.x & 31) == 0) s_null = 1;
+  if (__any_sync(kFull, unsorted) && (threadIdx.x & 31) == 0) s_unsorted = 1;
+  if ((threadIdx.x & 31) == 0) {
+    s_mn[threadIdx.x >> 5] = mn;
+    s_mx[threadIdx.x >> 5] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      mn = min(mn, s_mn[w]);
+      mx = max(mx, s_mx[w]);
+    }
+    if (mn <= mx) {
+      atomicMin(out, mn);
+      atomicMax(out + 1, mx);
+    }
+    if (s_null) atomicOr((unsigned long long*)out + 2, 1ull);
+    if (s_unsorted || s_null) atomicOr((unsigned long long*)out + 3, 1ull);
+  }
+}
+
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
                       tq_join_table** out, cudaStream_t st, uint64_t bloom_keys, bool semi_only, bool allow_direct) {
   Plan L;
@@ -1083,17 +1172,53 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   const bool exact = t->jt.kw == 1;
   const bool semi = semi_only && exact;
   uint64_t ewords = words;  // exact bitmap words (range 32 x ewords)
+  // The bitmap / direct range [0, 32 x ewords) must cover the keys.  A plain
+  // Int64 key column of a large build is measured first (k_key_range: one
+  // 8-B read per row + a host sync), so e.g. a hash-partitioned orders_f —
+  // 1/N of the rows, keys spread over the whole orderkey range — still gets
+  // an exact bitmap and a direct table; otherwise the range is 32 x rows.
+  uint64_t key_max = 0;
+  bool measured = false;
+  {
+    const Operand& ko = P.pb.root(kh[0]);
+    if (exact && ko.kind == K_COL_I64 && !P.has_pred && in->rows >= (1u << 16)) {
+      const tq_column& col = in->cols[P.pb.staged()[ko.idx]];
+      long long* kr = (long long*)dalloc(c, 32, st);
+      const long long init[4] = {0x7fffffffffffffffll, (long long)0x8000000000000000ull, 0, 0};
+      TQ_CUDA(cudaMemcpyAsync(kr, init, 32, cudaMemcpyHostToDevice, st));
+      k_key_range<<<c->sms * 4, 256, 0, st>>>((const long long*)col.values, col.validity, in->rows, kr);
+      counted_launch(c);
+      long long* pin = (long long*)pinned_scratch(c);
+      TQ_CUDA(cudaMemcpyAsync(pin, kr, 16, cudaMemcpyDeviceToHost, st));
+      { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+      dfree(c, kr, 32, st);
+      if (pin[0] >= 0 && pin[0] <= pin[1]) {
+        key_max = (uint64_t)pin[1];
+        measured = true;
+      }
+    }
+  }
+  auto range_words = [&](uint64_t base_words) {
+    uint64_t w = std::max<uint64_t>(words, base_words);
+    if (measured) w = std::max<uint64_t>(w, round_up(key_max / 32 + 1, 1024));
+    return w;
+  };
   bool direct = false;
   if (exact && !semi && allow_direct && in->rows < (1ull << 31)) {
     static const bool no_direct = [] { const char* e = getenv("TQ_DIRECT"); return e && e[0] == '0'; }();
-    const uint64_t dw = std::max<uint64_t>(words, round_up(in->rows, 1024));  // range >= 32 x rows
+    const uint64_t dw = range_words(round_up(in->rows, 1024));  // range >= 32 x rows and > the largest key
     const uint64_t room = c->budget ? (c->budget > c->in_use.load() ? c->budget - c->in_use.load() : 0) : (64ull << 30);
-    if (!no_direct && dw * 32 * 4 <= room / 4) {
+    // the slots are address space (never initialised); cap them at 64 slots per build row
+    if (!no_direct && dw * 32 * 4 <= room / 4 && dw * 32 <= std::max<uint64_t>(64 * in->rows, 1u << 20)) {
       direct = true;
       ewords = dw;
     }
   }
-  if (semi) ewords = std::max<uint64_t>(words, round_up(in->rows, 1024));  // bitmap only: 4 B per row
+  if (semi) ewords = range_words(round_up(in->rows, 1024));  // bitmap only
+  // a hash table keeps an exact bitmap over the measured key range too (1 bit
+  // per key value; the probes then never need the Bloom filter), up to 256 bits per row
+  if (exact && !semi && !direct && measured && range_words(words) * 32 <= 256 * std::max<uint64_t>(in->rows, 1024))
+    ewords = range_words(words);
   const bool hashed = !semi && !direct;
   uint64_t ebytes = hashed ? cap * t->jt.stride : 0;
   const uint64_t aux = words * 4 + 16 + (exact ? ewords * 4 : 0);  // Bloom, flags, exact bitmap
@@ -1317,86 +1442,6 @@ __device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 
       }
     }
     if (ao.validity && valid) bm_set_atomic(ao.validity, row);
-  }
-}
-
-// min / max of a plain Int64 key column (+ whether any row is null), for the
-// direct aggregation's range pass when there is no predicate: 16-B loads,
-// one set of atomics per block.
-// out[3] != 0: the column is NOT non-decreasing (or has a null).
-__global__ void __launch_bounds__(256) k_key_range(const long long* v, const uint8_t* valid, u64 rows, long long* out) {
-  __shared__ long long s_mn[8], s_mx[8];
-  __shared__ int s_null, s_unsorted;
-  if (threadIdx.x == 0) s_null = s_unsorted = 0;
-  __syncthreads();
-  long long mn = 0x7fffffffffffffffll, mx = (long long)0x8000000000000000ull;
-  bool nul = false, unsorted = false;
-  const u64 pairs = rows / 2;
-  const longlong2* v2 = (const longlong2*)v;
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (!valid) {  // no bitmap: four independent 16-B loads in flight per thread
-    const u64 lane = threadIdx.x & 31;
-    // (warp-uniform trip count: the shuffles below need every lane)
-    for (; i0 - lane + 31 + 3 * stride < pairs; i0 += 4 * stride) {
-      longlong2 x[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) x[k] = __ldg(v2 + i0 + k * stride);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        mn = min(mn, min(x[k].x, x[k].y));
-        mx = max(mx, max(x[k].x, x[k].y));
-        // sortedness: within the pair, and against the next pair's first value
-        // (the next lane's; lane 31 loads it)
-        long long nx = (long long)__shfl_down_sync(kFull, (unsigned long long)x[k].x, 1);
-        const u64 pi = i0 + k * stride;
-        if ((threadIdx.x & 31) == 31) nx = 2 * pi + 2 < rows ? __ldg(v + 2 * pi + 2) : x[k].y;
-        unsorted |= x[k].x > x[k].y || x[k].y > nx;
-      }
-    }
-  }
-  for (u64 i = i0; i < pairs + (rows & 1); i += stride) {
-    long long a, b;
-    bool va = true, vb = true;
-    if (i < pairs) {
-      const longlong2 x = __ldg(v2 + i);
-      a = x.x;
-      b = x.y;
-      if (valid) {
-        va = bm_get(valid, 2 * i);
-        vb = bm_get(valid, 2 * i + 1);
-      }
-    } else {  // odd tail row
-      a = b = v[rows - 1];
-      if (valid) va = vb = bm_get(valid, rows - 1);
-    }
-    if (va) { mn = min(mn, a); mx = max(mx, a); } else nul = true;
-    if (vb) { mn = min(mn, b); mx = max(mx, b); } else nul = true;
-    unsorted |= a > b || (2 * i + 2 < rows && b > __ldg(v + 2 * i + 2));
-  }
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) {
-    mn = min(mn, (long long)__shfl_xor_sync(kFull, (unsigned long long)mn, m));
-    mx = max(mx, (long long)__shfl_xor_sync(kFull, (unsigned long long)mx, m));
-  }
-  if (__any_sync(kFull, nul) && (threadIdx.x & 31) == 0) s_null = 1;
-  if (__any_sync(kFull, unsorted) && (threadIdx.x & 31) == 0) s_unsorted = 1;
-  if ((threadIdx.x & 31) == 0) {
-    s_mn[threadIdx.x >> 5] = mn;
-    s_mx[threadIdx.x >> 5] = mx;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) {
-      mn = min(mn, s_mn[w]);
-      mx = max(mx, s_mx[w]);
-    }
-    if (mn <= mx) {
-      atomicMin(out, mn);
-      atomicMax(out + 1, mx);
-    }
-    if (s_null) atomicOr((unsigned long long*)out + 2, 1ull);
-    if (s_unsorted || s_null) atomicOr((unsigned long long*)out + 3, 1ull);
   }
 }
 
