@@ -1238,7 +1238,7 @@ void XSideOp::run(Task& t, cudaStream_t st) {
       bool prefix_ok = true;
       for (auto& c : cols) prefix_ok &= c.kind != TQ_UTF8;
       if (prefix_ok && take < v.rows) {
-        take = take / 512 * 512 ? take / 512 * 512 : take;  // tile-aligned prefix view
+        if (take >= 512) take = take / 512 * 512;  // tile-aligned prefix view
         for (auto& c : cols) c.values_bytes = take * width_of(c.kind);
         v.rows = take;
         v.cols = cols.data();

@@ -11,27 +11,7 @@
 
 #include "../../include/tq_memexec.h"
 #include "ctx.h"
-
-struct tq_pool {
-  uint64_t buffer_size = 0, capacity = 0;
-  uint8_t* arena = nullptr;  // cudaHostAlloc(portable): one allocation, never grown
-  std::mutex mu;
-  std::vector<uint32_t> free_list;  // LIFO; low ids first
-  std::vector<bool> in_use;
-};
-
-struct Seg {
-  uint32_t buf, off, len;
-};
-struct tq_chunked {
-  tq_pool* pool = nullptr;
-  uint64_t rows = 0;
-  std::vector<tq_column> schema;           // kind / precision / scale (pointers unused)
-  std::vector<uint64_t> sec_len;           // 3 per column
-  std::vector<std::vector<Seg>> sec_segs;  // 3 per column
-  std::vector<uint32_t> buffers;
-  uint64_t total = 0, tail = 0;
-};
+#include "memexec_internal.h"
 
 namespace tq {
 namespace {
@@ -148,6 +128,9 @@ void validate(const tq_chunked* cb) {
 }
 
 }  // namespace
+
+tq_chunked* chunked_layout(tq_pool* pool, const tq_batch* b) { return layout(pool, b); }
+
 }  // namespace tq
 
 using namespace tq;

@@ -153,6 +153,23 @@ def lib():
         L.tq_pipeline_broadcast.argtypes = [V, B, E, E, C.c_uint32, B, V]
         L.tq_comm_last_exchange_capacity.restype = C.c_uint64
         L.tq_comm_last_exchange_capacity.argtypes = [V]
+        L.tq_tcf_write.argtypes = [C.c_char_p, B, P(C.c_char_p), C.c_uint64]
+        L.tq_tcf_open.argtypes = [C.c_char_p, P(V)]
+        L.tq_tcf_close.argtypes = [V]
+        for fn in ("tq_tcf_ncols", "tq_tcf_row_groups"):
+            getattr(L, fn).restype = C.c_uint32
+            getattr(L, fn).argtypes = [V]
+        L.tq_tcf_rows.restype = C.c_uint64
+        L.tq_tcf_rows.argtypes = [V, C.c_uint32]
+        L.tq_tcf_reads.restype = C.c_uint64
+        L.tq_tcf_reads.argtypes = [V]
+        L.tq_tcf_column.restype = C.c_char_p
+        L.tq_tcf_column.argtypes = [V, C.c_uint32, P(TqColumnC)]
+        L.tq_tcf_plan_ranges.argtypes = [V, P(C.c_uint32), C.c_uint32, P(C.c_uint32), C.c_uint32, P(C.c_uint64),
+                                         C.c_uint64, P(C.c_uint64)]
+        L.tq_coalesce_ranges.restype = C.c_uint64
+        L.tq_coalesce_ranges.argtypes = [P(C.c_uint64), C.c_uint64, C.c_uint64, C.c_uint64, P(C.c_uint64)]
+        L.tq_tcf_fetch.argtypes = [V, V, C.c_uint32, P(C.c_uint32), C.c_uint32, C.c_uint32, P(V)]
         L.tq_on_oom_decide.restype = C.c_int
         L.tq_on_oom_decide.argtypes = [C.c_uint64, C.c_uint64, C.c_int, P(C.c_uint64)]
         L.tq_estimate_reservation.restype = C.c_uint64
@@ -723,3 +740,75 @@ def engine_run_query(ctx: Context, query: int, tables: dict, comm: "Comm" = None
     finally:
         lib().tq_host_batch_free(C.byref(out))
     return res, json.loads(buf.value.decode() or "{}")
+
+
+class Tcf:
+    """A TCF file (include/tq_storage.h): footer read on open
+    (exactly two reads), per-row-group byte-range fetch into the pinned Host
+    pool (a Chunked batch: .decode() on the host, .load(ctx) to the device)."""
+
+    @staticmethod
+    def write(path: str, table: HostBatch, row_group_bytes: int, names: Sequence[str] = None):
+        hc = table.to_c()
+        nm = None
+        if names:
+            nm = (C.c_char_p * len(names))(*[n.encode() for n in names])
+        Context._check(lib().tq_tcf_write(path.encode(), C.byref(hc), nm, row_group_bytes))
+
+    def __init__(self, path: str):
+        h = C.c_void_p()
+        Context._check(lib().tq_tcf_open(path.encode(), C.byref(h)))
+        self.handle = h
+
+    @property
+    def row_groups(self) -> int:
+        return lib().tq_tcf_row_groups(self.handle)
+
+    @property
+    def ncols(self) -> int:
+        return lib().tq_tcf_ncols(self.handle)
+
+    def rows(self, rg: int) -> int:
+        return lib().tq_tcf_rows(self.handle, rg)
+
+    def reads(self) -> int:
+        return lib().tq_tcf_reads(self.handle)
+
+    def column(self, c: int):
+        col = TqColumnC()
+        name = lib().tq_tcf_column(self.handle, c, C.byref(col))
+        return (name.decode() if name else None), col.kind, col.precision, col.scale
+
+    def plan_ranges(self, cols: Sequence[int], row_groups: Sequence[int]) -> List[Tuple[int, int]]:
+        n = C.c_uint64()
+        cap = max(1, len(cols) * len(row_groups))
+        out = (C.c_uint64 * (2 * cap))()
+        Context._check(lib().tq_tcf_plan_ranges(self.handle, _u32(cols), len(cols), _u32(row_groups), len(row_groups),
+                                                out, cap, C.byref(n)))
+        return [(out[2 * i], out[2 * i + 1]) for i in range(n.value)]
+
+    def fetch(self, pool: "Pool", rg: int, cols: Sequence[int], max_connections: int = 4) -> "Chunked":
+        h = C.c_void_p()
+        Context._check(lib().tq_tcf_fetch(self.handle, pool.handle, rg, _u32(cols), len(cols), max_connections,
+                                          C.byref(h)))
+        return Chunked(h)
+
+    def close(self):
+        if self.handle:
+            lib().tq_tcf_close(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def coalesce_ranges(ranges: Sequence[Tuple[int, int]], max_gap: int, max_merged: int) -> List[Tuple[int, int]]:
+    """SPEC.md coalesce_ranges (tq_coalesce_ranges)."""
+    n = len(ranges)
+    flat = (C.c_uint64 * max(2, 2 * n))(*[v for r in ranges for v in r])
+    out = (C.c_uint64 * max(2, 2 * n))()
+    k = lib().tq_coalesce_ranges(flat, n, max_gap, max_merged, out)
+    return [(out[2 * i], out[2 * i + 1]) for i in range(k)]
