@@ -80,6 +80,14 @@ tq_status tq_engine_run_query(tq_ctx* ctx, tq_comm* comm, int query, const tq_ba
 enum { TQ_OOM_RETRY = 0, TQ_OOM_SPLIT = 1, TQ_OOM_ABORT = 2 };
 int tq_on_oom_decide(uint64_t estimate, uint64_t capacity, int splittable, uint64_t* new_estimate);
 
+/* The same query over TCF files (include/tq_storage.h): paths[t] is table t's
+ * file or NULL.  Every row group is a STORAGE-tier handle;
+ * the scan tasks — and the Pre-loading executor ahead of them — read its
+ * column ranges straight into the pinned Host pool (byte-range preload,
+ * SPEC.md:444-452) and move them to the device (tq_load). */
+tq_status tq_engine_run_query_tcf(tq_ctx* ctx, tq_comm* comm, int query, const char* const* paths,
+                                  const tq_engine_opts* opts, tq_batch* result, char* metrics_json, uint64_t cap);
+
 /* max(ema_peak, ema_ratio*input) * safety, or multiplier *
  * input without history; never below input_bytes. */
 uint64_t tq_estimate_reservation(uint64_t samples, double ema_peak, double ema_ratio, uint64_t input_bytes,

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/tq_engine.h"
+#include "../../include/tq_storage.h"
 #include "ctx.h"
 
 namespace tq {
@@ -42,7 +43,7 @@ struct EB {
 EB Col(uint32_t c) { EB b; b.col(c); return b; }
 
 // ------------------------------------------------------------------ handles / holders
-enum Tier { DEVICE = 0, HOST = 1 };
+enum Tier { DEVICE = 0, HOST = 1, STORAGE = 2 };
 
 struct Handle {
   uint64_t id = 0;
@@ -53,6 +54,8 @@ struct Handle {
   bool spilling = false;  // chosen as a spill victim (under rt->mu); the copy runs outside it
   tq_batch dev{};
   tq_chunked* host = nullptr;
+  tq_tcf* file = nullptr;  // STORAGE tier: a row group of a TCF file
+  uint32_t row_group = 0;
   std::mutex mu;
 };
 using HP = std::shared_ptr<Handle>;
@@ -193,6 +196,15 @@ class Runtime {
   void load(HP h, cudaStream_t st, bool preload) {
     std::lock_guard<std::mutex> g(h->mu);
     if (h->tier == DEVICE) return;
+    if (h->tier == STORAGE) {
+      // Storage -> Host: the row group's column ranges read straight into the
+      // pinned pool (byte-range preload), then on to Device
+      std::vector<uint32_t> cols(tq_tcf_ncols(h->file));
+      for (uint32_t k = 0; k < cols.size(); ++k) cols[k] = k;
+      check(tq_tcf_fetch(h->file, pool, h->row_group, cols.data(), (uint32_t)cols.size(), 4, &h->host));
+      h->tier = HOST;
+      m_storage_reads++;
+    }
     tq_batch b{};
     check(tq_load(ctx, h->host, &b, st));
     cudaStreamSynchronize(st);
@@ -256,7 +268,7 @@ class Runtime {
   bool poll_all();            // one coordination pass; caller holds mu
   // metrics
   std::atomic<uint64_t> m_tasks{0}, m_retries{0}, m_splits{0}, m_spills{0}, m_spill_bytes{0}, m_loads{0},
-      m_preloads{0}, m_load_bytes{0}, m_peak{0}, m_injected{0};
+      m_preloads{0}, m_load_bytes{0}, m_peak{0}, m_injected{0}, m_storage_reads{0};
   uint64_t spilling_bytes = 0;           // Device bytes of marked victims not yet freed (under mu)
   std::deque<std::vector<HP>> spill_q;   // watermark spills for the memory executor (under mu)
   struct Decision {
@@ -396,7 +408,7 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
   uint64_t in_bytes = 0, host_bytes = 0;
   for (HP& h : t.inputs) {
     in_bytes += h->bytes;
-    if (h->tier == HOST) host_bytes += h->bytes;
+    if (h->tier != DEVICE) host_bytes += h->bytes;
   }
   if (!t.estimate) t.estimate = estimate(*op, in_bytes);
   // ---- reserve(Device, estimate): new allocations only
@@ -554,7 +566,7 @@ void Runtime::preloader() {
       std::sort(top.begin(), top.end(), [](const Task* a, const Task* b) { return a->seq < b->seq; });
       for (size_t i = 0; i < top.size() && i < 4 && !h; ++i)
         for (const HP& x : top[i]->inputs)
-          if (x->tier == HOST && x->pins == 0) {
+          if (x->tier != DEVICE && x->pins == 0) {
             h = x;
             break;
           }
@@ -681,7 +693,8 @@ void Runtime::setup() {
 // through load_to_device.
 class ScanOp : public Op {
  public:
-  ScanOp(Runtime* rt, std::string n, const tq_batch* table) : Op(rt, std::move(n), 0, 4.0), table(*table) {}
+  ScanOp(Runtime* rt, std::string n, const tq_batch* table)
+      : Op(rt, std::move(n), 0, 4.0), table(*table), src(table) {}
   void poll(std::vector<Task>&) override {
     // (under rt->mu) publish every batch once, then close the output
     std::vector<HP> hs;
@@ -724,6 +737,7 @@ class ScanOp : public Op {
     return h;
   }
   tq_batch table;
+  const tq_batch* src;  // the caller's table entry (identifies a TCF-backed table)
   std::deque<std::vector<tq_column>> views;
   std::vector<HP> out_q, pending;
   uint64_t nbatches = 0;  // batches this scan publishes (phase-1 progress of the exchanges it drives)
@@ -1670,8 +1684,9 @@ int tq_on_oom_decide(uint64_t estimate, uint64_t capacity, int splittable, uint6
   return splittable ? TQ_OOM_SPLIT : TQ_OOM_ABORT;
 }
 
-tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batch* tables, const tq_engine_opts* o,
-                              tq_batch* result, char* metrics_json, uint64_t cap) {
+namespace {
+tq_status run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batch* tables, tq_tcf* const* files,
+                    const tq_engine_opts* o, tq_batch* result, char* metrics_json, uint64_t cap) {
   return guard([&] {
     tq_engine_opts opts{};
     if (o) opts = *o;
@@ -1686,12 +1701,16 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
     Runtime rt(c, comm, opts);
     rt.capacity = opts.device_budget ? opts.device_budget : c->budget;
     bool host_tables = false;
-    for (int t = 0; t < 8; ++t) host_tables |= tables[t].cols && tables[t].mem == TQ_MEM_HOST;
+    for (int t = 0; t < 8; ++t) host_tables |= (tables[t].cols && tables[t].mem == TQ_MEM_HOST) || files[t];
     if (!rt.opts.pool_capacity && (rt.capacity || host_tables)) {
       // Host tier sized for the host tables plus spill headroom
       uint64_t bytes = 4ull << 30;
       for (int t = 0; t < 8; ++t)
-        if (tables[t].cols && tables[t].mem == TQ_MEM_HOST) bytes += batch_bytes(tables[t]) + (tables[t].rows / 512 + 1) * 8 * tables[t].ncols * 2;
+        if (!files[t] && tables[t].cols && tables[t].mem == TQ_MEM_HOST)
+          bytes += batch_bytes(tables[t]) + (tables[t].rows / 512 + 1) * 8 * tables[t].ncols * 2;
+        else if (files[t])
+          for (uint32_t g = 0; g < tq_tcf_row_groups(files[t]); ++g)
+            bytes += tq_tcf_rows(files[t], g) * 64 + (2ull << 20);  // (+ one buffer tail per column)
       rt.opts.pool_capacity = bytes / rt.opts.pool_buffer_size + 1;
     }
     rt.setup();
@@ -1706,7 +1725,35 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
     // tables are encoded into the pinned pool (Host tier) and every scan task
     // goes through load_to_device
     for (ScanOp* s : P.scans) {
-      if (s->table.mem == TQ_MEM_HOST) {
+      tq_tcf* file = nullptr;
+      for (int t = 0; t < 8; ++t)
+        if (&tables[t] == (const tq_batch*)s->src && files[t]) file = files[t];
+      if (file) {
+        // a TCF table: one STORAGE-tier handle per row group; the scan tasks
+        // (and the Pre-loading executor ahead of them) fetch its byte ranges
+        // into the pinned pool and move them to the device
+        if (!rt.pool) fail(TQ_INVALID_PLAN, "TCF tables need a host pool");
+        for (uint32_t g = 0; g < tq_tcf_row_groups(file); ++g) {
+          HP h = std::make_shared<Handle>();
+          h->tier = STORAGE;
+          h->file = file;
+          h->row_group = g;
+          uint64_t n = 0;
+          std::vector<uint32_t> cols(tq_tcf_ncols(file)), gs{g};
+          for (uint32_t k = 0; k < cols.size(); ++k) cols[k] = k;
+          std::vector<tq_range> rs(cols.size());
+          check(tq_tcf_plan_ranges(file, cols.data(), (uint32_t)cols.size(), gs.data(), 1, rs.data(), rs.size(), &n));
+          for (uint64_t i = 0; i < n; ++i) h->bytes += rs[i].length;
+          {
+            std::lock_guard<std::mutex> lk(rt.mu);
+            h->id = ++rt.next_id;
+            rt.registry.push_back(h);
+          }
+          s->out->push(h);
+          s->nbatches++;
+        }
+        s->finished = true;
+      } else if (s->table.mem == TQ_MEM_HOST) {
         if (!rt.pool) fail(TQ_INVALID_PLAN, "host tables need a host pool");
         uint64_t br = std::max<uint64_t>(512, opts.batch_rows / 512 * 512);
         for (uint64_t r = 0; r < s->table.rows || (r == 0 && s->table.rows == 0); r += br) {
@@ -1780,6 +1827,7 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
       js << "{\"wall_ms\": " << wall << ", \"setup_ms\": " << setup_ms << ", \"run_ms\": " << run_ms << ", \"download_ms\": " << download_ms << ", \"tasks\": " << rt.m_tasks << ", \"oom_retries\": " << rt.m_retries
          << ", \"splits\": " << rt.m_splits << ", \"spills\": " << rt.m_spills << ", \"spill_bytes\": " << rt.m_spill_bytes
          << ", \"loads\": " << rt.m_loads << ", \"preloads\": " << rt.m_preloads << ", \"load_bytes\": " << rt.m_load_bytes
+         << ", \"storage_reads\": " << rt.m_storage_reads
          << ", \"peak_device_bytes\": " << rt.m_peak << ", \"device_capacity\": " << rt.capacity
          << ", \"exchange_decisions\": [";
       for (size_t i = 0; i < rt.decisions.size(); ++i) {
@@ -1809,6 +1857,36 @@ tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batc
       metrics_json[n] = 0;
     }
   });
+}
+}  // namespace
+
+tq_status tq_engine_run_query(tq_ctx* c, tq_comm* comm, int query, const tq_batch* tables, const tq_engine_opts* o,
+                              tq_batch* result, char* metrics_json, uint64_t cap) {
+  tq_tcf* none[8] = {};
+  return run_query(c, comm, query, tables, none, o, result, metrics_json, cap);
+}
+
+tq_status tq_engine_run_query_tcf(tq_ctx* c, tq_comm* comm, int query, const char* const* paths,
+                                  const tq_engine_opts* o, tq_batch* result, char* metrics_json, uint64_t cap) {
+  tq_tcf* files[8] = {};
+  tq_batch tabs[8] = {};
+  std::vector<std::vector<tq_column>> schemas(8);
+  tq_status st = TQ_OK;
+  for (int t = 0; t < 8 && st == TQ_OK; ++t) {
+    if (!paths[t]) continue;
+    st = tq_tcf_open(paths[t], &files[t]);
+    if (st != TQ_OK) break;
+    // a schema-only descriptor: the plans read the kinds; the rows come from the row groups
+    schemas[t].resize(tq_tcf_ncols(files[t]));
+    for (uint32_t k = 0; k < schemas[t].size(); ++k) tq_tcf_column(files[t], k, &schemas[t][k]);
+    for (uint32_t g = 0; g < tq_tcf_row_groups(files[t]); ++g) tabs[t].rows += tq_tcf_rows(files[t], g);
+    tabs[t].ncols = (uint32_t)schemas[t].size();
+    tabs[t].mem = TQ_MEM_HOST;
+    tabs[t].cols = schemas[t].data();
+  }
+  if (st == TQ_OK) st = run_query(c, comm, query, tabs, files, o, result, metrics_json, cap);
+  for (tq_tcf* f : files) tq_tcf_close(f);
+  return st;
 }
 
 }  // extern "C"

@@ -139,6 +139,8 @@ def lib():
         L.tq_chunked_release.argtypes = [V]
         # engine (include/tq_engine.h)
         L.tq_engine_run_query.argtypes = [V, V, C.c_int, P(TqBatchC), P(TqEngineOptsC), B, C.c_char_p, C.c_uint64]
+        L.tq_engine_run_query_tcf.argtypes = [V, V, C.c_int, P(C.c_char_p), P(TqEngineOptsC), B, C.c_char_p,
+                                              C.c_uint64]
         L.tq_agg_create.argtypes = [V, E, E, C.c_uint32, U32, C.c_uint32, P(TqAggC), C.c_uint32, P(V)]
         L.tq_agg_update.argtypes = [V, B, V]
         L.tq_agg_finalize.argtypes = [V, B, V]
@@ -812,3 +814,23 @@ def coalesce_ranges(ranges: Sequence[Tuple[int, int]], max_gap: int, max_merged:
     out = (C.c_uint64 * max(2, 2 * n))()
     k = lib().tq_coalesce_ranges(flat, n, max_gap, max_merged, out)
     return [(out[2 * i], out[2 * i + 1]) for i in range(k)]
+
+
+def engine_run_query_tcf(ctx: Context, query: int, paths: dict, comm: "Comm" = None, **opts):
+    """Run a query DAG on the C++ worker runtime over TCF files (paths:
+    {table_id: path}); every row group is a Storage-tier batch the executors
+    fetch into the pinned pool and move to the device.  Returns (HostBatch, metrics)."""
+    import json
+    arr = (C.c_char_p * 8)(*[paths[t].encode() if t in paths else None for t in range(8)])
+    o = TqEngineOptsC()
+    for k, v in opts.items():
+        setattr(o, k, v.encode() if isinstance(v, str) else v)
+    out = TqBatchC()
+    buf = C.create_string_buffer(1 << 16)
+    Context._check(lib().tq_engine_run_query_tcf(ctx.handle, comm.handle if comm else None, query, arr, C.byref(o),
+                                                 C.byref(out), buf, len(buf)))
+    try:
+        res = HostBatch.from_c(out)
+    finally:
+        lib().tq_host_batch_free(C.byref(out))
+    return res, json.loads(buf.value.decode() or "{}")

@@ -82,3 +82,22 @@ def test_engine_on_oom_paths(ctx, case):
         with pytest.raises(TqError) as e:
             engine_run_query(ctx, 3, tabs, task_batches=1, inject_oom_mode=2, inject_oom_count=1, **opts)
         assert e.value.errc == "OutOfMemoryUnsplittable"
+
+
+@pytest.mark.parametrize("q", [3, 9])
+def test_engine_over_tcf_files(ctx, q, tmp_path):
+    """The scan side end to end: the query's tables written as TCF files, every
+    row group a Storage-tier batch that the executors fetch into the pinned
+    pool (byte ranges) and move to the device; with a Device budget and the
+    Pre-loading executor.  Result == the oracle."""
+    from paper_2508_05029_b200.ops import Tcf, engine_run_query_tcf
+    sf = 0.05
+    host = {t: O.datagen(t, sf) for t in O.QUERY_TABLES[q]}
+    paths = {}
+    for t, b in host.items():
+        paths[t] = str(tmp_path / f"t{t}.tcf")
+        Tcf.write(paths[t], b, 256 << 10)
+    got, m = engine_run_query_tcf(ctx, q, paths, compute_threads=4, preload=1,
+                                  device_budget=max(sum(b.nbytes() for b in host.values()) // 3, 48 << 20))
+    assert_batches_equal(got, O.query(q, host, 8))
+    assert m["storage_reads"] >= sum(Tcf(p).row_groups for p in paths.values()), m
