@@ -1312,7 +1312,7 @@ struct FinalParams {
 };
 
 __device__ __forceinline__ bool agg_slot_used(const FinalParams& f, u64 s) {
-  return s < f.t.cap && (f.direct ? *direct_acc(f.t, f.cnt_acc, s) != 0 : f.t.state[s] == 2);
+  return s < f.t.cap && (f.direct ? __ldg(direct_acc(f.t, f.cnt_acc, s)) != 0 : __ldg(f.t.state + s) == 2);
 }
 __device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 row);
 
@@ -1398,16 +1398,17 @@ __device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 
   const u64* acc = f.t.acc + s * f.nacc * 2;
   for (u32 a = 0; a < f.naggs; ++a) {
     const AggOut& ao = f.aggs[a];
-    const u64* m = f.direct ? direct_acc(f.t, ao.acc, s) : acc + 2 * ao.acc;
-    u64 limb[2];
+    // read-only in this kernel: non-coherent loads, which the compiler may
+    // issue ahead of the previous group's stores (they cannot alias)
+    const u64* src = f.direct ? direct_acc(f.t, ao.acc, s) : acc + 2 * ao.acc;
+    u64 m[2] = {__ldg(src), (f.direct && f.t.dwidth[ao.acc] < 2) ? 0ull : __ldg(src + 1)};
     if (f.direct && (ao.kind == AO_SUM_I64 || ao.kind == AO_SUM_DEC || ao.kind == AO_AVG_I)) {
       // direct table: integer sums are kept as {low-limb sum, high-part sum}
       const i128 v = add128((i128)(long long)m[1] * ((i128)1 << 32), (i128)m[0]);
-      limb[0] = lo64(v);
-      limb[1] = hi64(v);
-      m = limb;
+      m[0] = lo64(v);
+      m[1] = hi64(v);
     }
-    u64 cnt = ao.cnt == 0xff ? 1 : f.direct ? *direct_acc(f.t, ao.cnt, s) : acc[2 * ao.cnt];
+    u64 cnt = ao.cnt == 0xff ? 1 : __ldg(f.direct ? direct_acc(f.t, ao.cnt, s) : acc + 2 * ao.cnt);
     bool valid = cnt != 0;
     switch (ao.kind) {
       case AO_SUM_I64:
