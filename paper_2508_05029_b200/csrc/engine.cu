@@ -405,16 +405,25 @@ uint64_t estimate(const Op& op, uint64_t input_bytes) {
 
 void Runtime::run_task(Task& t, cudaStream_t st) {
   Op* op = t.op;
-  uint64_t in_bytes = 0, host_bytes = 0;
-  for (HP& h : t.inputs) {
-    in_bytes += h->bytes;
-    if (h->tier != DEVICE) host_bytes += h->bytes;
-  }
+  uint64_t in_bytes = 0, host_bytes = 0, want = 0;
+  for (HP& h : t.inputs) in_bytes += h->bytes;
   if (!t.estimate) t.estimate = estimate(*op, in_bytes);
   // ---- reserve(Device, estimate): new allocations only
-  const uint64_t want = t.estimate > in_bytes ? t.estimate - in_bytes + host_bytes : host_bytes;
   {
     std::unique_lock<std::mutex> g(mu);
+    // pin the inputs first so this task's own reservation never picks them as
+    // victims; an input chosen as a victim before it was pinned is being
+    // copied out by another thread: let that finish (load() then brings it
+    // back) rather than run on a batch that is about to be freed
+    for (HP& h : t.inputs) h->pins++;
+    cv.wait(g, [&] {
+      for (HP& h : t.inputs)
+        if (h->spilling) return false;
+      return true;
+    });
+    for (HP& h : t.inputs)  // inputs not on the Device are loaded into the reservation
+      if (h->tier != DEVICE) host_bytes += h->bytes;
+    want = t.estimate > in_bytes ? t.estimate - in_bytes + host_bytes : host_bytes;
     if (capacity) {
       while (device_in_use() + reserved + want > capacity) {
         std::vector<HP> v = pick_victims(reserved + want, capacity);
@@ -430,7 +439,6 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
     }
     reserved += want;
     executing++;
-    for (HP& h : t.inputs) h->pins++;
   }
   auto release = [&] {
     std::lock_guard<std::mutex> g(mu);
@@ -956,11 +964,16 @@ class AggOp : public Op {
       return;
     }
     if (!in->empty()) {
+      // one batch per update task: an update that fails (on_oom) is retried
+      // as a whole, so a task must never hold an already-aggregated batch
       Task t;
       t.op = this;
-      if (first) t.inputs.push_back(first);
-      first = nullptr;
-      t.inputs.push_back(in->pop());
+      if (first) {
+        t.inputs.push_back(first);  // the next batch stays queued for the next task
+        first = nullptr;
+      } else {
+        t.inputs.push_back(in->pop());
+      }
       updated = true;
       ts.push_back(std::move(t));
       return;
