@@ -509,16 +509,25 @@ def run_suite(args, ctx, world, rank, stream, oracle, parity):
     runs = []
     for i in range(4):
         barrier(world)
+        if i == 3:
+            ctx.profile(True)
         res, m = engine_run_query(ctx, 3, tabs, comm=comm if world > 1 else None, compute_threads=4,
                                   batch_rows=1 << 40)
         if i:
             runs.append(m["run_ms"])
+    eprof = ctx.profile_report()
+    ctx.profile(False)
     key = f"q3_shuffle_engine_sf{sf:g}"
     ms = max_over_ranks(world, statistics.median(runs))
     results[key] = res
     suite[key] = {"ms": ms, "rows_per_s": rows / (ms * 1e-3), "scaling": "strong", "n_gpus": world,
                   "timing": "host wall clock of tq_engine_run_query's run phase (median of 3), max over ranks",
-                  "exchange_decisions": m.get("exchange_decisions"), "tasks": m.get("tasks")}
+                  "exchange_decisions": m.get("exchange_decisions"), "tasks": m.get("tasks"),
+                  "runs_ms_rank0": [round(r, 3) for r in runs], "spills": m.get("spills"),
+                  "ops_ms_last_run": {k: [round(v["ms"], 3), round(v.get("gpu_ms", 0.0), 3)] for k, v in
+                                      sorted(m.get("ops", {}).items(), key=lambda kv: -kv[1]["ms"])[:6]},
+                  "kernels_last_run": {k: (v[0], round(v[1], 3)) for k, v in eprof.items()},
+                  "timeline_last_run": [(n, k, round(a, 3), round(b, 3)) for n, k, a, b in m.get("timeline", [])]}
     for v in t.values():
         v.free()
     comm.close()

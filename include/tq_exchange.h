@@ -61,8 +61,9 @@ tq_status tq_pipeline_broadcast(tq_comm* comm, const tq_batch* in, const tq_expr
  * Passed as `semi` to tq_pipeline_partition_exchange, a row is checked only
  * against the part of the rank it is sent to.  Collective. */
 tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* table, tq_bloom** out, void* stream);
-/* Row capacity of the last tq_pipeline_partition_exchange's receive windows:
- * identical on every rank, >= the rows any rank received. */
+/* The most rows any rank received in the last tq_pipeline_partition_exchange
+ * (>= 1): identical on every rank, so a Bloom filter sized from it has the same
+ * word count everywhere (tq_join_build_sized -> tq_comm_gather_table_blooms). */
 uint64_t tq_comm_last_exchange_capacity(tq_comm* comm);
 /* Bytes this communicator has sent to other ranks (NVLink traffic). */
 uint64_t tq_comm_bytes_sent(tq_comm* comm);

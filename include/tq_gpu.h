@@ -102,10 +102,11 @@ tq_status tq_hash_partition(tq_ctx* ctx, const tq_batch* in, const uint32_t* key
  * build batch (which must stay alive until the table is destroyed). */
 tq_status tq_join_build(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
                         tq_join_table** out, void* stream);
-/* tq_join_build with the table's Bloom filter sized for max(build rows,
- * bloom_keys) keys: ranks that pass the same bloom_keys (e.g. the capacity of
- * the fused exchange that delivered the build side) get equal-size filters,
- * which tq_comm_gather_table_blooms (tq_exchange.h) can all-gather. */
+/* tq_join_build with the table's Bloom filter sized from bloom_keys (>= build
+ * rows) at 16 bits per key: ranks that pass the same bloom_keys (the most rows
+ * any rank received in the fused exchange that delivered the build side,
+ * tq_comm_last_exchange_capacity) get equal-size filters, which
+ * tq_comm_gather_table_blooms (tq_exchange.h) can all-gather. */
 tq_status tq_join_build_sized(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,
                               uint64_t bloom_keys, tq_join_table** out, void* stream);
 /* Build side of a SEMI-join (the probe takes no build columns, e.g. the
@@ -119,7 +120,7 @@ tq_status tq_join_build_semi(tq_ctx* ctx, const tq_batch* build, const uint32_t*
 tq_status tq_pipeline_build_semi(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
                                  uint32_t nkeys, tq_join_table** out, void* stream);
 /* tq_pipeline_build / _semi with the table's Bloom filter sized for
- * bloom_keys (>= rows; 0 = rows): a capacity every worker agrees on, so the
+ * bloom_keys (>= rows; 0 = rows), a row count every worker agrees on, so the
  * workers' filters can be all-gathered as one partitioned LIP filter. */
 tq_status tq_pipeline_build_ex(tq_ctx* ctx, const tq_batch* in, const tq_expr* pred, const uint32_t* keys,
                                uint32_t nkeys, uint64_t bloom_keys, int semi, tq_join_table** out, void* stream);

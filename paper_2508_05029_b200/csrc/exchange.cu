@@ -91,7 +91,7 @@ struct tq_comm {
   uint8_t* win = nullptr;
   uint64_t win_bytes = 0;
   std::vector<uint8_t*> win_peer;  // [n]; win_peer[rank] == win
-  uint64_t win_cap_rows = 0;       // capacity (rows) of the last fused exchange (identical on every rank)
+  uint64_t win_cap_rows = 0;       // most rows any rank received in the last fused exchange (identical on every rank)
   // the window is used as two halves, alternating per fused exchange (epoch parity)
   uint64_t epoch = 0;
 };

@@ -42,6 +42,11 @@ cudaError_t launch_pipeline_prog(tq_ctx* c, int sink, const PipeParams& p, u32 s
 
 // ================================================================== scan
 constexpr int kScanItems = 8;
+// partitioned LIP filter (tq_join_build_sized / tq_comm_gather_table_blooms):
+// bits per key of the most rows any rank received; 16 measured best at SF100
+// N=2 (8: more false positives shipped and probed, 32+: the gathered filter
+// falls out of L2)
+constexpr uint64_t kLipBloomBitsPerKey = 16;
 constexpr int kScanBlock = 256 * kScanItems;
 
 __device__ __forceinline__ u64 block_excl_scan(u64 v, u64* s_warp, u64& total) {
@@ -1036,7 +1041,10 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
     comm_epoch(cm) += 1;
     prof_end(c, ph_fix, st);
     if (rows_sent) *rows_sent = sent_rows;
-    comm_last_cap(cm) = cap;
+    // the Bloom size of the table built on this output (tq_join_build_sized)
+    // follows from it: the most rows any rank received (identical on every
+    // rank), not the window capacity, which only grows over the comm's life
+    comm_last_cap(cm) = std::max<u64>(rmax, 1);
     break;
   }
   dfree(c, plan, plan_words * 8, st);
@@ -1154,10 +1162,11 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
   t->jt.kw = p.key_words;
   t->jt.stride = (u32)round_up(8 * (1 + p.key_words), 16);
   // blocked Bloom filter, ~8 bits per build row: rejects non-matching probes in L2
-  // (bloom_keys: size for that many keys instead, e.g. a capacity every rank
-  // agrees on, so the ranks' filters can be all-gathered as one partitioned filter)
+  // (bloom_keys: size for that many keys at kLipBloomBitsPerKey instead, a row
+  // count every rank agrees on, so the ranks' filters can be all-gathered as one
+  // partitioned filter)
   uint64_t words = 1024;
-  while (words * 32 < std::max<uint64_t>(in->rows, bloom_keys) * 8) words <<= 1;
+  while (words * 32 < std::max<uint64_t>(in->rows * 8, bloom_keys * kLipBloomBitsPerKey)) words <<= 1;
   t->jt.bloom_mask = words - 1;
   // One-word keys also get an exact membership bitmap over [0, exact_range)
   // and the build's duplicate-key / exact-range flags.  A semi-only build (a
@@ -2980,7 +2989,7 @@ tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* t, tq_
     // so every filter has the same word count.  Checked locally against that
     // agreed value before the collective (no size all-gather, no host sync).
     uint64_t expect = 1024;
-    while (expect * 32 < comm_last_cap(comm) * 8) expect <<= 1;
+    while (expect * 32 < comm_last_cap(comm) * kLipBloomBitsPerKey) expect <<= 1;
     if (per != expect) {
       delete b;
       fail(TQ_INVALID_PLAN, "table Bloom filter not sized from the last exchange capacity (tq_join_build_sized)");

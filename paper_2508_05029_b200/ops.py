@@ -620,7 +620,7 @@ class Comm:
         return Bloom(self.ctx, h)
 
     def last_exchange_capacity(self) -> int:
-        """Receive-window rows of the last partition_exchange (same on every rank)."""
+        """Most rows any rank received in the last partition_exchange (same on every rank)."""
         return lib().tq_comm_last_exchange_capacity(self.handle)
 
     def bytes_sent(self) -> int:

@@ -23,6 +23,9 @@ def main():
     ap.add_argument("--sf", type=float, default=100)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--threads", type=int, default=4)
+    ap.add_argument("--pre-python", type=int, default=0, help="run the Python Q3 plans first (as bench.py)")
+    ap.add_argument("--pre5", type=int, default=0, help="run config 5 (Host-tier Q5/Q9) first (as bench.py)")
+    ap.add_argument("--keep", type=int, default=1)
     ap.add_argument("--kprof", type=int, default=0, help="per-kernel CUDA-event profile of the last rep")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -38,7 +41,36 @@ def main():
         dist.broadcast_object_list(uid, src=0)
     comm = Comm(ctx, rank, world, uid[0])
     names = queries.QUERY_TABLES[a.q]
+    if a.pre5:
+        # what bench.py runs before config 4: config 5 (Host-tier tables, Device budget)
+        for q in (5, 9):
+            host = {}
+            for n in queries.QUERY_TABLES[q]:
+                d = ctx.datagen(queries.TABLE_IDS[n], 12.5)
+                host[queries.TABLE_IDS[n]] = d.to_host()
+                d.free()
+            data_bytes = sum(b.nbytes() for b in host.values())
+            for _ in range(2):
+                engine_run_query(ctx, q, host, compute_threads=4, preload=1, batch_rows=4 << 20,
+                                 device_budget=max(int(data_bytes / 2.5), 1 << 30))
+            del host
+        if rank == 0:
+            print("pre5 done", flush=True)
     t = {queries.TABLE_IDS[n]: ctx.datagen(queries.TABLE_IDS[n], a.sf, shard=rank, nshards=world) for n in names}
+    if a.pre_python and a.q == 3:
+        # what bench.py runs before the engine line: the Python fused plan (results kept)
+        kept = []
+        for fused in ((True, False, True) if a.pre_python == 1 else (True,)):
+            if world > 1:
+                dist.barrier()
+            kept.append(queries.q3_distributed(ctx, comm, t[queries.TABLE_IDS["customer"]],
+                                               t[queries.TABLE_IDS["orders"]], t[queries.TABLE_IDS["lineitem"]],
+                                               {}, fused=fused, lip=a.pre_python != 2))
+        ctx.sync()
+        if not a.keep:
+            for k in kept:
+                k.free()
+            kept = []
     for i in range(a.reps + 1):
         if world > 1:
             dist.barrier()
