@@ -117,6 +117,10 @@ struct Task {
 
 struct XPair {
   int decide_turn = 0;
+  // the sides' phase-1 estimates start once the previous pair decided: they
+  // are off the critical path then, instead of competing with the first
+  // pair's estimates at the start of the query
+  int est_turn = 0;
   bool est_ready[2] = {false, false};
   uint64_t est[2] = {0, 0};
   bool decide_submitted = false, decided = false;
@@ -1097,7 +1101,10 @@ class DecideOp : public Op {
       mine[0] = x->est[0];
       mine[1] = x->est[1];
     }
-    check(tq_comm_allgather_host_u64(rt->comm, mine, all, 2, st));
+    {
+      TQ_HT("engine decide allgather");
+      check(tq_comm_allgather_host_u64(rt->comm, mine, all, 2, st));
+    }
     for (int r = 0; r < n; ++r) {
       est0[r] = all[2 * r];
       est1[r] = all[2 * r + 1];
@@ -1206,7 +1213,7 @@ void XSideOp::poll(std::vector<Task>& ts) {
   }
   // ---- phase 1: a local estimate once the driving scan
   // passed the sample fraction, or this side's input ended
-  if (!x->est_ready[side] && !est_submitted) {
+  if (!x->est_ready[side] && !est_submitted && rt->exchange_turn >= x->est_turn) {
     const uint64_t total = src ? src->nbatches : 0;
     const double progress = in->closed() ? 1.0 : total ? (double)got.size() / (double)total : 0.0;
     if (progress >= 1.0 || progress >= TQ_SAMPLE_FRACTION) {
@@ -1271,6 +1278,7 @@ void XSideOp::run(Task& t, cudaStream_t st) {
         v.cols = cols.data();
       }
       uint64_t rows = 0, rb = 0;
+      TQ_HT("engine side estimate");
       check(tq_pipeline_estimate(rt->ctx, &v, pp, ep, (uint32_t)ex.size(), &rows, &rb, st));
       out_bytes += rows * rb;
       sampled += v.rows;
@@ -1384,6 +1392,8 @@ struct Plan {
     rt->pairs.emplace_back(new XPair());
     XPair* x = rt->pairs.back().get();
     x->decide_turn = turns++;
+    x->est_turn = last_decide_turn + 1;
+    last_decide_turn = x->decide_turn;
     rt->op<DecideOp>("decide_" + name, x);
     return x;
   }
@@ -1396,6 +1406,7 @@ struct Plan {
     return wire(o);
   }
   int agg_turn() { return turns++; }
+  int last_decide_turn = -1;
 };
 
 EB rev() {  // ep * (1.00 - disc)

@@ -2589,7 +2589,7 @@ tq_status tq_pipeline_estimate(tq_ctx* c, const tq_batch* in, const tq_expr* pre
       scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
       {
         TQ_CUDA(cudaMemcpyAsync(pinned_scratch(c), offsets + ncnt, 8, cudaMemcpyDeviceToHost, st));
-        { TQ_HT("stream sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
+        { TQ_HT("estimate sync"); TQ_CUDA(cudaStreamSynchronize(st)); }
         rows = ((uint64_t*)pinned_scratch(c))[0];
       }
       dfree(c, counts, ncnt * 4, st);
