@@ -334,6 +334,26 @@ struct Gen {
            << "u))[(w.row0 >> 5) + v] >> w.lane) & 1u;\n";
     }
     os << "  }\n";
+    // the same columns straight from global memory (count_direct_body)
+    os << "  __device__ __forceinline__ static void load_g(const WCtx& w, u64 row, Raw& R) {\n"
+          "    const PipeParams& p = *w.p;\n    (void)p;\n";
+    for (u32 c = 0; c < p.nstaged; ++c) {
+      const std::string f = "R.c" + std::to_string(c);
+      const std::string col = "p.cols[" + std::to_string(c) + "]";
+      if (!((p.load_mask >> c) & 1)) {
+        os << "    " << f << " = 0;\n";
+        if (p.cols[c].validity) os << "    R.v" << c << " = false;\n";
+        continue;
+      }
+      if (p.cols[c].kind == TQ_DECIMAL)
+        os << "    { const ulonglong2 q = __ldg((const ulonglong2*)" << col << ".values + row); " << f
+           << " = mk128(q.x, q.y); }\n";
+      else
+        os << "    " << f << " = __ldg((const " << raw_type(p.cols[c].kind) << "*)" << col << ".values + row);\n";
+      if (p.cols[c].validity)
+        os << "    R.v" << c << " = (__ldg(" << col << ".validity + (row >> 3)) >> (row & 7)) & 1u;\n";
+    }
+    os << "  }\n";
     os << "  __device__ __forceinline__ static u32 tile_begin(WCtx& w, const DInstr*, u32* pm, const Raw* Rs) {\n"
           "    u32 any = 0;\n#pragma unroll\n    for (int v = 0; v < kV; ++v) {\n      const u32 r = trow(w, v);\n"
           "      const Raw& R = Rs[v];\n      (void)R;\n      bool pass = r < w.nrows;\n";
@@ -465,6 +485,12 @@ struct Gen {
       os << "    (void)r; (void)p; (void)pos; (void)brow;\n";
     }
     os << "  }\n};\n}  // namespace tq\n";
+    if (sink >= SINK_COUNT_DIRECT) {
+      os << "extern \"C\" __global__ void __launch_bounds__(256) tq_jit_main(const __grid_constant__ "
+            "tq::PipeParams p) {\n  tq::count_direct_loop<tq::Gen, "
+         << (sink - SINK_COUNT_DIRECT) << ">(p);\n}\n";
+      return os.str();
+    }
     os << "extern \"C\" __global__ void __launch_bounds__(tq::kBlock, " << min_blocks
        << ") tq_jit_main(const __grid_constant__ "
           "tq::PipeParams p) {\n  tq::pipe_body<"
@@ -609,17 +635,20 @@ cudaError_t launch_pipeline_prog(tq_ctx* c, int sink, const PipeParams& p, u32 s
     }
     {
       if (e.ok) {
-        cudaError_t err = cudaFuncSetAttribute((const void*)e.kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem);
+        cudaError_t err = cudaSuccess;
+        if (sink < SINK_COUNT_DIRECT)
+          err = cudaFuncSetAttribute((const void*)e.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err != cudaSuccess) return err;
         PipeParams pp = p;
         void* args[] = {&pp};
-        err = cudaLaunchKernel((const void*)e.kern, dim3(grid), dim3(kBlock), args, smem, st);
+        err = cudaLaunchKernel((const void*)e.kern, dim3(grid), dim3(sink >= SINK_COUNT_DIRECT ? 256 : kBlock), args,
+                               sink >= SINK_COUNT_DIRECT ? 0 : smem, st);
         if (err == cudaSuccess) c->jit_launches.fetch_add(1);
         return err;
       }
     }
   }
+  if (sink >= SINK_COUNT_DIRECT) return cudaErrorNotSupported;  // generated code only: the caller uses SINK_COUNT
   return launch_interp(sink, p, smem, grid, st);
 }
 

@@ -504,6 +504,110 @@ __device__ __forceinline__ void chunk_reserve(ChunkCursor* cc, u32 m, unsigned l
 // named barrier over the consumer warps only
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory"); }
 
+// ------------------------------------------------------------------ COUNT without the stage ring
+// The COUNT pass of a two-pass FILTER / PARTITION reads only the predicate and
+// key columns (often one 8-B column).  Through the TMA stage ring that is 4 KB
+// per 512-row tile and the per-tile barrier / issue overhead, not HBM, bounds it
+// (~1.7 TB/s).  Here every warp reads its 32-row slices straight from global
+// memory (coalesced, U slices in flight per warp), runs the same generated
+// predicate / keys / LIP check on registers (P::load_g, generated policies
+// only) and writes the same per-slice counts the pipeline's COUNT sink writes
+// (slice = row / 32, counts[d * nslices + slice]), so the EMIT pass is unchanged.
+// One mode per generated kernel (the host picks it: SINK_COUNT_DIRECT + mode,
+// part of the JIT cache key): no per-slice branches on the destination kind,
+// the LIP filter or the destination count's class.
+template <class P, int MODE>
+__device__ __forceinline__ void count_direct_loop(const PipeParams& p) {
+#ifndef TQ_CD_U
+#define TQ_CD_U 4
+#endif
+  constexpr int U = TQ_CD_U;  // slices in flight per warp; their counts leave as 16-B stores per destination
+  static_assert(U % 4 == 0 && kWarps % U == 0, "nslices must be a multiple of U, U of 4");
+  __shared__ u32 s_wc[8][kMaxDest];  // CD_PART_MANY: per-warp counters (blockDim 256)
+  const u32 lane = threadIdx.x & 31;
+  u32* wc = s_wc[threadIdx.x >> 5];
+  if (MODE == CD_PART_MANY) {
+    for (u32 d = lane; d < kMaxDest; d += 32) wc[d] = 0;
+    __syncwarp();
+  }
+  const u64 gw = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u64 nw = ((u64)gridDim.x * blockDim.x) >> 5;
+  const u64 nslices = (u64)p.ntiles * kWarps;  // padded like the pipeline's: empty slices count 0
+  const u32 ndest = p.ndest;
+  const u32 dbits = ndest > 1 ? 32u - (u32)__clz((int)(ndest - 1)) : 0u;
+  WCtx w;
+  w.p = &p;
+  w.stage = nullptr;
+  w.lits = p.lits;
+  w.vslot = nullptr;
+  w.vvalid = nullptr;
+  w.bslot = nullptr;
+  w.row0 = 0;
+  w.lane = lane;
+  w.out_delta = 0;
+  w.vmask = kFull;
+  for (u64 s0 = gw * U; s0 < nslices; s0 += nw * U) {
+    typename P::Raw raw[U];
+    // rows past the end re-read the last row (no branch around the loads, so
+    // the ballots below need no divergence handling); tile_begin masks them
+#pragma unroll
+    for (int u = 0; u < U; ++u) P::load_g(w, min((u64)((s0 + u) * 32 + lane), (u64)(p.rows - 1)), raw[u]);
+    u32 cnt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const u64 r0 = (s0 + u) * 32;
+      w.nrows = r0 < p.rows ? (u32)min((u64)32, p.rows - r0) : 0u;
+      u32 pm = 0;
+      P::tile_begin(w, nullptr, &pm, &raw[u]);
+      if (MODE == CD_FILTER) {
+        cnt[u] = (u32)__popc(pm);
+        continue;
+      }
+      bool pass = (pm >> lane) & 1u;
+      // every lane hashes its row (no divergent branch); non-passing lanes are masked below
+      u64 kw[kMaxKeyWords + 1];
+      const bool has_null = P::keys(w, 0, kw, raw[u]);
+      const u32 dest = partition_of_p<P>(p, kw);
+      if (MODE == CD_PART_FEW_LIP && pass) {  // LIP, as the pipeline's COUNT sink
+        const u64 hb = key_hash(kw, P::kKw > 0 ? P::kKw : (int)p.key_words);
+        const u32 bb = bloom_bits(hb);
+        const uint32_t* sb = p.semi_bloom + (u64)dest * p.semi_part_words;
+        if (has_null || (__ldg(sb + bloom_word(hb, p.semi_mask)) & bb) != bb) pass = false;
+      }
+      if (MODE != CD_PART_MANY) {
+        // lane d's rows = passing rows whose destination bits equal d's: one
+        // ballot per destination bit (log2 ndest <= 5), one popc
+        // (ballots outside any branch: no divergence-safe collective code)
+        u32 m = __ballot_sync(kFull, pass);
+#pragma unroll
+        for (u32 b = 0; b < 5; ++b) {
+          const u32 bb = __ballot_sync(kFull, (dest >> b) & 1u);
+          m &= b >= dbits ? ~0u : ((lane >> b) & 1u) ? bb : ~bb;
+        }
+        cnt[u] = (u32)__popc(m);
+      } else {
+        const u32 peers = __match_any_sync(kFull, pass ? dest : 0xffffffffu);
+        if (pass && (peers & lanemask_lt()) == 0) wc[dest] += (u32)__popc(peers);
+        __syncwarp();
+        for (u32 d = lane; d < ndest; d += 32) {
+          p.tile_counts[(u64)d * nslices + s0 + u] = wc[d];
+          wc[d] = 0;
+        }
+        __syncwarp();
+      }
+    }
+    if (MODE != CD_PART_MANY) {
+      const u32 nd = MODE == CD_FILTER ? 1u : ndest;
+      if (lane < nd) {
+#pragma unroll
+        for (int j = 0; j < U; j += 4)
+          *(uint4*)(p.tile_counts + (u64)lane * nslices + s0 + j) =
+              make_uint4(cnt[j], cnt[j + 1], cnt[j + 2], cnt[j + 3]);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ the kernel body
 template <int SINK, class P>
 __device__ __forceinline__ void pipe_body(const PipeParams& p) {

@@ -77,13 +77,27 @@ __device__ __forceinline__ u64 block_excl_scan(u64 v, u64* s_warp, u64& total) {
   return r;
 }
 
+// a thread's kScanItems (8) consecutive counts: two 16-B loads when whole and
+// aligned (the scans of a 15M-slice partition count are bandwidth-bound)
+__device__ __forceinline__ void scan_load8(const u32* in, u64 n, u64 base, u32* v) {
+  static_assert(kScanItems == 8, "two uint4 per thread");
+  if (base + 8 <= n && ((uintptr_t)(in + base) & 15) == 0) {
+    const uint4 a = __ldg((const uint4*)(in + base)), b = __ldg((const uint4*)(in + base) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = base + i < n ? in[base + i] : 0;
+  }
+}
+
 __global__ void k_scan_partials(const u32* in, u64 n, u64* partial) {
   __shared__ u64 s[24];
   u64 base = (u64)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
   u64 sum = 0;
+  u32 v[kScanItems];
+  scan_load8(in, n, base, v);
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i)
-    if (base + i < n) sum += in[base + i];
+  for (int i = 0; i < kScanItems; ++i) sum += v[i];
   u64 tot;
   block_excl_scan(sum, s, tot);
   if (threadIdx.x == 0) partial[blockIdx.x] = tot;
@@ -108,13 +122,19 @@ __global__ void k_scan_apply(const u32* in, u64 n, const u64* partial, u64* out)
   u64 base = (u64)blockIdx.x * kScanBlock + threadIdx.x * kScanItems;
   u32 v[kScanItems];
   u64 sum = 0;
+  scan_load8(in, n, base, v);
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    v[i] = base + i < n ? in[base + i] : 0;
-    sum += v[i];
-  }
+  for (int i = 0; i < kScanItems; ++i) sum += v[i];
   u64 tot;
   u64 run = partial[blockIdx.x] + block_excl_scan(sum, s, tot);
+  if (base + 8 <= n && ((uintptr_t)(out + base) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < kScanItems; i += 2) {
+      *(ulonglong2*)(out + base + i) = make_ulonglong2(run, run + v[i]);
+      run += v[i] + v[i + 1];
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i)
     if (base + i < n) {
@@ -349,6 +369,35 @@ static void launch(tq_ctx* c, int sink, Plan& L, const Prog& P, cudaStream_t st)
   TQ_CUDA(launch_pipeline_prog(c, sink, L.p, L.smem, L.grid, st, P.pb.code(), P.pb.lits()));
   prof_end(c, h, st);
   counted_launch(c);
+}
+
+// COUNT pass of a two-pass FILTER / PARTITION: the generated predicate / keys
+// over plain coalesced loads (count_direct_body) instead of the stage ring;
+// falls back to the pipeline's COUNT sink when there is no generated code.
+// TQ_COUNT_DIRECT=0: always the pipeline (A/B measurements).
+static void launch_count(tq_ctx* c, Plan& L, const Prog& P, cudaStream_t st) {
+  static const bool on = [] {
+    const char* e = getenv("TQ_COUNT_DIRECT");
+    return !(e && e[0] == '0');
+  }();
+  if (L.p.ntiles == 0) return;
+  if (on && kV == 1 && (L.p.dest_kind == DEST_FILTER || L.p.dest_kind == DEST_PARTITION)) {
+    TQ_HT("launch(count_direct)");
+    int h = prof_begin(c, "count_direct", st);
+    const int mode = L.p.dest_kind == DEST_FILTER ? CD_FILTER
+                     : L.p.ndest > 32             ? CD_PART_MANY
+                     : L.p.semi_bloom             ? CD_PART_FEW_LIP
+                                                  : CD_PART_FEW;
+    const cudaError_t e = launch_pipeline_prog(c, SINK_COUNT_DIRECT + mode, L.p, 0, (u32)c->sms * 8, st,
+                                               P.pb.code(), P.pb.lits());
+    prof_end(c, h, st);
+    if (e == cudaSuccess) {
+      counted_launch(c);
+      return;
+    }
+    if (e != cudaErrorNotSupported) TQ_CUDA(e);
+  }
+  launch(c, SINK_COUNT, L, P, st);
 }
 
 static void set_keys(PipeParams& p, const ProgramBuilder& pb, const std::vector<int>& handles) {
@@ -767,7 +816,7 @@ two_pass:
       if (P.has_pred) need.push_back(P.pred_h);
       const u32 all = p.load_mask;
       p.load_mask = P.pb.column_deps(need);
-      launch(c, SINK_COUNT, L, P, st);
+      launch_count(c, L, P, st);
       p.load_mask = all;
     }
     scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
@@ -2585,7 +2634,7 @@ tq_status tq_pipeline_estimate(tq_ctx* c, const tq_batch* in, const tq_expr* pre
       u64* offsets = (u64*)dalloc(c, (ncnt + 1) * 8, st);
       p.tile_counts = counts;
       p.load_mask = P.pb.column_deps({P.pred_h});
-      launch(c, SINK_COUNT, L, P, st);
+      launch_count(c, L, P, st);
       scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
       {
         TQ_CUDA(cudaMemcpyAsync(pinned_scratch(c), offsets + ncnt, 8, cudaMemcpyDeviceToHost, st));
