@@ -546,6 +546,8 @@ __device__ __forceinline__ void count_direct_loop(const PipeParams& p) {
   w.lane = lane;
   w.out_delta = 0;
   w.vmask = kFull;
+  // CD_PROBE: the build's exact membership bitmap replaces the Bloom pre-check
+  const bool exact = MODE == CD_PROBE && p.jt.exact_flag && *p.jt.exact_flag == 0;
   for (u64 s0 = gw * U; s0 < nslices; s0 += nw * U) {
     typename P::Raw raw[U];
     // rows past the end re-read the last row (no branch around the loads, so
@@ -564,6 +566,17 @@ __device__ __forceinline__ void count_direct_loop(const PipeParams& p) {
         continue;
       }
       bool pass = (pm >> lane) & 1u;
+      if (MODE == CD_PROBE) {  // output rows = matches per probe row (null keys never match)
+        u32 mult = 0;
+        if (pass) {
+          u64 kw[kMaxKeyWords + 1];
+          if (!P::keys(w, 0, kw, raw[u])) mult = jt_probe_count<P::kKw>(p.jt, kw, exact);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mult += __shfl_xor_sync(kFull, mult, o);
+        cnt[u] = mult;
+        continue;
+      }
       // every lane hashes its row (no divergent branch); non-passing lanes are masked below
       u64 kw[kMaxKeyWords + 1];
       const bool has_null = P::keys(w, 0, kw, raw[u]);
@@ -597,7 +610,7 @@ __device__ __forceinline__ void count_direct_loop(const PipeParams& p) {
       }
     }
     if (MODE != CD_PART_MANY) {
-      const u32 nd = MODE == CD_FILTER ? 1u : ndest;
+      const u32 nd = MODE == CD_FILTER || MODE == CD_PROBE ? 1u : ndest;
       if (lane < nd) {
 #pragma unroll
         for (int j = 0; j < U; j += 4)

@@ -381,10 +381,12 @@ static void launch_count(tq_ctx* c, Plan& L, const Prog& P, cudaStream_t st) {
     return !(e && e[0] == '0');
   }();
   if (L.p.ntiles == 0) return;
-  if (on && kV == 1 && (L.p.dest_kind == DEST_FILTER || L.p.dest_kind == DEST_PARTITION)) {
+  if (on && kV == 1 &&
+      (L.p.dest_kind == DEST_FILTER || L.p.dest_kind == DEST_PARTITION || L.p.dest_kind == DEST_PROBE)) {
     TQ_HT("launch(count_direct)");
     int h = prof_begin(c, "count_direct", st);
-    const int mode = L.p.dest_kind == DEST_FILTER ? CD_FILTER
+    const int mode = L.p.dest_kind == DEST_FILTER  ? CD_FILTER
+                     : L.p.dest_kind == DEST_PROBE ? CD_PROBE
                      : L.p.ndest > 32             ? CD_PART_MANY
                      : L.p.semi_bloom             ? CD_PART_FEW_LIP
                                                   : CD_PART_FEW;
@@ -1104,7 +1106,8 @@ static void run_partition_exchange(tq_ctx* c, tq_comm* cm, const tq_batch* in, P
 // direct aggregation's range pass when there is no predicate: 16-B loads,
 // one set of atomics per block.
 // out[3] != 0: the column is NOT non-decreasing (or has a null).
-__global__ void __launch_bounds__(256) k_key_range(const long long* v, const uint8_t* valid, u64 rows, long long* out) {
+template <int MB>
+__global__ void __launch_bounds__(256, MB) k_key_range(const long long* v, const uint8_t* valid, u64 rows, long long* out) {
   __shared__ long long s_mn[8], s_mx[8];
   __shared__ int s_null, s_unsorted;
   if (threadIdx.x == 0) s_null = s_unsorted = 0;
@@ -1180,6 +1183,20 @@ __global__ void __launch_bounds__(256) k_key_range(const long long* v, const uin
   }
 }
 
+// occupancy of the range pass: 6 CTAs per SM (<= 42 registers, a 28-B spill)
+// measured 0.116-0.122 ms vs 0.129-0.134 at 4 (63 registers) on SF10 orderkey
+// (TQ_KR_MB: experiments only)
+static void launch_key_range(tq_ctx* c, cudaStream_t st, const long long* v, const uint8_t* valid, u64 rows,
+                             long long* out) {
+  static const int mb = [] {
+    const char* e = getenv("TQ_KR_MB");
+    return e ? atoi(e) : 6;
+  }();
+  if (mb == 6) k_key_range<6><<<c->sms * 6, 256, 0, st>>>(v, valid, rows, out);
+  else if (mb == 5) k_key_range<5><<<c->sms * 5, 256, 0, st>>>(v, valid, rows, out);
+  else k_key_range<4><<<c->sms * 4, 256, 0, st>>>(v, valid, rows, out);
+}
+
 static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<uint32_t>& key_roots,
                       tq_join_table** out, cudaStream_t st, uint64_t bloom_keys, bool semi_only, bool allow_direct) {
   Plan L;
@@ -1244,7 +1261,7 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
       long long* kr = (long long*)dalloc(c, 32, st);
       const long long init[4] = {0x7fffffffffffffffll, (long long)0x8000000000000000ull, 0, 0};
       TQ_CUDA(cudaMemcpyAsync(kr, init, 32, cudaMemcpyHostToDevice, st));
-      k_key_range<<<c->sms * 4, 256, 0, st>>>((const long long*)col.values, col.validity, in->rows, kr);
+      launch_key_range(c, st, (const long long*)col.values, col.validity, in->rows, kr);
       counted_launch(c);
       long long* pin = (long long*)pinned_scratch(c);
       TQ_CUDA(cudaMemcpyAsync(pin, kr, 16, cudaMemcpyDeviceToHost, st));
@@ -1373,6 +1390,9 @@ __device__ __forceinline__ bool agg_slot_used(const FinalParams& f, u64 s) {
   return s < f.t.cap && (f.direct ? __ldg(direct_acc(f.t, f.cnt_acc, s)) != 0 : __ldg(f.t.state + s) == 2);
 }
 __device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 row);
+__device__ __forceinline__ void agg_emit_keys(const FinalParams& f, u64 s, u64 row);
+__device__ __forceinline__ void agg_store_value(const FinalParams& f, const AggOut& ao, u64 row, u64 m0, u64 m1,
+                                                u64 cnt);
 
 // Compaction of the occupied slots into output rows, in slot order.  A block
 // takes chunks of kFinItems x 256 contiguous slots; item i of thread t is slot
@@ -1427,16 +1447,44 @@ __global__ void __launch_bounds__(256) k_agg_final(const __grid_constant__ Final
     const u64 base = s_base;
     // (4 items unrolled: independent accumulator loads in flight; 16 unrolled
     // copies of the emit body stalled on instruction fetch)
+    if (f.direct && f.naggs == 1) {
+      // one aggregate over a direct table (e.g. a high-cardinality Sum): the
+      // accumulator words of all kFinItems slots are loaded (predicated, no
+      // branch) before any store, so their latencies overlap instead of
+      // serialising item by item
+      const AggOut& ao = f.aggs[0];
+      const bool two = f.t.dwidth[ao.acc] >= 2;
+      u64 m0[kFinItems], m1[kFinItems], cn[kFinItems];
 #pragma unroll
-    for (u32 i = 0; i < kFinItems; ++i) {
-      const u32 b = s_ball[i][warp];
-      if ((b >> lane) & 1u) agg_emit_group(f, s0 + (u64)i * 256, base + s_off[i][warp] + __popc(b & lanemask_lt()));
+      for (u32 i = 0; i < kFinItems; ++i) {
+        const bool occ = (s_ball[i][warp] >> lane) & 1u;
+        const u64 sl = occ ? s0 + (u64)i * 256 : 0;
+        const u64* src = direct_acc(f.t, ao.acc, sl);
+        m0[i] = occ ? __ldg(src) : 0ull;
+        m1[i] = occ && two ? __ldg(src + 1) : 0ull;
+        cn[i] = ao.cnt == 0xff ? 1ull : occ ? __ldg(direct_acc(f.t, ao.cnt, sl)) : 0ull;
+      }
+#pragma unroll
+      for (u32 i = 0; i < kFinItems; ++i) {
+        const u32 b = s_ball[i][warp];
+        if ((b >> lane) & 1u) {
+          const u64 row = base + s_off[i][warp] + __popc(b & lanemask_lt());
+          agg_emit_keys(f, s0 + (u64)i * 256, row);
+          agg_store_value(f, ao, row, m0[i], m1[i], cn[i]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (u32 i = 0; i < kFinItems; ++i) {
+        const u32 b = s_ball[i][warp];
+        if ((b >> lane) & 1u) agg_emit_group(f, s0 + (u64)i * 256, base + s_off[i][warp] + __popc(b & lanemask_lt()));
+      }
     }
     __syncthreads();  // s_off / s_base are rewritten next chunk
   }
 }
 
-__device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 row) {
+__device__ __forceinline__ void agg_emit_keys(const FinalParams& f, u64 s, u64 row) {
   u64 dk[2] = {(u64)f.key_min + s, s == f.null_slot ? 1ull : 0ull};  // direct: key word, null word
   const u64* kw = f.direct ? dk : f.t.keys + s * f.kwa;
   u64 nullw = kw[f.kwa - 1];
@@ -1453,20 +1501,19 @@ __device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 
     }
     if (ko.validity && !isnull) bm_set_atomic(ko.validity, row);
   }
-  const u64* acc = f.t.acc + s * f.nacc * 2;
-  for (u32 a = 0; a < f.naggs; ++a) {
-    const AggOut& ao = f.aggs[a];
-    // read-only in this kernel: non-coherent loads, which the compiler may
-    // issue ahead of the previous group's stores (they cannot alias)
-    const u64* src = f.direct ? direct_acc(f.t, ao.acc, s) : acc + 2 * ao.acc;
-    u64 m[2] = {__ldg(src), (f.direct && f.t.dwidth[ao.acc] < 2) ? 0ull : __ldg(src + 1)};
-    if (f.direct && (ao.kind == AO_SUM_I64 || ao.kind == AO_SUM_DEC || ao.kind == AO_AVG_I)) {
-      // direct table: integer sums are kept as {low-limb sum, high-part sum}
-      const i128 v = add128((i128)(long long)m[1] * ((i128)1 << 32), (i128)m[0]);
-      m[0] = lo64(v);
-      m[1] = hi64(v);
-    }
-    u64 cnt = ao.cnt == 0xff ? 1 : __ldg(f.direct ? direct_acc(f.t, ao.cnt, s) : acc + 2 * ao.cnt);
+}
+
+// one aggregate's output at `row` from its raw accumulator words and count
+__device__ __forceinline__ void agg_store_value(const FinalParams& f, const AggOut& ao, u64 row, u64 m0, u64 m1,
+                                                u64 cnt) {
+  u64 m[2] = {m0, m1};
+  if (f.direct && (ao.kind == AO_SUM_I64 || ao.kind == AO_SUM_DEC || ao.kind == AO_AVG_I)) {
+    // direct table: integer sums are kept as {low-limb sum, high-part sum}
+    const i128 v = add128((i128)(long long)m[1] * ((i128)1 << 32), (i128)m[0]);
+    m[0] = lo64(v);
+    m[1] = hi64(v);
+  }
+  {
     bool valid = cnt != 0;
     switch (ao.kind) {
       case AO_SUM_I64:
@@ -1501,6 +1548,20 @@ __device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 
       }
     }
     if (ao.validity && valid) bm_set_atomic(ao.validity, row);
+  }
+}
+
+__device__ __forceinline__ void agg_emit_group(const FinalParams& f, u64 s, u64 row) {
+  agg_emit_keys(f, s, row);
+  const u64* acc = f.t.acc + s * f.nacc * 2;
+  for (u32 a = 0; a < f.naggs; ++a) {
+    const AggOut& ao = f.aggs[a];
+    // read-only in this kernel: non-coherent loads, which the compiler may
+    // issue ahead of the previous group's stores (they cannot alias)
+    const u64* src = f.direct ? direct_acc(f.t, ao.acc, s) : acc + 2 * ao.acc;
+    const u64 m0 = __ldg(src), m1 = (f.direct && f.t.dwidth[ao.acc] < 2) ? 0ull : __ldg(src + 1);
+    const u64 cnt = ao.cnt == 0xff ? 1 : __ldg(f.direct ? direct_acc(f.t, ao.cnt, s) : acc + 2 * ao.cnt);
+    agg_store_value(f, ao, row, m0, m1, cnt);
   }
 }
 
@@ -1679,7 +1740,7 @@ static void agg_core(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<i
         const tq_column& col = in->cols[P.pb.staged()[ko.idx]];
         TQ_CUDA(cudaMemsetAsync(kr + 3, 0, 8, st));
         const int ph = prof_begin(c, "key_range", st);
-        k_key_range<<<c->sms * 4, 256, 0, st>>>((const long long*)col.values, in->rows ? col.validity : nullptr,
+        launch_key_range(c, st, (const long long*)col.values, in->rows ? col.validity : nullptr,
                                                  in->rows, kr);
         prof_end(c, ph, st);
         counted_launch(c);

@@ -39,7 +39,7 @@ constexpr int kChunk = 512;  // DEST_PROBE1 output rows a CTA reserves per globa
 enum SinkKind { SINK_COUNT = 0, SINK_EMIT = 1, SINK_AGG = 2, SINK_BUILD = 3,
                 SINK_COUNT_DIRECT = 4 };  // + CdMode: COUNT without the stage ring (generated code only)
 // count_direct_loop modes
-enum CdMode { CD_FILTER = 0, CD_PART_FEW = 1, CD_PART_FEW_LIP = 2, CD_PART_MANY = 3 };
+enum CdMode { CD_FILTER = 0, CD_PART_FEW = 1, CD_PART_FEW_LIP = 2, CD_PART_MANY = 3, CD_PROBE = 4 };
 // FILTER/PARTITION/PROBE: two passes (COUNT then EMIT), stable order.
 // PROBE1: single EMIT pass for unique build keys (<= 1 match per row);
 //         output rows are reserved with a warp-aggregated atomic cursor.
