@@ -28,6 +28,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <string_view>
 #include <unordered_map>
 #include <vector>
 
@@ -883,7 +884,70 @@ OBatch agg_output(const BV& in, const KeySpec& ks, const std::vector<AggInfo>& a
 }
 
 OBatch aggregate_exec(const BV& in, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs, uint32_t naggs,
+                      int naive, uint32_t nthreads);
+
+// Utf8 group keys (groups are equal key VALUES, a string by its
+// bytes): each Utf8 key column is interned to the row index of its string's first
+// occurrence (exact byte equality; a null string stays null), the aggregate runs
+// on those ids, and each output key column takes the strings back at the ids with
+// take (its bitmap iff the input column had one, transform.cpp:90-120).
+OBatch aggregate_utf8_keys(const BV& in, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs, uint32_t naggs,
+                           int naive, uint32_t nthreads) {
+  for (uint32_t j = 0; j < naggs; ++j)
+    if (aggs[j].fn != TQ_AGG_COUNT_STAR && aggs[j].column < in.cols.size() &&
+        in.cols[aggs[j].column].kind == TQ_UTF8)
+      fail(TQ_INVALID_PLAN, "utf8 aggregate unsupported");
+  BV ids_in = in;
+  std::vector<std::vector<int64_t>> ids(in.cols.size());
+  std::vector<uint64_t> null_row(in.cols.size(), 0);
+  for (uint32_t k = 0; k < nkeys; ++k) {
+    const uint32_t col = keys[k];
+    if (col >= in.cols.size()) fail(TQ_INVALID_PLAN, "key column out of range");
+    const CV& c = in.cols[col];
+    if (c.kind != TQ_UTF8 || !ids[col].empty()) continue;
+    std::unordered_map<std::string_view, int64_t> first;
+    ids[col].assign(std::max<uint64_t>(1, in.rows), 0);
+    for (uint64_t r = 0; r < in.rows; ++r) {
+      if (!c.valid(r)) {
+        null_row[col] = r;
+        continue;
+      }
+      std::string_view sv(reinterpret_cast<const char*>(c.values) + c.offsets[r], size_t(c.offsets[r + 1] - c.offsets[r]));
+      ids[col][r] = first.emplace(sv, int64_t(r)).first->second;
+    }
+    CV v;
+    v.kind = TQ_INT64;
+    v.values = reinterpret_cast<const uint8_t*>(ids[col].data());
+    v.values_bytes = in.rows * 8;
+    v.validity = c.validity;
+    ids_in.cols[col] = v;
+  }
+  OBatch o = aggregate_exec(ids_in, keys, nkeys, aggs, naggs, naive, nthreads);
+  for (uint32_t k = 0; k < nkeys; ++k) {
+    const uint32_t col = keys[k];
+    if (in.cols[col].kind != TQ_UTF8) continue;
+    const OCol& kc = o.cols[k];
+    std::vector<uint64_t> at(o.rows);
+    for (uint64_t g = 0; g < o.rows; ++g) {
+      const bool valid = !kc.has_valid || bit_get(kc.validity.data(), g);
+      int64_t id = 0;
+      std::memcpy(&id, &kc.values[g * 8], 8);
+      at[g] = valid ? uint64_t(id) : null_row[col];
+    }
+    BV one;
+    one.rows = in.rows;
+    one.cols.push_back(in.cols[col]);
+    OBatch t = take(one, at.data(), at.size());
+    o.cols[k] = std::move(t.cols[0]);
+  }
+  return o;
+}
+
+OBatch aggregate_exec(const BV& in, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs, uint32_t naggs,
                       int naive, uint32_t nthreads) {
+  for (uint32_t k = 0; k < nkeys; ++k)
+    if (keys[k] < in.cols.size() && in.cols[keys[k]].kind == TQ_UTF8)
+      return aggregate_utf8_keys(in, keys, nkeys, aggs, naggs, naive, nthreads);
   KeySpec ks = key_spec(in, keys, nkeys);
   std::vector<AggInfo> ai = agg_infos(in, aggs, naggs);
   if (naive) {  // SPEC.md:699 style: linear search over materialised groups

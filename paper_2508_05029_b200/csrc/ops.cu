@@ -1985,6 +1985,14 @@ static void run_aggregate(tq_ctx* c, const tq_batch* in, Prog& P, const uint32_t
   agg_core(c, in, P, key_handles(P, keys, nkeys), S.acc, &S.ap, out, st);
 }
 
+// aggregate_execute over fixed-width key columns (every input column projected)
+void run_aggregate_plain(tq_ctx* c, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs,
+                         uint32_t naggs, tq_batch* out, cudaStream_t st) {
+  Prog P(schema_of(in));
+  compile_prog(P, in, nullptr, nullptr, 0, true);
+  run_aggregate(c, in, P, keys, nkeys, aggs, naggs, out, st);
+}
+
 // ================================================================== take / concat / slice
 // dst already points at the first destination row; validity bits land at
 // dbit + i of dvalid (bitmap zeroed by the allocator).
@@ -2464,6 +2472,145 @@ void utf8_raise(tq_ctx* c, const tq_batch* in, const std::vector<int>& src, uint
   out->ncols = std::min(out->ncols, keep);
 }
 
+// ---- Utf8 group keys (aggregate_execute: a group is one key
+// VALUE, a string by its bytes).  The kernels group fixed-width words, so each
+// Utf8 key column is replaced by the fnv1a64 of its bytes (a null string stays
+// null) and every group also takes MIN(row id), a representative row whose
+// string becomes the output key (take, transform.cpp:90-120).  Grouping by the
+// hash equals grouping by the string iff no two different strings share a hash:
+// that is CHECKED, not assumed — one row per hash (MIN(row id) by hash) is
+// joined back to every row and the bytes are compared; a collision fails the
+// operator (Internal) instead of merging two groups.
+
+// flag = 1 if the strings at rows a[i] and b[i] differ, for any i
+__global__ void k_utf8_pairs_differ(const uint8_t* bytes, const int32_t* off, const long long* a,
+                                    const long long* b, u64 n, u32* flag) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const long long x = a[i], y = b[i];
+    if (x == y) continue;
+    const int32_t x0 = off[x], xl = off[x + 1] - x0, y0 = off[y], yl = off[y + 1] - y0;
+    bool diff = xl != yl;
+    for (int32_t j = 0; !diff && j < xl; ++j) diff = bytes[x0 + j] != bytes[y0 + j];
+    if (diff) atomicOr(flag, 1u);
+  }
+}
+
+static void status_check(tq_status s) {
+  if (s != TQ_OK) fail(s, tq_last_error());
+}
+
+struct DevBufs {  // scratch buffers freed on every exit path
+  tq_ctx* c;
+  cudaStream_t st;
+  std::vector<std::pair<void*, uint64_t>> v;
+  void* get(uint64_t bytes) {
+    v.push_back({dalloc(c, bytes, st), bytes});
+    return v.back().first;
+  }
+  ~DevBufs() {
+    for (auto& b : v) dfree(c, b.first, b.second, st);
+  }
+};
+
+// every non-null row's string equals the string of the first row with its hash
+static void check_utf8_hash_unique(tq_ctx* c, const tq_batch* in, const tq_batch* aug, uint32_t col, uint32_t rid,
+                                   cudaStream_t st, DevBufs& B) {
+  tq_batch reps{};  // [hash, MIN(row id)] per distinct hash
+  const tq_agg mn{TQ_AGG_MIN, rid};
+  run_aggregate_plain(c, aug, &col, 1, &mn, 1, &reps, st);
+  tq_join_table* jt = nullptr;
+  tq_batch pairs{};
+  const uint32_t k0 = 0;
+  try {
+    status_check(tq_join_build(c, &reps, &k0, 1, &jt, st));
+    tq_column pc[2] = {aug->cols[col], aug->cols[rid]};
+    tq_batch probe{aug->rows, 2, TQ_MEM_DEVICE, pc, nullptr};
+    status_check(tq_join_probe(c, jt, &probe, &k0, 1, &pairs, st));  // [hash, rep, hash, row id]
+    u32* flag = (u32*)B.get(4);
+    TQ_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+    if (pairs.rows) {
+      const tq_column& s = in->cols[col];
+      k_utf8_pairs_differ<<<grid_for(c, pairs.rows), 256, 0, st>>>(
+          (const uint8_t*)s.values, s.offsets, (const long long*)pairs.cols[1].values,
+          (const long long*)pairs.cols[3].values, pairs.rows, flag);
+      counted_launch(c);
+      TQ_CUDA(cudaGetLastError());
+    }
+    u32* pin = (u32*)pinned_scratch(c);
+    TQ_CUDA(cudaMemcpyAsync(pin, flag, 4, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaStreamSynchronize(st));
+    if (pin[0]) fail(TQ_INTERNAL, "utf8 group key: two different strings share a 64-bit hash (aggregate refused)");
+  } catch (...) {
+    if (pairs.cols) tq_batch_free(c, &pairs);
+    if (jt) tq_join_table_destroy(c, jt);
+    tq_batch_free(c, &reps);
+    throw;
+  }
+  tq_batch_free(c, &pairs);
+  tq_join_table_destroy(c, jt);
+  tq_batch_free(c, &reps);
+}
+
+void aggregate_utf8_keys(tq_ctx* c, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, const tq_agg* aggs,
+                         uint32_t naggs, tq_batch* out, cudaStream_t st) {
+  for (uint32_t a = 0; a < naggs; ++a)
+    if (aggs[a].fn != TQ_AGG_COUNT_STAR && aggs[a].column < in->ncols && in->cols[aggs[a].column].kind == TQ_UTF8)
+      fail(TQ_INVALID_PLAN, "utf8 aggregate unsupported");
+  const uint64_t rows = in->rows, bytes = std::max<uint64_t>(8, rows * 8);
+  DevBufs B{c, st, {}};
+  u64* rid = (u64*)B.get(bytes);
+  k_iota<<<grid_for(c, rows), 256, 0, st>>>(rid, rows);
+  counted_launch(c);
+  tq_column rc{};
+  rc.kind = TQ_INT64;
+  rc.values = rid;
+  rc.values_bytes = rows * 8;
+  std::vector<tq_column> cols(in->cols, in->cols + in->ncols);
+  std::vector<uint32_t> hashed;
+  std::vector<int> src(nkeys + naggs, -1);  // output key column j -> its Utf8 input column
+  for (uint32_t k = 0; k < nkeys; ++k) {
+    const uint32_t col = keys[k];
+    if (col >= in->ncols) fail(TQ_INVALID_PLAN, "key column out of range");
+    if (in->cols[col].kind != TQ_UTF8) continue;
+    src[k] = (int)col;
+    if (std::find(hashed.begin(), hashed.end(), col) != hashed.end()) continue;
+    HashKeys K{};
+    K.n = 1;
+    K.k[0] = HashKeyCol{(const uint8_t*)in->cols[col].values, in->cols[col].offsets,
+                        rows ? in->cols[col].validity : nullptr, 0u};
+    u64* h = (u64*)B.get(bytes);
+    k_partition_hash<<<grid_for(c, rows), 256, 0, st>>>(K, rows, h);
+    counted_launch(c);
+    tq_column hc{};
+    hc.kind = TQ_INT64;
+    hc.values = h;
+    hc.values_bytes = rows * 8;
+    hc.validity = rows ? in->cols[col].validity : nullptr;
+    cols[col] = hc;
+    hashed.push_back(col);
+  }
+  for (auto& col : cols)  // Utf8 columns no key or aggregate reads: fixed-width stand-ins
+    if (col.kind == TQ_UTF8) col = rc;
+  TQ_CUDA(cudaGetLastError());
+  const uint32_t ridc = (uint32_t)cols.size();
+  cols.push_back(rc);
+  tq_batch aug = *in;
+  aug.ncols = (uint32_t)cols.size();
+  aug.cols = cols.data();
+  aug.owner = nullptr;
+  for (uint32_t col : hashed) check_utf8_hash_unique(c, in, &aug, col, ridc, st, B);
+  std::vector<tq_agg> ag(aggs, aggs + naggs);
+  ag.push_back(tq_agg{TQ_AGG_MIN, ridc});
+  run_aggregate_plain(c, &aug, keys, nkeys, ag.data(), (uint32_t)ag.size(), out, st);
+  // the representative row ids into the Utf8 key columns, then gather their strings
+  const tq_column& rep = out->cols[out->ncols - 1];
+  for (uint32_t k = 0; k < nkeys; ++k)
+    if (src[k] >= 0 && out->rows)
+      TQ_CUDA(cudaMemcpyAsync(out->cols[k].values, rep.values, out->rows * 8, cudaMemcpyDeviceToDevice, st));
+  src.resize(out->ncols, -1);
+  utf8_raise(c, in, src, out->ncols - 1, out, st);
+}
+
 }  // namespace tq
 
 // ================================================================== operator entry points
@@ -2764,9 +2911,12 @@ tq_status tq_aggregate(tq_ctx* c, const tq_batch* in, const uint32_t* keys, uint
                        uint32_t naggs, tq_batch* out, void* stream) {
   return guard([&] {
     check_device_batch(in);
-    Prog P(schema_of(in));
-    compile_all(P, in, nullptr);
-    run_aggregate(c, in, P, keys, nkeys, aggs, naggs, out, pick(c, stream));
+    for (uint32_t k = 0; k < nkeys; ++k)
+      if (keys[k] < in->ncols && in->cols[keys[k]].kind == TQ_UTF8) {
+        aggregate_utf8_keys(c, in, keys, nkeys, aggs, naggs, out, pick(c, stream));
+        return;
+      }
+    run_aggregate_plain(c, in, keys, nkeys, aggs, naggs, out, pick(c, stream));
   });
 }
 

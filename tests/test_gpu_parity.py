@@ -432,3 +432,37 @@ def test_utf8_payload_and_partition_keys(ctx, seed):
         assert offs[-1] == b.rows
         for p in range(n):
             assert_batches_equal(O.slice_(got, offs[p], offs[p + 1] - offs[p]), want[p], ordered=True)
+
+
+def _utf8_group_batch(seed, rows, null_frac):
+    rng = np.random.default_rng(seed)
+    words = ["", "a", "ab", "abc", "b", "ba", "ASIA", "EUROPE", "ünï", "a" * 40] + [f"w{i}" for i in range(50)]
+    names = [words[i] for i in rng.integers(0, len(words), rows)]
+    b = HostBatch(rows)
+    b.cols.append(HostBatch.col_utf8(names, (rng.random(rows) >= null_frac) if null_frac else None))
+    b.cols.append(HostBatch.col_i64(rng.integers(0, 3, rows)))
+    b.cols.append(HostBatch.col_dec(rng.integers(-5000, 5000, rows).astype(np.int64), 11, 2))
+    b.cols.append(HostBatch.col_utf8([words[i] for i in rng.integers(0, 4, rows)]))  # a second Utf8 column
+    return b
+
+
+@pytest.mark.parametrize("seed,rows,null_frac", [(0, 0, 0.0), (1, 1, 0.0), (2, 700, 0.0), (3, 5000, 0.2),
+                                                 (4, 40000, 0.1)])
+def test_utf8_group_keys(ctx, seed, rows, null_frac):
+    """aggregate_execute with Utf8 group keys (alone, with an Int64 key, two Utf8
+    keys): the GPU groups by the strings' fnv1a64 after checking every row's
+    string against its hash's representative row, and gathers each group's
+    string back — equal to the oracle's byte-exact interning."""
+    b = _utf8_group_batch(seed, rows, null_frac)
+    d = ctx.upload(b)
+    aggs = [(0, 2), (2, 0), (3, 1), (5, 2)]  # SUM(dec), COUNT(*), MIN(k), AVG(dec)
+    for keys in ([0], [1, 0], [0, 3], [3, 0, 1]):
+        got = ctx.aggregate_execute(d, keys, aggs).to_host()
+        assert_batches_equal(got, O.aggregate_execute(b, keys, aggs), ordered=False)
+
+
+def test_utf8_group_key_errors(ctx):
+    b = _utf8_group_batch(9, 100, 0.0)
+    d = ctx.upload(b)
+    with pytest.raises(Exception, match="InvalidPlan"):
+        ctx.aggregate_execute(d, [0], [(3, 3)])  # MIN over a Utf8 column

@@ -276,3 +276,58 @@ def test_datagen_shards_concat_to_full_table(t):
     assert cat.rows == full.rows
     for a, b in zip(cat.cols, full.cols):
         assert (a.values == b.values).all()
+
+
+# ---------------------------------------------------------------- Utf8 group keys
+def _utf8_key_batch(seed, rows, null_frac):
+    """(Utf8 name, Int64 k, Int64 v): few distinct strings, incl. the empty one
+    and strings that share prefixes, so byte equality (not a prefix) decides."""
+    rng = np.random.default_rng(seed)
+    words = ["", "a", "ab", "abc", "b", "ba", "ASIA", "EUROPE", "ünï", "a" * 40]
+    names = [words[i] for i in rng.integers(0, len(words), rows)]
+    nv = rng.random(rows) >= null_frac
+    b = HostBatch(rows)
+    b.cols.append(HostBatch.col_utf8(names, nv if null_frac else None))
+    b.cols.append(HostBatch.col_i64(rng.integers(0, 3, rows)))
+    b.cols.append(HostBatch.col_i64(rng.integers(-100, 100, rows)))
+    return b, names, nv
+
+
+def _py_group(names, nv, ks, vs, use_k):
+    out = {}
+    for i in range(len(names)):
+        key = (names[i] if nv[i] else None,) + ((int(ks[i]),) if use_k else ())
+        s, n, mn = out.get(key, (0, 0, None))
+        v = int(vs[i])
+        out[key] = (s + v, n + 1, v if mn is None else min(mn, v))
+    return out
+
+
+@pytest.mark.parametrize("seed,rows,null_frac", [(0, 0, 0.0), (1, 1, 0.0), (2, 500, 0.0), (3, 3000, 0.2)])
+@pytest.mark.parametrize("naive", [False, True])
+def test_oracle_utf8_group_keys(seed, rows, null_frac, naive):
+    """aggregate_execute over a Utf8 key (alone and with an Int64 key): one group
+    per distinct string by its bytes, a null string its own group — against a
+    Python dict; the output key column is Utf8 (bitmap iff the input had one)."""
+    b, names, nv = _utf8_key_batch(seed, rows, null_frac)
+    ks, vs = b.cols[1].i64(), b.cols[2].i64()
+    for keys, use_k in (([0], False), ([1, 0], True)):
+        got = O.aggregate_execute(b, keys, [(AGG_SUM, 2), (AGG_COUNT_STAR, 0), (AGG_MIN, 2)], naive=naive)
+        want = _py_group(names, nv, ks, vs, use_k)
+        ucol = keys.index(0)
+        assert got.cols[ucol].kind == UTF8
+        assert (got.cols[ucol].validity is not None) == (null_frac > 0 and rows > 0)
+        rows_got = {}
+        strs = got.column_py(ucol)
+        kcol = got.column_py(1 - ucol) if use_k else None
+        sums, cnts, mins = got.column_py(len(keys)), got.column_py(len(keys) + 1), got.column_py(len(keys) + 2)
+        for g in range(got.rows):
+            key = (strs[g],) + ((kcol[g],) if use_k else ())
+            rows_got[key] = (sums[g], cnts[g], mins[g])
+        assert rows_got == want
+
+
+def test_oracle_utf8_aggregate_input_rejected():
+    b, _, _ = _utf8_key_batch(5, 10, 0.0)
+    with pytest.raises(Exception, match="InvalidPlan"):
+        O.aggregate_execute(b, [1], [(AGG_MIN, 0)])
