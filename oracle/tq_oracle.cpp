@@ -992,7 +992,7 @@ void check_join_keys(const BV& build, const BV& probe, const uint32_t* bk, const
     const CV& b = probe.cols[pk[k]];
     if (a.kind != b.kind || (a.kind == TQ_DECIMAL && a.scale != b.scale))
       fail(TQ_INVALID_PLAN, "join key types differ");
-    if (a.kind == TQ_UTF8 || a.kind == TQ_FLOAT64) fail(TQ_INVALID_PLAN, "unsupported join key type");
+    if (a.kind == TQ_FLOAT64) fail(TQ_INVALID_PLAN, "unsupported join key type");
   }
 }
 
@@ -1019,10 +1019,10 @@ struct JoinTable {
   }
 };
 
-OBatch join_exec(const BV& build, const BV& probe, const uint32_t* bk, const uint32_t* pk, uint32_t nk, int naive,
-                 uint32_t nthreads) {
-  check_join_keys(build, probe, bk, pk, nk);
-  std::vector<uint64_t> bids, pids;
+// matching (build row, probe row) pairs: probe rows in order, each probe row's
+// matches in build-row order
+void join_match(const BV& build, const BV& probe, const uint32_t* bk, const uint32_t* pk, uint32_t nk, int naive,
+                uint32_t nthreads, std::vector<uint64_t>& bids, std::vector<uint64_t>& pids) {
   if (naive) {  // SPEC.md:699 nested loop
     KeySpec bks = key_spec(build, bk, nk), pks = key_spec(probe, pk, nk);
     std::vector<uint64_t> wb(bks.total), wp(pks.total);
@@ -1033,7 +1033,7 @@ OBatch join_exec(const BV& build, const BV& probe, const uint32_t* bk, const uin
         if (std::memcmp(wb.data(), wp.data(), bks.total * 8) == 0) { bids.push_back(b); pids.push_back(p); }
       }
     }
-    return join_pairs(build, probe, bids, pids);
+    return;
   }
   JoinTable t(build, bk, nk);
   KeySpec pks = key_spec(probe, pk, nk);
@@ -1057,6 +1057,43 @@ OBatch join_exec(const BV& build, const BV& probe, const uint32_t* bk, const uin
     bids.insert(bids.end(), vb[m].begin(), vb[m].end());
     pids.insert(pids.end(), vp[m].begin(), vp[m].end());
   }
+  }
+
+// Utf8 join keys (equal key VALUES match, a string by its
+// bytes): each Utf8 key pair is matched on ids from one dictionary over both
+// sides' strings (a null string stays null and never matches); the output rows
+// are the original columns taken at the matched rows.
+OBatch join_exec(const BV& build, const BV& probe, const uint32_t* bk, const uint32_t* pk, uint32_t nk, int naive,
+                 uint32_t nthreads) {
+  check_join_keys(build, probe, bk, pk, nk);
+  std::vector<uint64_t> bids, pids;
+  BV bl = build, pl = probe;
+  std::vector<uint32_t> nbk(bk, bk + nk), npk(pk, pk + nk);
+  std::vector<std::unique_ptr<std::vector<int64_t>>> store;
+  auto lower = [&](const CV& c, uint64_t rows, std::unordered_map<std::string_view, int64_t>& dict) {
+    store.emplace_back(new std::vector<int64_t>(std::max<uint64_t>(1, rows), 0));
+    std::vector<int64_t>& ids = *store.back();
+    for (uint64_t r = 0; r < rows; ++r) {
+      if (!c.valid(r)) continue;
+      std::string_view sv(reinterpret_cast<const char*>(c.values) + c.offsets[r], size_t(c.offsets[r + 1] - c.offsets[r]));
+      ids[r] = dict.emplace(sv, int64_t(dict.size())).first->second;
+    }
+    CV v;
+    v.kind = TQ_INT64;
+    v.values = reinterpret_cast<const uint8_t*>(ids.data());
+    v.values_bytes = rows * 8;
+    v.validity = c.validity;
+    return v;
+  };
+  for (uint32_t k = 0; k < nk; ++k) {
+    if (build.cols[bk[k]].kind != TQ_UTF8) continue;
+    std::unordered_map<std::string_view, int64_t> dict;
+    bl.cols.push_back(lower(build.cols[bk[k]], build.rows, dict));
+    pl.cols.push_back(lower(probe.cols[pk[k]], probe.rows, dict));
+    nbk[k] = uint32_t(bl.cols.size() - 1);
+    npk[k] = uint32_t(pl.cols.size() - 1);
+  }
+  join_match(bl, pl, nbk.data(), npk.data(), nk, naive, nthreads, bids, pids);
   return join_pairs(build, probe, bids, pids);
 }
 

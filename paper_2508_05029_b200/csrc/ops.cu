@@ -33,6 +33,16 @@ struct tq_join_table {
   // stream, so it is retired and freed with the table
   std::mutex mu;
   std::vector<std::pair<uint8_t*, uint64_t>> retired;
+  // Utf8 build columns (tq_join_build): the table is built over a lowered copy
+  // of the batch — Utf8 keys as the fnv1a64 of their bytes, Utf8 payloads as row
+  // ids, plus a row-id column — whose buffers it owns; the probe compares the
+  // key strings of every candidate pair and gathers the output strings.
+  bool utf8 = false;
+  std::vector<tq_column> orig_cols;  // the caller's build columns (descriptors)
+  uint64_t orig_rows = 0;
+  std::vector<uint8_t> key_utf8;     // per key: a Utf8 key
+  std::vector<uint32_t> key_cols;    // per key: its build column
+  std::vector<std::pair<void*, uint64_t>> own;
 };
 
 namespace tq {
@@ -2611,6 +2621,105 @@ void aggregate_utf8_keys(tq_ctx* c, const tq_batch* in, const uint32_t* keys, ui
   utf8_raise(c, in, src, out->ncols - 1, out, st);
 }
 
+// ---- Utf8 join keys and payloads (join_execute).  Both sides
+// are lowered like the aggregate's keys (Utf8 keys -> fnv1a64 of the bytes, Utf8
+// payloads -> row ids, + a row-id column); the hash join produces candidate
+// pairs, every pair whose key strings differ (a hash collision) is dropped — so
+// the result is exact — and the output strings are gathered by row id.
+struct Utf8Side {
+  std::vector<tq_column> cols;
+  tq_batch b{};
+  uint32_t rid = 0;
+  std::vector<std::pair<void*, uint64_t>> bufs;
+};
+static void utf8_lower_side(tq_ctx* c, const tq_batch* in, const uint32_t* keys, uint32_t nkeys, Utf8Side& S,
+                            cudaStream_t st) {
+  const uint64_t rows = in->rows, bytes = std::max<uint64_t>(8, rows * 8);
+  u64* rid = (u64*)dalloc(c, bytes, st);
+  S.bufs.push_back({rid, bytes});
+  k_iota<<<grid_for(c, rows), 256, 0, st>>>(rid, rows);
+  counted_launch(c);
+  tq_column rc{};
+  rc.kind = TQ_INT64;
+  rc.values = rid;
+  rc.values_bytes = rows * 8;
+  S.cols.assign(in->cols, in->cols + in->ncols);
+  std::vector<bool> is_key(in->ncols, false);
+  for (uint32_t k = 0; k < nkeys; ++k) {
+    if (keys[k] >= in->ncols) fail(TQ_INVALID_PLAN, "join key out of range");
+    is_key[keys[k]] = true;
+  }
+  for (uint32_t i = 0; i < in->ncols; ++i) {
+    if (in->cols[i].kind != TQ_UTF8) continue;
+    if (!is_key[i]) {
+      S.cols[i] = rc;
+      continue;
+    }
+    HashKeys K{};
+    K.n = 1;
+    K.k[0] = HashKeyCol{(const uint8_t*)in->cols[i].values, in->cols[i].offsets, rows ? in->cols[i].validity : nullptr,
+                        0u};
+    u64* h = (u64*)dalloc(c, bytes, st);
+    S.bufs.push_back({h, bytes});
+    k_partition_hash<<<grid_for(c, rows), 256, 0, st>>>(K, rows, h);
+    counted_launch(c);
+    tq_column hc{};
+    hc.kind = TQ_INT64;
+    hc.values = h;
+    hc.values_bytes = rows * 8;
+    hc.validity = rows ? in->cols[i].validity : nullptr;
+    S.cols[i] = hc;
+  }
+  TQ_CUDA(cudaGetLastError());
+  S.rid = (uint32_t)S.cols.size();
+  S.cols.push_back(rc);
+  S.b = *in;
+  S.b.ncols = (uint32_t)S.cols.size();
+  S.b.cols = S.cols.data();
+  S.b.owner = nullptr;
+}
+
+// keep[i] = 0 if the key strings of output row i differ (build row a[i], probe row b[i])
+__global__ void k_utf8_pair_keep(const uint8_t* bb, const int32_t* bo, const uint8_t* pb, const int32_t* po,
+                                 const long long* a, const long long* b, u64 n, uint8_t* keep, u32* any_drop) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const long long x = a[i], y = b[i];
+    const int32_t x0 = bo[x], xl = bo[x + 1] - x0, y0 = po[y], yl = po[y + 1] - y0;
+    bool diff = xl != yl;
+    for (int32_t j = 0; !diff && j < xl; ++j) diff = bb[x0 + j] != pb[y0 + j];
+    if (diff) {
+      keep[i] = 0;
+      atomicOr(any_drop, 1u);
+    }
+  }
+}
+
+// drop output columns (their buffers released), keeping the others in order
+static void drop_columns(tq_ctx* c, tq_batch* out, const std::vector<bool>& drop, cudaStream_t st) {
+  Owner* own = (Owner*)out->owner;
+  auto release = [&](void* p) {
+    for (size_t b = 0; b < own->bufs.size(); ++b)
+      if (own->bufs[b].first == p) {
+        dfree(c, p, own->bufs[b].second, st);
+        own->bufs.erase(own->bufs.begin() + b);
+        return;
+      }
+  };
+  uint32_t w = 0;
+  for (uint32_t j = 0; j < out->ncols; ++j) {
+    if (j < drop.size() && drop[j]) {
+      release(out->cols[j].values);
+      if (out->cols[j].validity) release(out->cols[j].validity);
+      continue;
+    }
+    out->cols[w++] = out->cols[j];
+  }
+  out->ncols = w;
+}
+
+void join_probe_utf8(tq_ctx* c, const tq_join_table* t, const tq_batch* probe, const uint32_t* keys, uint32_t nkeys,
+                     tq_batch* out, cudaStream_t st);
+
 }  // namespace tq
 
 // ================================================================== operator entry points
@@ -2778,6 +2887,31 @@ tq_status tq_join_build_sized(tq_ctx* c, const tq_batch* build, const uint32_t* 
                               uint64_t bloom_keys, tq_join_table** out, void* stream) {
   return guard([&] {
     check_device_batch(build);
+    if (has_utf8(build)) {  // Utf8 keys / payloads: a table over the lowered batch
+      cudaStream_t st = pick(c, stream);
+      Utf8Side S;
+      try {
+        utf8_lower_side(c, build, keys, nkeys, S, st);
+      } catch (...) {
+        for (auto& b : S.bufs) dfree(c, b.first, b.second, st);
+        throw;
+      }
+      tq_status r = tq_join_build_sized(c, &S.b, keys, nkeys, bloom_keys, out, stream);
+      if (r != TQ_OK) {
+        for (auto& b : S.bufs) dfree(c, b.first, b.second, st);
+        fail(r, tq_last_error());
+      }
+      tq_join_table* t = *out;
+      t->utf8 = true;
+      t->orig_cols.assign(build->cols, build->cols + build->ncols);
+      t->orig_rows = build->rows;
+      for (uint32_t k = 0; k < nkeys; ++k) {
+        t->key_utf8.push_back(build->cols[keys[k]].kind == TQ_UTF8 ? 1 : 0);
+        t->key_cols.push_back(keys[k]);
+      }
+      t->own = std::move(S.bufs);
+      return;
+    }
     Prog P(schema_of(build));
     std::vector<tq_expr_node> nodes(nkeys);
     std::vector<tq_expr> ex(nkeys);
@@ -2870,6 +3004,10 @@ tq_status tq_join_probe(tq_ctx* c, const tq_join_table* t, const tq_batch* probe
                         uint32_t nkeys, tq_batch* out, void* stream) {
   return guard([&] {
     check_device_batch(probe);
+    if (t->utf8 || has_utf8(probe)) {
+      join_probe_utf8(c, t, probe, keys, nkeys, out, pick(c, stream));
+      return;
+    }
     Prog P(schema_of(probe));
     compile_all(P, probe, nullptr);
     MatArgs A;
@@ -2903,6 +3041,7 @@ void tq_join_table_destroy(tq_ctx* c, tq_join_table* t) {
   (void)c;
   dfree(t->ctx, t->mem, t->bytes, t->ctx->stream);  // see tq_batch_free
   for (auto& r : t->retired) dfree(t->ctx, r.first, r.second, t->ctx->stream);
+  for (auto& b : t->own) dfree(t->ctx, b.first, b.second, t->ctx->stream);
   std::free(t->build.cols);
   delete t;
 }
@@ -3314,3 +3453,119 @@ tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, cons
 }
 
 }  // extern "C"
+
+namespace tq {
+// join_execute probe with Utf8 keys / payloads on either side (see Utf8Side)
+void join_probe_utf8(tq_ctx* c, const tq_join_table* t, const tq_batch* probe, const uint32_t* keys, uint32_t nkeys,
+                     tq_batch* out, cudaStream_t st) {
+  if (nkeys != t->key_cols.size() && t->utf8) fail(TQ_INVALID_PLAN, "join key count differs from the build's");
+  for (uint32_t k = 0; k < nkeys; ++k) {
+    if (keys[k] >= probe->ncols) fail(TQ_INVALID_PLAN, "join key out of range");
+    const bool pu = probe->cols[keys[k]].kind == TQ_UTF8, bu = t->utf8 && t->key_utf8[k];
+    if (pu != bu) fail(TQ_INVALID_PLAN, "join key types differ");
+  }
+  Utf8Side S;
+  struct Free {
+    tq_ctx* c;
+    cudaStream_t st;
+    Utf8Side& S;
+    ~Free() {
+      for (auto& b : S.bufs) dfree(c, b.first, b.second, st);
+    }
+  } fr{c, st, S};
+  utf8_lower_side(c, probe, keys, nkeys, S, st);
+  const tq_batch& tb = t->build;  // lowered build (its last column the build row id when t->utf8)
+  const uint32_t nb = tb.ncols, np = S.b.ncols;
+  // the build columns of the output: the lowered build's (incl. its row ids)
+  {
+    Prog P(schema_of(&S.b));
+    compile_prog(P, &S.b, nullptr, nullptr, 0, true);
+    MatArgs A;
+    A.mode = MAT_PROBE;
+    A.key_roots.assign(keys, keys + nkeys);
+    A.table = t;
+    A.build_cols = iota_u32(nb);
+    run_materialize(c, &S.b, P, A, out, nullptr, st);
+  }
+  // out: [lowered build (nb) | lowered probe (np)]; row ids at nb - 1 (if t->utf8) and nb + np - 1
+  const uint32_t brid = t->utf8 ? nb - 1 : UINT32_MAX, prid = nb + np - 1;
+  // exactness: drop the pairs whose Utf8 key strings differ (fnv1a64 collisions)
+  bool any_utf8_key = false;
+  for (uint32_t k = 0; k < nkeys; ++k) any_utf8_key |= probe->cols[keys[k]].kind == TQ_UTF8;
+  if (any_utf8_key && out->rows) {
+    const uint64_t n = out->rows;
+    uint8_t* keep = (uint8_t*)dalloc(c, std::max<uint64_t>(8, n), st);
+    u32* drop = (u32*)dalloc(c, 8, st);
+    TQ_CUDA(cudaMemsetAsync(keep, 1, n, st));
+    TQ_CUDA(cudaMemsetAsync(drop, 0, 4, st));
+    for (uint32_t k = 0; k < nkeys; ++k) {
+      if (probe->cols[keys[k]].kind != TQ_UTF8) continue;
+      const tq_column& bc = t->orig_cols[t->key_cols[k]];
+      const tq_column& pc = probe->cols[keys[k]];
+      k_utf8_pair_keep<<<grid_for(c, n), 256, 0, st>>>(
+          (const uint8_t*)bc.values, bc.offsets, (const uint8_t*)pc.values, pc.offsets,
+          (const long long*)out->cols[brid].values, (const long long*)out->cols[prid].values, n, keep, drop);
+      counted_launch(c);
+    }
+    TQ_CUDA(cudaGetLastError());
+    u32* pin = (u32*)pinned_scratch(c);
+    TQ_CUDA(cudaMemcpyAsync(pin, drop, 4, cudaMemcpyDeviceToHost, st));
+    TQ_CUDA(cudaStreamSynchronize(st));
+    const bool dropped = pin[0] != 0;
+    if (dropped) {
+      std::vector<tq_column> cols(out->cols, out->cols + out->ncols);
+      tq_column kc{};
+      kc.kind = TQ_BOOL;
+      kc.values = keep;
+      kc.values_bytes = n;
+      cols.push_back(kc);
+      tq_batch with{n, (uint32_t)cols.size(), TQ_MEM_DEVICE, cols.data(), nullptr};
+      tq_expr_node pn{};
+      pn.tag = TQ_EX_COL;
+      pn.column = (uint32_t)cols.size() - 1;
+      tq_batch f{};
+      const tq_status r = tq_filter(c, &with, tq_expr{&pn, 1, 0}, &f, st);
+      if (r == TQ_OK) {
+        tq_batch_free(c, out);
+        *out = f;
+        std::vector<bool> d(out->ncols, false);
+        d[out->ncols - 1] = true;  // the keep column
+        drop_columns(c, out, d, st);
+      }
+      dfree(c, keep, std::max<uint64_t>(8, n), st);
+      dfree(c, drop, 8, st);
+      if (r != TQ_OK) fail(r, tq_last_error());
+    } else {
+      dfree(c, keep, std::max<uint64_t>(8, n), st);
+      dfree(c, drop, 8, st);
+    }
+  }
+  // the output strings: a Utf8 column's output holds its side's row ids (a Utf8
+  // payload's stand-in is the row-id column; a Utf8 key's hash is replaced by them)
+  std::vector<bool> d(out->ncols, false);
+  auto gather = [&](uint32_t j, const tq_column& src, uint64_t src_rows, uint32_t rid_col, bool was_key) {
+    if (was_key && out->rows)
+      TQ_CUDA(cudaMemcpyAsync(out->cols[j].values, out->cols[rid_col].values, out->rows * 8, cudaMemcpyDeviceToDevice,
+                              st));
+    tq_batch one{src_rows, 1, TQ_MEM_DEVICE, const_cast<tq_column*>(&src), nullptr};
+    std::vector<int> sv(out->ncols, -1);
+    sv[j] = 0;
+    utf8_raise(c, &one, sv, out->ncols, out, st);
+  };
+  if (t->utf8) {
+    std::vector<bool> bkey(t->orig_cols.size(), false);
+    for (uint32_t k = 0; k < nkeys; ++k) bkey[t->key_cols[k]] = true;
+    for (uint32_t j = 0; j < t->orig_cols.size(); ++j)
+      if (t->orig_cols[j].kind == TQ_UTF8) gather(j, t->orig_cols[j], t->orig_rows, brid, bkey[j]);
+    d[brid] = true;
+  }
+  {
+    std::vector<bool> pkey(probe->ncols, false);
+    for (uint32_t k = 0; k < nkeys; ++k) pkey[keys[k]] = true;
+    for (uint32_t j = 0; j < probe->ncols; ++j)
+      if (probe->cols[j].kind == TQ_UTF8) gather(nb + j, probe->cols[j], probe->rows, prid, pkey[j]);
+  }
+  d[prid] = true;
+  drop_columns(c, out, d, st);
+}
+}  // namespace tq

@@ -466,3 +466,26 @@ def test_utf8_group_key_errors(ctx):
     d = ctx.upload(b)
     with pytest.raises(Exception, match="InvalidPlan"):
         ctx.aggregate_execute(d, [0], [(3, 3)])  # MIN over a Utf8 column
+
+
+@pytest.mark.parametrize("seed,nb,np_,null_frac", [(0, 0, 50, 0.0), (1, 60, 0, 0.0), (2, 120, 1500, 0.0),
+                                                  (3, 200, 4000, 0.15)])
+def test_utf8_join_keys_and_payloads(ctx, seed, nb, np_, null_frac):
+    """join_execute with Utf8 keys (alone / with an Int64 key) and Utf8 payloads
+    on both sides: candidate pairs from the fnv1a64 of the bytes, pairs whose
+    strings differ dropped, strings gathered by row id — equal to the oracle's
+    byte-exact dictionary join.  Also Int64 keys with Utf8 payloads only."""
+    b = _utf8_group_batch(seed, nb, null_frac)
+    p = _utf8_group_batch(seed + 50, np_, null_frac)
+    db, dp = ctx.upload(b), ctx.upload(p)
+    # ([1], [1]): an Int64 key with 3 values — Utf8 payloads only (the output is ~nb x np / 3 rows)
+    for bk, pk in (([0], [0]), ([1, 0], [1, 0]), ([3], [0])) + ((([1], [1]),) if nb * np_ <= 200000 else ()):
+        got = ctx.join_execute(db, dp, bk, pk).to_host()
+        assert_batches_equal(got, O.join_execute(b, p, bk, pk), ordered=False)
+
+
+def test_utf8_join_key_type_mismatch(ctx):
+    b = _utf8_group_batch(7, 50, 0.0)
+    db = ctx.upload(b)
+    with pytest.raises(Exception, match="InvalidPlan"):
+        ctx.join_execute(db, db, [0], [1])  # Utf8 build key vs Int64 probe key

@@ -331,3 +331,28 @@ def test_oracle_utf8_aggregate_input_rejected():
     b, _, _ = _utf8_key_batch(5, 10, 0.0)
     with pytest.raises(Exception, match="InvalidPlan"):
         O.aggregate_execute(b, [1], [(AGG_MIN, 0)])
+
+
+@pytest.mark.parametrize("seed,nb,np_,null_frac", [(0, 0, 5, 0.0), (1, 7, 0, 0.0), (2, 60, 300, 0.0),
+                                                  (3, 200, 900, 0.2)])
+@pytest.mark.parametrize("naive", [False, True])
+def test_oracle_utf8_join_keys(seed, nb, np_, null_frac, naive):
+    """join_execute on (Utf8) and (Int64, Utf8) keys: rows match iff the strings'
+    bytes are equal (a null string never matches), duplicates on both sides give
+    every pair — against a Python nested loop over the row tuples."""
+    bb, bnames, bnv = _utf8_key_batch(seed, nb, null_frac)
+    pb, pnames, pnv = _utf8_key_batch(seed + 100, np_, null_frac)
+    for bk, pk in (([0], [0]), ([1, 0], [1, 0])):
+        got = O.join_execute(bb, pb, bk, pk, naive=naive)
+        want = []
+        for p in range(np_):
+            for b in range(nb):
+                if not (bnv[b] and pnv[p]) or bnames[b] != pnames[p]:
+                    continue
+                if len(bk) == 2 and bb.cols[1].i64()[b] != pb.cols[1].i64()[p]:
+                    continue
+                want.append((bnames[b], int(bb.cols[1].i64()[b]), int(bb.cols[2].i64()[b]),
+                             pnames[p], int(pb.cols[1].i64()[p]), int(pb.cols[2].i64()[p])))
+        assert got.cols[0].kind == UTF8 and got.cols[3].kind == UTF8
+        rows = list(zip(*[got.column_py(c) for c in range(6)])) if got.rows else []
+        assert sorted(rows) == sorted(want)
