@@ -2314,7 +2314,9 @@ tq_status tq_rebatch(tq_ctx* c, const tq_batch* ins, uint32_t n, uint64_t target
 // partition hash — fnv1a64 chained over the key columns' bytes, the string's
 // bytes for Utf8 (a null string adds none, a null fixed-width key its width in
 // zero bytes) — and the kernel partitions on it as is (key_prehashed).
-// Utf8 in predicates, arithmetic, join / group keys: InvalidPlan.
+// Utf8 group keys (aggregate_execute) and join keys / payloads (join_execute):
+// aggregate_utf8_keys / join_probe_utf8 below.  Utf8 in predicates and
+// arithmetic: InvalidPlan.
 namespace tq {
 
 __global__ void k_iota(u64* v, u64 n) {
