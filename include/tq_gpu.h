@@ -98,6 +98,21 @@ tq_status tq_project(tq_ctx* ctx, const tq_batch* in, const tq_expr* exprs, uint
  * (host array of nparts+1). */
 tq_status tq_hash_partition(tq_ctx* ctx, const tq_batch* in, const uint32_t* keys, uint32_t nkeys,
                             uint32_t nparts, tq_batch* out, uint64_t* part_offsets, void* stream);
+/* Asynchronous filter / hash partition (a data-dependent count is
+ * returned through a pinned host slot, valid once the stream reaches the end of
+ * the call — no host sync inside).  `out` is allocated at the input's row count
+ * (every row can pass) and carries that capacity as its row count until the
+ * caller, after the stream event, trims it with tq_batch_set_rows(out,
+ * slot[nparts]).  slot: caller-owned pinned memory (tq_pinned_alloc) of 2
+ * (filter: 0, rows) or nparts + 1 (partition: part starts, then the total)
+ * uint64 values — the part_offsets of the synchronous forms.  Batches with Utf8
+ * columns: TQ_INVALID_PLAN (their gather needs the count on the host). */
+tq_status tq_filter_async(tq_ctx* ctx, const tq_batch* in, tq_expr pred, tq_batch* out, uint64_t* slot,
+                          void* stream);
+tq_status tq_hash_partition_async(tq_ctx* ctx, const tq_batch* in, const uint32_t* keys, uint32_t nkeys,
+                                  uint32_t nparts, tq_batch* out, uint64_t* slot, void* stream);
+/* logical trim of a batch to its first `rows` rows (rows <= b->rows; buffers kept) */
+void tq_batch_set_rows(tq_batch* b, uint64_t rows);
 /* join_execute build side: open-addressing table over the
  * build batch (which must stay alive until the table is destroyed). */
 tq_status tq_join_build(tq_ctx* ctx, const tq_batch* build, const uint32_t* keys, uint32_t nkeys,

@@ -168,6 +168,11 @@ static void scan_u32(tq_ctx* c, const u32* in, u64 n, u64* out, u64* total_dev, 
   dfree(c, partial, nb * 8, st);
 }
 
+__global__ void k_set_u64_one(u64* p, u64 v) { *p = v; }
+static void k_set_u64_ext(u64* p, u64 v, cudaStream_t st) {
+  k_set_u64_one<<<1, 1, 0, st>>>(p, v);
+}
+
 // offsets[d*ntiles] for each dest + total -> pinned[0..ndest]
 __global__ void k_dest_starts(const u64* offsets, u32 nslices, u32 ndest, const u64* total, u64* pinned) {
   u32 d = threadIdx.x;
@@ -443,6 +448,11 @@ struct MatArgs {
   const tq_join_table* table = nullptr;
   std::vector<uint32_t> build_cols;
   bool prehashed = false;  // the one key is the row's partition hash (Utf8 keys)
+  // asynchronous form (tq_filter_async / tq_hash_partition_async): no host sync;
+  // the output is allocated at the input's row count and the part starts + total
+  // (ndest + 1 values) land in this caller-owned pinned slot, valid once the
+  // stream reaches the end of the call
+  uint64_t* async_slot = nullptr;
 };
 
 // ---- closing the holes of DEST_PROBE1's chunked output (kernel_common.cuh,
@@ -818,6 +828,48 @@ two_pass:
   u64* offsets = nullptr;
   const u64 nslices = (u64)p.ntiles * kWarps;
   u64 ncnt = (u64)p.ndest * nslices;
+  if (A.async_slot) {
+    if (A.mode == MAT_PROBE) fail(TQ_INVALID_PLAN, "no asynchronous probe (its output is not bounded by its input)");
+    u64* dev_starts = (u64*)dalloc(c, (p.ndest + 1) * 8, st);
+    if (!dense && p.ntiles > 0) {
+      counts = (u32*)dalloc(c, ncnt * 4, st);
+      offsets = (u64*)dalloc(c, (ncnt + 1) * 8, st);
+      p.tile_counts = counts;
+      std::vector<int> need = kh;
+      if (P.has_pred) need.push_back(P.pred_h);
+      const u32 all = p.load_mask;
+      p.load_mask = P.pb.column_deps(need);
+      launch_count(c, L, P, st);
+      p.load_mask = all;
+      scan_u32(c, counts, ncnt, offsets, offsets + ncnt, st);
+      k_dest_starts<<<1, 128, 0, st>>>(offsets, (u32)nslices, p.ndest, offsets + ncnt, dev_starts);
+      counted_launch(c);
+      p.tile_offsets = offsets;
+    } else {
+      for (u32 d = 0; d <= p.ndest; ++d) k_set_u64_ext(dev_starts + d, d == 0 || !dense ? 0 : in->rows, st);
+    }
+    TQ_CUDA(cudaGetLastError());
+    TQ_CUDA(cudaMemcpyAsync(A.async_slot, dev_starts, (p.ndest + 1) * 8, cudaMemcpyDeviceToHost, st));
+    dfree(c, dev_starts, (p.ndest + 1) * 8, st);
+    // every input row can pass: the output's capacity (trimmed by tq_batch_set_rows)
+    try {
+      alloc_batch(c, in->rows, sch, wv, out, st);
+    } catch (...) {
+      if (counts) dfree(c, counts, ncnt * 4, st);
+      if (offsets) dfree(c, offsets, (ncnt + 1) * 8, st);
+      throw;
+    }
+    p.nout = (u32)outs.size();
+    for (size_t i = 0; i < outs.size(); ++i) {
+      outs[i].values = (uint8_t*)out->cols[i].values;
+      outs[i].validity = out->cols[i].validity;
+      p.out[i] = outs[i];
+    }
+    if (in->rows > 0) launch(c, SINK_EMIT, L, P, st);
+    if (counts) dfree(c, counts, ncnt * 4, st);
+    if (offsets) dfree(c, offsets, (ncnt + 1) * 8, st);
+    return;
+  }
   if (!dense && p.ntiles > 0) {
     counts = (u32*)dalloc(c, ncnt * 4, st);
     offsets = (u64*)dalloc(c, (ncnt + 1) * 8, st);
@@ -2855,6 +2907,44 @@ tq_status tq_hash_partition(tq_ctx* c, const tq_batch* in, const uint32_t* keys,
     A.nparts = nparts;
     run_materialize(c, in, P, A, out, part_offsets, pick(c, stream));
   });
+}
+
+tq_status tq_filter_async(tq_ctx* c, const tq_batch* in, tq_expr pred, tq_batch* out, uint64_t* slot,
+                          void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    if (!slot) fail(TQ_INVALID_PLAN, "asynchronous filter without a count slot");
+    if (has_utf8(in)) fail(TQ_INVALID_PLAN, "no asynchronous form for Utf8 columns (their gather needs the count)");
+    Prog P(schema_of(in));
+    compile_all(P, in, &pred);
+    MatArgs A;
+    A.async_slot = slot;
+    run_materialize(c, in, P, A, out, nullptr, pick(c, stream));
+  });
+}
+
+tq_status tq_hash_partition_async(tq_ctx* c, const tq_batch* in, const uint32_t* keys, uint32_t nkeys,
+                                  uint32_t nparts, tq_batch* out, uint64_t* slot, void* stream) {
+  return guard([&] {
+    check_device_batch(in);
+    if (!slot) fail(TQ_INVALID_PLAN, "asynchronous partition without a count slot");
+    if (has_utf8(in)) fail(TQ_INVALID_PLAN, "no asynchronous form for Utf8 columns (their gather needs the count)");
+    Prog P(schema_of(in));
+    compile_all(P, in, nullptr);
+    MatArgs A;
+    A.mode = MAT_PARTITION;
+    A.key_roots.assign(keys, keys + nkeys);
+    A.nparts = nparts;
+    A.async_slot = slot;
+    run_materialize(c, in, P, A, out, nullptr, pick(c, stream));
+  });
+}
+
+void tq_batch_set_rows(tq_batch* b, uint64_t rows) {
+  if (!b || rows > b->rows) return;
+  b->rows = rows;
+  for (uint32_t i = 0; i < b->ncols; ++i)
+    if (b->cols[i].kind != TQ_UTF8) b->cols[i].values_bytes = rows * width_of(b->cols[i].kind);
 }
 
 tq_status tq_pipeline_partition(tq_ctx* c, const tq_batch* in, const tq_expr* pred, const tq_expr* exprs,

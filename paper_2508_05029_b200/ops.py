@@ -84,6 +84,10 @@ def lib():
         L.tq_project.argtypes = [V, B, P(TqExprC), C.c_uint32, B, V]
         U32 = P(C.c_uint32)
         L.tq_hash_partition.argtypes = [V, B, U32, C.c_uint32, C.c_uint32, B, P(C.c_uint64), V]
+        L.tq_filter_async.argtypes = [V, B, TqExprC, B, V, V]
+        L.tq_hash_partition_async.argtypes = [V, B, U32, C.c_uint32, C.c_uint32, B, V, V]
+        L.tq_batch_set_rows.argtypes = [B, C.c_uint64]
+        L.tq_batch_set_rows.restype = None
         L.tq_join_build.argtypes = [V, B, U32, C.c_uint32, P(V), V]
         L.tq_join_build_sized.argtypes = [V, B, U32, C.c_uint32, C.c_uint64, P(V), V]
         L.tq_join_probe.argtypes = [V, V, B, U32, C.c_uint32, B, V]
@@ -219,6 +223,27 @@ def _pred(pred: Optional[Expr]):
     return res
 
 
+class PinnedU64:
+    """Caller-owned pinned host slot of n uint64 values (tq_pinned_alloc): the
+    count slot of the asynchronous operators."""
+
+    def __init__(self, n: int):
+        self.ptr = C.c_void_p()
+        Context._check(lib().tq_pinned_alloc(8 * max(1, n), C.byref(self.ptr)))
+        self.n = n
+
+    def __getitem__(self, i: int) -> int:
+        return int(C.cast(self.ptr, C.POINTER(C.c_uint64))[i])
+
+    def values(self) -> List[int]:
+        return [self[i] for i in range(self.n)]
+
+    def free(self):
+        if self.ptr:
+            lib().tq_pinned_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+
 class DeviceBatch:
     """A device-resident batch owned by a Context (freed on close/GC).
     Views (`select`) borrow the parent's buffers and are never freed."""
@@ -246,6 +271,10 @@ class DeviceBatch:
 
     def to_host(self) -> HostBatch:
         return self.ctx.download(self)
+
+    def set_rows(self, rows: int):
+        """Trim to the first `rows` rows (an asynchronous operator's count)."""
+        lib().tq_batch_set_rows(C.byref(self.c), rows)
 
     def free(self):
         if self.parent is not None:
@@ -404,6 +433,23 @@ class Context:
         s = pred.serialize()
         out = TqBatchC()
         return self._wrap(lib().tq_filter(self.handle, C.byref(b.c), s.c(), C.byref(out), stream), out)
+
+    # ---- asynchronous forms: the count arrives in a pinned slot ----
+    def filter_async(self, b: DeviceBatch, pred: Expr, slot: "PinnedU64", stream=None) -> DeviceBatch:
+        """No host sync: returns a batch with the input's row count as capacity;
+        after the stream reaches this point, slot[1] is the row count — trim with
+        DeviceBatch.set_rows(slot[1])."""
+        s = pred.serialize()
+        out = TqBatchC()
+        return self._wrap(lib().tq_filter_async(self.handle, C.byref(b.c), s.c(), C.byref(out), slot.ptr, stream),
+                          out)
+
+    def hash_partition_async(self, b: DeviceBatch, keys: Sequence[int], nparts: int, slot: "PinnedU64",
+                             stream=None) -> DeviceBatch:
+        """slot[0..nparts]: part starts then the total, valid after the stream event."""
+        out = TqBatchC()
+        return self._wrap(lib().tq_hash_partition_async(self.handle, C.byref(b.c), _u32(keys), len(keys), nparts,
+                                                        C.byref(out), slot.ptr, stream), out)
 
     def project_execute(self, b: DeviceBatch, exprs: Sequence[Expr], stream=None) -> DeviceBatch:
         arr, n, _keep = _exprs(exprs)

@@ -489,3 +489,37 @@ def test_utf8_join_key_type_mismatch(ctx):
     db = ctx.upload(b)
     with pytest.raises(Exception, match="InvalidPlan"):
         ctx.join_execute(db, db, [0], [1])  # Utf8 build key vs Int64 probe key
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_async_filter_and_partition(ctx, seed):
+    """tq_filter_async / tq_hash_partition_async: no host sync; the
+    output carries the input's row count as capacity, the count / part starts
+    arrive in a pinned slot after the stream event, and the trimmed batch equals
+    the synchronous operator's (stable order, same part offsets)."""
+    from paper_2508_05029_b200.ops import PinnedU64
+    rows = [0, 1, 3000, 70000][seed]
+    b = rand_batch(seed, rows, (INT64, DECIMAL, BOOL, INT64), null_frac=0.1 if seed % 2 else 0.0)
+    d = ctx.upload(b)
+    pred = rand_pred(random.Random(seed), (INT64, DECIMAL, BOOL, INT64), 2)
+    slot = PinnedU64(2)
+    try:
+        got = ctx.filter_async(d, pred, slot)
+        assert got.rows == rows  # capacity until trimmed
+        ctx.sync()
+        assert slot[0] == 0
+        got.set_rows(slot[1])
+        assert_batches_equal(got.to_host(), ctx.filter_execute(d, pred).to_host(), ordered=True)
+    finally:
+        slot.free()
+    for nparts in (1, 7):
+        slot = PinnedU64(nparts + 1)
+        try:
+            got = ctx.hash_partition_async(d, [0, 3], nparts, slot)
+            ctx.sync()
+            want, offs = ctx.hash_partition(d, [0, 3], nparts)
+            assert slot.values() == offs
+            got.set_rows(slot[nparts])
+            assert_batches_equal(got.to_host(), want.to_host(), ordered=True)
+        finally:
+            slot.free()
