@@ -872,6 +872,12 @@ class BuildOp : public Op {
       check(tq_concat(rt->ctx, bs.data(), (uint32_t)bs.size(), &cat, st));
       cudaStreamSynchronize(st);
       b = rt->adopt(cat, false);
+      {
+        // pinned before anything reads it: an unpinned handle in the registry
+        // is a spill victim, and the build and every probe read its columns
+        std::lock_guard<std::mutex> g(rt->mu);
+        b->pins++;
+      }
       for (HP& h : t.inputs)
         if (!h->view) rt->free_handle(h);
     }
@@ -882,7 +888,7 @@ class BuildOp : public Op {
                                bloom_keys, semi ? 1 : 0, &jt, st));
     cudaStreamSynchronize(st);
     std::lock_guard<std::mutex> g(rt->mu);
-    b->pins++;  // the probe gathers build columns by row id until the query ends
+    if (t.inputs.size() == 1) b->pins++;  // the probe gathers build columns by row id until the query ends
     rt->keep.push_back(b);
     build = b;
     table = jt;
