@@ -150,6 +150,8 @@ class Op {
 };
 
 // ------------------------------------------------------------------ runtime
+thread_local int tl_worker = -1;  // compute thread index (watchdog phases)
+
 class Runtime {
  public:
   Runtime(tq_ctx* c, tq_comm* comm, const tq_engine_opts& o) : ctx(c), comm(comm), opts(o) {}
@@ -261,6 +263,13 @@ class Runtime {
   std::vector<Task> queue;
   std::vector<std::weak_ptr<Handle>> registry;
   std::vector<std::thread> threads;  // executor threads (start_threads .. stop_threads)
+  // TQ_ENGINE_WATCHDOG=<seconds> (diagnostics): per compute thread, what it is
+  // doing (0 idle, 1 reserving, 2 waiting for an input's spill, 3 loading,
+  // 4 executing) and for which operator, dumped when a query runs that long
+  std::atomic<int> phase[64]{};
+  std::atomic<int> mem_phase{0}, pre_phase{0};  // 0 waiting, 1 spilling / loading, 2 exited
+  std::atomic<const char*> phase_op[64]{};
+  void dump_state();
   uint64_t next_id = 0, next_seq = 0, reserved = 0;
   int running_tasks = 0;
   int executing = 0;  // tasks past their reservation (the ones that can free memory)
@@ -359,7 +368,7 @@ void Runtime::watermark_tick() {
   if (!capacity) return;
   uint64_t use = device_in_use();
   m_peak = std::max<uint64_t>(m_peak.load(), use);
-  if (use >= (uint64_t)(opts.high_watermark * capacity)) {
+  if (use >= (uint64_t)(opts.high_watermark * capacity) && !stop) {
     std::vector<HP> v = pick_victims(0, (uint64_t)(opts.low_watermark * capacity));
     if (!v.empty()) {
       spill_q.push_back(std::move(v));
@@ -378,12 +387,15 @@ void Runtime::memory_executor() {
     {
       std::unique_lock<std::mutex> g(mu);
       cv.wait(g, [&] { return stop || !spill_q.empty(); });
-      if (spill_q.empty()) break;  // stop
+      if (spill_q.empty()) break;  // stop (queued victims are drained first)
       v = std::move(spill_q.front());
       spill_q.pop_front();
     }
+    mem_phase = 1;
     spill_victims(v);
+    mem_phase = 0;
   }
+  mem_phase = 2;
 }
 
 bool Runtime::pick(Task& t) {
@@ -420,14 +432,21 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
     // copied out by another thread: let that finish (load() then brings it
     // back) rather than run on a batch that is about to be freed
     for (HP& h : t.inputs) h->pins++;
+    if (tl_worker >= 0 && tl_worker < 64) phase[tl_worker] = 2;
     cv.wait(g, [&] {
+      if (stop) return true;
       for (HP& h : t.inputs)
         if (h->spilling) return false;
       return true;
     });
+    if (stop) {  // the query is being torn down (another task failed): leave
+      for (HP& h : t.inputs) h->pins--;
+      fail(TQ_INTERNAL, op->name + ": query aborted");
+    }
     for (HP& h : t.inputs)  // inputs not on the Device are loaded into the reservation
       if (h->tier != DEVICE) host_bytes += h->bytes;
     want = t.estimate > in_bytes ? t.estimate - in_bytes + host_bytes : host_bytes;
+    if (tl_worker >= 0 && tl_worker < 64) phase[tl_worker] = 1;
     if (capacity) {
       while (device_in_use() + reserved + want > capacity) {
         std::vector<HP> v = pick_victims(reserved + want, capacity);
@@ -438,6 +457,10 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
           continue;
         }
         if (executing == 0 && spilling_bytes == 0) break;  // nobody can free memory: try it, on_oom on failure
+        if (stop) {  // torn down: queued spills will not run
+          for (HP& h : t.inputs) h->pins--;
+          fail(TQ_INTERNAL, op->name + ": query aborted");
+        }
         cv.wait_for(g, std::chrono::milliseconds(2));
       }
     }
@@ -461,7 +484,9 @@ void Runtime::run_task(Task& t, cudaStream_t st) {
       if (opts.inject_oom_mode == 2) t.estimate = std::max<uint64_t>(t.estimate, capacity);  // oversize
       fail(TQ_RESERVATION_EXCEEDED, op->name + ": injected");
     }
+    if (tl_worker >= 0 && tl_worker < 64) phase[tl_worker] = 3;
     for (HP& h : t.inputs) load(h, st, false);  // load_to_device
+    if (tl_worker >= 0 && tl_worker < 64) phase[tl_worker] = 4;
     op->run(t, st);                             // execute + deposit (all-or-nothing per task)
     cudaStreamSynchronize(st);
   } catch (const Fail& f) {
@@ -542,12 +567,17 @@ void Runtime::worker(int idx) {
       if (!pick(t)) continue;
       running_tasks++;
     }
+    if (idx < 64) {
+      tl_worker = idx;
+      phase_op[idx] = t.op->name.c_str();
+    }
     try {
       run_task(t, st);
     } catch (...) {
       std::lock_guard<std::mutex> g(mu);
       if (!error) error = std::current_exception();
     }
+    if (idx < 64) phase[idx] = 0;
     {
       std::lock_guard<std::mutex> g(mu);
       running_tasks--;
@@ -585,10 +615,12 @@ void Runtime::preloader() {
       if (!h) continue;
       h->pins++;
     }
+    pre_phase = 1;
     try {
       load(h, preload_stream, true);
     } catch (...) {
     }
+    pre_phase = 0;
     std::lock_guard<std::mutex> g(mu);
     h->pins--;
   }
@@ -647,9 +679,54 @@ void Runtime::stop_threads() {
   threads.clear();
 }
 
+void Runtime::dump_state() {
+  fprintf(stderr, "[tq watchdog] in_use %.3f GB capacity %.3f GB memexec %d preloader %d stop %d error %d\n",
+          device_in_use() / 1e9, capacity / 1e9, mem_phase.load(), pre_phase.load(), (int)stop, (int)(bool)error);
+  for (uint32_t i = 0; i < std::max<uint32_t>(1, opts.compute_threads) && i < 64; ++i) {
+    const char* n = phase_op[i].load();
+    fprintf(stderr, "[tq watchdog] worker %u phase %d op %s\n", i, phase[i].load(), n ? n : "-");
+  }
+  std::unique_lock<std::mutex> g(mu, std::defer_lock);
+  for (int k = 0; k < 200 && !g.try_lock(); ++k) std::this_thread::sleep_for(std::chrono::milliseconds(5));
+  if (!g.owns_lock()) {
+    fprintf(stderr, "[tq watchdog] runtime lock held\n");
+    return;
+  }
+  fprintf(stderr, "[tq watchdog] queue %zu executing %d reserved %.3f GB running %d spilling %.3f GB spill_q %zu\n",
+          queue.size(), executing, reserved / 1e9, running_tasks, spilling_bytes / 1e9, spill_q.size());
+  for (auto& o : ops)
+    if (!o->finished)
+      fprintf(stderr, "[tq watchdog] op %s running %d\n", o->name.c_str(), o->running);
+  int n_spilling = 0, n_pinned = 0;
+  for (auto& w : registry)
+    if (HP h = w.lock()) {
+      n_spilling += h->spilling;
+      n_pinned += h->pins > 0;
+    }
+  fprintf(stderr, "[tq watchdog] handles spilling %d pinned %d\n", n_spilling, n_pinned);
+}
+
 void Runtime::run() {
   run_start = Clock::now();
   if (threads.empty()) start_threads();
+  std::atomic<bool> finished_run{false};
+  std::thread watchdog;
+  static const int wd_s = [] { const char* e = getenv("TQ_ENGINE_WATCHDOG"); return e ? atoi(e) : 0; }();
+  if (wd_s > 0)
+    watchdog = std::thread([this, &finished_run] {
+      for (int s = 0; !finished_run.load(); ++s) {
+        std::this_thread::sleep_for(std::chrono::seconds(1));
+        if (s + 1 >= wd_s && (s + 1) % wd_s == 0 && !finished_run.load()) dump_state();
+      }
+    });
+  struct Join {
+    std::thread& t;
+    std::atomic<bool>& f;
+    ~Join() {
+      f = true;
+      if (t.joinable()) t.join();
+    }
+  } join_wd{watchdog, finished_run};
   // coordinator: poll operators for runnable tasks until every operator finished
   {
     std::unique_lock<std::mutex> g(mu);

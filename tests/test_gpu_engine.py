@@ -3,6 +3,8 @@ Memory / Pre-loading / Compute executors, run_task lifecycle) running the
 benchmark query DAGs vs the oracle — with resident tables, with Host-tier
 tables under a Device budget (spill / load_to_device / preload), and through
 the on_oom retry path."""
+import os
+
 import numpy as np
 import pytest
 
@@ -10,6 +12,8 @@ import oracle as O
 from helpers import rand_batch
 from paper_2508_05029_b200.columnar import BOOL, DECIMAL, FLOAT64, INT64, assert_batches_equal
 from paper_2508_05029_b200.ops import Context, Pool, engine_run_query
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 pytestmark = pytest.mark.gpu
 
@@ -101,3 +105,58 @@ def test_engine_over_tcf_files(ctx, q, tmp_path):
                                   device_budget=max(sum(b.nbytes() for b in host.values()) // 3, 48 << 20))
     assert_batches_equal(got, O.query(q, host, 8))
     assert m["storage_reads"] >= sum(Tcf(p).row_groups for p in paths.values()), m
+
+
+@pytest.mark.parametrize("q", [5, 9])
+def test_engine_host_tier_spill_stress(ctx, q):
+    """The config-5 shape at SF1 (Host-tier tables, a Device budget below the
+    data, several batches per table) repeated: spills run on the Memory executor
+    concurrently with the compute threads, so every handle a kernel reads must be
+    pinned first (a concatenated build batch once was not — wrong Q9 groups in
+    about half of the runs).  Every repetition equals the oracle."""
+    sf = 1.0
+    host = {t: O.datagen(t, sf) for t in O.QUERY_TABLES[q]}
+    total = sum(b.nbytes() for b in host.values())
+    want = O.query(q, host, 8)
+    spills = 0
+    for _ in range(4):
+        got, m = engine_run_query(ctx, q, host, compute_threads=4, batch_rows=256 * 1024, preload=1,
+                                  device_budget=max(int(total / 1.5), 64 << 20))
+        assert_batches_equal(got, want)
+        spills += m["spills"]
+    assert spills > 0
+
+
+@pytest.mark.timeout(300)
+def test_engine_abort_does_not_hang():
+    """Q9 under a Device budget tight enough that a probe task may not fit
+    (OutOfMemoryUnsplittable) while other tasks wait for memory
+    and spills are queued: whichever way each run goes (an exact result or the
+    abort), the query returns — the tear-down releases waiting tasks (one once
+    kept the executor threads from joining: a hang).  Run in a subprocess with a
+    deadline, 4 times."""
+    import subprocess
+    import sys
+    code = r"""
+import os, sys
+sys.path[:0] = [%r, %r]
+import oracle as O
+from paper_2508_05029_b200.ops import Context, engine_run_query
+from paper_2508_05029_b200.columnar import TqError, assert_batches_equal
+ctx = Context(0)
+host = {t: O.datagen(t, 1.0) for t in O.QUERY_TABLES[9]}
+total = sum(b.nbytes() for b in host.values())
+want = O.query(9, host, 8)
+for _ in range(4):
+    try:
+        got, m = engine_run_query(ctx, 9, host, compute_threads=4, batch_rows=512 * 1024, preload=1,
+                                  device_budget=int(total / 2.5))
+        assert_batches_equal(got, want)
+        print("exact", flush=True)
+    except TqError as e:
+        assert "OutOfMemoryUnsplittable" in str(e), e
+        print("aborted", flush=True)
+""" % (ROOT, os.path.join(ROOT, "oracle"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert len(r.stdout.split()) == 4, r.stdout
