@@ -57,9 +57,11 @@ tq_status tq_pipeline_broadcast(tq_comm* comm, const tq_batch* in, const tq_expr
                                 uint32_t nexprs, tq_batch* out, void* stream);
 /* Partitioned LIP filter (PAPER.md:394 Lookahead Information Passing, after
  * the build side's shuffle): all-gather every rank's join-table Bloom filter
- * (equal sizes: tq_join_build_sized) into one filter whose part d is rank d's.
- * Passed as `semi` to tq_pipeline_partition_exchange, a row is checked only
- * against the part of the rank it is sent to.  Collective. */
+ * (equal sizes: every rank built its table with tq_join_build_sized and the
+ * same agreed bloom_keys; checked against the table's own count before the
+ * collective, TQ_INVALID_PLAN otherwise) into one filter whose part d is rank
+ * d's.  Passed as `semi` to tq_pipeline_partition_exchange, a row is checked
+ * only against the part of the rank it is sent to.  Collective. */
 tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* table, tq_bloom** out, void* stream);
 /* The most rows any rank received in the last tq_pipeline_partition_exchange
  * (>= 1): identical on every rank, so a Bloom filter sized from it has the same

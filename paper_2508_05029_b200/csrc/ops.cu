@@ -24,6 +24,10 @@ struct tq_join_table {
   std::shared_ptr<void> semi_prog;  // Prog
   std::vector<uint32_t> semi_keys;
   uint64_t semi_bloom_keys = 0;
+  // the agreed row count the Bloom filter was sized from (tq_join_build_sized /
+  // tq_pipeline_build_ex; 0 = the table's own rows): the partitioned LIP
+  // all-gather needs every rank's filter sized from the same count
+  uint64_t bloom_keys = 0;
   uint64_t bytes;
   cudaStream_t stream;
   tq_batch build;                      // borrowed descriptors (cols copied)
@@ -1414,6 +1418,7 @@ static void run_build(tq_ctx* c, const tq_batch* in, Prog& P, const std::vector<
     t->semi_keys = key_roots;
     t->semi_bloom_keys = bloom_keys;
   }
+  t->bloom_keys = bloom_keys;
   // No uniqueness pass and no host sync: a probe first assumes unique build
   // keys (the PK side of a PK-FK join) and runs in one pass.  One-word keys
   // are proven unique (or not) by the build itself (jt.dup_dev); otherwise the
@@ -3475,15 +3480,16 @@ tq_status tq_comm_gather_table_blooms(tq_comm* comm, const tq_join_table* t, tq_
     b->key_scale = t->key_scale;
     b->nwords = per;
     b->parts = (uint32_t)n;
-    // Precondition (collective): every rank built its table with bloom_keys =
-    // the capacity of the last fused exchange, which is identical on all ranks,
-    // so every filter has the same word count.  Checked locally against that
-    // agreed value before the collective (no size all-gather, no host sync).
+    // Precondition (collective): every rank built its table with the same
+    // agreed bloom_keys (e.g. tq_comm_last_exchange_capacity right after the
+    // exchange that delivered the build side), so every filter has the same
+    // word count.  Checked locally against the table's own agreed count before
+    // the collective (no size all-gather, no host sync).
     uint64_t expect = 1024;
-    while (expect * 32 < comm_last_cap(comm) * kLipBloomBitsPerKey) expect <<= 1;
-    if (per != expect) {
+    while (expect * 32 < t->bloom_keys * kLipBloomBitsPerKey) expect <<= 1;
+    if (t->bloom_keys == 0 || per != expect) {
       delete b;
-      fail(TQ_INVALID_PLAN, "table Bloom filter not sized from the last exchange capacity (tq_join_build_sized)");
+      fail(TQ_INVALID_PLAN, "table Bloom filter not sized from an agreed row count (tq_join_build_sized)");
     }
     b->words = (uint32_t*)dalloc(c, per * 4 * n, st);
     const int ph = prof_begin(c, "nccl_gather_blooms", st);
