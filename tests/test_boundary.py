@@ -9,7 +9,8 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADERS = [os.path.join(ROOT, "include", h) for h in ("tq_gpu.h", "tq_exchange.h", "tq_memexec.h", "tq_engine.h")]
+HEADERS = [os.path.join(ROOT, "include", h)
+           for h in ("tq_gpu.h", "tq_exchange.h", "tq_memexec.h", "tq_engine.h", "tq_storage.h")]
 
 
 def declared_functions():
@@ -37,6 +38,24 @@ def test_struct_layouts_match_header():
     assert C.sizeof(TqColumnC) == 40
     assert C.sizeof(TqBatchC) == 32
     assert C.sizeof(TqExprNodeC) == 32
+
+
+def test_batch_set_rows_trims_the_descriptor():
+    """tq_batch_set_rows (the asynchronous operators' trim) is host-only: it
+    shortens rows and every fixed-width column's values_bytes, never grows."""
+    import numpy as np
+    from paper_2508_05029_b200 import ops
+    from paper_2508_05029_b200.columnar import DECIMAL, INT64, HostBatch
+    b = HostBatch(10)
+    b.cols.append(HostBatch.col_i64(np.arange(10)))
+    b.cols.append(HostBatch.col_dec(np.arange(10), 12, 2))
+    c = b.to_c()
+    ops.lib().tq_batch_set_rows(C.byref(c), 4)
+    assert c.rows == 4
+    assert [c.cols[i].values_bytes for i in range(2)] == [32, 64]
+    ops.lib().tq_batch_set_rows(C.byref(c), 7)  # larger than the current rows: ignored
+    assert c.rows == 4
+    assert (c.cols[0].kind, c.cols[1].kind) == (INT64, DECIMAL)
 
 
 def test_errc_names_mirror_reference():
