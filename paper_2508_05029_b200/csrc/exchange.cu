@@ -3,6 +3,7 @@
 // NVLink/NVSwitch, one communicator per GPU/process.  NCCL is dlopen'd
 // (libnccl.so.2: the copy torch already loaded, else the system one), so the
 // library still loads on machines without it.
+#include <algorithm>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -17,6 +18,8 @@
 #include "peer.h"
 
 namespace tq {
+// exclusive scan of n u32 -> u64 (+ total), ops.cu
+void scan_u32_public(tq_ctx* c, const u32* in, u64 n, u64* out, u64* total_dev, cudaStream_t st);
 namespace {
 
 struct Nccl {
@@ -61,6 +64,15 @@ void nccl_check(ncclResult_t r, const char* what) {
 }
 
 // bitmap (or all-valid) -> one byte per row
+__global__ void k_utf8_lengths(const int32_t* off, u64 n, u32* len) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    len[i] = (u32)(off[i + 1] - off[i]);
+}
+__global__ void k_u64_to_i32(const u64* in, u64 n, int32_t* out) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    out[i] = (int32_t)in[i];
+}
+
 __global__ void k_bits_to_bytes(const uint8_t* bm, u64 n, uint8_t* out) {
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
     out[i] = bm ? ((bm[i >> 3] >> (i & 7)) & 1) : 1;
@@ -194,11 +206,39 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
   Nccl& N = nccl();
   const int n = cm->n, me = cm->rank;
   if (in->mem != TQ_MEM_DEVICE) fail(TQ_INTERNAL, "exchange needs a device batch");
-  for (uint32_t k = 0; k < in->ncols; ++k)
-    if (in->cols[k].kind == TQ_UTF8) fail(TQ_INVALID_PLAN, "utf8 columns are not supported on the GPU exchange");
   if (in->ncols > 62) fail(TQ_INVALID_PLAN, "too many columns to exchange");
+  // Utf8 columns travel as per-row lengths (int32) + the bytes of each part's
+  // row range; the receiver rebuilds the offsets by a scan over the lengths
+  std::vector<uint32_t> ucols;
+  for (uint32_t k = 0; k < in->ncols; ++k)
+    if (in->cols[k].kind == TQ_UTF8) ucols.push_back(k);
+  const int nu = (int)ucols.size();
+  std::vector<std::vector<int32_t>> ubound(nu, std::vector<int32_t>(n + 1, 0));  // offsets at the part bounds
+  std::vector<u32*> ulen(nu, nullptr);
+  const u64 in_len_bytes = std::max<u64>(4, in->rows * 4);
+  if (nu) {
+    if ((u64)(n + 1) * nu * 4 > 4096) fail(TQ_INVALID_PLAN, "too many utf8 columns for one exchange");
+    std::vector<u64> bidx(n + 1);
+    for (int p = 0; p < n; ++p) bidx[p] = send_off[p];
+    bidx[n] = n ? send_off[n - 1] + send_cnt[n - 1] : 0;
+    int32_t* pin = (int32_t*)pinned_scratch(c);  // (n + 1) * nu ints <= 4 KB for n <= 16, nu <= 62
+    for (int j = 0; j < nu; ++j) {
+      const tq_column& col = in->cols[ucols[j]];
+      for (int p = 0; p <= n; ++p)
+        TQ_CUDA(cudaMemcpyAsync(pin + j * (n + 1) + p, col.offsets + bidx[p], 4, cudaMemcpyDeviceToHost, st));
+      ulen[j] = (u32*)dalloc(c, in_len_bytes, st);
+      if (in->rows)
+        k_utf8_lengths<<<(u32)std::max<u64>(1, std::min<u64>((in->rows + 255) / 256, 4096)), 256, 0, st>>>(
+            col.offsets, in->rows, ulen[j]);
+      counted_launch(c);
+    }
+    TQ_CUDA(cudaStreamSynchronize(st));
+    for (int j = 0; j < nu; ++j)
+      for (int p = 0; p <= n; ++p) ubound[j][p] = pin[j * (n + 1) + p];
+  }
   // 1) header all-gather: counts for every peer + a validity-presence mask
-  const int hw = n + 1;
+  //    (+ per Utf8 column, the bytes for every peer)
+  const int hw = n + 1 + n * nu;
   u64* hdr = (u64*)dalloc(c, (size_t)hw * (n + 1) * 8, st);
   std::vector<u64> mine(hw);
   for (int p = 0; p < n; ++p) mine[p] = send_cnt[p];
@@ -206,6 +246,8 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
   for (uint32_t k = 0; k < in->ncols; ++k)
     if (in->rows > 0 && in->cols[k].validity) vmask |= 1ull << k;
   mine[n] = vmask;
+  for (int j = 0; j < nu; ++j)
+    for (int p = 0; p < n; ++p) mine[n + 1 + j * n + p] = (u64)(ubound[j][p + 1] - ubound[j][p]);
   TQ_CUDA(cudaMemcpyAsync(hdr + (size_t)hw * n, mine.data(), hw * 8, cudaMemcpyHostToDevice, st));
   nccl_check(N.all_gather(hdr + (size_t)hw * n, hdr, hw, ncclUint64, cm->comm, st), "ncclAllGather");
   std::vector<u64> all((size_t)hw * n);
@@ -222,11 +264,22 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
   if (recv_offsets)
     for (int s = 0; s <= n; ++s) recv_offsets[s] = recv_off[s];
   const uint64_t rows = recv_off[n];
+  // Utf8: received bytes per source (in source order) and in total
+  std::vector<std::vector<u64>> ubyte_off(nu, std::vector<u64>(n + 1, 0));
+  std::vector<uint64_t> ub(in->ncols, 0);
+  for (int j = 0; j < nu; ++j) {
+    for (int s = 0; s < n; ++s) ubyte_off[j][s + 1] = ubyte_off[j][s] + all[(size_t)s * hw + n + 1 + j * n + me];
+    if (ubyte_off[j][n] > 0x7fffffffull) fail(TQ_INVALID_PLAN, "utf8 column over 2 GiB after the exchange");
+    ub[ucols[j]] = ubyte_off[j][n];
+  }
   // 2) output batch
   std::vector<tq_column> sch(in->cols, in->cols + in->ncols);
   std::vector<bool> wv;
   for (uint32_t k = 0; k < in->ncols; ++k) wv.push_back((any_valid >> k) & 1);
-  alloc_batch(c, rows, sch, wv, out, st);
+  alloc_batch(c, rows, sch, wv, out, st, &ub);
+  const u64 out_len_bytes = std::max<u64>(4, rows * 4);
+  std::vector<u32*> urecv(nu, nullptr);
+  for (int j = 0; j < nu; ++j) urecv[j] = (u32*)dalloc(c, out_len_bytes, st);
   // validity travels as one byte per row
   uint8_t* vsend = nullptr;
   uint8_t* vrecv = nullptr;
@@ -250,12 +303,31 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
   for (int p = 0; p < n; ++p) {
     int j = 0;
     for (uint32_t k = 0; k < in->ncols; ++k) {
-      const size_t w = width_of(in->cols[k].kind);
-      const uint8_t* sv = (const uint8_t*)in->cols[k].values;
-      uint8_t* rv = (uint8_t*)out->cols[k].values;
-      if (send_cnt[p]) nccl_check(N.send(sv + send_off[p] * w, send_cnt[p] * w, ncclUint8, p, cm->comm, st), "ncclSend");
-      if (recv_cnt[p]) nccl_check(N.recv(rv + recv_off[p] * w, recv_cnt[p] * w, ncclUint8, p, cm->comm, st), "ncclRecv");
-      if (p != me) sent += send_cnt[p] * w;
+      if (in->cols[k].kind == TQ_UTF8) {
+        const int j = (int)(std::find(ucols.begin(), ucols.end(), k) - ucols.begin());
+        const u64 sb = (u64)(ubound[j][p + 1] - ubound[j][p]);
+        const u64 rb = ubyte_off[j][p + 1] - ubyte_off[j][p];
+        if (send_cnt[p]) {
+          nccl_check(N.send(ulen[j] + send_off[p], send_cnt[p] * 4, ncclUint8, p, cm->comm, st), "ncclSend");
+          if (sb)
+            nccl_check(N.send((const uint8_t*)in->cols[k].values + ubound[j][p], sb, ncclUint8, p, cm->comm, st),
+                       "ncclSend");
+        }
+        if (recv_cnt[p]) {
+          nccl_check(N.recv(urecv[j] + recv_off[p], recv_cnt[p] * 4, ncclUint8, p, cm->comm, st), "ncclRecv");
+          if (rb)
+            nccl_check(N.recv((uint8_t*)out->cols[k].values + ubyte_off[j][p], rb, ncclUint8, p, cm->comm, st),
+                       "ncclRecv");
+        }
+        if (p != me) sent += send_cnt[p] * 4 + sb;
+      } else {
+        const size_t w = width_of(in->cols[k].kind);
+        const uint8_t* sv = (const uint8_t*)in->cols[k].values;
+        uint8_t* rv = (uint8_t*)out->cols[k].values;
+        if (send_cnt[p]) nccl_check(N.send(sv + send_off[p] * w, send_cnt[p] * w, ncclUint8, p, cm->comm, st), "ncclSend");
+        if (recv_cnt[p]) nccl_check(N.recv(rv + recv_off[p] * w, recv_cnt[p] * w, ncclUint8, p, cm->comm, st), "ncclRecv");
+        if (p != me) sent += send_cnt[p] * w;
+      }
       if ((any_valid >> k) & 1) {
         if (send_cnt[p])
           nccl_check(N.send(vsend + (u64)j * in->rows + send_off[p], send_cnt[p], ncclUint8, p, cm->comm, st), "ncclSend");
@@ -280,6 +352,17 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
     }
     dfree(c, vsend, std::max<u64>(1, in->rows) * nv, st);
     dfree(c, vrecv, std::max<u64>(1, rows) * nv, st);
+  }
+  // Utf8 offsets of the output: exclusive scan of the received lengths
+  for (int j = 0; j < nu; ++j) {
+    u64* scan = (u64*)dalloc(c, (rows + 1) * 8, st);
+    scan_u32_public(c, urecv[j], rows, scan, scan + rows, st);
+    k_u64_to_i32<<<(u32)std::max<u64>(1, std::min<u64>((rows + 1 + 255) / 256, 4096)), 256, 0, st>>>(
+        scan, rows + 1, out->cols[ucols[j]].offsets);
+    counted_launch(c);
+    dfree(c, scan, (rows + 1) * 8, st);
+    dfree(c, urecv[j], out_len_bytes, st);
+    dfree(c, ulen[j], in_len_bytes, st);
   }
   TQ_CUDA(cudaGetLastError());
 }

@@ -5,6 +5,7 @@ mismatch.  Modes (TQ_MODE):
             which columns can be null (rank 0 has nulls, rank 1 has no
             bitmaps, rank 2 an empty input): every rank must lay out its
             window identically and the output must carry the nulls.
+  utf8      Utf8 payload / key columns through the NCCL exchange.
   engine    the C++ worker runtime's distributed plans (tq_engine_run_query
             with a communicator) for Q1 / Q3 / Q5 / Q6 / Q9: exchange_decide
             (adaptive), forced Broadcast and forced HashPartition (SPEC.md:613
@@ -43,6 +44,38 @@ def validity(ctx, comm, rank, world):
     want_bc = O.project_execute(O.filter_execute(allin, Col(2) < 5), [Col(1), Col(0)])
     for o in outs:  # every rank receives every broadcast row
         assert_batches_equal(o[1], want_bc)
+    return True
+
+
+def utf8(ctx, comm, rank, world):
+    """Utf8 columns through the NCCL exchange (tq_comm_exchange): each rank
+    hash-partitions a batch with Utf8 payload and key columns (nulls on rank 0,
+    an empty input on rank 2) and exchanges it; rank r must receive, in sender
+    order, every sender's part r — strings, offsets and bitmaps exactly."""
+    import numpy as np
+    import oracle as O
+    from paper_2508_05029_b200.columnar import HostBatch, assert_batches_equal
+    rng = np.random.default_rng(70 + rank)
+    rows = 0 if rank == 2 else 3000 + 500 * rank
+    words = ["", "a", "bc", "def", "ASIA", "ünï", "x" * 50] + [f"w{i}" for i in range(40)]
+    b = HostBatch(rows)
+    b.cols.append(HostBatch.col_utf8([words[i] for i in rng.integers(0, len(words), rows)],
+                                     (rng.random(rows) > 0.1) if rank == 0 else None))
+    b.cols.append(HostBatch.col_i64(rng.integers(0, 100, rows)))
+    b.cols.append(HostBatch.col_utf8([words[i] for i in rng.integers(0, len(words), rows)]))
+    d = ctx.upload(b)
+    parts, offs = ctx.hash_partition(d, [0, 1], world)
+    got, _ = comm.exchange(parts, offs)
+    got = got.to_host()
+    ins = [None] * world
+    outs = [None] * world
+    dist.all_gather_object(ins, b)
+    dist.all_gather_object(outs, got)
+    if rank != 0:
+        return True
+    for r in range(world):
+        want = O.concat([O.hash_partition(ins[s], [0, 1], world)[r] for s in range(world)])
+        assert_batches_equal(outs[r], want, ordered=True)
     return True
 
 
@@ -90,7 +123,7 @@ def main():
     mode = os.environ.get("TQ_MODE", "validity")
     rc = 0
     try:
-        {"validity": validity, "engine": engine}[mode](ctx, comm, rank, world)
+        {"validity": validity, "engine": engine, "utf8": utf8}[mode](ctx, comm, rank, world)
         dist.barrier()
         if rank == 0:
             print(f"mgpu ops ok: mode={mode} world={world}")

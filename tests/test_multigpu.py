@@ -30,7 +30,7 @@ def test_distributed_q3_nccl(world, mode):
     assert "mgpu q3 ok" in r.stdout
 
 
-@pytest.mark.parametrize("mode", ["validity", "engine"])
+@pytest.mark.parametrize("mode", ["validity", "engine", "utf8"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_distributed_ops(world, mode):
     if ngpus() < world:
