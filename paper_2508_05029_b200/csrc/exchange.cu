@@ -213,19 +213,21 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
   for (uint32_t k = 0; k < in->ncols; ++k)
     if (in->cols[k].kind == TQ_UTF8) ucols.push_back(k);
   const int nu = (int)ucols.size();
-  std::vector<std::vector<int32_t>> ubound(nu, std::vector<int32_t>(n + 1, 0));  // offsets at the part bounds
+  // per Utf8 column and peer: the byte range [ustart, uend) of the rows sent to it
+  // (parts of a partition are adjacent; an all-gather sends every peer all rows)
+  std::vector<std::vector<int32_t>> ustart(nu, std::vector<int32_t>(n, 0)), uend(nu, std::vector<int32_t>(n, 0));
   std::vector<u32*> ulen(nu, nullptr);
   const u64 in_len_bytes = std::max<u64>(4, in->rows * 4);
   if (nu) {
-    if ((u64)(n + 1) * nu * 4 > 4096) fail(TQ_INVALID_PLAN, "too many utf8 columns for one exchange");
-    std::vector<u64> bidx(n + 1);
-    for (int p = 0; p < n; ++p) bidx[p] = send_off[p];
-    bidx[n] = n ? send_off[n - 1] + send_cnt[n - 1] : 0;
-    int32_t* pin = (int32_t*)pinned_scratch(c);  // (n + 1) * nu ints <= 4 KB for n <= 16, nu <= 62
+    if ((u64)2 * n * nu * 4 > 4096) fail(TQ_INVALID_PLAN, "too many utf8 columns for one exchange");
+    int32_t* pin = (int32_t*)pinned_scratch(c);  // 2 n nu ints <= 4 KB
     for (int j = 0; j < nu; ++j) {
       const tq_column& col = in->cols[ucols[j]];
-      for (int p = 0; p <= n; ++p)
-        TQ_CUDA(cudaMemcpyAsync(pin + j * (n + 1) + p, col.offsets + bidx[p], 4, cudaMemcpyDeviceToHost, st));
+      for (int p = 0; p < n; ++p) {
+        TQ_CUDA(cudaMemcpyAsync(pin + (j * n + p) * 2, col.offsets + send_off[p], 4, cudaMemcpyDeviceToHost, st));
+        TQ_CUDA(cudaMemcpyAsync(pin + (j * n + p) * 2 + 1, col.offsets + send_off[p] + send_cnt[p], 4,
+                                cudaMemcpyDeviceToHost, st));
+      }
       ulen[j] = (u32*)dalloc(c, in_len_bytes, st);
       if (in->rows)
         k_utf8_lengths<<<(u32)std::max<u64>(1, std::min<u64>((in->rows + 255) / 256, 4096)), 256, 0, st>>>(
@@ -234,7 +236,10 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
     }
     TQ_CUDA(cudaStreamSynchronize(st));
     for (int j = 0; j < nu; ++j)
-      for (int p = 0; p <= n; ++p) ubound[j][p] = pin[j * (n + 1) + p];
+      for (int p = 0; p < n; ++p) {
+        ustart[j][p] = pin[(j * n + p) * 2];
+        uend[j][p] = pin[(j * n + p) * 2 + 1];
+      }
   }
   // 1) header all-gather: counts for every peer + a validity-presence mask
   //    (+ per Utf8 column, the bytes for every peer)
@@ -247,7 +252,7 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
     if (in->rows > 0 && in->cols[k].validity) vmask |= 1ull << k;
   mine[n] = vmask;
   for (int j = 0; j < nu; ++j)
-    for (int p = 0; p < n; ++p) mine[n + 1 + j * n + p] = (u64)(ubound[j][p + 1] - ubound[j][p]);
+    for (int p = 0; p < n; ++p) mine[n + 1 + j * n + p] = (u64)(uend[j][p] - ustart[j][p]);
   TQ_CUDA(cudaMemcpyAsync(hdr + (size_t)hw * n, mine.data(), hw * 8, cudaMemcpyHostToDevice, st));
   nccl_check(N.all_gather(hdr + (size_t)hw * n, hdr, hw, ncclUint64, cm->comm, st), "ncclAllGather");
   std::vector<u64> all((size_t)hw * n);
@@ -305,12 +310,12 @@ void exchange_impl(tq_comm* cm, const tq_batch* in, const std::vector<uint64_t>&
     for (uint32_t k = 0; k < in->ncols; ++k) {
       if (in->cols[k].kind == TQ_UTF8) {
         const int j = (int)(std::find(ucols.begin(), ucols.end(), k) - ucols.begin());
-        const u64 sb = (u64)(ubound[j][p + 1] - ubound[j][p]);
+        const u64 sb = (u64)(uend[j][p] - ustart[j][p]);
         const u64 rb = ubyte_off[j][p + 1] - ubyte_off[j][p];
         if (send_cnt[p]) {
           nccl_check(N.send(ulen[j] + send_off[p], send_cnt[p] * 4, ncclUint8, p, cm->comm, st), "ncclSend");
           if (sb)
-            nccl_check(N.send((const uint8_t*)in->cols[k].values + ubound[j][p], sb, ncclUint8, p, cm->comm, st),
+            nccl_check(N.send((const uint8_t*)in->cols[k].values + ustart[j][p], sb, ncclUint8, p, cm->comm, st),
                        "ncclSend");
         }
         if (recv_cnt[p]) {

@@ -3507,6 +3507,15 @@ tq_status tq_pipeline_broadcast(tq_comm* comm, const tq_batch* in, const tq_expr
   return guard([&] {
     tq_ctx* c = comm_ctx(comm);
     check_device_batch(in);
+    if (has_utf8(in)) {  // fixed-width windows: Utf8 columns take the NCCL all-gather (every rank: same schema)
+      tq_batch m{};
+      tq_status r = tq_pipeline_materialize(c, in, pred, exprs, nexprs, &m, stream);
+      if (r != TQ_OK) fail(r, tq_last_error());
+      r = tq_comm_allgather(comm, &m, out, nullptr, stream);
+      tq_batch_free(c, &m);
+      if (r != TQ_OK) fail(r, tq_last_error());
+      return;
+    }
     Prog P(schema_of(in));
     compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
     uint64_t sent_rows = 0;
@@ -3523,6 +3532,27 @@ tq_status tq_pipeline_partition_exchange(tq_comm* comm, const tq_batch* in, cons
   return guard([&] {
     tq_ctx* c = comm_ctx(comm);
     check_device_batch(in);
+    if (has_utf8(in)) {
+      // the receive window is fixed-width: Utf8 columns take the NCCL exchange
+      // (a schema property, so every rank takes this same path)
+      if (semi) fail(TQ_INVALID_PLAN, "no LIP filter on a partition exchange with utf8 columns");
+      const int n = comm_size(comm);
+      std::vector<uint64_t> offs(n + 1);
+      tq_batch part{};
+      tq_status r = tq_pipeline_partition(c, in, pred, exprs, nexprs, keys, nkeys, (uint32_t)n, &part, offs.data(),
+                                          stream);
+      if (r != TQ_OK) fail(r, tq_last_error());
+      r = tq_comm_exchange(comm, &part, offs.data(), out, nullptr, stream);
+      tq_batch_free(c, &part);
+      if (r != TQ_OK) fail(r, tq_last_error());
+      // the agreed row count for a following tq_join_build_sized: the most rows any rank received
+      std::vector<uint64_t> got(n);
+      const uint64_t mine = out->rows;
+      r = tq_comm_allgather_host_u64(comm, &mine, got.data(), 1, stream);
+      if (r != TQ_OK) fail(r, tq_last_error());
+      comm_last_cap(comm) = std::max<uint64_t>(1, *std::max_element(got.begin(), got.end()));
+      return;
+    }
     Prog P(schema_of(in));
     compile_prog(P, in, pred, exprs, nexprs, exprs == nullptr);
     std::vector<uint32_t> kr(keys, keys + nkeys);

@@ -67,15 +67,20 @@ def utf8(ctx, comm, rank, world):
     parts, offs = ctx.hash_partition(d, [0, 1], world)
     got, _ = comm.exchange(parts, offs)
     got = got.to_host()
+    # the fused API with Utf8 columns (routed through the NCCL exchange / all-gather)
+    px = comm.partition_exchange(d, None, None, [0, 1]).to_host()
+    bc = comm.broadcast(d, None, None).to_host()
     ins = [None] * world
     outs = [None] * world
     dist.all_gather_object(ins, b)
-    dist.all_gather_object(outs, got)
+    dist.all_gather_object(outs, (got, px, bc))
     if rank != 0:
         return True
     for r in range(world):
         want = O.concat([O.hash_partition(ins[s], [0, 1], world)[r] for s in range(world)])
-        assert_batches_equal(outs[r], want, ordered=True)
+        assert_batches_equal(outs[r][0], want, ordered=True)
+        assert_batches_equal(outs[r][1], want, ordered=True)
+        assert_batches_equal(outs[r][2], O.concat(ins), ordered=True)
     return True
 
 
@@ -111,6 +116,9 @@ def engine(ctx, comm, rank, world):
 
 
 def main():
+    if os.environ.get("TQ_MGPU_TRACE"):
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ["TQ_MGPU_TRACE"]), exit=True)
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     dist.init_process_group("gloo")
@@ -124,12 +132,15 @@ def main():
     rc = 0
     try:
         {"validity": validity, "engine": engine, "utf8": utf8}[mode](ctx, comm, rank, world)
-        dist.barrier()
-        if rank == 0:
-            print(f"mgpu ops ok: mode={mode} world={world}")
     except AssertionError as e:
-        print("MISMATCH", mode, e)
+        print("MISMATCH", mode, str(e)[:2000], flush=True)
         rc = 1
+    # every rank reaches the same barrier whether its check passed or not
+    flags = [None] * world
+    dist.all_gather_object(flags, rc)
+    rc = max(flags)
+    if rank == 0 and rc == 0:
+        print(f"mgpu ops ok: mode={mode} world={world}")
     comm.close()
     ctx.close()
     dist.barrier()
